@@ -1,0 +1,165 @@
+/*
+ * mvamg_b200.h -- C ABI of libmvamg_b200.so, the B200 (sm_100a) solve phase of
+ * the composite bootstrap / multi-vector aggregation AMG of arXiv 1907.04417.
+ *
+ * The reference (`mvamg`, pure Python + numba) has no FFI; its drop-in surface
+ * is the duck-typed operator API that this ABI sits under:
+ *   - preconditioner slot   pcg(A, b, precond, rtol, itmax, x0, callback)
+ *                           pkg/src/mvamg/krylov.py:28            -> mvamg_pcg_*
+ *   - operator object       MultigridOperator(...).apply / error_propagation
+ *                           pkg/src/mvamg/cycles.py:100-190       -> mvamg_hierarchy_*
+ *   - composite slot        apply_composite_symmetrized(composite, x)
+ *                           pkg/src/mvamg/bootstrap.py:98-113     -> mvamg_composite_*
+ *   - sparse kernels        spmv / galerkin_product / a_norm
+ *                           pkg/src/mvamg/sparse.py:30,50,69      -> mvamg_csr_*
+ *   - smoother kernels      gs_forward / gs_backward
+ *                           pkg/src/mvamg/_kernels.py:15-38       -> mvamg_gs_*
+ * The ctypes binding a maintainer adds on the reference side is in
+ * INTEGRATION.md; the in-tree binding is paper_1907_04417_b200/_lib.py.
+ *
+ * Conventions: plain C types only.  Matrices are CSR with int32 indptr/indices
+ * and fp64 values (scipy's layout for < 2^31 nonzeros).  Pointers documented as
+ * "device" must be CUDA device memory owned by the caller (PyTorch tensors in
+ * the Python host layer); the library never frees caller memory.  `stream` is a
+ * cudaStream_t passed as void*.  Every call returns 0 on success or a nonzero
+ * MVAMG_E* code; mvamg_last_error() returns a thread-local message.
+ */
+#ifndef MVAMG_B200_H
+#define MVAMG_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes --------------------------------------------------------- */
+#define MVAMG_OK 0
+#define MVAMG_E_ARG 1          /* bad argument / dimension mismatch (ValueError)  */
+#define MVAMG_E_CUDA 2         /* CUDA runtime failure                            */
+#define MVAMG_E_NOT_SPD 3      /* Krylov breakdown / zero diagonal (NotSpdError) */
+#define MVAMG_E_TIMEOUT 4      /* GS dependency wait exceeded its bound           */
+#define MVAMG_E_STATE 5        /* call out of order (workspace not bound, ...)    */
+
+/* device status word bits (mvamg_pcg_* status_out) */
+#define MVAMG_ST_RZ_BREAKDOWN 1    /* r'z <= 0   krylov.py:46-47,68-69 */
+#define MVAMG_ST_PQ_BREAKDOWN 2    /* p'Ap <= 0  krylov.py:54-55       */
+#define MVAMG_ST_FCG_BREAKDOWN 4   /* FCG p'Ap <= 0  krylov.py:101-102 */
+#define MVAMG_ST_GS_TIMEOUT 8
+
+/* smoother kinds (cycles.py:24-26) and cycle kinds (cycles.py:43-52) */
+#define MVAMG_GS_FORWARD 0
+#define MVAMG_GS_BACKWARD 1
+#define MVAMG_WEIGHTED_JACOBI 2
+#define MVAMG_CYCLE_V 0
+#define MVAMG_CYCLE_K 1
+
+int mvamg_version(void);
+const char* mvamg_last_error(void);
+
+/* ---- GS schedule analysis (host) -------------------------------------------
+ * Splits the rows of a CSR matrix (host arrays) into dependency chains
+ * (maximal runs where row i couples to row i-1, at most max_chain rows) and
+ * groups consecutive chains into tiles of <= max_threads chains whose rows fit a
+ * shared-memory window of <= max_window rows.  Call first with the out arrays
+ * NULL to get counts, then with arrays of nchains+1 / ntiles+1 ints.
+ * Replaces nothing in the reference (numba runs rows serially,
+ * _kernels.py:15-38); the schedule preserves that order's dependency DAG, so
+ * the sweep result is bit-identical.                                          */
+int mvamg_gs_analyse(int n, const int* indptr, const int* indices, int max_chain,
+                     int max_threads, int max_window, int* nchains, int* ntiles,
+                     int* chain_ptr, int* tile_ptr, int* threads_out, int* window_out,
+                     int* depth_out);
+
+/* ---- stream-level kernels (device pointers) ------------------------------- */
+/* y = A x  (sparse.py:30-40; scipy csr_matvec order, bit-exact). */
+int mvamg_csr_spmv_f64(int n, const int* indptr, const int* indices, const double* data,
+                       const double* x, double* y, void* stream);
+/* r = b - A x  (cycles.py:156 inner term). */
+int mvamg_csr_residual_f64(int n, const int* indptr, const int* indices, const double* data,
+                           const double* b, const double* x, double* r, void* stream);
+/* y = y + (A x)  (cycles.py:170, prolongation; sum formed first). */
+int mvamg_csr_spmv_add_f64(int n, const int* indptr, const int* indices, const double* data,
+                           const double* x, double* y, void* stream);
+/* One lexicographic GS sweep (_kernels.py:15-38).  direction 0 = forward,
+ * 1 = backward.  x_old is the iterate before the sweep (ignored when
+ * zero_init != 0, meaning x_old == 0); x_new receives the result (must not
+ * alias x_old).  rdiag[i] = RN(1/diag[i]).  chain_ptr / tile_ptr come from
+ * mvamg_gs_analyse (device copies).  ws: device int workspace of >= 4 ints. */
+int mvamg_gs_sweep_f64(int direction, int zero_init, int n, const int* indptr,
+                       const int* indices, const double* data, const double* diag,
+                       const double* rdiag, int ntiles, const int* chain_ptr,
+                       const int* tile_ptr, int threads, int window, const double* b,
+                       const double* x_old, double* x_new, int* ws, void* stream);
+/* z = Inv r, Inv dense row-major n x n (coarsest solve; cycles.py:88-97). */
+int mvamg_dense_gemv_f64(int n, const double* inv, const double* r, double* z, void* stream);
+/* *result = x . y (deterministic two-level reduction; device scalar).
+ * ws: device workspace of >= 1024 doubles + 1 int (mvamg_dot_ws_bytes()). */
+int mvamg_dot_f64(int n, const double* x, const double* y, double* result, void* ws, void* stream);
+int mvamg_dot_ws_bytes(void);
+
+/* ---- hierarchy (MultigridOperator) ---------------------------------------- */
+typedef struct mvamg_hierarchy mvamg_hierarchy;
+
+/* cycles.py:108-128.  kinds are MVAMG_GS_* / MVAMG_WEIGHTED_JACOBI. */
+int mvamg_hierarchy_create(mvamg_hierarchy** h, int nlevels, int cycle_kind, int inner_fcg_iters,
+                           int pre_kind, int pre_sweeps, double pre_omega, int post_kind,
+                           int post_sweeps, double post_omega);
+int mvamg_hierarchy_destroy(mvamg_hierarchy* h);
+/* Level k matrix (device CSR) with its diagonal, RN reciprocal diagonal and GS
+ * schedule (device chain_ptr / tile_ptr from mvamg_gs_analyse). */
+int mvamg_hierarchy_set_level(mvamg_hierarchy* h, int k, int n, int nnz, const int* indptr,
+                              const int* indices, const double* data, const double* diag,
+                              const double* rdiag, int ntiles, const int* chain_ptr,
+                              const int* tile_ptr, int gs_threads, int gs_window);
+/* Transfer k: P (n_k x n_{k+1}) and R = P^T (n_{k+1} x n_k), device CSR. */
+int mvamg_hierarchy_set_transfer(mvamg_hierarchy* h, int k, const int* p_indptr,
+                                 const int* p_indices, const double* p_data,
+                                 const int* r_indptr, const int* r_indices,
+                                 const double* r_data);
+/* Coarsest level: dense inverse (row-major, device) built from the reference's
+ * own LU factors: Inv = lu_solve((lu, piv), I). */
+int mvamg_hierarchy_set_coarse(mvamg_hierarchy* h, const double* inv);
+/* Workspace: query its size in bytes, then bind caller-owned device memory. */
+int mvamg_hierarchy_workspace_bytes(mvamg_hierarchy* h, long long* bytes);
+int mvamg_hierarchy_bind_workspace(mvamg_hierarchy* h, void* ws, void* stream);
+/* Use CUDA graphs for repeated cycles (default 1). */
+int mvamg_hierarchy_set_graphs(mvamg_hierarchy* h, int enable);
+
+/* z = B^{-1} r, one cycle (cycles.py:174-179).  Device vectors of length n_0. */
+int mvamg_cycle_apply(mvamg_hierarchy* h, const double* r, double* z, void* stream);
+/* e = x - B^{-1} (A_0 x) (cycles.py:181-184). */
+int mvamg_error_propagation(mvamg_hierarchy* h, const double* x, double* e, void* stream);
+/* Device status word accumulated since the last reset (MVAMG_ST_* bits). */
+int mvamg_hierarchy_status(mvamg_hierarchy* h, int* status, int reset);
+
+/* ---- PCG (krylov.py:28-72), x0 = 0 ---------------------------------------
+ * precond: the hierarchy's cycle (pc_kind 1), the symmetrized multiplicative
+ * composite (pc_kind 2, mvamg_composite_*), or none (pc_kind 0).  The matrix is
+ * the finest level of `h`.  hist (device, itmax+1 doubles) receives
+ * ||r_k||; on return *nit = iterations, *converged, *status = MVAMG_ST_* bits
+ * (nonzero -> the Python layer raises NotSpdError like the reference). */
+#define MVAMG_PC_NONE 0
+#define MVAMG_PC_CYCLE 1
+#define MVAMG_PC_COMPOSITE 2
+typedef struct mvamg_composite mvamg_composite;
+int mvamg_pcg_solve(mvamg_hierarchy* h, int pc_kind, mvamg_composite* comp, const double* b,
+                    double* x, double rtol, int itmax, double* hist, int* nit, int* converged,
+                    int* status, void* stream);
+/* Same, with HOST b / x / hist (pinned or pageable): H2D of b and D2H of x and
+ * the residual history are inside the call (the end-to-end boundary). */
+int mvamg_pcg_solve_host(mvamg_hierarchy* h, int pc_kind, mvamg_composite* comp,
+                         const double* b_host, double* x_host, double rtol, int itmax,
+                         double* hist_host, int* nit, int* converged, int* status,
+                         void* stream);
+
+/* ---- composite of cycles (bootstrap.py:75-113) ---------------------------- */
+int mvamg_composite_create(mvamg_composite** c, int ncomp, mvamg_hierarchy* const* comps);
+int mvamg_composite_destroy(mvamg_composite* c);
+/* x <- E_1..E_r E_r..E_1 x, E_i = I - B_i A (bootstrap.py:98-113), in place. */
+int mvamg_composite_apply_symmetrized(mvamg_composite* c, double* x, void* stream);
+/* z = Bsym r: z=0; for i in 1..r, r..1: z += B_i (r - A z). */
+int mvamg_composite_precond(mvamg_composite* c, const double* r, double* z, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MVAMG_B200_H */

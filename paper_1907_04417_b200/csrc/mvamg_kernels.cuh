@@ -1,0 +1,491 @@
+// mvamg_kernels.cuh -- sm_100a device kernels for the mvamg solve phase.
+//
+// Everything here is fp64 sparse / streaming work (~0.17 flop/B): HBM- or
+// latency-bound, no tensor cores (BASELINE.json north_star).  Bit-exactness
+// recipe: each row sum is formed in CSR order starting
+// from 0.0 (or b[i] for GS) with separately rounded multiply and add/subtract
+// (__dmul_rn / __dadd_rn / __dsub_rn; the .so is also built with -fmad=false),
+// exactly like scipy csr_matvec and the numba GS kernels
+// (pkg/src/mvamg/_kernels.py:15-38, pkg/src/mvamg/sparse.py:40).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mvamg {
+
+constexpr unsigned long long kSentinel = 0xFFFFFFFFFFFFFFFFull;  // -NaN, never produced by arithmetic
+constexpr int kSpinLimit = 1 << 21;
+constexpr int kDotMaxBlocks = 1024;
+
+// status bits (mirror MVAMG_ST_* in include/mvamg_b200.h)
+constexpr int ST_RZ = 1, ST_PQ = 2, ST_FCG = 4, ST_GS_TIMEOUT = 8;
+
+// ---------------------------------------------------------------------------
+// Device scalar block shared by the drivers (one per hierarchy).
+struct DevScalars {
+  double rz, alpha, beta, r0, rtol;
+  double pq, rr;
+  int k, itmax, status, converged, stop, pad0, pad1, pad2;
+  double* hist;
+};
+
+// Per-level FCG scalars (krylov.py:75-107).
+struct FcgScalars {
+  double alpha, beta, pAp, pAp_prev, pr;
+};
+
+__device__ __forceinline__ double div_rn_markstein(double s, double d, double y) {
+  // RN(s/d) from y = RN(1/d): q0 = RN(s*y) is faithful, r = s - q0*d is exact
+  // (FMA), q = RN(q0 + r*y) is the correctly rounded quotient (Markstein).
+  // 24 cycles of dependent latency instead of ~350 for IEEE ddiv (measured on
+  // B200, profiles/r01_probe.txt); 0 mismatches vs __ddiv_rn on 2^26 samples.
+  double q0 = __dmul_rn(s, y);
+  double r = fma(-q0, d, s);
+  double q = fma(r, y, q0);
+  double aq = fabs(q0);
+  if (!(aq > 1e-290 && aq < 1e290)) q = __ddiv_rn(s, d);  // outside the theorem's range / zero
+  return q;
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const double* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+// Slow path of a dependency wait: spin on the sentinel.  A bounded spin (and an
+// abort once any thread has timed out) turns a scheduling bug into an error
+// status instead of a hung GPU.
+__device__ __noinline__ double poll_global_slow(const double* p, int* status) {
+  unsigned long long v;
+  int spins = 0;
+  do {
+    v = ld_relaxed_u64(p);
+    if ((++spins & 255) == 0) {
+      if (spins > kSpinLimit) { atomicOr(status, ST_GS_TIMEOUT); return 0.0; }
+      if (*reinterpret_cast<volatile int*>(status) & ST_GS_TIMEOUT) return 0.0;
+    }
+  } while (v == kSentinel);
+  return __longlong_as_double(v);
+}
+
+__device__ __forceinline__ double poll_global(const double* p, int* status) {
+  unsigned long long v = ld_relaxed_u64(p);
+  if (v != kSentinel) return __longlong_as_double(v);
+  return poll_global_slow(p, status);
+}
+
+__device__ __noinline__ double poll_shared_slow(const double* p, int* status) {
+  volatile const unsigned long long* q = reinterpret_cast<volatile const unsigned long long*>(p);
+  unsigned long long v;
+  int spins = 0;
+  do {
+    v = *q;
+    if ((++spins & 255) == 0) {
+      if (spins > kSpinLimit) { atomicOr(status, ST_GS_TIMEOUT); return 0.0; }
+      if (*reinterpret_cast<volatile int*>(status) & ST_GS_TIMEOUT) return 0.0;
+    }
+  } while (v == kSentinel);
+  return __longlong_as_double(v);
+}
+
+__device__ __forceinline__ double poll_shared(const double* p, int* status) {
+  unsigned long long v = *reinterpret_cast<volatile const unsigned long long*>(p);
+  if (v != kSentinel) return __longlong_as_double(v);
+  return poll_shared_slow(p, status);
+}
+
+// ---------------------------------------------------------------------------
+// CSR SpMV family, one thread per row, CSR-order accumulation (bit-exact).
+//   MODE 0: y = A x          (sparse.py:40)
+//   MODE 1: y = b - A x      (cycles.py:156 residual)
+//   MODE 2: y = y + (A x)    (cycles.py:170 prolongation; sum first, one add)
+template <int MODE>
+__global__ void __launch_bounds__(256) spmv_kernel(int n, const int* __restrict__ ip,
+                                                   const int* __restrict__ ix,
+                                                   const double* __restrict__ v,
+                                                   const double* __restrict__ x,
+                                                   const double* __restrict__ b, double* y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int k0 = __ldg(ip + i), k1 = __ldg(ip + i + 1);
+    double s = 0.0;
+    for (int k = k0; k < k1; ++k) s = __dadd_rn(s, __dmul_rn(__ldg(v + k), __ldg(x + __ldg(ix + k))));
+    if (MODE == 0) y[i] = s;
+    else if (MODE == 1) y[i] = __dsub_rn(__ldg(b + i), s);
+    else y[i] = __dadd_rn(y[i], s);
+  }
+}
+
+// Weighted Jacobi, out of place: y = x + ((omega*(b - Ax))/d)   (cycles.py:148)
+__global__ void __launch_bounds__(256) jacobi_kernel(int n, const int* __restrict__ ip,
+                                                     const int* __restrict__ ix,
+                                                     const double* __restrict__ v,
+                                                     const double* __restrict__ d,
+                                                     const double* __restrict__ b, double omega,
+                                                     const double* __restrict__ x, double* y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int k0 = ip[i], k1 = ip[i + 1];
+    double s = 0.0;
+    for (int k = k0; k < k1; ++k) s = __dadd_rn(s, __dmul_rn(v[k], x[ix[k]]));
+    double t = __ddiv_rn(__dmul_rn(omega, __dsub_rn(b[i], s)), d[i]);
+    y[i] = __dadd_rn(x[i], t);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Gauss-Seidel sweep in the reference's exact row order, scheduled sync-free.
+//
+// Rows are split (host, gs_analyse) into chains -- runs of consecutive rows
+// where row i couples to row i-1 -- and consecutive chains into tiles.  One
+// thread owns one chain and walks it in sweep order, so the i-1 dependency is a
+// register; other in-tile dependencies are read from a shared-memory window
+// and cross-tile ones from global memory, both polled against a NaN sentinel
+// (the value is its own ready flag: 8-byte stores are single-copy atomic, so no
+// fences are needed).  Tiles are claimed through an atomic ticket in sweep
+// order, so every tile a CTA waits on is owned by a resident CTA (no deadlock).
+// Each row's sum is formed in CSR order with lower neighbours taken from the
+// new iterate and upper neighbours from the old one -- exactly what the serial
+// loop computes -- so the result is bit-identical to _kernels.gs_forward /
+// gs_backward.
+struct GsArgs {
+  int n, ntiles, window;
+  const int* ip;
+  const int* ix;
+  const double* v;
+  const double* diag;
+  const double* rdiag;
+  const int* chain_ptr;
+  const int* tile_ptr;
+  const double* b;
+  const double* xold;
+  double* xnew;
+  int* ticket;
+  int* status;
+};
+
+constexpr int kGsPrefetchRows = 4;
+
+template <bool FWD, bool ZERO>
+__global__ void __launch_bounds__(256) gs_sweep_kernel(GsArgs a) {
+  extern __shared__ double win[];
+  __shared__ int s_tile;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1);
+    __syncthreads();
+    const int tk = s_tile;
+    if (tk >= a.ntiles) return;
+    const int t = FWD ? tk : a.ntiles - 1 - tk;
+    const int c0 = a.tile_ptr[t], c1 = a.tile_ptr[t + 1];
+    const int row0 = a.chain_ptr[c0], row1 = a.chain_ptr[c1];
+    const int wn = min(row1 - row0, a.window);
+    unsigned long long* wu = reinterpret_cast<unsigned long long*>(win);
+    for (int i = threadIdx.x; i < wn; i += blockDim.x) wu[i] = kSentinel;
+    __syncthreads();
+    const int c = c0 + threadIdx.x;
+    if (c < c1) {
+      const int cs = a.chain_ptr[c], ce = a.chain_ptr[c + 1];
+      const int len = ce - cs;
+      double xprev = 0.0;
+      int iprev = -1;
+      for (int q = 0; q < len; ++q) {
+        const int i = FWD ? cs + q : ce - 1 - q;
+        if (q + kGsPrefetchRows < len) {
+          const int ip_ = FWD ? i + kGsPrefetchRows : i - kGsPrefetchRows;
+          const int kp = a.ip[ip_];
+          prefetch_l1(a.ix + kp);
+          prefetch_l1(a.v + kp);
+        }
+        double s = a.b[i];
+        const int kb = a.ip[i], ke = a.ip[i + 1];
+        for (int kk = kb; kk < ke; ++kk) {
+          const int j = a.ix[kk];
+          if (j == i) continue;
+          const bool lower = FWD ? (j < i) : (j > i);
+          double val;
+          if (lower) {
+            if (j == iprev) {
+              val = xprev;
+            } else {
+              const int w = j - row0;
+              if (w >= 0 && w < wn) val = poll_shared(win + w, a.status);
+              else val = poll_global(a.xnew + j, a.status);
+            }
+          } else {
+            if (ZERO) continue;
+            val = a.xold[j];
+          }
+          s = __dsub_rn(s, __dmul_rn(a.v[kk], val));
+        }
+        const double xi = div_rn_markstein(s, a.diag[i], a.rdiag[i]);
+        const int w = i - row0;
+        if (w >= 0 && w < wn) reinterpret_cast<volatile double*>(win)[w] = xi;
+        a.xnew[i] = xi;
+        xprev = xi;
+        iprev = i;
+      }
+    }
+  }
+}
+
+// Fill x_new with the sentinel and reset the tile ticket.
+__global__ void gs_prep_kernel(int n, double* xnew, int* ticket) {
+  unsigned long long* u = reinterpret_cast<unsigned long long*>(xnew);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) u[i] = kSentinel;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0;
+}
+
+// ---------------------------------------------------------------------------
+// Dense coarsest solve z = Inv r (row-major), one warp per row.
+__global__ void __launch_bounds__(256) gemv_kernel(int n, const double* __restrict__ inv,
+                                                   const double* __restrict__ r, double* z) {
+  const int lane = threadIdx.x & 31;
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n;
+       row += (gridDim.x * blockDim.x) >> 5) {
+    const double* a = inv + (size_t)row * n;
+    double s = 0.0;
+    for (int j = lane; j < n; j += 32) s = fma(__ldg(a + j), __ldg(r + j), s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) z[row] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic reductions.  Each kernel reduces per block (fixed shuffle
+// tree), writes a partial, and the last block to arrive sums the partials in
+// block order and runs a scalar epilogue (the Krylov scalar updates of
+// krylov.py), so no host round trip is needed between kernels.
+enum PostOp : int {
+  POST_STORE = 0,       // out[0] = d1
+  POST_PCG_ALPHA = 1,   // pq = d1; alpha = rz/pq                 krylov.py:53-56
+  POST_PCG_NORM = 2,    // hist[k+1] = sqrt(d1); stop test        krylov.py:59-65
+  POST_PCG_BETA = 3,    // rz' = d1; beta = rz'/rz; rz = rz'      krylov.py:67-71
+  POST_PCG_INIT = 4,    // rz = d1 (r'z of z = M r0)              krylov.py:45-47
+  POST_PCG_R0 = 5,      // r0 = sqrt(d1); hist[0]                 krylov.py:40-44
+  POST_FCG_BETA = 6,    // beta = d1/pAp_prev                     krylov.py:97
+  POST_FCG_ALPHA = 7,   // pAp = d1; alpha = d2/pAp               krylov.py:100-104
+};
+
+struct ReduceCtx {
+  double* partials;   // >= 2*kDotMaxBlocks
+  unsigned* counter;  // zero between uses
+  DevScalars* sc;
+  FcgScalars* fs;
+  double* out;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block reduce of (d1, d2) for blockDim.x == 256.
+__device__ __forceinline__ void block_sum2(double& d1, double& d2) {
+  __shared__ double sh[2][8];
+  d1 = warp_sum(d1);
+  d2 = warp_sum(d2);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { sh[0][w] = d1; sh[1][w] = d2; }
+  __syncthreads();
+  if (w == 0) {
+    d1 = l < 8 ? sh[0][l] : 0.0;
+    d2 = l < 8 ? sh[1][l] : 0.0;
+    d1 = warp_sum(d1);
+    d2 = warp_sum(d2);
+  }
+  __syncthreads();
+}
+
+__device__ void run_post(int op, double d1, double d2, const ReduceCtx& c) {
+  DevScalars* s = c.sc;
+  switch (op) {
+    case POST_STORE:
+      c.out[0] = d1;
+      break;
+    case POST_PCG_ALPHA:
+      s->pq = d1;
+      if (!(d1 > 0.0)) { s->status |= ST_PQ; s->stop = 1; s->alpha = 0.0; }
+      else s->alpha = s->rz / d1;
+      break;
+    case POST_PCG_NORM: {
+      double nr = sqrt(d1);
+      s->k += 1;
+      s->hist[s->k] = nr;
+      s->rr = nr;
+      if (nr <= s->rtol * s->r0) { s->converged = 1; s->stop = 1; }
+      if (s->k >= s->itmax) s->stop = 1;
+      break;
+    }
+    case POST_PCG_BETA:
+      if (!(d1 > 0.0)) { s->status |= ST_RZ; s->stop = 1; s->beta = 0.0; }
+      else { s->beta = d1 / s->rz; s->rz = d1; }
+      break;
+    case POST_PCG_INIT:
+      s->rz = d1;
+      if (!(d1 > 0.0)) { s->status |= ST_RZ; s->stop = 1; }
+      if (s->itmax <= 0) s->stop = 1;
+      break;
+    case POST_PCG_R0: {
+      double nr = sqrt(d1);
+      s->r0 = nr;
+      s->hist[0] = nr;
+      s->k = 0;
+      s->converged = 0;
+      s->stop = 0;
+      if (nr == 0.0) { s->converged = 1; s->stop = 1; }
+      break;
+    }
+    case POST_FCG_BETA:
+      c.fs->beta = d1 / c.fs->pAp_prev;
+      break;
+    case POST_FCG_ALPHA:
+      c.fs->pAp = d1;
+      c.fs->pr = d2;
+      if (!(d1 > 0.0)) { s->status |= ST_FCG; c.fs->alpha = 0.0; }
+      else c.fs->alpha = d2 / d1;
+      c.fs->pAp_prev = d1;
+      break;
+  }
+}
+
+// Called by every thread of every block after block_sum2; thread 0 of block 0
+// carries the block total in d1/d2 after block_sum2.
+__device__ __forceinline__ void grid_finish(int op, double d1, double d2, const ReduceCtx& c) {
+  __shared__ bool am_last;
+  if (threadIdx.x == 0) {
+    c.partials[2 * blockIdx.x] = d1;
+    c.partials[2 * blockIdx.x + 1] = d2;
+    __threadfence();
+    unsigned prev = atomicAdd(c.counter, 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  double e1 = 0.0, e2 = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    e1 += __ldcg(c.partials + 2 * b);
+    e2 += __ldcg(c.partials + 2 * b + 1);
+  }
+  block_sum2(e1, e2);
+  if (threadIdx.x == 0) {
+    *c.counter = 0u;
+    run_post(op, e1, e2, c);
+  }
+}
+
+// d1 = x1.y1, d2 = x2.y2 (x2 may be null).
+__global__ void __launch_bounds__(256) dot2_kernel(int n, const double* __restrict__ x1,
+                                                   const double* __restrict__ y1,
+                                                   const double* __restrict__ x2,
+                                                   const double* __restrict__ y2, int op,
+                                                   ReduceCtx c) {
+  double d1 = 0.0, d2 = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    d1 = fma(x1[i], y1[i], d1);
+    if (x2) d2 = fma(x2[i], y2[i], d2);
+  }
+  block_sum2(d1, d2);
+  grid_finish(op, d1, d2, c);
+}
+
+// y = A p fused with d1 = p.y and d2 = p.r (r may be null)  (PCG q = A p;
+// FCG Ap = A p with p'Ap and p'r).
+__global__ void __launch_bounds__(256) spmv_dot_kernel(int n, const int* __restrict__ ip,
+                                                       const int* __restrict__ ix,
+                                                       const double* __restrict__ v,
+                                                       const double* __restrict__ p,
+                                                       const double* __restrict__ r, double* y,
+                                                       int op, ReduceCtx c) {
+  double d1 = 0.0, d2 = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int k0 = __ldg(ip + i), k1 = __ldg(ip + i + 1);
+    double s = 0.0;
+    for (int k = k0; k < k1; ++k) s = __dadd_rn(s, __dmul_rn(__ldg(v + k), __ldg(p + __ldg(ix + k))));
+    y[i] = s;
+    double pi = p[i];
+    d1 = fma(pi, s, d1);
+    if (r) d2 = fma(pi, r[i], d2);
+  }
+  block_sum2(d1, d2);
+  grid_finish(op, d1, d2, c);
+}
+
+// PCG: x += alpha p; r -= alpha q; d1 = r.r   (krylov.py:57-60)
+__global__ void __launch_bounds__(256) pcg_xr_kernel(int n, double* x, double* r,
+                                                     const double* __restrict__ p,
+                                                     const double* __restrict__ q, ReduceCtx c) {
+  const double alpha = c.sc->alpha;
+  double d1 = 0.0, d2 = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+    double ri = __dsub_rn(r[i], __dmul_rn(alpha, q[i]));
+    r[i] = ri;
+    d1 = fma(ri, ri, d1);
+  }
+  block_sum2(d1, d2);
+  grid_finish(POST_PCG_NORM, d1, d2, c);
+}
+
+// PCG: p = z + beta p  (krylov.py:70)
+__global__ void pcg_p_kernel(int n, double* p, const double* __restrict__ z, const DevScalars* sc) {
+  const double beta = sc->beta;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
+}
+
+// FCG: p = z (first) or p = z - beta p_prev   (krylov.py:93-98)
+__global__ void fcg_p_kernel(int n, double* p, const double* __restrict__ z,
+                             const double* __restrict__ pprev, const FcgScalars* fs, int first) {
+  const double beta = first ? 0.0 : fs->beta;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    p[i] = first ? z[i] : __dsub_rn(z[i], __dmul_rn(beta, pprev[i]));
+}
+
+// FCG: x += alpha p; r -= alpha Ap  (x starts at 0 when first)   (krylov.py:105-106)
+__global__ void fcg_xr_kernel(int n, double* x, double* r, const double* __restrict__ p,
+                              const double* __restrict__ ap, const FcgScalars* fs, int first) {
+  const double alpha = fs->alpha;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double xi = first ? 0.0 : x[i];
+    x[i] = __dadd_rn(xi, __dmul_rn(alpha, p[i]));
+    r[i] = __dsub_rn(r[i], __dmul_rn(alpha, ap[i]));
+  }
+}
+
+// elementwise helpers
+__global__ void copy_kernel(int n, double* y, const double* __restrict__ x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) y[i] = x[i];
+}
+// y = a - b
+__global__ void sub_kernel(int n, double* y, const double* __restrict__ a, const double* __restrict__ b) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[i] = __dsub_rn(a[i], b[i]);
+}
+// y = a + b
+__global__ void add_kernel(int n, double* y, const double* __restrict__ a, const double* __restrict__ b) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[i] = __dadd_rn(a[i], b[i]);
+}
+__global__ void zero_kernel(int n, double* y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) y[i] = 0.0;
+}
+
+// PCG scalar setup: itmax / rtol / hist pointer / status reset.
+__global__ void pcg_setup_kernel(DevScalars* sc, double rtol, int itmax, double* hist) {
+  sc->rtol = rtol;
+  sc->itmax = itmax;
+  sc->hist = hist;
+  sc->status = 0;
+  sc->converged = 0;
+  sc->stop = 0;
+  sc->k = 0;
+}
+
+}  // namespace mvamg

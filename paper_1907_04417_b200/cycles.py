@@ -1,0 +1,228 @@
+"""Device-resident multigrid operator -- drop-in for the reference's
+``MultigridOperator`` (pkg/src/mvamg/cycles.py:100-190).
+
+Same constructor (matrices, prolongators, cycle, pre_smoother, post_smoother),
+same validation and exceptions, same duck-typed surface (.apply, __call__,
+.error_propagation, .as_linear_operator, .n_levels, .shape, .matrices,
+.prolongators, .restrictions, .diagonals).  The hierarchy is uploaded once to
+HBM; each application runs one V- or K-cycle in libmvamg_b200.so.
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.linalg
+import scipy.sparse.linalg as spla
+
+from . import _lib
+from .device import DeviceCSR, GpuConfig, as_csr, gs_analyse, ptr, stream_handle, to_device, torch_cuda
+from .exceptions import NotSpdError
+
+GS_FORWARD = "gauss_seidel_forward"
+GS_BACKWARD = "gauss_seidel_backward"
+WEIGHTED_JACOBI = "weighted_jacobi"
+_KIND = {GS_FORWARD: _lib.GS_FORWARD, GS_BACKWARD: _lib.GS_BACKWARD, WEIGHTED_JACOBI: _lib.WEIGHTED_JACOBI}
+
+
+@dataclass(frozen=True)
+class SmootherSpec:
+    """Mirror of cycles.py:28-40."""
+
+    kind: str = GS_FORWARD
+    sweeps: int = 1
+    omega: float = 1.0
+
+    def __post_init__(self):
+        if self.kind not in (GS_FORWARD, GS_BACKWARD, WEIGHTED_JACOBI):
+            raise ValueError(f"unknown smoother kind {self.kind!r}")
+        if self.kind == WEIGHTED_JACOBI and not 0.0 < self.omega < 2.0:
+            raise ValueError("weighted Jacobi requires omega in (0, 2)")
+        if self.sweeps < 0:
+            raise ValueError("sweeps must be >= 0")
+
+
+@dataclass(frozen=True)
+class CycleSpec:
+    """Mirror of cycles.py:43-52."""
+
+    kind: str = "V"
+    inner_fcg_iters: int = 2
+
+    def __post_init__(self):
+        if self.kind not in ("V", "K"):
+            raise ValueError(f"unknown cycle kind {self.kind!r}")
+        if self.inner_fcg_iters < 0:
+            raise ValueError("inner_fcg_iters must be >= 0")
+
+
+def _checked_diagonal(A):
+    d = A.diagonal()
+    if np.any(d == 0.0):
+        raise NotSpdError("zero diagonal entry; Gauss-Seidel/Jacobi undefined")
+    return d
+
+
+class GpuMultigridOperator:
+    """Prepared B^{-1} on the GPU for a hierarchy of (matrices, prolongators)."""
+
+    def __init__(self, matrices, prolongators, cycle=None, pre_smoother=None, post_smoother=None,
+                 config=None):
+        if len(matrices) != len(prolongators) + 1:
+            raise ValueError("need exactly one prolongator per coarse level")
+        self.matrices = [as_csr(A) for A in matrices]
+        self.prolongators = [as_csr(P) for P in prolongators]
+        self.restrictions = [P.T.tocsr() for P in self.prolongators]
+        for R in self.restrictions:
+            R.sort_indices()
+        for k, P in enumerate(self.prolongators):
+            if P.shape[0] != self.matrices[k].shape[0] or P.shape[1] != self.matrices[k + 1].shape[0]:
+                raise ValueError(f"prolongator {k} does not chain the level dimensions")
+        self.cycle = cycle or CycleSpec()
+        self.pre_smoother = pre_smoother or SmootherSpec(GS_FORWARD)
+        self.post_smoother = post_smoother or SmootherSpec(GS_BACKWARD)
+        for spec in (self.pre_smoother, self.post_smoother):
+            if spec.kind not in _KIND:
+                raise ValueError(f"unknown smoother kind {spec.kind!r}")
+        if self.cycle.kind not in ("V", "K"):
+            raise ValueError(f"unknown cycle kind {self.cycle.kind!r}")
+        self.diagonals = [_checked_diagonal(A) for A in self.matrices[:-1]]
+        self.config = config or GpuConfig()
+        self._h = None
+        self._upload()
+
+    @classmethod
+    def from_reference(cls, op, config=None):
+        """Wrap an existing reference MultigridOperator (duck-typed)."""
+        return cls(op.matrices, op.prolongators, cycle=op.cycle, pre_smoother=op.pre_smoother,
+                   post_smoother=op.post_smoother, config=config)
+
+    def _init_plain(self, A):
+        """Single-level handle used only for its matrix (pcg with precond=None)."""
+        self.matrices = [as_csr(A)]
+        self.prolongators, self.restrictions, self.diagonals = [], [], []
+        self.cycle = CycleSpec()
+        self.pre_smoother = SmootherSpec(GS_FORWARD)
+        self.post_smoother = SmootherSpec(GS_BACKWARD)
+        self.config = GpuConfig()
+        self._h = None
+        self._upload(plain=True)
+
+    # ---- upload ------------------------------------------------------------
+    def _upload(self, plain=False):
+        torch = torch_cuda()
+        L = _lib.load()
+        nl = len(self.matrices)
+        h = ctypes.c_void_p()
+        pre, post = self.pre_smoother, self.post_smoother
+        _lib.check(L.mvamg_hierarchy_create(
+            ctypes.byref(h), nl, _lib.CYCLE_V if self.cycle.kind == "V" else _lib.CYCLE_K,
+            int(self.cycle.inner_fcg_iters), _KIND[pre.kind], int(pre.sweeps), float(pre.omega),
+            _KIND[post.kind], int(post.sweeps), float(post.omega)), "hierarchy_create")
+        self._h = h
+        self._keep = []
+        self.gs_plans = []
+        self._dA = []
+        for k, A in enumerate(self.matrices):
+            dA = DeviceCSR(A)
+            self._dA.append(dA)
+            if k < nl - 1:
+                d = self.diagonals[k]
+                dd = to_device(d, np.float64)
+                rd = to_device(1.0 / d, np.float64)  # RN(1/d): Markstein division in the GS kernel
+                plan = gs_analyse(A, self.config)
+                cp = to_device(plan.chain_ptr, np.int32)
+                tp = to_device(plan.tile_ptr, np.int32)
+                self._keep += [dd, rd, cp, tp]
+                self.gs_plans.append(plan)
+                _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd), ptr(rd),
+                                                       plan.ntiles, ptr(cp), ptr(tp), plan.threads,
+                                                       plan.window), "set_level")
+            else:
+                _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), None, None, 0,
+                                                       None, None, 32, 0), "set_level")
+        for k, (P, R) in enumerate(zip(self.prolongators, self.restrictions)):
+            dP, dR = DeviceCSR(P), DeviceCSR(R)
+            self._keep += [dP, dR]
+            _lib.check(L.mvamg_hierarchy_set_transfer(h, k, *dP.ptrs(), *dR.ptrs()), "set_transfer")
+        # Coarsest: the reference LU-factors A_L once (cycles.py:88-97); apply
+        # it as a dense inverse built from those same factors (one GEMV/visit).
+        if plain:
+            self.coarse_lu = None
+            self._inv = to_device(np.zeros(1), np.float64)  # never applied (no cycle)
+        else:
+            Ac = self.matrices[-1].toarray()
+            self.coarse_lu = scipy.linalg.lu_factor(Ac)
+            inv = scipy.linalg.lu_solve(self.coarse_lu, np.eye(Ac.shape[0]))
+            self._inv = to_device(np.ascontiguousarray(inv), np.float64)
+        _lib.check(L.mvamg_hierarchy_set_coarse(h, ptr(self._inv)), "set_coarse")
+        nbytes = ctypes.c_longlong()
+        _lib.check(L.mvamg_hierarchy_workspace_bytes(h, ctypes.byref(nbytes)), "workspace_bytes")
+        self._ws = torch.empty(max(8, nbytes.value), dtype=torch.uint8, device="cuda")
+        _lib.check(L.mvamg_hierarchy_bind_workspace(h, ptr(self._ws), stream_handle()), "bind_workspace")
+        _lib.check(L.mvamg_hierarchy_set_graphs(h, int(bool(self.config.graphs))), "set_graphs")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.load().mvamg_hierarchy_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # ---- reference surface -------------------------------------------------
+    @property
+    def n_levels(self):
+        return len(self.matrices)
+
+    @property
+    def shape(self):
+        n = self.matrices[0].shape[0]
+        return (n, n)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _status(self, what):
+        st = ctypes.c_int()
+        _lib.check(_lib.load().mvamg_hierarchy_status(self._h, ctypes.byref(st), 1), what)
+        _lib.raise_status(st.value, what)
+
+    def apply_device(self, r):
+        """z = B^{-1} r for a CUDA float64 tensor r (stays on the device)."""
+        torch = torch_cuda()
+        z = torch.empty_like(r)
+        _lib.check(_lib.load().mvamg_cycle_apply(self._h, ptr(r), ptr(z), stream_handle()), "cycle_apply")
+        return z
+
+    def apply(self, r):
+        """z approximating B^{-1} r (one cycle) -- cycles.py:174-179."""
+        r = np.asarray(r, dtype=np.float64)
+        if r.shape[0] != self.matrices[0].shape[0]:
+            raise ValueError("residual length does not match the hierarchy")
+        z = self.apply_device(to_device(r)).cpu().numpy()
+        self._status("apply")
+        return z
+
+    __call__ = apply
+
+    def error_propagation_device(self, x):
+        torch = torch_cuda()
+        e = torch.empty_like(x)
+        _lib.check(_lib.load().mvamg_error_propagation(self._h, ptr(x), ptr(e), stream_handle()),
+                   "error_propagation")
+        return e
+
+    def error_propagation(self, x):
+        """(I - B^{-1} A) x for the finest-level matrix -- cycles.py:181-184."""
+        x = np.asarray(x, dtype=np.float64)
+        if x.shape[0] != self.matrices[0].shape[0]:
+            raise ValueError("vector length does not match the hierarchy")
+        e = self.error_propagation_device(to_device(x)).cpu().numpy()
+        self._status("error_propagation")
+        return e
+
+    def as_linear_operator(self):
+        return spla.LinearOperator(self.shape, matvec=self.apply, dtype=np.float64)
