@@ -62,14 +62,21 @@ inline int grid_for(int n, int threads = 256, int per_sm = 8) {
 inline int dot_grid(int n) { return std::min(grid_for(n, 256, 8), kDotMaxBlocks); }
 
 bool g_attr_done = false;
+int g_max_dyn_smem = 48 * 1024;
 void set_kernel_attrs() {
   if (g_attr_done) return;
   g_attr_done = true;
-  int maxsm = 227 * 1024;
-  cudaFuncSetAttribute(gs_sweep_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-  cudaFuncSetAttribute(gs_sweep_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-  cudaFuncSetAttribute(gs_sweep_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-  cudaFuncSetAttribute(gs_sweep_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int maxsm = optin - 1024;  // leave room for the kernel's static shared memory
+  if (maxsm < 48 * 1024) maxsm = 48 * 1024;
+  bool ok = cudaFuncSetAttribute(gs_sweep_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) == cudaSuccess;
+  ok &= cudaFuncSetAttribute(gs_sweep_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) == cudaSuccess;
+  ok &= cudaFuncSetAttribute(gs_sweep_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) == cudaSuccess;
+  ok &= cudaFuncSetAttribute(gs_sweep_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) == cudaSuccess;
+  g_max_dyn_smem = ok ? maxsm : 48 * 1024;
+  cudaGetLastError();
 }
 
 struct Csr {
@@ -123,6 +130,8 @@ int launch_gs(bool fwd, bool zero, const Csr& A, const double* diag, const doubl
               int* status, cudaStream_t s) {
   if (A.n == 0) return 0;
   set_kernel_attrs();
+  if ((size_t)p.window * sizeof(double) > (size_t)g_max_dyn_smem)
+    return fail(MVAMG_E_ARG, "gs: window of " + std::to_string(p.window) + " rows exceeds shared memory");
   gs_prep_kernel<<<grid_for(A.n), 256, 0, s>>>(A.n, xnew, ticket);
   GsArgs a;
   a.n = A.n;
@@ -687,6 +696,9 @@ int mvamg_hierarchy_bind_workspace(mvamg_hierarchy* h, void* ws, void* stream) {
     if (!h->lv[k].A.ip) return fail(MVAMG_E_STATE, "bind_workspace: level " + std::to_string(k) + " not set");
   if (!h->inv) return fail(MVAMG_E_STATE, "bind_workspace: coarse inverse not set");
   workspace_layout(h, (char*)ws);
+  set_kernel_attrs();
+  for (int k = 0; k < h->L - 1; ++k)
+    if (h->lv[k].plan.ntiles > 0) gs_blocks(h->lv[k].plan);
   cudaStream_t s = (cudaStream_t)stream;
   CUDA_TRY(cudaMemsetAsync(h->counter, 0, 64, s));
   CUDA_TRY(cudaMemsetAsync(h->ticket, 0, 64, s));
