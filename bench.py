@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""bench.py -- PCG solve time to rtol 1e-6 and cycle HBM GB/s on B200.
+
+One "step" = one full PCG solve (x0 = 0, rtol 1e-6) preconditioned by the
+multi-vector V-cycle (the reference's solve path, pkg/src/mvamg/estimator.py:
+138-145 -> krylov.py:28-72 -> cycles.py:150-179) on a hierarchy resident in
+HBM.  Prints ONE JSON line (rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c3|c4]
+  python bench.py --impl reference ...   # the reference algorithm on host cores
+
+Keys beyond the base contract:
+  roofline      dominant kernel (fine-level exact-order GS sweep) GB/s vs the
+                measured HBM copy bandwidth (MEASURED_PEAKS.json)
+  cycle         one V-cycle: SURVEY.md 8(d) byte model / CUDA-event time
+  cpu_baseline  the CPU oracle (plain-C restatement of the reference solve,
+                oracle/) timed on this host, rank 0, N=1
+  e2e           the same solve through the C ABI with host buffers
+                (mvamg_pcg_solve_host: H2D of b, D2H of x and the history)
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCG solve time (s) to rtol 1e-6 and cycle HBM GB/s vs roofline at 1/2/4/8 B200"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=None)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", default=os.environ.get("MVAMG_BENCH_CONFIG", "c1"))
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------- workloads --
+def load_workload(name):
+    """(matrices, prolongators, b, description) for a bench configuration."""
+    name = name.lower()
+    if name == "c1":
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from _fixtures import golden, hierarchy
+
+        d = golden("c1")
+        mats, pros = hierarchy(d, "mv")
+        desc = ("C1: 2D Poisson 5-point 128x128 (n=16,384), rhs U[-1,1] seed 0, x0=0, rtol 1e-6; "
+                "hierarchy = reference MultiVectorAMG() defaults (golden fixture)")
+        return mats, pros, d["b"], desc
+    raise SystemExit(f"unknown --config {name!r}")
+
+
+# -------------------------------------------------------------------- clocks --
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = max(smax, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------- helpers --
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_baseline(mats, pros, b, budget_s=12.0):
+    """The CPU oracle (oracle/, C restatement of the reference solve) on host cores."""
+    from oracle.oracle import OracleOperator, oracle_pcg
+
+    op = OracleOperator(mats, pros)
+    t0 = time.perf_counter()
+    _, hist, nit, _ = oracle_pcg(op, b, rtol=1e-6)
+    t1 = time.perf_counter()
+    first = t1 - t0
+    times = [first]
+    while sum(times) < budget_s and len(times) < 50 and first < budget_s / 2:
+        t0 = time.perf_counter()
+        oracle_pcg(op, b, rtol=1e-6)
+        times.append(time.perf_counter() - t0)
+    return {"value": statistics.median(times), "unit": "s", "cores": 1, "kind": "port",
+            "sample": f"{len(times)} full PCG solves (nit={nit}) of the same workload, median; "
+                      "oracle/mvamg_oracle.c is single-threaded like the reference solve"}, nit
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    mats, pros, b, desc = load_workload(args.config)
+    steps = args.steps if args.steps is not None else 10
+    from oracle.oracle import OracleOperator, oracle_pcg
+
+    op = OracleOperator(mats, pros)
+    for _ in range(max(0, args.warmup)):
+        oracle_pcg(op, b, rtol=1e-6)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        _, hist, nit, conv = oracle_pcg(op, b, rtol=1e-6)
+        times.append(time.perf_counter() - t0)
+    v = statistics.mean(times)
+    out = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": 0,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "n": mats[0].shape[0], "nit": nit, "converged": bool(conv)},
+        "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port",
+                         "sample": f"{steps} full PCG solves, mean (oracle/ C port of the reference "
+                                   "solve path, single-threaded like the reference)"},
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def run_b200(args, world, rank, local):
+    import ctypes
+
+    import torch
+
+    import paper_1907_04417_b200 as mv
+    from paper_1907_04417_b200 import _lib
+    from paper_1907_04417_b200.device import ptr, stream_handle
+    from paper_1907_04417_b200.roofline import (cycle_bytes, gs_sweep_bytes, measured_peak_gbs,
+                                                pcg_iteration_bytes)
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L = _lib.load()
+    mats, pros, b, desc = load_workload(args.config)
+    n = mats[0].shape[0]
+    op = mv.GpuMultigridOperator(mats, pros)
+    h = op.handle
+    s = stream_handle()
+    steps = args.steps if args.steps is not None else 50
+    warm = max(3, args.warmup)
+
+    b_dev = torch.from_numpy(b).cuda()
+    x_dev = torch.empty_like(b_dev)
+    itmax = 1000
+    hist_dev = torch.empty(itmax + 1, dtype=torch.float64, device="cuda")
+    nit, conv, st = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+
+    def solve_device():
+        _lib.check(L.mvamg_pcg_solve(h, _lib.PC_CYCLE, None, ptr(b_dev), ptr(x_dev), 1e-6, itmax,
+                                     ptr(hist_dev), ctypes.byref(nit), ctypes.byref(conv),
+                                     ctypes.byref(st), s), "pcg")
+        _lib.raise_status(st.value, "pcg")
+
+    hier_bytes = sum(12 * M.nnz + 4 * M.shape[0] for M in mats + pros) * 2
+    small = hier_bytes < 2 * L2_BYTES
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda") if small else None
+
+    def l2_flush():
+        if flush is not None:
+            flush.fill_(1.0)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    for _ in range(warm):
+        solve_device()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    # ---- timed region: K solves, device-resident inputs ------------------------
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    L.mvamg_kernel_launches(None, 1)
+    tot = 0.0
+    for _ in range(steps):
+        l2_flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        solve_device()
+        e1.record(stream)
+        e1.synchronize()
+        tot += e0.elapsed_time(e1) / 1e3
+    torch.cuda.synchronize()
+    launches = ctypes.c_longlong()
+    L.mvamg_kernel_launches(ctypes.byref(launches), 1)
+    t_solve = tot / steps
+    if dist:
+        tt = torch.tensor([t_solve], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_solve = float(tt.item())
+    n_iters = nit.value
+    # ---- e2e: same solve through the C ABI with host buffers ------------------
+    b_host = torch.from_numpy(b.copy()).pin_memory()
+    x_host = torch.empty(n, dtype=torch.float64).pin_memory()
+    hist_host = torch.empty(itmax + 1, dtype=torch.float64).pin_memory()
+
+    def solve_host():
+        _lib.check(L.mvamg_pcg_solve_host(h, _lib.PC_CYCLE, None, ptr(b_host), ptr(x_host), 1e-6,
+                                          itmax, ptr(hist_host), ctypes.byref(nit),
+                                          ctypes.byref(conv), ctypes.byref(st), s), "pcg_host")
+        _lib.raise_status(st.value, "pcg_host")
+
+    for _ in range(2):
+        solve_host()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    tot = 0.0
+    for _ in range(steps):
+        l2_flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        solve_host()
+        e1.record(stream)
+        e1.synchronize()
+        tot += e0.elapsed_time(e1) / 1e3
+    t_e2e = tot / steps
+    if dist:
+        tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    clocks = sampler.stop()
+    # ---- one V-cycle and the dominant kernel (fine-level GS sweep) -----------
+    reps = 50
+    r_dev = torch.from_numpy(b).cuda()
+    for _ in range(3):
+        op.apply_device(r_dev)
+    torch.cuda.synchronize()
+    tc = 0.0
+    for _ in range(reps):
+        l2_flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        op.apply_device(r_dev)
+        e1.record(stream)
+        e1.synchronize()
+        tc += e0.elapsed_time(e1) / 1e3
+    t_cycle = tc / reps
+    lv = op.level_dev[0]
+    gp = lv["gs"]
+    xn = torch.empty(n, dtype=torch.float64, device="cuda")
+    ws = torch.zeros(8, dtype=torch.int32, device="cuda")
+
+    def gs_once():
+        gp.sweep(0, r_dev, None, xn, ws, s)
+
+    for _ in range(3):
+        gs_once()
+    torch.cuda.synchronize()
+    tg = 0.0
+    for _ in range(reps):
+        l2_flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        gs_once()
+        e1.record(stream)
+        e1.synchronize()
+        tg += e0.elapsed_time(e1) / 1e3
+    t_gs = tg / reps  # includes the sentinel-fill prep kernel
+    peak, peak_src = measured_peak_gbs(ROOT)
+    gs_bytes = gs_sweep_bytes(mats[0], True)
+    gs_gbs = gs_bytes / t_gs / 1e9
+    cyc_bytes = cycle_bytes(mats, pros)
+    it_bytes = pcg_iteration_bytes(mats, pros)
+    out = {
+        "metric": METRIC, "value": t_solve, "unit": "s", "n_gpus": world, "steps": steps,
+        "warmup": warm, "ms_per_step": t_solve * 1e3, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {
+            "workload": desc, "n": n, "nnz": int(mats[0].nnz), "levels": [M.shape[0] for M in mats],
+            "nit": n_iters, "converged": bool(conv.value),
+            "l2": "flushed (256 MiB write) before every timed step" if small else "inputs larger than L2",
+            "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (one per GPU)",
+        },
+        "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n + 8 * (n_iters + 1)},
+        "gpu_launches": int(round(launches.value / steps)),
+        "cycle": {"ms": t_cycle * 1e3, "model_bytes": cyc_bytes, "gbs": cyc_bytes / t_cycle / 1e9,
+                  "frac": cyc_bytes / t_cycle / 1e9 / peak},
+        "pcg_model": {"bytes_per_iteration": it_bytes, "gbs": it_bytes * n_iters / t_solve / 1e9,
+                      "frac": it_bytes * n_iters / t_solve / 1e9 / peak},
+        "roofline": {"bound": "hbm", "kernel": "gs_sweep_kernel<fwd,zero> level 0 (+sentinel prep)",
+                     "achieved": gs_gbs, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": gs_gbs / peak, "traffic": None, "algorithmic_bytes": gs_bytes,
+                     "ms": t_gs * 1e3},
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb, cnit = cpu_baseline(mats, pros, b)
+        cb["nit"] = cnit
+        out["cpu_baseline"] = cb
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_b200(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

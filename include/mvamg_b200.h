@@ -54,12 +54,21 @@ extern "C" {
 
 int mvamg_version(void);
 const char* mvamg_last_error(void);
+/* Kernels launched by this library since the last reset (CUDA-graph replays
+ * count every kernel node).  Host-side counter, for the benchmark's
+ * gpu_launches figure. */
+int mvamg_kernel_launches(long long* count, int reset);
+/* Diagnostics: when trace_dev (device, 8 x long long per warp of the largest GS
+ * launch, zeroed by the caller) is non-NULL, GS sweeps accumulate per-warp
+ * rounds / progress rounds / cycles.  NULL (default) disables tracing. */
+int mvamg_gs_set_trace(long long* trace_dev);
 
 /* ---- GS schedule analysis (host) -------------------------------------------
  * Splits the rows of a CSR matrix (host arrays) into dependency chains
  * (maximal runs where row i couples to row i-1, at most max_chain rows) and
- * groups consecutive chains into tiles of <= max_threads chains whose rows fit a
- * shared-memory window of <= max_window rows.  Call first with the out arrays
+ * groups consecutive chains into tiles of <= max_threads (<= 1024) chains whose
+ * position-major shared window (threads x longest chain slots) fits
+ * max_window slots.  Call first with the out arrays
  * NULL to get counts, then with arrays of nchains+1 / ntiles+1 ints.
  * Replaces nothing in the reference (numba runs rows serially,
  * _kernels.py:15-38); the schedule preserves that order's dependency DAG, so
@@ -79,16 +88,41 @@ int mvamg_csr_residual_f64(int n, const int* indptr, const int* indices, const d
 /* y = y + (A x)  (cycles.py:170, prolongation; sum formed first). */
 int mvamg_csr_spmv_add_f64(int n, const int* indptr, const int* indices, const double* data,
                            const double* x, double* y, void* stream);
-/* One lexicographic GS sweep (_kernels.py:15-38).  direction 0 = forward,
- * 1 = backward.  x_old is the iterate before the sweep (ignored when
- * zero_init != 0, meaning x_old == 0); x_new receives the result (must not
- * alias x_old).  rdiag[i] = RN(1/diag[i]).  chain_ptr / tile_ptr come from
- * mvamg_gs_analyse (device copies).  ws: device int workspace of >= 4 ints. */
-int mvamg_gs_sweep_f64(int direction, int zero_init, int n, const int* indptr,
-                       const int* indices, const double* data, const double* diag,
-                       const double* rdiag, int ntiles, const int* chain_ptr,
-                       const int* tile_ptr, int threads, int window, const double* b,
-                       const double* x_old, double* x_new, int* ws, void* stream);
+/* GS static round schedule (host).  For sweep `mode` (0 forward from x = 0,
+ * 1 forward from a nonzero guess, 2 backward) and the chains / tiles of
+ * mvamg_gs_analyse, assigns every row a round inside its warp (one more than
+ * its chain predecessor and every same-warp row it depends on) and writes the
+ * row records round-major, lane-minor (word w of lane L of global round g at
+ * round_off[g] + 32 w + L): [cnt | flags][diag][RN(1/diag)] then cnt pairs
+ * [coefficient][source code] -- the entries still contributing to the serial
+ * loop's sum at sweep time, in CSR order.  Rounds of a warp are padded to a
+ * multiple of R; uniform_S > 0 pads every round to that many words (the lean
+ * kernel's fixed record size).  perm[i] = 32 * (global round of row i) + lane.  Query with
+ * rec == NULL for *nwords / *nrounds / *nwarps / *max_S; then round_off holds
+ * nrounds+1, tbase nwarps+1, tile_wbase ntiles+1, perm n ints. */
+int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double* data, int ntiles,
+                      const int* chain_ptr, const int* tile_ptr, int window, int mode, int R,
+                      int uniform_S, long long* nwords, int* nrounds, int* nwarps, int* max_S,
+                      unsigned long long* rec, int* round_off, int* tbase, int* tile_wbase,
+                      int* perm);
+/* One lexicographic GS sweep (_kernels.py:15-38) on device data.  direction
+ * 0 = forward, 1 = backward; x_old is the iterate before the sweep (NULL for a
+ * zero guess); x_new receives the result and must not alias x_old.  The CSR
+ * matrix is read by the backward sweep from a nonzero guess (old upper
+ * neighbours folded into the right-hand side).  tperm: device buffer of
+ * 32 * nrounds doubles.  R (rounds per chunk: 1, 2, 4, 8), D (ring slots:
+ * 2, 4, 8), slot_words (>= R*(32*max_S+32), even) and rec_words_max
+ * (R*32*max_S) size the per-warp TMA ring.  lean_C > 0 selects the lean
+ * kernel: records built with uniform_S = 3 + 2*lean_C, no x_old sources,
+ * (R, D) in {(8,4), (4,4), (2,8), (1,8)}.  ws: device
+ * int workspace (>= 4 ints: tile ticket, status word).  Bit-identical to the
+ * serial loop. */
+int mvamg_gs_sweep_f64(int direction, int n, const int* indptr, const int* indices, const double* data,
+                       const unsigned long long* rec, const int* round_off, const int* tbase,
+                       const int* tile_wbase, const int* perm, double* tperm, int R, int D,
+                       int lean_C, int slot_words, int rec_words_max, int ntiles,
+                       const int* chain_ptr, const int* tile_ptr, int threads, int window,
+                       const double* b, const double* x_old, double* x_new, int* ws, void* stream);
 /* z = Inv r, Inv dense row-major n x n (coarsest solve; cycles.py:88-97). */
 int mvamg_dense_gemv_f64(int n, const double* inv, const double* r, double* z, void* stream);
 /* *result = x . y (deterministic two-level reduction; device scalar).
@@ -110,6 +144,11 @@ int mvamg_hierarchy_set_level(mvamg_hierarchy* h, int k, int n, int nnz, const i
                               const int* indices, const double* data, const double* diag,
                               const double* rdiag, int ntiles, const int* chain_ptr,
                               const int* tile_ptr, int gs_threads, int gs_window);
+/* GS schedule of level k for sweep `mode` (see mvamg_gs_schedule), device. */
+int mvamg_hierarchy_set_gs_schedule(mvamg_hierarchy* h, int k, int mode, const unsigned long long* rec,
+                                    const int* round_off, const int* tbase, const int* tile_wbase,
+                                    const int* perm, double* tperm, int R, int D, int lean_C,
+                                    int slot_words, int rec_words_max);
 /* Transfer k: P (n_k x n_{k+1}) and R = P^T (n_{k+1} x n_k), device CSR. */
 int mvamg_hierarchy_set_transfer(mvamg_hierarchy* h, int k, const int* p_indptr,
                                  const int* p_indices, const double* p_data,

@@ -34,17 +34,23 @@ _PI = ctypes.POINTER(ctypes.c_int)
 SIGNATURES = [
     ("mvamg_version", _I, []),
     ("mvamg_last_error", ctypes.c_char_p, []),
+    ("mvamg_kernel_launches", _I, [ctypes.POINTER(_LL), _I]),
+    ("mvamg_gs_set_trace", _I, [_P]),
     ("mvamg_gs_analyse", _I, [_I, _P, _P, _I, _I, _I, _PI, _PI, _P, _P, _PI, _PI, _PI]),
     ("mvamg_csr_spmv_f64", _I, [_I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_csr_residual_f64", _I, [_I, _P, _P, _P, _P, _P, _P, _P]),
     ("mvamg_csr_spmv_add_f64", _I, [_I, _P, _P, _P, _P, _P, _P]),
-    ("mvamg_gs_sweep_f64", _I, [_I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _I, _P, _P, _P, _P, _P]),
+    ("mvamg_gs_schedule", _I, [_I, _P, _P, _P, _I, _P, _P, _I, _I, _I, _I, ctypes.POINTER(_LL), _PI, _PI,
+                               _PI, _P, _P, _P, _P, _P]),
+    ("mvamg_gs_sweep_f64", _I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P,
+                                _I, _I, _P, _P, _P, _P, _P]),
     ("mvamg_dense_gemv_f64", _I, [_I, _P, _P, _P, _P]),
     ("mvamg_dot_f64", _I, [_I, _P, _P, _P, _P, _P]),
     ("mvamg_dot_ws_bytes", _I, []),
     ("mvamg_hierarchy_create", _I, [ctypes.POINTER(_P), _I, _I, _I, _I, _I, _D, _I, _I, _D]),
     ("mvamg_hierarchy_destroy", _I, [_P]),
     ("mvamg_hierarchy_set_level", _I, [_P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _I]),
+    ("mvamg_hierarchy_set_gs_schedule", _I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I]),
     ("mvamg_hierarchy_set_transfer", _I, [_P, _I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_hierarchy_set_coarse", _I, [_P, _P]),
     ("mvamg_hierarchy_workspace_bytes", _I, [_P, ctypes.POINTER(_LL)]),

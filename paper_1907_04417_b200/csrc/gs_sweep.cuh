@@ -1,0 +1,538 @@
+// gs_sweep.cuh -- exact-order Gauss-Seidel sweep for sm_100a.
+//
+// Reference: gs_forward / gs_backward (pkg/src/mvamg/_kernels.py:15-38): for
+// i in order, s = b[i]; s -= a_ij * x[j] for j != i in CSR order; x[i] = s / d_i.
+// The result of that loop depends only on its dependency DAG (row i reads the
+// new x_j of every earlier row j it couples to), so any schedule that respects
+// the DAG and keeps each row's CSR-order rounding reproduces it bit for bit.
+//
+// Schedule (host, mvamg_gs_analyse + mvamg_gs_schedule):
+//   chains  -- runs of consecutive rows where row i couples to row i-1 (grid
+//              lines of a natural ordering); one chain per lane, so the i-1
+//              dependency stays in a register;
+//   tiles   -- consecutive chains owned by one CTA, sharing a position-major
+//              shared-memory window of published x values;
+//   rounds  -- inside a warp, every row gets a static round: one more than its
+//              chain predecessor and than every same-warp row it depends on.
+//              Lanes therefore run as a skewed systolic wavefront with no
+//              intra-warp waiting; a dependency on another warp or tile is
+//              polled (the value's NaN sentinel is its own ready flag).
+// Data: the host lays each warp's row records out round-major and lane-minor
+// (word w of lane L in round r at round_off[r] + 32 w + L), so one elected lane
+// streams R rounds at a time into a shared-memory ring with a TMA bulk copy
+// (cp.async.bulk + mbarrier) and every lane's read is a conflict-free LDS.  The
+// right-hand side is written in the same order by gs_prepare_kernel.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#ifndef MVAMG_GS_PHASES
+#define MVAMG_GS_PHASES 0
+#endif
+#if MVAMG_GS_PHASES
+#define GS_STAMP(k) do { if (lane == 0) { long long _t = clock64(); ph_acc[k] += _t - ph_last; ph_last = _t; } } while (0)
+#else
+#define GS_STAMP(k) do {} while (0)
+#endif
+
+namespace mvamg {
+
+// Record words (per row, per lane):
+//   w0: cnt (bits 0-15, 0xffff = no row this round) | window-only flag (bit 16)
+//   w1: diag          w2: RN(1/diag)
+//   then cnt entries of 2 words: [coefficient][int code]
+// holding, in CSR order, the entries still contributing to the serial loop's
+// sum at sweep time: forward sweeps j < i (and from a nonzero guess the upper
+// j > i after them); backward sweeps j > i (the upper j < i precede the
+// diagonal in CSR order and are folded into the right-hand side by
+// gs_prepare_kernel with the same roundings).  Value sources:
+//   code & 3 == 0   x_new of the previous row of this chain (a register)
+//   code & 3 == 1   the tile's shared window, slot code>>2 (polled)
+//   code & 3 == 2   x_new[code>>2] in global memory (another tile, polled)
+//   code & 3 == 3   x_old[code>>2] (forward sweep from a nonzero guess)
+constexpr unsigned kGsNoRow = 0xffffu;
+constexpr long long kGsIdleLimit = 1LL << 22;  // spins on one round before giving up
+
+struct GsArgs {
+  int n, ntiles, window;         // window: shared slots per tile
+  int slot_words;                // words of one ring slot (R rounds of records + R*32 rhs)
+  int rec_words_max;             // words of records in one slot (R * Smax * 32)
+  const unsigned long long* rec; // round-major records of all warps
+  const int* round_off;          // word offset of every (warp, round); one terminal entry
+  const int* tbase;              // first global round of each warp (nwarps + 1)
+  const int* tile_wbase;         // first warp of each tile (ntiles + 1)
+  const int* chain_ptr;
+  const int* tile_ptr;
+  const double* tperm;           // right-hand side in (round, lane) order
+  const double* xold;
+  double* xnew;
+  int* ticket;
+  int* status;
+  long long* trace;              // optional per-warp cycle trace (diagnostics)
+  int debug;                     // diagnostics: bit0 = ignore readiness (timing only, wrong results)
+};
+
+__device__ __forceinline__ unsigned long long ld_shared_volatile_u64(unsigned saddr) {
+  unsigned long long v;
+  asm volatile("ld.volatile.shared.b64 %0, [%1];" : "=l"(v) : "r"(saddr));
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_shared_u64(unsigned saddr) {
+  unsigned long long v;
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(saddr));
+  return v;
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned bar, unsigned parity) {
+  unsigned ok;
+  asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+               : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+  return ok != 0;
+}
+
+// Value multiplying one record entry (any source).  `win` is the tile's
+// shared window; plain (volatile) C++ accesses so the compiler can predicate.
+__device__ __forceinline__ unsigned long long gs_src(int code, const volatile unsigned long long* win,
+                                                     const double* xnew, const double* xold, double xprev) {
+  const int t = code & 3, idx = code >> 2;
+  unsigned long long v = (unsigned long long)__double_as_longlong(xprev);
+  if (t == 1) v = win[idx];
+  if (t == 2) v = ld_relaxed_u64(xnew + idx);
+  if (t == 3) v = (unsigned long long)__double_as_longlong(__ldg(xold + idx));
+  return v;
+}
+
+__device__ __forceinline__ bool gs_published(unsigned long long v) {
+  return (unsigned)(v >> 32) != 0xffffffffu;  // the sentinel's high word; arithmetic never makes it
+}
+
+// Generic gather of entries [u0, u0+4) of a row (any sources).
+__device__ __forceinline__ bool gs_gather4(const GsArgs& a, const volatile unsigned long long* win,
+                                           const unsigned long long* rec, int cnt, int u0, double xprev,
+                                           double av[4], unsigned long long xb[4]) {
+  bool ready = true;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    av[u] = 0.0;
+    xb[u] = (unsigned long long)__double_as_longlong(xprev);
+    if (u0 + u < cnt) {
+      av[u] = __longlong_as_double((long long)rec[32 * (3 + 2 * (u0 + u))]);
+      const int code = (int)(unsigned)rec[32 * (4 + 2 * (u0 + u))];
+      xb[u] = gs_src(code, win, a.xnew, a.xold, xprev);
+    }
+    ready &= gs_published(xb[u]);
+  }
+  return ready;
+}
+
+// Fast gather: <= C entries, all sourced from the previous row (code 0) or the
+// shared window (code 1).  Straight-line; every load is predicated.
+template <int C>
+__device__ __forceinline__ bool gs_fast_gather(const volatile unsigned long long* win,
+                                               const unsigned long long* rec, int cnt, double xprev,
+                                               double av[4], double xv[4]) {
+  bool ready = true;
+#pragma unroll
+  for (int u = 0; u < C; ++u) {
+    const bool in = u < cnt;
+    const unsigned code = in ? (unsigned)rec[32 * (4 + 2 * u)] : 0u;
+    av[u] = in ? __longlong_as_double((long long)rec[32 * (3 + 2 * u)]) : 0.0;
+    unsigned long long v = (unsigned long long)__double_as_longlong(xprev);
+    if (code & 1u) v = win[code >> 2];
+    ready &= gs_published(v);
+    xv[u] = __longlong_as_double((long long)v);
+  }
+  return ready;
+}
+
+template <int C>
+__device__ __forceinline__ double gs_fast_sum(double s, int cnt, const double av[4], const double xv[4]) {
+#pragma unroll
+  for (int u = 0; u < C; ++u)
+    if (u < cnt) s = __dsub_rn(s, __dmul_rn(av[u], xv[u]));
+  return s;
+}
+
+template <bool FWD, int R, int D>
+__global__ void __launch_bounds__(256, 1) gs_sweep_kernel(GsArgs a) {
+  extern __shared__ __align__(16) unsigned long long smem_u64[];
+  __shared__ int s_tile;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps_blk = blockDim.x >> 5;
+  volatile unsigned long long* win = smem_u64;                             // window slots
+  const int ring_off = ((a.window + 1) & ~1) + warp * D * a.slot_words;    // words
+  const unsigned long long* ringp = smem_u64 + ring_off;
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_u64);
+  const unsigned ring = sbase + 8u * (unsigned)ring_off;
+  const unsigned bars = sbase + 8u * (unsigned)(((a.window + 1) & ~1) + nwarps_blk * D * a.slot_words) +
+                        8u * (unsigned)(warp * D);
+  if (lane == 0) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) mbar_init(bars + 8u * d, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  unsigned parity = 0;  // bit d: parity of slot d's next completion
+  const bool tracing = a.trace != nullptr;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1);
+    __syncthreads();
+    const int tk = s_tile;
+    if (tk >= a.ntiles) return;
+    const int t = FWD ? tk : a.ntiles - 1 - tk;
+    const int c0 = a.tile_ptr[t], c1 = a.tile_ptr[t + 1];
+    const int TS = ((c1 - c0 + 31) / 32) * 32;  // window slot stride of this tile
+    for (int i = threadIdx.x; i < a.window; i += blockDim.x) smem_u64[i] = kSentinel;
+    __syncthreads();
+    const int w0 = a.tile_wbase[t], nw = a.tile_wbase[t + 1] - w0;
+    if (warp < nw) {
+      const int g = w0 + warp;
+      const int gr_base = a.tbase[g], nr = a.tbase[g + 1] - gr_base, nch = nr / R;
+      const int c = c0 + warp * 32 + lane;
+      int cs = 0, len = 0;
+      if (c < c1) {
+        cs = a.chain_ptr[c];
+        len = a.chain_ptr[c + 1] - cs;
+      }
+      const int ce = cs + len;
+      volatile unsigned long long* wslot = win + (c - c0);  // + q * TS: this lane's published rows
+      // chunk k (rounds [kR, kR+R)) -> slot k % D.  `ko` holds the chunk's round
+      // offsets (lane j: round j), loaded a full ring cycle earlier, so issuing
+      // never waits on memory.
+      auto issue = [&](int k, int ko) {
+        const int o0 = __shfl_sync(FULL, ko, 0), o1 = __shfl_sync(FULL, ko, R);
+        if (lane == 0) {
+          const int d = k % D;
+          const int gr0 = gr_base + k * R;
+          const unsigned rb = 8u * (unsigned)(o1 - o0), tb = 8u * 32u * R;
+          const unsigned dst = ring + 8u * (unsigned)(d * a.slot_words);
+          const unsigned bar = bars + 8u * d;
+          mbar_expect_tx(bar, rb + tb);
+          bulk_g2s(dst, a.rec + o0, rb, bar);
+          bulk_g2s(dst + 8u * (unsigned)a.rec_words_max, a.tperm + (size_t)gr0 * 32, tb, bar);
+        }
+      };
+      auto load_offs = [&](int k) { return (k < nch && lane <= R) ? a.round_off[gr_base + k * R + lane] : 0; };
+      unsigned pend = 0;  // slots with a copy in flight (uniform across the warp)
+      // offsets of chunks k .. k+2D-1 (lane j: round j of the chunk), shifted
+      // down one place per chunk so the chunk loop needs no unrolling
+      int oq[2 * D];
+#pragma unroll
+      for (int j = 0; j < 2 * D; ++j) oq[j] = load_offs(j);
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        if (d < nch) {
+          issue(d, oq[d]);
+          pend |= 1u << d;
+        }
+      }
+      int q = 0;
+      double xprev = 0.0;
+      long long tr_spin = 0, tr_t0 = tracing ? clock64() : 0;
+      bool abort = false;
+#pragma unroll 1
+      for (int k = 0; k < nch && !abort; ++k) {
+        const int d = k % D;
+        const unsigned long long* slot = ringp + d * a.slot_words;
+        if (!(a.debug & 16)) while (!mbar_try_wait(bars + 8u * d, (parity >> d) & 1u)) {}
+        parity ^= 1u << d;
+        pend &= ~(1u << d);
+        const int my_off = oq[0];
+        const int o0 = __shfl_sync(FULL, my_off, 0);
+        const double* tchunk = reinterpret_cast<const double*>(slot + a.rec_words_max) + lane;
+#pragma unroll 1
+        for (int rr = 0; rr < R; ++rr) {
+          const int ob = __shfl_sync(FULL, my_off, rr), oe = __shfl_sync(FULL, my_off, rr + 1);
+          const int cmax = ((oe - ob) / 32 - 3) / 2;  // uniform bound on this round's entries
+          const unsigned long long* rec = slot + (ob - o0) + lane;
+          const unsigned hw = (unsigned)rec[0];
+          const int cnt = (int)(hw & 0xffffu);
+          const bool active = cnt != (int)kGsNoRow;
+          const int ca = active ? cnt : 0;
+          double s = tchunk[rr * 32];
+          long long spins = 0;
+          const bool fastround = cmax <= 4 && __all_sync(FULL, !active || (hw & 0x10000u));
+          if (fastround) {
+            double av[4], xv[4];
+            for (;;) {
+              bool ready;
+              if (cmax <= 2) ready = gs_fast_gather<2>(win, rec, ca, xprev, av, xv);
+              else ready = gs_fast_gather<4>(win, rec, ca, xprev, av, xv);
+              if (__all_sync(FULL, ready) || (a.debug & 1)) break;
+              if ((++spins & 255) == 0) {
+                bool ab = (*reinterpret_cast<volatile int*>(a.status) & ST_GS_TIMEOUT) != 0;
+                if (spins > kGsIdleLimit) {
+                  if (lane == 0) atomicOr(a.status, ST_GS_TIMEOUT);
+                  ab = true;
+                }
+                if (__any_sync(FULL, ab)) { abort = true; break; }
+              }
+            }
+            if (abort) break;
+            if (cmax <= 2) s = gs_fast_sum<2>(s, ca, av, xv);
+            else s = gs_fast_sum<4>(s, ca, av, xv);
+          } else {
+            double av[4];
+            unsigned long long xb[4];
+            for (;;) {  // the whole warp waits until every lane's row is ready
+              bool ready = true;
+              for (int u0 = 4; u0 < ca; u0 += 4) ready &= gs_gather4(a, win, rec, ca, u0, xprev, av, xb);
+              ready &= gs_gather4(a, win, rec, ca, 0, xprev, av, xb);
+              if (__all_sync(FULL, ready) || (a.debug & 1)) break;
+              if ((++spins & 255) == 0) {
+                bool ab = (*reinterpret_cast<volatile int*>(a.status) & ST_GS_TIMEOUT) != 0;
+                if (spins > kGsIdleLimit) {
+                  if (lane == 0) atomicOr(a.status, ST_GS_TIMEOUT);
+                  ab = true;
+                }
+                if (__any_sync(FULL, ab)) { abort = true; break; }
+              }
+            }
+            if (abort) break;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (u < ca) s = __dsub_rn(s, __dmul_rn(av[u], __longlong_as_double((long long)xb[u])));
+            for (int u0 = 4; u0 < ca; u0 += 4) {
+              gs_gather4(a, win, rec, ca, u0, xprev, av, xb);  // published: ready
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (u0 + u < ca) s = __dsub_rn(s, __dmul_rn(av[u], __longlong_as_double((long long)xb[u])));
+            }
+          }
+          tr_spin += spins;
+          if (active) {
+            const double xi = (a.debug & 8) ? s * __longlong_as_double((long long)rec[64])
+                                            : div_rn_markstein(s, __longlong_as_double((long long)rec[32]),
+                                                               __longlong_as_double((long long)rec[64]));
+            const int i = FWD ? cs + q : ce - 1 - q;
+            if (!(a.debug & 4)) wslot[q * TS] = (unsigned long long)__double_as_longlong(xi);
+            if (!(a.debug & 2)) a.xnew[i] = xi;
+            xprev = xi;
+            ++q;
+          }
+          __syncwarp();
+        }
+        __syncwarp();
+        if (!abort && k + D < nch) {
+          issue(k + D, oq[D]);
+          pend |= 1u << d;
+        }
+#pragma unroll
+        for (int j = 0; j < 2 * D - 1; ++j) oq[j] = oq[j + 1];
+        oq[2 * D - 1] = load_offs(k + 2 * D);
+      }
+      // an aborted sweep leaves copies in flight: land them before reuse / exit
+      for (int d = 0; d < D; ++d) {
+        if (pend & (1u << d)) {
+          while (!mbar_try_wait(bars + 8u * d, (parity >> d) & 1u)) {}
+          parity ^= 1u << d;
+        }
+      }
+      if (tracing && lane == 0) {
+        long long* tr = a.trace + 16 * (blockIdx.x * nwarps_blk + warp);
+        tr[0] += nr; tr[1] += tr_spin; tr[5] += clock64() - tr_t0; tr[6] += 1;
+      }
+    }
+  }
+}
+
+
+// Lean sweep for the common case (host-verified per level and mode): every row
+// has <= C record entries, sourced from the previous row, the shared window or
+// another tile's x_new -- no old values -- and every round has the same record
+// size S = 3 + 2C (rows padded), so a chunk is a fixed R x 32 x S words and a
+// record's position needs no lookup.  Sources are selected branch-free
+// (predicated loads), and the R rounds of a chunk are unrolled so the next
+// round's record and right-hand-side loads are issued ahead of the current
+// round's dependent arithmetic.
+// Predicated loads: the destination keeps its value when the predicate is off,
+// so a source select is one instruction each and never a branch.
+__device__ __forceinline__ void ld_shared_if(unsigned long long& v, bool p, unsigned saddr) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n @q ld.volatile.shared.u64 %0, [%2];\n}"
+               : "+l"(v) : "r"((unsigned)p), "r"(saddr));
+}
+__device__ __forceinline__ void ld_global_if(unsigned long long& v, bool p, const void* gaddr) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n @q ld.relaxed.gpu.global.u64 %0, [%2];\n}"
+               : "+l"(v) : "r"((unsigned)p), "l"(gaddr));
+}
+
+template <int C>
+__device__ __forceinline__ bool gs_lean_gather(const unsigned long long* rec, int cnt, unsigned wbase,
+                                               const double* xnew, double xprev, double av[C],
+                                               double xv[C]) {
+  bool ready = true;
+#pragma unroll
+  for (int u = 0; u < C; ++u) {
+    const bool in = u < cnt;
+    const unsigned code = in ? (unsigned)rec[32 * (4 + 2 * u)] : 0u;
+    av[u] = in ? __longlong_as_double((long long)rec[32 * (3 + 2 * u)]) : 0.0;
+    const unsigned t = code & 3u, idx = code >> 2;
+    unsigned long long v = (unsigned long long)__double_as_longlong(xprev);
+    ld_shared_if(v, t == 1u, wbase + 8u * idx);
+    ld_global_if(v, t == 2u, xnew + idx);
+    ready &= gs_published(v);
+    xv[u] = __longlong_as_double((long long)v);
+  }
+  return ready;
+}
+
+template <bool FWD, int C, int R, int D>
+__global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
+  constexpr int S = 3 + 2 * C;
+  constexpr int RW = R * 32 * S;  // record words of one chunk
+  extern __shared__ __align__(16) unsigned long long smem_u64[];
+  __shared__ int s_tile;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps_blk = blockDim.x >> 5;
+  volatile unsigned long long* win = smem_u64;
+  const int ring_off = ((a.window + 1) & ~1) + warp * D * a.slot_words;
+  const unsigned long long* ringp = smem_u64 + ring_off;
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_u64);
+  const unsigned ring = sbase + 8u * (unsigned)ring_off;
+  const unsigned bars = sbase + 8u * (unsigned)(((a.window + 1) & ~1) + nwarps_blk * D * a.slot_words) +
+                        8u * (unsigned)(warp * D);
+  if (lane == 0) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) mbar_init(bars + 8u * d, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  unsigned parity = 0;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1);
+    __syncthreads();
+    const int tk = s_tile;
+    if (tk >= a.ntiles) return;
+    const int t = FWD ? tk : a.ntiles - 1 - tk;
+    const int c0 = a.tile_ptr[t], c1 = a.tile_ptr[t + 1];
+    const int TS = ((c1 - c0 + 31) / 32) * 32;
+    for (int i = threadIdx.x; i < a.window; i += blockDim.x) smem_u64[i] = kSentinel;
+    __syncthreads();
+    const int w0 = a.tile_wbase[t], nw = a.tile_wbase[t + 1] - w0;
+    if (warp >= nw) continue;
+    const int g = w0 + warp;
+    const int gr_base = a.tbase[g], nch = (a.tbase[g + 1] - gr_base) / R;
+    const int c = c0 + warp * 32 + lane;
+    int cs = 0, len = 0;
+    if (c < c1) {
+      cs = a.chain_ptr[c];
+      len = a.chain_ptr[c + 1] - cs;
+    }
+    const int ce = cs + len;
+    volatile unsigned long long* wslot = win + (c - c0);
+    auto issue = [&](int k) {
+      if (lane == 0) {
+        const int d = k % D;
+        const size_t gr0 = (size_t)gr_base + (size_t)k * R;
+        const unsigned dst = ring + 8u * (unsigned)(d * a.slot_words);
+        const unsigned bar = bars + 8u * d;
+        mbar_expect_tx(bar, 8u * RW + 8u * 32u * R);
+        bulk_g2s(dst, a.rec + gr0 * 32 * S, 8u * RW, bar);
+        bulk_g2s(dst + 8u * RW, a.tperm + gr0 * 32, 8u * 32u * R, bar);
+      }
+    };
+    int issued = 0, consumed = 0;
+    for (; issued < D && issued < nch; ++issued) issue(issued);
+    int q = 0;
+    double xprev = 0.0;
+    bool abort = false;
+#pragma unroll 1
+    for (int k = 0; k < nch && !abort; ++k) {
+      const int d = k % D;
+      const unsigned long long* slot = ringp + d * a.slot_words;
+      while (!mbar_try_wait(bars + 8u * d, (parity >> d) & 1u)) {}
+      parity ^= 1u << d;
+      ++consumed;
+      const double* rhs = reinterpret_cast<const double*>(slot + RW) + lane;
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        const unsigned long long* rec = slot + rr * 32 * S + lane;
+        const int cnt = (int)((unsigned)rec[0] & 0xffffu);
+        const bool active = cnt != (int)kGsNoRow;
+        const int ca = active ? cnt : 0;
+        double av[C], xv[C];
+        bool ready = gs_lean_gather<C>(rec, ca, sbase, a.xnew, xprev, av, xv);
+        if (!__all_sync(FULL, ready)) {
+          long long spins = 0;
+          do {
+            ready = gs_lean_gather<C>(rec, ca, sbase, a.xnew, xprev, av, xv);
+            if ((++spins & 255) == 0) {
+              bool ab = (*reinterpret_cast<volatile int*>(a.status) & ST_GS_TIMEOUT) != 0;
+              if (spins > kGsIdleLimit) {
+                if (lane == 0) atomicOr(a.status, ST_GS_TIMEOUT);
+                ab = true;
+              }
+              if (__any_sync(FULL, ab)) { abort = true; break; }
+            }
+          } while (!__all_sync(FULL, ready));
+          if (abort) break;
+        }
+        double sacc = rhs[rr * 32];
+#pragma unroll
+        for (int u = 0; u < C; ++u)
+          if (u < ca) sacc = __dsub_rn(sacc, __dmul_rn(av[u], xv[u]));
+        if (active) {
+          const double xi = div_rn_markstein(sacc, __longlong_as_double((long long)rec[32]),
+                                             __longlong_as_double((long long)rec[64]));
+          wslot[q * TS] = (unsigned long long)__double_as_longlong(xi);
+          a.xnew[FWD ? cs + q : ce - 1 - q] = xi;
+          xprev = xi;
+          ++q;
+        }
+        __syncwarp();
+      }
+      __syncwarp();
+      if (!abort && k + D < nch) {
+        issue(k + D);
+        ++issued;
+      }
+    }
+    // an aborted sweep leaves copies in flight: land them before reuse / exit
+    for (; consumed < issued; ++consumed) {
+      const int d = consumed % D;
+      while (!mbar_try_wait(bars + 8u * d, (parity >> d) & 1u)) {}
+      parity ^= 1u << d;
+    }
+  }
+}
+
+// Per-sweep preparation: the right-hand side in (round, lane) order -- for a
+// backward sweep from a nonzero guess t_i = b_i - sum_{j<i} a_ij x_old_j in CSR
+// order (exactly the serial loop's partial sum before the diagonal, since the
+// j < i entries come first in a sorted row), otherwise t_i = b_i -- plus the
+// sentinel fill of x_new and the tile-ticket reset.
+__global__ void __launch_bounds__(256) gs_prepare_kernel(int n, const int* __restrict__ ip,
+                                                         const int* __restrict__ ix,
+                                                         const double* __restrict__ v,
+                                                         const double* __restrict__ b,
+                                                         const double* __restrict__ xold,
+                                                         const int* __restrict__ perm, double* tperm,
+                                                         double* xnew, int* ticket, int fold) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double s = __ldg(b + i);
+    if (fold) {
+      const int k1 = __ldg(ip + i + 1);
+      for (int k = __ldg(ip + i); k < k1; ++k) {
+        const int j = __ldg(ix + k);
+        if (j >= i) break;
+        s = __dsub_rn(s, __dmul_rn(__ldg(v + k), __ldg(xold + j)));
+      }
+    }
+    tperm[__ldg(perm + i)] = s;
+    reinterpret_cast<unsigned long long*>(xnew)[i] = kSentinel;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0;
+}
+
+}  // namespace mvamg

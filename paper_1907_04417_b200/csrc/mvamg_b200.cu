@@ -13,6 +13,8 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -40,6 +42,12 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 int g_num_sms = 0;
+long long g_kernel_launches = 0;
+long long* g_gs_trace = nullptr;  // diagnostics: per-warp GS round/cycle counters (device)
+int g_gs_debug = [] {
+  const char* e = getenv("MVAMG_GS_DEBUG");
+  return e ? atoi(e) : 0;
+}();  // kernels launched by this library (graph nodes counted per replay)
 
 int num_sms() {
   if (g_num_sms == 0) {
@@ -71,10 +79,21 @@ void set_kernel_attrs() {
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   int maxsm = optin - 1024;  // leave room for the kernel's static shared memory
   if (maxsm < 48 * 1024) maxsm = 48 * 1024;
-  bool ok = cudaFuncSetAttribute(gs_sweep_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) == cudaSuccess;
-  ok &= cudaFuncSetAttribute(gs_sweep_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) == cudaSuccess;
-  ok &= cudaFuncSetAttribute(gs_sweep_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) == cudaSuccess;
-  ok &= cudaFuncSetAttribute(gs_sweep_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) == cudaSuccess;
+  bool ok = true;
+#define MVAMG_GS_ATTR(F, R, D) \
+  ok &= cudaFuncSetAttribute(gs_sweep_kernel<F, R, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) == cudaSuccess;
+#define MVAMG_GS_ATTR_D(F, R) MVAMG_GS_ATTR(F, R, 2) MVAMG_GS_ATTR(F, R, 4) MVAMG_GS_ATTR(F, R, 8)
+  MVAMG_GS_ATTR_D(true, 1) MVAMG_GS_ATTR_D(true, 2) MVAMG_GS_ATTR_D(true, 4) MVAMG_GS_ATTR_D(true, 8)
+  MVAMG_GS_ATTR_D(false, 1) MVAMG_GS_ATTR_D(false, 2) MVAMG_GS_ATTR_D(false, 4) MVAMG_GS_ATTR_D(false, 8)
+#undef MVAMG_GS_ATTR_D
+#undef MVAMG_GS_ATTR
+#define MVAMG_LEAN_ATTR(F, CC, RR, DD) \
+  ok &= cudaFuncSetAttribute(gs_lean_kernel<F, CC, RR, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) == cudaSuccess;
+#define MVAMG_LEAN_ATTR_C(F, RR, DD) MVAMG_LEAN_ATTR(F, 2, RR, DD) MVAMG_LEAN_ATTR(F, 4, RR, DD) MVAMG_LEAN_ATTR(F, 8, RR, DD)
+  MVAMG_LEAN_ATTR_C(true, 8, 4) MVAMG_LEAN_ATTR_C(true, 4, 4) MVAMG_LEAN_ATTR_C(true, 2, 8) MVAMG_LEAN_ATTR_C(true, 1, 8)
+  MVAMG_LEAN_ATTR_C(false, 8, 4) MVAMG_LEAN_ATTR_C(false, 4, 4) MVAMG_LEAN_ATTR_C(false, 2, 8) MVAMG_LEAN_ATTR_C(false, 1, 8)
+#undef MVAMG_LEAN_ATTR_C
+#undef MVAMG_LEAN_ATTR
   g_max_dyn_smem = ok ? maxsm : 48 * 1024;
   cudaGetLastError();
 }
@@ -90,6 +109,20 @@ struct GsPlan {
   int ntiles = 0, threads = 32, window = 0;
   const int* chain_ptr = nullptr;
   const int* tile_ptr = nullptr;
+};
+
+// Static round schedule of one sweep mode (0 forward from x = 0, 1 forward,
+// 2 backward): round-major records, per-round offsets, per-warp round bases,
+// per-tile warp bases, the row -> (round, lane) permutation and its rhs buffer.
+struct GsList {
+  int lean_C = 0;  // > 0: uniform records of 3 + 2C words, lean kernel
+  const unsigned long long* rec = nullptr;
+  const int* round_off = nullptr;
+  const int* tbase = nullptr;
+  const int* tile_wbase = nullptr;
+  const int* perm = nullptr;
+  double* tperm = nullptr;
+  int R = 1, D = 2, slot_words = 0, rec_words_max = 0;
 };
 
 struct Smoother {
@@ -108,53 +141,102 @@ int launch_spmv(int mode, const Csr& A, const double* x, const double* b, double
   return 0;
 }
 
-int gs_blocks(const GsPlan& p) {
-  static std::map<std::pair<int, int>, int> occ_cache;
-  size_t smem = (size_t)p.window * sizeof(double);
-  auto key = std::make_pair(p.threads, p.window);
+size_t gs_smem_bytes(const GsPlan& p, const GsList& ls) {
+  const int warps = p.threads / 32;
+  size_t words = (size_t)((p.window + 1) & ~1) + (size_t)warps * ls.D * ls.slot_words;
+  return words * 8 + (size_t)warps * ls.D * 8;  // + one mbarrier per slot
+}
+
+int gs_blocks(const GsPlan& p, const GsList& ls) {
+  static std::map<std::pair<int, size_t>, int> occ_cache;
+  size_t smem = gs_smem_bytes(p, ls);
+  auto key = std::make_pair(p.threads, smem);
   auto it = occ_cache.find(key);
   int per_sm;
   if (it != occ_cache.end()) {
     per_sm = it->second;
   } else {
     per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs_sweep_kernel<true, true>, p.threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs_sweep_kernel<true, 4, 2>, p.threads, smem);
     if (per_sm < 1) per_sm = 1;
     occ_cache[key] = per_sm;
   }
   return std::max(1, std::min(p.ntiles, per_sm * num_sms()));
 }
 
-int launch_gs(bool fwd, bool zero, const Csr& A, const double* diag, const double* rdiag,
-              const GsPlan& p, const double* b, const double* xold, double* xnew, int* ticket,
-              int* status, cudaStream_t s) {
-  if (A.n == 0) return 0;
+// One sweep: gs_prepare_kernel writes the right-hand side in (round, lane)
+// order (folding the backward sweep's old upper neighbours), fills x_new with
+// the sentinel and resets the ticket; gs_sweep_kernel then runs the schedule.
+int launch_gs(bool fwd, const Csr& A, const GsList& ls, const GsPlan& p, const double* b,
+              const double* xold, double* xnew, int* ticket, int* status, cudaStream_t s) {
+  const int n = A.n;
+  if (n == 0) return 0;
+  if (!ls.rec) return fail(MVAMG_E_STATE, "gs: schedule for this sweep mode was not set");
   set_kernel_attrs();
-  if ((size_t)p.window * sizeof(double) > (size_t)g_max_dyn_smem)
-    return fail(MVAMG_E_ARG, "gs: window of " + std::to_string(p.window) + " rows exceeds shared memory");
-  gs_prep_kernel<<<grid_for(A.n), 256, 0, s>>>(A.n, xnew, ticket);
+  const size_t smem = gs_smem_bytes(p, ls);
+  if (smem > (size_t)g_max_dyn_smem)
+    return fail(MVAMG_E_ARG, "gs: shared memory plan of " + std::to_string(smem) + " bytes exceeds the limit");
+  const int fold = (!fwd && xold != nullptr) ? 1 : 0;
+  gs_prepare_kernel<<<grid_for(n), 256, 0, s>>>(n, A.ip, A.ix, A.v, b, xold, ls.perm, ls.tperm, xnew,
+                                                ticket, fold);
   GsArgs a;
-  a.n = A.n;
+  a.n = n;
   a.ntiles = p.ntiles;
   a.window = p.window;
-  a.ip = A.ip;
-  a.ix = A.ix;
-  a.v = A.v;
-  a.diag = diag;
-  a.rdiag = rdiag;
+  a.slot_words = ls.slot_words;
+  a.rec_words_max = ls.rec_words_max;
+  a.rec = ls.rec;
+  a.round_off = ls.round_off;
+  a.tbase = ls.tbase;
+  a.tile_wbase = ls.tile_wbase;
   a.chain_ptr = p.chain_ptr;
   a.tile_ptr = p.tile_ptr;
-  a.b = b;
+  a.tperm = ls.tperm;
   a.xold = xold;
   a.xnew = xnew;
   a.ticket = ticket;
   a.status = status;
-  int g = gs_blocks(p);
-  size_t smem = (size_t)p.window * sizeof(double);
-  if (fwd && zero) gs_sweep_kernel<true, true><<<g, p.threads, smem, s>>>(a);
-  else if (fwd) gs_sweep_kernel<true, false><<<g, p.threads, smem, s>>>(a);
-  else if (zero) gs_sweep_kernel<false, true><<<g, p.threads, smem, s>>>(a);
-  else gs_sweep_kernel<false, false><<<g, p.threads, smem, s>>>(a);
+  a.trace = g_gs_trace;
+  a.debug = g_gs_debug;
+  const int g = gs_blocks(p, ls);
+  if (ls.lean_C > 0) {
+#define MVAMG_LEAN(F, CC, RR, DD) gs_lean_kernel<F, CC, RR, DD><<<g, p.threads, smem, s>>>(a)
+#define MVAMG_LEAN_C(F, RR, DD)                                                   \
+  do {                                                                            \
+    if (ls.lean_C <= 2) MVAMG_LEAN(F, 2, RR, DD);                                 \
+    else if (ls.lean_C <= 4) MVAMG_LEAN(F, 4, RR, DD);                            \
+    else MVAMG_LEAN(F, 8, RR, DD);                                                \
+  } while (0)
+#define MVAMG_LEAN_R(F)                                                           \
+  do {                                                                            \
+    if (ls.R >= 8) MVAMG_LEAN_C(F, 8, 4);                                         \
+    else if (ls.R >= 4) MVAMG_LEAN_C(F, 4, 4);                                    \
+    else if (ls.R >= 2) MVAMG_LEAN_C(F, 2, 8);                                    \
+    else MVAMG_LEAN_C(F, 1, 8);                                                   \
+  } while (0)
+    if (fwd) MVAMG_LEAN_R(true); else MVAMG_LEAN_R(false);
+#undef MVAMG_LEAN_R
+#undef MVAMG_LEAN_C
+#undef MVAMG_LEAN
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+#define MVAMG_GS_LAUNCH(F, RR, DD) gs_sweep_kernel<F, RR, DD><<<g, p.threads, smem, s>>>(a)
+#define MVAMG_GS_LAUNCH_D(F, RR)                                     \
+  do {                                                               \
+    if (ls.D >= 8) MVAMG_GS_LAUNCH(F, RR, 8);                        \
+    else if (ls.D >= 4) MVAMG_GS_LAUNCH(F, RR, 4);                   \
+    else MVAMG_GS_LAUNCH(F, RR, 2);                                  \
+  } while (0)
+  if (fwd) {
+    if (ls.R >= 8) MVAMG_GS_LAUNCH_D(true, 8); else if (ls.R >= 4) MVAMG_GS_LAUNCH_D(true, 4);
+    else if (ls.R >= 2) MVAMG_GS_LAUNCH_D(true, 2); else MVAMG_GS_LAUNCH_D(true, 1);
+  } else {
+    if (ls.R >= 8) MVAMG_GS_LAUNCH_D(false, 8); else if (ls.R >= 4) MVAMG_GS_LAUNCH_D(false, 4);
+    else if (ls.R >= 2) MVAMG_GS_LAUNCH_D(false, 2); else MVAMG_GS_LAUNCH_D(false, 1);
+  }
+#undef MVAMG_GS_LAUNCH_D
+#undef MVAMG_GS_LAUNCH
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -169,6 +251,7 @@ struct Level {
   const double* diag = nullptr;
   const double* rdiag = nullptr;
   GsPlan plan;
+  GsList gl[3];
   Csr P, R;  // valid for k < L-1
   double *xa = nullptr, *xb = nullptr, *t = nullptr, *r = nullptr, *z = nullptr;
   double *fr = nullptr, *fx = nullptr, *fp[2] = {nullptr, nullptr}, *fap[2] = {nullptr, nullptr};
@@ -190,6 +273,7 @@ struct mvamg_hierarchy {
          *pz = nullptr, *in = nullptr;
   DevScalars* host_sc = nullptr;  // pinned mirror
   std::map<std::string, cudaGraphExec_t> graphs;
+  std::map<std::string, int> graph_kernels;
 
   ReduceCtx ctx(FcgScalars* fs = nullptr, double* out = nullptr) const {
     ReduceCtx c;
@@ -231,8 +315,8 @@ struct mvamg_hierarchy {
                                                        sp.omega, x_cur, out);
       } else {
         bool fwd = sp.kind == MVAMG_GS_FORWARD;
-        st = launch_gs(fwd, x_cur == nullptr, l.A, l.diag, l.rdiag, l.plan, b, x_cur, out, ticket,
-                       status_ptr(), s);
+        int mode = fwd ? (x_cur == nullptr ? 0 : 1) : 2;
+        st = launch_gs(fwd, l.A, l.gl[mode], l.plan, b, x_cur, out, ticket, status_ptr(), s);
         if (st) return st;
       }
       x_cur = out;
@@ -317,13 +401,24 @@ struct mvamg_hierarchy {
       cudaStreamDestroy(cs);
       if (st) return st;
       if (e != cudaSuccess) return fail(MVAMG_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+      size_t nn = 0;
+      cudaGraphGetNodes(graph, nullptr, &nn);
+      std::vector<cudaGraphNode_t> nodes(nn);
+      if (nn) cudaGraphGetNodes(graph, nodes.data(), &nn);
+      int nk = 0;
+      for (auto nd : nodes) {
+        cudaGraphNodeType ty;
+        if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) ++nk;
+      }
       cudaGraphExec_t exec;
       e = cudaGraphInstantiate(&exec, graph, 0);
       cudaGraphDestroy(graph);
       if (e != cudaSuccess) return fail(MVAMG_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
       it = graphs.emplace(key, exec).first;
+      graph_kernels[key] = nk;
     }
     CUDA_TRY(cudaGraphLaunch(it->second, s));
+    g_kernel_launches += graph_kernels[key];
     return 0;
   }
 };
@@ -400,6 +495,7 @@ int pcg_device(mvamg_hierarchy* h, int pc, mvamg_composite* comp, const double* 
   zero_kernel<<<g, 256, 0, s>>>(n, h->px);
   dot2_kernel<<<gd, 256, 0, s>>>(n, h->pr, h->pr, nullptr, nullptr, POST_PCG_R0, h->ctx());
   CUDA_TRY(cudaGetLastError());
+  g_kernel_launches += 4;
   auto sync_flags = [&]() -> int {
     CUDA_TRY(cudaMemcpyAsync(h->host_sc, h->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -457,6 +553,17 @@ int pcg_device(mvamg_hierarchy* h, int pc, mvamg_composite* comp, const double* 
 extern "C" {
 
 int mvamg_version(void) { return 1; }
+
+int mvamg_gs_set_trace(long long* trace_dev) {
+  g_gs_trace = trace_dev;
+  return 0;
+}
+
+int mvamg_kernel_launches(long long* count, int reset) {
+  if (count) *count = g_kernel_launches;
+  if (reset) g_kernel_launches = 0;
+  return 0;
+}
 const char* mvamg_last_error(void) { return g_err.c_str(); }
 
 int mvamg_gs_analyse(int n, const int* indptr, const int* indices, int max_chain, int max_threads,
@@ -486,34 +593,37 @@ int mvamg_gs_analyse(int n, const int* indptr, const int* indices, int max_chain
   }
   cp.push_back(n);
   int nc = (int)cp.size() - 1;
-  // tiles: consecutive chains, <= max_threads chains, rows <= max_window
+  // tiles: consecutive chains, <= max_threads chains, and a position-major
+  // shared window of roundup32(chains) x (longest chain) slots <= max_window
+  if (max_threads > 256) max_threads = 256;
+  auto r32 = [](int v) { return ((v + 31) / 32) * 32; };
   std::vector<int> tp;
   tp.push_back(0);
-  int cnt = 0, rows = 0, maxcnt = 1, maxrows = 0;
+  int cnt = 0, maxlen = 0, maxcnt = 1, maxslots = 1;
   for (int c = 0; c < nc; ++c) {
     int cl = cp[c + 1] - cp[c];
-    if (cnt > 0 && (cnt + 1 > max_threads || rows + cl > max_window)) {
+    if (cnt > 0 && (cnt + 1 > max_threads || (long long)r32(cnt + 1) * std::max(maxlen, cl) > max_window)) {
       tp.push_back(c);
       maxcnt = std::max(maxcnt, cnt);
-      maxrows = std::max(maxrows, rows);
+      maxslots = std::max(maxslots, r32(cnt) * maxlen);
       cnt = 0;
-      rows = 0;
+      maxlen = 0;
     }
     ++cnt;
-    rows += cl;
+    maxlen = std::max(maxlen, cl);
   }
   if (nc > 0) {
     tp.push_back(nc);
     maxcnt = std::max(maxcnt, cnt);
-    maxrows = std::max(maxrows, rows);
+    maxslots = std::max(maxslots, r32(cnt) * maxlen);
   }
   int nt = (int)tp.size() - 1;
   *nchains = nc;
   *ntiles = nt;
   if (chain_ptr) std::copy(cp.begin(), cp.end(), chain_ptr);
   if (tile_ptr) std::copy(tp.begin(), tp.end(), tile_ptr);
-  if (threads_out) *threads_out = std::min(256, ((maxcnt + 31) / 32) * 32);
-  if (window_out) *window_out = std::min(maxrows, max_window);
+  if (threads_out) *threads_out = r32(maxcnt);
+  if (window_out) *window_out = maxslots;
   if (depth_out) {
     // level-set depth of the forward sweep DAG (diagnostic: the critical path)
     std::vector<int> lvl(n, 0);
@@ -529,7 +639,6 @@ int mvamg_gs_analyse(int n, const int* indptr, const int* indices, int max_chain
     }
     *depth_out = depth;
   }
-  if (max_threads > 256) return fail(MVAMG_E_ARG, "gs_analyse: max_threads > 256");
   return 0;
 }
 
@@ -554,18 +663,159 @@ int mvamg_csr_spmv_add_f64(int n, const int* indptr, const int* indices, const d
   return launch_spmv(2, A, x, nullptr, y, (cudaStream_t)stream);
 }
 
-int mvamg_gs_sweep_f64(int direction, int zero_init, int n, const int* indptr, const int* indices,
-                       const double* data, const double* diag, const double* rdiag, int ntiles,
+int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double* data, int ntiles,
+                      const int* chain_ptr, const int* tile_ptr, int window, int mode, int R,
+                      int uniform_S, long long* nwords, int* nrounds, int* nwarps, int* max_S,
+                      unsigned long long* rec, int* round_off, int* tbase, int* tile_wbase,
+                      int* perm) {
+  if (n < 0 || !indptr || !chain_ptr || !tile_ptr || !nwords || !nrounds || !nwarps || mode < 0 ||
+      mode > 2 || R < 1 || R > 31)
+    return fail(MVAMG_E_ARG, "gs_schedule: bad arguments");
+  if (n >= (1 << 29)) return fail(MVAMG_E_ARG, "gs_schedule: n >= 2^29 not encodable");
+  const bool fwd = mode < 2, with_old = mode == 1;
+  auto dbits = [](double d) {
+    unsigned long long u;
+    std::memcpy(&u, &d, 8);
+    return u;
+  };
+  auto keep = [&](int i, int j) {  // entries a row's record holds, in CSR order
+    if (j == i) return false;
+    if (fwd) return j < i || with_old;
+    return j > i;
+  };
+  auto lower = [&](int i, int j) { return fwd ? (j < i) : (j > i); };
+  const int nch = tile_ptr[ntiles];
+  std::vector<int> chain_of(n > 0 ? n : 1);
+  for (int c = 0; c < nch; ++c)
+    for (int i = chain_ptr[c]; i < chain_ptr[c + 1]; ++i) chain_of[i] = c;
+  long long w = 0;
+  int gr = 0, gw = 0, smax = 1;
+  std::vector<int> rnd, rows_of_round, cnt_of;
+  for (int t = 0; t < ntiles; ++t) {
+    const int c0 = tile_ptr[t], c1 = tile_ptr[t + 1];
+    const int TS = ((c1 - c0 + 31) / 32) * 32;
+    if (tile_wbase) tile_wbase[t] = gw;
+    for (int cA = c0; cA < c1; cA += 32, ++gw) {
+      const int cB = std::min(cA + 32, c1);
+      const int rlo = chain_ptr[cA], rhi = chain_ptr[cB];
+      rnd.assign(rhi - rlo, 0);
+      int last[32];
+      for (int L = 0; L < 32; ++L) last[L] = -1;
+      int nr = 0;
+      for (int q = 0; q < rhi - rlo; ++q) {
+        const int i = fwd ? rlo + q : rhi - 1 - q;
+        const int L = chain_of[i] - cA;
+        int r = last[L] + 1;
+        for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+          const int j = indices[k];
+          if (j != i && lower(i, j) && j >= rlo && j < rhi) r = std::max(r, rnd[j - rlo] + 1);
+        }
+        rnd[i - rlo] = r;
+        last[L] = r;
+        nr = std::max(nr, r + 1);
+      }
+      nr = ((nr + R - 1) / R) * R;
+      if (nr == 0) nr = R;
+      if (tbase) tbase[gw] = gr;
+      // rows of each round, one per lane
+      rows_of_round.assign((size_t)nr * 32, -1);
+      for (int i = rlo; i < rhi; ++i) rows_of_round[(size_t)rnd[i - rlo] * 32 + (chain_of[i] - cA)] = i;
+      for (int r = 0; r < nr; ++r, ++gr) {
+        int maxcnt = -1;
+        for (int L = 0; L < 32; ++L) {
+          const int i = rows_of_round[(size_t)r * 32 + L];
+          if (i < 0) continue;
+          int cnt = 0;
+          for (int k = indptr[i]; k < indptr[i + 1]; ++k) cnt += keep(i, indices[k]);
+          maxcnt = std::max(maxcnt, cnt);
+        }
+        int S = maxcnt < 0 ? 1 : 3 + 2 * maxcnt;
+        if (uniform_S > 0) {
+          if (S > uniform_S) return fail(MVAMG_E_ARG, "gs_schedule: row longer than the uniform record");
+          S = uniform_S;
+        }
+        smax = std::max(smax, S);
+        if (round_off) round_off[gr] = (int)w;
+        if (rec) {
+          unsigned long long* blk = rec + w;
+          std::memset(blk, 0, sizeof(unsigned long long) * 32 * S);
+          for (int L = 0; L < 32; ++L) {
+            const int i = rows_of_round[(size_t)r * 32 + L];
+            if (i < 0) {
+              blk[L] = kGsNoRow;
+              continue;
+            }
+            const int c = chain_of[i], cs = chain_ptr[c], ce = chain_ptr[c + 1];
+            int cnt = 0;
+            bool fast = true;
+            double dg = 0.0;
+            for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+              const int j = indices[k];
+              if (j == i) dg = data[k];
+              if (!keep(i, j)) continue;
+              int code;
+              if (!lower(i, j)) {
+                code = (j << 2) | 3;
+              } else if ((fwd && j == i - 1 && j >= cs) || (!fwd && j == i + 1 && j < ce)) {
+                code = 0;
+              } else if (chain_of[j] >= c0 && chain_of[j] < c1) {
+                const int cj = chain_of[j];
+                const int pos = fwd ? j - chain_ptr[cj] : chain_ptr[cj + 1] - 1 - j;
+                const long long slot = (long long)pos * TS + (cj - c0);
+                if (slot >= window) return fail(MVAMG_E_ARG, "gs_schedule: window slot out of range");
+                code = (int)(slot << 2) | 1;
+              } else {
+                code = (j << 2) | 2;
+              }
+              blk[(size_t)32 * (3 + 2 * cnt) + L] = dbits(data[k]);
+              blk[(size_t)32 * (4 + 2 * cnt) + L] = (unsigned long long)(unsigned)code;
+              fast = fast && ((code & 3) == 0 || (code & 3) == 1);
+              ++cnt;
+            }
+            if (cnt >= (int)kGsNoRow) return fail(MVAMG_E_ARG, "gs_schedule: row with too many entries");
+            blk[L] = (unsigned long long)(unsigned)cnt | (fast ? 0x10000ull : 0ull);
+            blk[32 + L] = dbits(dg);
+            blk[64 + L] = dbits(1.0 / dg);
+            if (perm) perm[i] = gr * 32 + L;
+          }
+        }
+        w += (long long)32 * S;
+        if (w >= (1LL << 31)) return fail(MVAMG_E_ARG, "gs_schedule: record stream exceeds 2^31 words");
+        if ((long long)gr * 32 >= (1LL << 31)) return fail(MVAMG_E_ARG, "gs_schedule: too many rounds");
+      }
+    }
+  }
+  if (round_off) round_off[gr] = (int)w;
+  if (tbase) tbase[gw] = gr;
+  if (tile_wbase) tile_wbase[ntiles] = gw;
+  *nwords = w;
+  *nrounds = gr;
+  *nwarps = gw;
+  if (max_S) *max_S = smax;
+  return 0;
+}
+
+int mvamg_gs_sweep_f64(int direction, int n, const int* indptr, const int* indices, const double* data,
+                       const unsigned long long* rec, const int* round_off, const int* tbase,
+                       const int* tile_wbase, const int* perm, double* tperm, int R, int D,
+                       int lean_C, int slot_words, int rec_words_max, int ntiles,
                        const int* chain_ptr, const int* tile_ptr, int threads, int window,
                        const double* b, const double* x_old, double* x_new, int* ws, void* stream) {
   if (threads < 32 || threads > 256 || threads % 32) return fail(MVAMG_E_ARG, "gs: threads must be 32..256, multiple of 32");
-  if (!zero_init && x_old == x_new) return fail(MVAMG_E_ARG, "gs: x_new must not alias x_old");
+  if (R != 1 && R != 2 && R != 4 && R != 8) return fail(MVAMG_E_ARG, "gs: R must be 1, 2, 4 or 8");
+  if (D != 2 && D != 4 && D != 8) return fail(MVAMG_E_ARG, "gs: D must be 2, 4 or 8");
+  if (x_old != nullptr && x_old == x_new) return fail(MVAMG_E_ARG, "gs: x_new must not alias x_old");
   Csr A;
   A.n = n; A.ip = indptr; A.ix = indices; A.v = data;
+  GsList ls;
+  ls.rec = rec; ls.round_off = round_off; ls.tbase = tbase; ls.tile_wbase = tile_wbase; ls.perm = perm;
+  ls.tperm = tperm; ls.R = R; ls.D = D; ls.slot_words = slot_words; ls.rec_words_max = rec_words_max;
+  ls.lean_C = lean_C;
+  if (lean_C > 0 && ((R == 8 && D != 4) || (R == 4 && D != 4) || (R <= 2 && D != 8)))
+    return fail(MVAMG_E_ARG, "gs: lean kernel ring must be (R, D) in {(8,4), (4,4), (2,8), (1,8)}");
   GsPlan p;
   p.ntiles = ntiles; p.threads = threads; p.window = window; p.chain_ptr = chain_ptr; p.tile_ptr = tile_ptr;
-  return launch_gs(direction == 0, zero_init != 0, A, diag, rdiag, p, b, x_old, x_new, ws, ws + 1,
-                   (cudaStream_t)stream);
+  return launch_gs(direction == 0, A, ls, p, b, x_old, x_new, ws, ws + 1, (cudaStream_t)stream);
 }
 
 int mvamg_dense_gemv_f64(int n, const double* inv, const double* r, double* z, void* stream) {
@@ -625,6 +875,18 @@ int mvamg_hierarchy_set_level(mvamg_hierarchy* h, int k, int n, int nnz, const i
   l.plan.tile_ptr = tile_ptr;
   l.plan.threads = gs_threads;
   l.plan.window = gs_window;
+  return 0;
+}
+
+int mvamg_hierarchy_set_gs_schedule(mvamg_hierarchy* h, int k, int mode, const unsigned long long* rec,
+                                    const int* round_off, const int* tbase, const int* tile_wbase,
+                                    const int* perm, double* tperm, int R, int D, int lean_C,
+                                    int slot_words, int rec_words_max) {
+  if (!h || k < 0 || k >= h->L || mode < 0 || mode > 2) return fail(MVAMG_E_ARG, "set_gs_schedule: bad index");
+  GsList& g = h->lv[k].gl[mode];
+  g.lean_C = lean_C;
+  g.rec = rec; g.round_off = round_off; g.tbase = tbase; g.tile_wbase = tile_wbase; g.perm = perm;
+  g.tperm = tperm; g.R = R; g.D = D; g.slot_words = slot_words; g.rec_words_max = rec_words_max;
   return 0;
 }
 
@@ -698,7 +960,8 @@ int mvamg_hierarchy_bind_workspace(mvamg_hierarchy* h, void* ws, void* stream) {
   workspace_layout(h, (char*)ws);
   set_kernel_attrs();
   for (int k = 0; k < h->L - 1; ++k)
-    if (h->lv[k].plan.ntiles > 0) gs_blocks(h->lv[k].plan);
+    for (int m = 0; m < 3; ++m)
+      if (h->lv[k].plan.ntiles > 0 && h->lv[k].gl[m].rec) gs_blocks(h->lv[k].plan, h->lv[k].gl[m]);
   cudaStream_t s = (cudaStream_t)stream;
   CUDA_TRY(cudaMemsetAsync(h->counter, 0, 64, s));
   CUDA_TRY(cudaMemsetAsync(h->ticket, 0, 64, s));

@@ -34,6 +34,8 @@ struct FcgScalars {
   double alpha, beta, pAp, pAp_prev, pr;
 };
 
+__device__ __noinline__ double div_rn_slow(double s, double d) { return __ddiv_rn(s, d); }
+
 __device__ __forceinline__ double div_rn_markstein(double s, double d, double y) {
   // RN(s/d) from y = RN(1/d): q0 = RN(s*y) is faithful, r = s - q0*d is exact
   // (FMA), q = RN(q0 + r*y) is the correctly rounded quotient (Markstein).
@@ -43,13 +45,13 @@ __device__ __forceinline__ double div_rn_markstein(double s, double d, double y)
   double r = fma(-q0, d, s);
   double q = fma(r, y, q0);
   double aq = fabs(q0);
-  if (!(aq > 1e-290 && aq < 1e290)) q = __ddiv_rn(s, d);  // outside the theorem's range / zero
+  if (__builtin_expect(!(aq > 1e-290 && aq < 1e290), 0)) q = div_rn_slow(s, d);  // outside the theorem's range / zero
   return q;
 }
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const double* p) {
   unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 }
 
@@ -136,108 +138,11 @@ __global__ void __launch_bounds__(256) jacobi_kernel(int n, const int* __restric
   }
 }
 
-// ---------------------------------------------------------------------------
-// Gauss-Seidel sweep in the reference's exact row order, scheduled sync-free.
-//
-// Rows are split (host, gs_analyse) into chains -- runs of consecutive rows
-// where row i couples to row i-1 -- and consecutive chains into tiles.  One
-// thread owns one chain and walks it in sweep order, so the i-1 dependency is a
-// register; other in-tile dependencies are read from a shared-memory window
-// and cross-tile ones from global memory, both polled against a NaN sentinel
-// (the value is its own ready flag: 8-byte stores are single-copy atomic, so no
-// fences are needed).  Tiles are claimed through an atomic ticket in sweep
-// order, so every tile a CTA waits on is owned by a resident CTA (no deadlock).
-// Each row's sum is formed in CSR order with lower neighbours taken from the
-// new iterate and upper neighbours from the old one -- exactly what the serial
-// loop computes -- so the result is bit-identical to _kernels.gs_forward /
-// gs_backward.
-struct GsArgs {
-  int n, ntiles, window;
-  const int* ip;
-  const int* ix;
-  const double* v;
-  const double* diag;
-  const double* rdiag;
-  const int* chain_ptr;
-  const int* tile_ptr;
-  const double* b;
-  const double* xold;
-  double* xnew;
-  int* ticket;
-  int* status;
-};
+}  // namespace mvamg
 
-constexpr int kGsPrefetchRows = 4;
+#include "gs_sweep.cuh"
 
-template <bool FWD, bool ZERO>
-__global__ void __launch_bounds__(256) gs_sweep_kernel(GsArgs a) {
-  extern __shared__ double win[];
-  __shared__ int s_tile;
-  for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1);
-    __syncthreads();
-    const int tk = s_tile;
-    if (tk >= a.ntiles) return;
-    const int t = FWD ? tk : a.ntiles - 1 - tk;
-    const int c0 = a.tile_ptr[t], c1 = a.tile_ptr[t + 1];
-    const int row0 = a.chain_ptr[c0], row1 = a.chain_ptr[c1];
-    const int wn = min(row1 - row0, a.window);
-    unsigned long long* wu = reinterpret_cast<unsigned long long*>(win);
-    for (int i = threadIdx.x; i < wn; i += blockDim.x) wu[i] = kSentinel;
-    __syncthreads();
-    const int c = c0 + threadIdx.x;
-    if (c < c1) {
-      const int cs = a.chain_ptr[c], ce = a.chain_ptr[c + 1];
-      const int len = ce - cs;
-      double xprev = 0.0;
-      int iprev = -1;
-      for (int q = 0; q < len; ++q) {
-        const int i = FWD ? cs + q : ce - 1 - q;
-        if (q + kGsPrefetchRows < len) {
-          const int ip_ = FWD ? i + kGsPrefetchRows : i - kGsPrefetchRows;
-          const int kp = a.ip[ip_];
-          prefetch_l1(a.ix + kp);
-          prefetch_l1(a.v + kp);
-        }
-        double s = a.b[i];
-        const int kb = a.ip[i], ke = a.ip[i + 1];
-        for (int kk = kb; kk < ke; ++kk) {
-          const int j = a.ix[kk];
-          if (j == i) continue;
-          const bool lower = FWD ? (j < i) : (j > i);
-          double val;
-          if (lower) {
-            if (j == iprev) {
-              val = xprev;
-            } else {
-              const int w = j - row0;
-              if (w >= 0 && w < wn) val = poll_shared(win + w, a.status);
-              else val = poll_global(a.xnew + j, a.status);
-            }
-          } else {
-            if (ZERO) continue;
-            val = a.xold[j];
-          }
-          s = __dsub_rn(s, __dmul_rn(a.v[kk], val));
-        }
-        const double xi = div_rn_markstein(s, a.diag[i], a.rdiag[i]);
-        const int w = i - row0;
-        if (w >= 0 && w < wn) reinterpret_cast<volatile double*>(win)[w] = xi;
-        a.xnew[i] = xi;
-        xprev = xi;
-        iprev = i;
-      }
-    }
-  }
-}
-
-// Fill x_new with the sentinel and reset the tile ticket.
-__global__ void gs_prep_kernel(int n, double* xnew, int* ticket) {
-  unsigned long long* u = reinterpret_cast<unsigned long long*>(xnew);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) u[i] = kSentinel;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0;
-}
+namespace mvamg {
 
 // ---------------------------------------------------------------------------
 // Dense coarsest solve z = Inv r (row-major), one warp per row.

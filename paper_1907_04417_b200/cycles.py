@@ -16,7 +16,7 @@ import scipy.linalg
 import scipy.sparse.linalg as spla
 
 from . import _lib
-from .device import DeviceCSR, GpuConfig, as_csr, gs_analyse, ptr, stream_handle, to_device, torch_cuda
+from .device import DeviceCSR, DeviceGsPlan, GpuConfig, as_csr, ptr, stream_handle, to_device, torch_cuda
 from .exceptions import NotSpdError
 
 GS_FORWARD = "gauss_seidel_forward"
@@ -97,6 +97,20 @@ class GpuMultigridOperator:
         return cls(op.matrices, op.prolongators, cycle=op.cycle, pre_smoother=op.pre_smoother,
                    post_smoother=op.post_smoother, config=config)
 
+    def _gs_modes(self):
+        """GS record modes the cycle needs (0 fwd from x=0, 1 fwd, 2 bwd)."""
+        modes = set()
+        for spec, first_zero in ((self.pre_smoother, True), (self.post_smoother, False)):
+            if spec.kind == WEIGHTED_JACOBI or spec.sweeps == 0:
+                continue
+            if spec.kind == GS_BACKWARD:
+                modes.add(2)
+            else:
+                modes.add(0 if first_zero else 1)
+                if first_zero and spec.sweeps > 1:
+                    modes.add(1)
+        return sorted(modes)
+
     def _init_plain(self, A):
         """Single-level handle used only for its matrix (pcg with precond=None)."""
         self.matrices = [as_csr(A)]
@@ -122,22 +136,27 @@ class GpuMultigridOperator:
         self._h = h
         self._keep = []
         self.gs_plans = []
+        self.level_dev = []
         self._dA = []
         for k, A in enumerate(self.matrices):
             dA = DeviceCSR(A)
             self._dA.append(dA)
             if k < nl - 1:
-                d = self.diagonals[k]
-                dd = to_device(d, np.float64)
-                rd = to_device(1.0 / d, np.float64)  # RN(1/d): Markstein division in the GS kernel
-                plan = gs_analyse(A, self.config)
-                cp = to_device(plan.chain_ptr, np.int32)
-                tp = to_device(plan.tile_ptr, np.int32)
-                self._keep += [dd, rd, cp, tp]
-                self.gs_plans.append(plan)
-                _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd), ptr(rd),
-                                                       plan.ntiles, ptr(cp), ptr(tp), plan.threads,
-                                                       plan.window), "set_level")
+                gp = DeviceGsPlan(A, self.config)
+                self.gs_plans.append(gp.plan)
+                self.level_dev.append(dict(A=dA, gs=gp, plan=gp.plan))
+                dd = to_device(self.diagonals[k], np.float64)
+                self._keep.append(dd)
+                _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
+                                                       None, gp.plan.ntiles, ptr(gp.chain_ptr),
+                                                       ptr(gp.tile_ptr), gp.plan.threads,
+                                                       gp.plan.window), "set_level")
+                for m in self._gs_modes():
+                    sch = gp.mode(m)
+                    _lib.check(L.mvamg_hierarchy_set_gs_schedule(
+                        h, k, m, ptr(sch["rec"]), ptr(sch["round_off"]), ptr(sch["tbase"]),
+                        ptr(sch["tile_wbase"]), ptr(sch["perm"]), ptr(sch["tperm"]), sch["R"], sch["D"],
+                        sch["lean_C"], sch["slot_words"], sch["rec_words_max"]), "set_gs_schedule")
             else:
                 _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), None, None, 0,
                                                        None, None, 32, 0), "set_level")

@@ -61,9 +61,13 @@ class GpuConfig:
     """
 
     max_chain: int = 4096
-    max_threads: int = 128
-    max_window: int = 24576
+    max_threads: int = 256
+    max_window: int = 1 << 20
     graphs: bool = True
+    smem_budget: int = 220 * 1024   # bytes of shared memory per GS CTA (window + rings)
+    ring_bytes: int = 48 * 1024     # TMA ring size per warp (D slots of R rounds)
+    rounds_in_flight: int = 16      # rounds of records the ring keeps ahead (generic kernel)
+    generic_gs: bool = False        # force the generic GS kernel (tests / diagnostics)
 
 
 class DeviceCSR:
@@ -96,25 +100,193 @@ class GsPlanHost:
     tile_ptr: np.ndarray
 
 
+LEAN_RINGS = ((8, 4), (4, 4), (2, 8), (1, 8))  # (R, D) pairs the lean kernel is built for
+
+
+def _row_counts(A):
+    """Per-row counts of strictly lower / strictly upper stored entries."""
+    n = A.shape[0]
+    rows = np.repeat(np.arange(n), np.diff(A.indptr))
+    lo = np.bincount(rows[A.indices < rows], minlength=n)
+    up = np.bincount(rows[A.indices > rows], minlength=n)
+    return lo, up
+
+
+def _gs_ring(A, cfg):
+    """Ring plan (lean_C, R, D, slot_words, S) for matrix A.
+
+    The lean kernel (lean_C > 0) serves sweeps whose rows have <= 8 dependent
+    entries: uniform records of S = 3 + 2C words, slots of R rounds of records
+    plus R x 32 right-hand-side values.  Otherwise the generic kernel, S bounded
+    by the longest row.  Aims for many rounds in flight within cfg.ring_bytes."""
+    lo, up = _row_counts(A)
+    cmax = int(max(lo.max(initial=0), up.max(initial=0)))
+    if cmax <= 8 and not cfg.generic_gs:
+        C = 2 if cmax <= 2 else (4 if cmax <= 4 else 8)
+        S = 3 + 2 * C
+        for R, D in LEAN_RINGS:
+            slot = R * 32 * (S + 1)
+            if D * slot * 8 <= cfg.ring_bytes:
+                return C, R, D, slot, S
+        R, D = LEAN_RINGS[-1]
+        return C, R, D, R * 32 * (S + 1), S
+    nnz_row = np.diff(A.indptr)
+    maxcnt = int(nnz_row.max()) if nnz_row.size else 1
+    S = 3 + 2 * max(maxcnt - 1, 0)
+    per_round = (32 * S + 32) * 8
+    best = (1, 2)
+    for R in (8, 4, 2, 1):
+        for D in (8, 4, 2):
+            if R * D * per_round <= cfg.ring_bytes and R * D <= cfg.rounds_in_flight:
+                if R * D > best[0] * best[1] or (R * D == best[0] * best[1] and D > best[1]):
+                    best = (R, D)
+    R, D = best
+    return 0, R, D, R * (32 * S + 32), S
+
+
 def gs_analyse(A, cfg=None):
-    """Chain/tile schedule of a CSR matrix for the sync-free GS sweep (host)."""
+    """Chain/tile schedule of a CSR matrix for the exact-order GS sweep (host).
+
+    Warps per tile and the shared window (position-major slots) are sized so
+    that window + per-warp rings + mbarriers fit cfg.smem_budget."""
     cfg = cfg or GpuConfig()
     A = as_csr(A)
     L = _lib.load()
     ip = np.ascontiguousarray(A.indptr, dtype=np.int32)
     ix = np.ascontiguousarray(A.indices, dtype=np.int32)
-    nch, nt, thr, win, dep = (ctypes.c_int() for _ in range(5))
     n = A.shape[0]
+    C, R, D, slot, S = _gs_ring(A, cfg)
+    ring_warp = D * (slot * 8 + 8)
+    T = max(1, min(256, cfg.max_threads))  # chains per tile (block <= 256 threads)
+    while True:
+        Tr = (T + 31) // 32 * 32
+        slots = (cfg.smem_budget - (Tr // 32) * ring_warp) // 8 - 2
+        if slots >= Tr * 16 or T <= 32:
+            break
+        T = max(32, T // 2)
+    if slots < 32:
+        raise ValueError(f"GS ring of {ring_warp} bytes per warp does not fit shared memory")
+    slots = min(slots, cfg.max_window)
+    max_chain = max(1, min(cfg.max_chain, slots // 32))
+    nch, nt, thr, win, dep = (ctypes.c_int() for _ in range(5))
     c_ip = ip.ctypes.data_as(ctypes.c_void_p)
     c_ix = ix.ctypes.data_as(ctypes.c_void_p)
-    _lib.check(L.mvamg_gs_analyse(n, c_ip, c_ix, cfg.max_chain, cfg.max_threads, cfg.max_window,
-                                  ctypes.byref(nch), ctypes.byref(nt), None, None, None, None,
-                                  None), "gs_analyse")
+    _lib.check(L.mvamg_gs_analyse(n, c_ip, c_ix, max_chain, T, slots, ctypes.byref(nch),
+                                  ctypes.byref(nt), None, None, None, None, None), "gs_analyse")
     cp = np.empty(nch.value + 1, dtype=np.int32)
     tp = np.empty(nt.value + 1, dtype=np.int32)
-    _lib.check(L.mvamg_gs_analyse(n, c_ip, c_ix, cfg.max_chain, cfg.max_threads, cfg.max_window,
-                                  ctypes.byref(nch), ctypes.byref(nt),
-                                  cp.ctypes.data_as(ctypes.c_void_p),
+    _lib.check(L.mvamg_gs_analyse(n, c_ip, c_ix, max_chain, T, slots, ctypes.byref(nch),
+                                  ctypes.byref(nt), cp.ctypes.data_as(ctypes.c_void_p),
                                   tp.ctypes.data_as(ctypes.c_void_p), ctypes.byref(thr),
                                   ctypes.byref(win), ctypes.byref(dep)), "gs_analyse")
-    return GsPlanHost(nch.value, nt.value, max(32, thr.value), win.value, dep.value, cp, tp)
+    plan = GsPlanHost(nch.value, nt.value, max(32, thr.value), max(win.value, 1), dep.value, cp, tp)
+    plan.lean_C, plan.R, plan.D = C, R, D
+    plan.smem_budget = cfg.smem_budget
+    return plan
+
+
+@dataclass
+class GsScheduleHost:
+    rec: np.ndarray        # uint64 words, round-major records
+    round_off: np.ndarray  # int32, nrounds + 1
+    tbase: np.ndarray      # int32, nwarps + 1
+    tile_wbase: np.ndarray # int32, ntiles + 1
+    perm: np.ndarray       # int32, n
+    nrounds: int
+    max_S: int
+
+
+def gs_schedule(A, plan, mode, R=None, uniform_S=0):
+    """Static round schedule of one GS sweep mode (0 forward from x=0, 1 forward, 2 backward)."""
+    A = as_csr(A)
+    L = _lib.load()
+    n = A.shape[0]
+    ip = np.ascontiguousarray(A.indptr, dtype=np.int32)
+    ix = np.ascontiguousarray(A.indices, dtype=np.int32)
+    v = np.ascontiguousarray(A.data, dtype=np.float64)
+    cp = np.ascontiguousarray(plan.chain_ptr, dtype=np.int32)
+    tp = np.ascontiguousarray(plan.tile_ptr, dtype=np.int32)
+    vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    nw, nr, nwarps, smax = ctypes.c_longlong(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    args = (n, vp(ip), vp(ix), vp(v), plan.ntiles, vp(cp), vp(tp), plan.window, int(mode),
+            int(R or plan.R), int(uniform_S), ctypes.byref(nw), ctypes.byref(nr), ctypes.byref(nwarps),
+            ctypes.byref(smax))
+    _lib.check(L.mvamg_gs_schedule(*args, None, None, None, None, None), "gs_schedule")
+    rec = np.zeros(max(2, nw.value), dtype=np.uint64)
+    round_off = np.empty(nr.value + 1, dtype=np.int32)
+    tbase = np.empty(nwarps.value + 1, dtype=np.int32)
+    tile_wbase = np.empty(plan.ntiles + 1, dtype=np.int32)
+    perm = np.empty(max(1, n), dtype=np.int32)
+    _lib.check(L.mvamg_gs_schedule(*args, vp(rec), vp(round_off), vp(tbase), vp(tile_wbase), vp(perm)),
+               "gs_schedule")
+    return GsScheduleHost(rec, round_off, tbase, tile_wbase, perm, nr.value, smax.value)
+
+
+class DeviceGsPlan:
+    """Schedule of one matrix on the device: chains/tiles plus, per sweep mode
+    (built on demand), the round-major records and the rhs buffer."""
+
+    def __init__(self, A, cfg=None, plan=None):
+        self.A = as_csr(A)
+        self.cfg = cfg or GpuConfig()
+        self.plan = plan or gs_analyse(self.A, self.cfg)
+        self.chain_ptr = to_device(self.plan.chain_ptr, np.int32)
+        self.tile_ptr = to_device(self.plan.tile_ptr, np.int32)
+        self.modes = {}
+        self._csr = None
+
+    def mode(self, m):
+        """Device schedule dict for mode m."""
+        if m not in self.modes:
+            import torch
+
+            p = self.plan
+            if p.lean_C > 0 and m != 1:
+                S = 3 + 2 * p.lean_C
+                R, D = p.R, p.D
+                h = gs_schedule(self.A, p, m, R=R, uniform_S=S)
+                rec_words_max = R * 32 * S
+                slot_words = rec_words_max + R * 32
+                lean = p.lean_C
+            else:
+                # generic kernel: pick the deepest ring that fits beside the window
+                h = gs_schedule(self.A, p, m, R=1)
+                S = h.max_S
+                avail = p.smem_budget - 8 * ((p.window + 1) & ~1)
+                R, D = 1, 2
+                for R_, D_ in ((8, 4), (4, 4), (4, 2), (2, 4), (2, 2), (1, 4), (1, 2)):
+                    if (p.threads // 32) * D_ * (R_ * (32 * S + 32) + 1) * 8 <= avail:
+                        R, D = R_, D_
+                        break
+                if R > 1:
+                    h = gs_schedule(self.A, p, m, R=R)
+                    S = h.max_S
+                rec_words_max = R * 32 * S
+                slot_words = rec_words_max + R * 32
+                slot_words += slot_words & 1
+                lean = 0
+            self.modes[m] = dict(
+                rec=to_device(h.rec.view(np.int64)), round_off=to_device(h.round_off),
+                tbase=to_device(h.tbase), tile_wbase=to_device(h.tile_wbase), perm=to_device(h.perm),
+                tperm=torch.empty(max(32, 32 * h.nrounds), dtype=torch.float64, device="cuda"),
+                R=R, D=D, lean_C=lean, slot_words=slot_words, rec_words_max=rec_words_max,
+                nrounds=h.nrounds, max_S=h.max_S)
+        return self.modes[m]
+
+    def nbytes(self, m):
+        s = self.mode(m)
+        return s["rec"].numel() * 8 + s["round_off"].numel() * 4 + s["perm"].numel() * 4
+
+    def sweep(self, direction, b, x_old, x_new, ws, stream=None, work=None):
+        """x_new = one GS sweep (direction 0 fwd / 1 bwd) from x_old (None: zero)."""
+        m = (0 if x_old is None else 1) if direction == 0 else 2
+        sch = self.mode(m)
+        p = self.plan
+        if self._csr is None:
+            self._csr = DeviceCSR(self.A)
+        _lib.check(_lib.load().mvamg_gs_sweep_f64(
+            direction, self.A.shape[0], *self._csr.ptrs(), ptr(sch["rec"]), ptr(sch["round_off"]),
+            ptr(sch["tbase"]), ptr(sch["tile_wbase"]), ptr(sch["perm"]), ptr(sch["tperm"]), sch["R"],
+            sch["D"], sch["lean_C"], sch["slot_words"], sch["rec_words_max"], p.ntiles, ptr(self.chain_ptr), ptr(self.tile_ptr),
+            p.threads, p.window, ptr(b), ptr(x_old), ptr(x_new), ptr(ws), stream or stream_handle()),
+            "gs_sweep")

@@ -62,23 +62,15 @@ def _dev(a, dtype=np.float64):
 
 def _gs_gpu(mv, A, b, x_old, direction, zero, cfg=None):
     import torch
-    from paper_1907_04417_b200 import _lib
-    from paper_1907_04417_b200.device import DeviceCSR, gs_analyse, ptr, stream_handle
+    from paper_1907_04417_b200.device import DeviceGsPlan
 
     A = sp.csr_matrix(A)
-    plan = gs_analyse(A, cfg)
-    dA = DeviceCSR(A)
-    d = A.diagonal()
-    dd, rd = _dev(d), _dev(1.0 / d)
-    cp, tp = _dev(plan.chain_ptr, np.int32), _dev(plan.tile_ptr, np.int32)
+    gp = DeviceGsPlan(A, cfg)
     bd = _dev(b)
-    xo = _dev(x_old) if x_old is not None else None
+    xo = None if zero else _dev(x_old)
     xn = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
     ws = torch.zeros(8, dtype=torch.int32, device="cuda")
-    _lib.check(_lib.load().mvamg_gs_sweep_f64(
-        0 if direction == "forward" else 1, int(zero), A.shape[0], *dA.ptrs(), ptr(dd), ptr(rd),
-        plan.ntiles, ptr(cp), ptr(tp), plan.threads, plan.window, ptr(bd), ptr(xo), ptr(xn),
-        ptr(ws), stream_handle()), "gs")
+    gp.sweep(0 if direction == "forward" else 1, bd, xo, xn, ws)
     torch.cuda.synchronize()
     assert int(ws[1].item()) == 0, "GS timeout"
     return xn.cpu().numpy()
@@ -151,8 +143,10 @@ def _structures():
     yield "dense", random_spd_csr(60, density=0.9, seed=9)
 
 
-@pytest.mark.parametrize("cfg", [None, dict(max_chain=3, max_threads=32, max_window=17),
-                                 dict(max_chain=64, max_threads=64, max_window=1)])
+@pytest.mark.parametrize("cfg", [None, dict(max_chain=3, max_threads=32, max_window=97),
+                                 dict(max_chain=64, max_threads=64, max_window=40),
+                                 dict(max_threads=256, ring_bytes=4096),
+                                 dict(generic_gs=True), dict(generic_gs=True, max_chain=5, max_threads=40)])
 def test_gs_structures_bit_exact(mv, cfg):
     """Chains, tiles and the smem window do not change a single bit."""
     config = mv.GpuConfig(**cfg) if cfg else None
