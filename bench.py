@@ -296,12 +296,21 @@ def run_b200(args, world, rank, local):
         tc += e0.elapsed_time(e1) / 1e3
     t_cycle = tc / reps
     lv = op.level_dev[0]
-    gp = lv["gs"]
     xn = torch.empty(n, dtype=torch.float64, device="cuda")
     ws = torch.zeros(8, dtype=torch.int32, device="cuda")
+    if lv.get("levels"):
+        small = lv["levels"][0]
+        gs_kernel = "gs_level_kernel (single-CTA level-set sweep) level 0, forward from x=0 (+prepare)"
 
-    def gs_once():
-        gp.sweep(0, r_dev, None, xn, ws, s)
+        def gs_once():
+            small.sweep(r_dev, None, xn, ws, s)
+    else:
+        gp = lv["gs"]
+        gs_kernel = ("gs_lean_kernel" if gp.plan.lean_C else "gs_sweep_kernel") + \
+            " level 0, forward from x=0 (+prepare)"
+
+        def gs_once():
+            gp.sweep(0, r_dev, None, xn, ws, s)
 
     for _ in range(3):
         gs_once()
@@ -338,7 +347,7 @@ def run_b200(args, world, rank, local):
                   "frac": cyc_bytes / t_cycle / 1e9 / peak},
         "pcg_model": {"bytes_per_iteration": it_bytes, "gbs": it_bytes * n_iters / t_solve / 1e9,
                       "frac": it_bytes * n_iters / t_solve / 1e9 / peak},
-        "roofline": {"bound": "hbm", "kernel": "gs_sweep_kernel<fwd,zero> level 0 (+sentinel prep)",
+        "roofline": {"bound": "hbm", "kernel": gs_kernel,
                      "achieved": gs_gbs, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": gs_gbs / peak, "traffic": None, "algorithmic_bytes": gs_bytes,
                      "ms": t_gs * 1e3},

@@ -44,6 +44,9 @@ SIGNATURES = [
                                _PI, _P, _P, _P, _P, _P]),
     ("mvamg_gs_sweep_f64", _I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P,
                                 _I, _I, _P, _P, _P, _P, _P]),
+    ("mvamg_gs_levels", _I, [_I, _P, _P, _P, _I, _PI, ctypes.POINTER(_LL), _PI, _PI, _P, _P, _P, _P, _P]),
+    ("mvamg_gs_level_sweep_f64", _I, [_I, _I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P,
+                                      _P, _P, _P]),
     ("mvamg_dense_gemv_f64", _I, [_I, _P, _P, _P, _P]),
     ("mvamg_dot_f64", _I, [_I, _P, _P, _P, _P, _P]),
     ("mvamg_dot_ws_bytes", _I, []),
@@ -51,6 +54,7 @@ SIGNATURES = [
     ("mvamg_hierarchy_destroy", _I, [_P]),
     ("mvamg_hierarchy_set_level", _I, [_P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _I]),
     ("mvamg_hierarchy_set_gs_schedule", _I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I]),
+    ("mvamg_hierarchy_set_gs_levels", _I, [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_hierarchy_set_transfer", _I, [_P, _I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_hierarchy_set_coarse", _I, [_P, _P]),
     ("mvamg_hierarchy_workspace_bytes", _I, [_P, ctypes.POINTER(_LL)]),

@@ -536,3 +536,116 @@ __global__ void __launch_bounds__(256) gs_prepare_kernel(int n, const int* __res
 }
 
 }  // namespace mvamg
+
+namespace mvamg {
+
+// ---------------------------------------------------------------------------
+// Small levels (n <= ~24k rows): one CTA, x resident in shared memory, rows in
+// level-set order of the sweep's dependency DAG with one __syncthreads per
+// level.  Shared x starts from x_old (or zero), so every entry of a row reads
+// x[j] from shared memory: lower neighbours were finished in earlier levels,
+// upper neighbours (same sweep, later levels) still hold x_old -- exactly the
+// values the serial loop reads.  Each level's rows are contiguous in the
+// host-built layout, so the whole CTA stages level l+2 with coalesced cp.async
+// while it computes level l.
+struct GsLevelRow {  // 32 bytes, level order
+  int row, estart, cnt, pad;
+  double diag, rdiag;
+};
+struct GsLevelEntry {  // 16 bytes, CSR order within the row
+  double coef;
+  int src, pad;
+};
+
+struct GsLevelArgs {
+  int n, nlev, zero_init;
+  int max_rows, max_ents;        // per level
+  const int* lev_ptr;            // nlev + 1, level-order row ranges
+  const int* lev_eptr;           // nlev + 1, entry ranges
+  const GsLevelRow* rows;        // n
+  const GsLevelEntry* ents;      // total entries
+  const double* tperm;           // right-hand side in level order
+  const double* xold;
+  double* xnew;
+};
+
+__device__ __forceinline__ void cp_async16(unsigned dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(1024, 1) gs_level_kernel(GsLevelArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* x = reinterpret_cast<double*>(smem);
+  const int xw = (a.n + 1) & ~1;  // doubles, keeps 16-byte alignment
+  // per buffer: rows (32 B each), entries (16 B each), rhs (8 B each + 2 for alignment slack)
+  const int rows_b = a.max_rows * 32, ents_b = a.max_ents * 16, rhs_b = (a.max_rows + 2) * 8;
+  const int buf_b = rows_b + ents_b + ((rhs_b + 15) & ~15);
+  unsigned char* bufs = smem + 8 * xw;
+  const unsigned bufs_s = (unsigned)__cvta_generic_to_shared(bufs);
+  const int T = blockDim.x, tid = threadIdx.x;
+  // x <- x_old or 0
+  for (int i = tid; i < a.n; i += T) x[i] = a.zero_init ? 0.0 : __ldg(a.xold + i);
+  auto stage = [&](int l) {
+    if (l < a.nlev) {
+      const int b = l % 3;
+      const unsigned base = bufs_s + (unsigned)(b * buf_b);
+      const int r0 = __ldg(a.lev_ptr + l), r1 = __ldg(a.lev_ptr + l + 1);
+      // rows
+      const char* src = reinterpret_cast<const char*>(a.rows + r0);
+      for (int c = tid; c < (r1 - r0) * 2; c += T) cp_async16(base + 16u * c, src + 16 * c);
+      // entries
+      const int e0 = __ldg(a.lev_eptr + l), e1 = __ldg(a.lev_eptr + l + 1);
+      const char* esrc = reinterpret_cast<const char*>(a.ents + e0);
+      for (int c = tid; c < e1 - e0; c += T) cp_async16(base + rows_b + 16u * c, esrc + 16 * c);
+      // rhs (aligned superset)
+      const int t0 = r0 & ~1, t1 = (r1 + 1) & ~1;
+      const char* tsrc = reinterpret_cast<const char*>(a.tperm + t0);
+      for (int c = tid; c < (t1 - t0) / 2; c += T) cp_async16(base + rows_b + ents_b + 16u * c, tsrc + 16 * c);
+    }
+    cp_async_commit();
+  };
+  stage(0);
+  stage(1);
+  for (int l = 0; l < a.nlev; ++l) {
+    cp_async_wait<1>();  // this thread's copies of level l have landed
+    __syncthreads();     // ... everyone's; and level l-1's x writes are visible
+    stage(l + 2);
+    const int b = l % 3;
+    const unsigned char* base = bufs + b * buf_b;
+    const GsLevelRow* rows = reinterpret_cast<const GsLevelRow*>(base);
+    const GsLevelEntry* ents = reinterpret_cast<const GsLevelEntry*>(base + rows_b);
+    const double* rhs = reinterpret_cast<const double*>(base + rows_b + ents_b);
+    const int r0 = __ldg(a.lev_ptr + l), r1 = __ldg(a.lev_ptr + l + 1);
+    const int e0 = __ldg(a.lev_eptr + l), toff = r0 & 1;
+    for (int r = tid; r < r1 - r0; r += T) {
+      const GsLevelRow m = rows[r];
+      double s = rhs[toff + r];
+      const GsLevelEntry* e = ents + (m.estart - e0);
+      // chunks of 8: all loads and products first (independent), then the
+      // subtractions in CSR order
+      for (int k0 = 0; k0 < m.cnt; k0 += 8) {
+        double p[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          p[u] = 0.0;
+          if (k0 + u < m.cnt) {
+            const GsLevelEntry en = e[k0 + u];
+            p[u] = __dmul_rn(en.coef, x[en.src]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (k0 + u < m.cnt) s = __dsub_rn(s, p[u]);
+      }
+      x[m.row] = div_rn_markstein(s, m.diag, m.rdiag);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  for (int i = tid; i < a.n; i += T) a.xnew[i] = x[i];
+}
+
+}  // namespace mvamg

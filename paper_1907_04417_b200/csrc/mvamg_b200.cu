@@ -125,6 +125,18 @@ struct GsList {
   int R = 1, D = 2, slot_words = 0, rec_words_max = 0;
 };
 
+// Level-set schedule of one sweep mode for the single-CTA small-level kernel
+// (0 forward from x = 0, 1 forward, 2 backward from x = 0, 3 backward).
+struct GsLevels {
+  const int* lev_ptr = nullptr;
+  const int* lev_eptr = nullptr;
+  const GsLevelRow* rows = nullptr;
+  const GsLevelEntry* ents = nullptr;
+  const int* perm = nullptr;
+  double* tperm = nullptr;
+  int nlev = 0, max_rows = 0, max_ents = 0, threads = 256;
+};
+
 struct Smoother {
   int kind, sweeps;
   double omega;
@@ -241,6 +253,47 @@ int launch_gs(bool fwd, const Csr& A, const GsList& ls, const GsPlan& p, const d
   return 0;
 }
 
+size_t gs_level_smem(int n, const GsLevels& g) {
+  const size_t xw = (size_t)((n + 1) & ~1);
+  const size_t buf = (size_t)g.max_rows * 32 + (size_t)g.max_ents * 16 + (((size_t)(g.max_rows + 2) * 8 + 15) & ~(size_t)15);
+  return xw * 8 + 3 * buf;
+}
+
+bool g_level_attr = false;
+int launch_gs_levels(const Csr& A, const GsLevels& g, bool zero, const double* b, const double* xold,
+                     double* xnew, int* ticket, cudaStream_t s) {
+  const int n = A.n;
+  if (n == 0) return 0;
+  if (!g_level_attr) {
+    g_level_attr = true;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(gs_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+  }
+  const size_t smem = gs_level_smem(n, g);
+  if (smem > (size_t)g_max_dyn_smem) return fail(MVAMG_E_ARG, "gs levels: shared memory plan too large");
+  // right-hand side in level order (no fold: x_old is read from shared memory)
+  gs_prepare_kernel<<<grid_for(n), 256, 0, s>>>(n, A.ip, A.ix, A.v, b, xold, g.perm, g.tperm, xnew,
+                                                ticket, 0);
+  GsLevelArgs a;
+  a.n = n;
+  a.nlev = g.nlev;
+  a.zero_init = zero ? 1 : 0;
+  a.max_rows = g.max_rows;
+  a.max_ents = g.max_ents;
+  a.lev_ptr = g.lev_ptr;
+  a.lev_eptr = g.lev_eptr;
+  a.rows = g.rows;
+  a.ents = g.ents;
+  a.tperm = g.tperm;
+  a.xold = xold;
+  a.xnew = xnew;
+  gs_level_kernel<<<1, g.threads, smem, s>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 }  // namespace
 
 // ============================================================================
@@ -252,6 +305,7 @@ struct Level {
   const double* rdiag = nullptr;
   GsPlan plan;
   GsList gl[3];
+  GsLevels glv[4];  // small-level single-CTA schedules (used when set)
   Csr P, R;  // valid for k < L-1
   double *xa = nullptr, *xb = nullptr, *t = nullptr, *r = nullptr, *z = nullptr;
   double *fr = nullptr, *fx = nullptr, *fp[2] = {nullptr, nullptr}, *fap[2] = {nullptr, nullptr};
@@ -315,8 +369,13 @@ struct mvamg_hierarchy {
                                                        sp.omega, x_cur, out);
       } else {
         bool fwd = sp.kind == MVAMG_GS_FORWARD;
-        int mode = fwd ? (x_cur == nullptr ? 0 : 1) : 2;
-        st = launch_gs(fwd, l.A, l.gl[mode], l.plan, b, x_cur, out, ticket, status_ptr(), s);
+        int lmode = (fwd ? 0 : 2) + (x_cur == nullptr ? 0 : 1);
+        if (l.glv[lmode].rows) {
+          st = launch_gs_levels(l.A, l.glv[lmode], x_cur == nullptr, b, x_cur, out, ticket, s);
+        } else {
+          int mode = fwd ? (x_cur == nullptr ? 0 : 1) : 2;
+          st = launch_gs(fwd, l.A, l.gl[mode], l.plan, b, x_cur, out, ticket, status_ptr(), s);
+        }
         if (st) return st;
       }
       x_cur = out;
@@ -816,6 +875,110 @@ int mvamg_gs_sweep_f64(int direction, int n, const int* indptr, const int* indic
   GsPlan p;
   p.ntiles = ntiles; p.threads = threads; p.window = window; p.chain_ptr = chain_ptr; p.tile_ptr = tile_ptr;
   return launch_gs(direction == 0, A, ls, p, b, x_old, x_new, ws, ws + 1, (cudaStream_t)stream);
+}
+
+int mvamg_gs_levels(int n, const int* indptr, const int* indices, const double* data, int mode,
+                    int* nlev, long long* nents, int* max_rows, int* max_ents, int* lev_ptr,
+                    int* lev_eptr, void* rows_out, void* ents_out, int* perm) {
+  if (n < 0 || !indptr || !nlev || !nents || !max_rows || !max_ents || mode < 0 || mode > 3)
+    return fail(MVAMG_E_ARG, "gs_levels: bad arguments");
+  const bool fwd = mode < 2, zero = (mode % 2) == 0;
+  auto keep = [&](int i, int j) {
+    if (j == i) return false;
+    if (!zero) return true;
+    return fwd ? j < i : j > i;
+  };
+  std::vector<int> lvl(n > 0 ? n : 1, 0);
+  int nl = 0;
+  for (int q = 0; q < n; ++q) {
+    const int i = fwd ? q : n - 1 - q;
+    int m = 0;
+    for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+      const int j = indices[k];
+      if (fwd ? j < i : j > i) m = std::max(m, lvl[j] + 1);
+    }
+    lvl[i] = m;
+    nl = std::max(nl, m + 1);
+  }
+  std::vector<int> cnt_l(nl + 1, 0), ents_l(nl + 1, 0);
+  std::vector<int> rowcnt(n > 0 ? n : 1, 0);
+  for (int i = 0; i < n; ++i) {
+    int c = 0;
+    for (int k = indptr[i]; k < indptr[i + 1]; ++k) c += keep(i, indices[k]);
+    rowcnt[i] = c;
+    cnt_l[lvl[i] + 1] += 1;
+    ents_l[lvl[i] + 1] += c;
+  }
+  int mr = 0, me = 0;
+  for (int l = 0; l < nl; ++l) {
+    mr = std::max(mr, cnt_l[l + 1]);
+    me = std::max(me, ents_l[l + 1]);
+  }
+  for (int l = 0; l < nl; ++l) {
+    cnt_l[l + 1] += cnt_l[l];
+    ents_l[l + 1] += ents_l[l];
+  }
+  *nlev = nl;
+  *nents = ents_l[nl];
+  *max_rows = mr;
+  *max_ents = me;
+  if (!rows_out) return 0;
+  std::copy(cnt_l.begin(), cnt_l.end(), lev_ptr);
+  std::copy(ents_l.begin(), ents_l.end(), lev_eptr);
+  GsLevelRow* R = static_cast<GsLevelRow*>(rows_out);
+  GsLevelEntry* E = static_cast<GsLevelEntry*>(ents_out);
+  std::vector<int> fillr(cnt_l.begin(), cnt_l.end() - 1), fille(ents_l.begin(), ents_l.end() - 1);
+  for (int i = 0; i < n; ++i) {  // rows of a level in ascending index order
+    const int l = lvl[i];
+    const int pos = fillr[l]++;
+    GsLevelRow& r = R[pos];
+    r.row = i;
+    r.estart = fille[l];
+    r.cnt = rowcnt[i];
+    r.pad = 0;
+    double dg = 0.0;
+    for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+      const int j = indices[k];
+      if (j == i) dg = data[k];
+      if (!keep(i, j)) continue;
+      GsLevelEntry& e = E[fille[l]++];
+      e.coef = data[k];
+      e.src = j;
+      e.pad = 0;
+    }
+    r.diag = dg;
+    r.rdiag = 1.0 / dg;
+    if (perm) perm[i] = pos;
+  }
+  return 0;
+}
+
+int mvamg_gs_level_sweep_f64(int direction, int n, const int* indptr, const int* indices,
+                             const double* data, int nlev, int max_rows, int max_ents, int threads,
+                             const int* lev_ptr, const int* lev_eptr, const void* rows,
+                             const void* ents, const int* perm, double* tperm, const double* b,
+                             const double* x_old, double* x_new, int* ws, void* stream) {
+  if (threads < 32 || threads > 1024 || threads % 32) return fail(MVAMG_E_ARG, "gs levels: bad thread count");
+  Csr A;
+  A.n = n; A.ip = indptr; A.ix = indices; A.v = data;
+  GsLevels g;
+  g.lev_ptr = lev_ptr; g.lev_eptr = lev_eptr; g.rows = static_cast<const GsLevelRow*>(rows);
+  g.ents = static_cast<const GsLevelEntry*>(ents); g.perm = perm; g.tperm = tperm;
+  g.nlev = nlev; g.max_rows = max_rows; g.max_ents = max_ents; g.threads = threads;
+  (void)direction;  // encoded in the schedule
+  set_kernel_attrs();
+  return launch_gs_levels(A, g, x_old == nullptr, b, x_old, x_new, ws, (cudaStream_t)stream);
+}
+
+int mvamg_hierarchy_set_gs_levels(mvamg_hierarchy* h, int k, int mode, int nlev, int max_rows,
+                                  int max_ents, int threads, const int* lev_ptr, const int* lev_eptr,
+                                  const void* rows, const void* ents, const int* perm, double* tperm) {
+  if (!h || k < 0 || k >= h->L || mode < 0 || mode > 3) return fail(MVAMG_E_ARG, "set_gs_levels: bad index");
+  GsLevels& g = h->lv[k].glv[mode];
+  g.lev_ptr = lev_ptr; g.lev_eptr = lev_eptr; g.rows = static_cast<const GsLevelRow*>(rows);
+  g.ents = static_cast<const GsLevelEntry*>(ents); g.perm = perm; g.tperm = tperm;
+  g.nlev = nlev; g.max_rows = max_rows; g.max_ents = max_ents; g.threads = threads;
+  return 0;
 }
 
 int mvamg_dense_gemv_f64(int n, const double* inv, const double* r, double* z, void* stream) {

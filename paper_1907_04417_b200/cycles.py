@@ -16,7 +16,8 @@ import scipy.linalg
 import scipy.sparse.linalg as spla
 
 from . import _lib
-from .device import DeviceCSR, DeviceGsPlan, GpuConfig, as_csr, ptr, stream_handle, to_device, torch_cuda
+from .device import (DeviceCSR, DeviceGsLevels, DeviceGsPlan, GpuConfig, as_csr, level_gs_fits, ptr,
+                     stream_handle, to_device, torch_cuda)
 from .exceptions import NotSpdError
 
 GS_FORWARD = "gauss_seidel_forward"
@@ -111,6 +112,21 @@ class GpuMultigridOperator:
                     modes.add(1)
         return sorted(modes)
 
+    def _gs_level_modes(self):
+        """Level-set sweep modes the cycle needs (0 fwd x=0, 1 fwd, 2 bwd x=0, 3 bwd)."""
+        modes = set()
+        for spec, first_zero in ((self.pre_smoother, True), (self.post_smoother, False)):
+            if spec.kind == WEIGHTED_JACOBI or spec.sweeps == 0:
+                continue
+            base = 0 if spec.kind == GS_FORWARD else 2
+            if first_zero:
+                modes.add(base)
+                if spec.sweeps > 1:
+                    modes.add(base + 1)
+            else:
+                modes.add(base + 1)
+        return sorted(modes)
+
     def _init_plain(self, A):
         """Single-level handle used only for its matrix (pcg with precond=None)."""
         self.matrices = [as_csr(A)]
@@ -142,11 +158,25 @@ class GpuMultigridOperator:
             dA = DeviceCSR(A)
             self._dA.append(dA)
             if k < nl - 1:
-                gp = DeviceGsPlan(A, self.config)
-                self.gs_plans.append(gp.plan)
-                self.level_dev.append(dict(A=dA, gs=gp, plan=gp.plan))
                 dd = to_device(self.diagonals[k], np.float64)
                 self._keep.append(dd)
+                small = None
+                if level_gs_fits(A, self.config):
+                    small = {m: DeviceGsLevels(A, m) for m in self._gs_level_modes()}
+                    if any(s.smem_bytes() > self.config.smem_limit for s in small.values()):
+                        small = None
+                if small is not None:
+                    # single-CTA level-set sweeps; no wavefront schedule needed
+                    self.gs_plans.append(None)
+                    self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=small))
+                    _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
+                                                           None, 0, None, None, 32, 0), "set_level")
+                    for m, s in small.items():
+                        _lib.check(L.mvamg_hierarchy_set_gs_levels(h, k, m, *s.args()), "set_gs_levels")
+                    continue
+                gp = DeviceGsPlan(A, self.config)
+                self.gs_plans.append(gp.plan)
+                self.level_dev.append(dict(A=dA, gs=gp, plan=gp.plan, levels=None))
                 _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
                                                        None, gp.plan.ntiles, ptr(gp.chain_ptr),
                                                        ptr(gp.tile_ptr), gp.plan.threads,

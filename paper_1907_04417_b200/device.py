@@ -68,6 +68,9 @@ class GpuConfig:
     ring_bytes: int = 48 * 1024     # TMA ring size per warp (D slots of R rounds)
     rounds_in_flight: int = 16      # rounds of records the ring keeps ahead (generic kernel)
     generic_gs: bool = False        # force the generic GS kernel (tests / diagnostics)
+    level_gs_max_rows: int = 24576  # levels up to this size may use the single-CTA level-set sweep
+    force_level_gs: bool = False    # use it for every small level (tests / diagnostics)
+    smem_limit: int = 227 * 1024 - 1024
 
 
 class DeviceCSR:
@@ -290,3 +293,74 @@ class DeviceGsPlan:
             sch["D"], sch["lean_C"], sch["slot_words"], sch["rec_words_max"], p.ntiles, ptr(self.chain_ptr), ptr(self.tile_ptr),
             p.threads, p.window, ptr(b), ptr(x_old), ptr(x_new), ptr(ws), stream or stream_handle()),
             "gs_sweep")
+
+
+LEVEL_ROW_DTYPE = np.dtype([("row", "<i4"), ("estart", "<i4"), ("cnt", "<i4"), ("pad", "<i4"),
+                            ("diag", "<f8"), ("rdiag", "<f8")])
+LEVEL_ENT_DTYPE = np.dtype([("coef", "<f8"), ("src", "<i4"), ("pad", "<i4")])
+
+
+class DeviceGsLevels:
+    """Single-CTA level-set GS schedule of one small matrix and sweep mode
+    (0 fwd from x=0, 1 fwd, 2 bwd from x=0, 3 bwd), resident on the device."""
+
+    def __init__(self, A, mode):
+        import torch
+
+        A = as_csr(A)
+        L = _lib.load()
+        n = A.shape[0]
+        ip = np.ascontiguousarray(A.indptr, dtype=np.int32)
+        ix = np.ascontiguousarray(A.indices, dtype=np.int32)
+        v = np.ascontiguousarray(A.data, dtype=np.float64)
+        vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        nlev, mr, me = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        ne = ctypes.c_longlong()
+        _lib.check(L.mvamg_gs_levels(n, vp(ip), vp(ix), vp(v), int(mode), ctypes.byref(nlev),
+                                     ctypes.byref(ne), ctypes.byref(mr), ctypes.byref(me), None, None,
+                                     None, None, None), "gs_levels")
+        lev_ptr = np.empty(nlev.value + 1, dtype=np.int32)
+        lev_eptr = np.empty(nlev.value + 1, dtype=np.int32)
+        rows = np.zeros(max(1, n), dtype=LEVEL_ROW_DTYPE)
+        ents = np.zeros(max(1, ne.value), dtype=LEVEL_ENT_DTYPE)
+        perm = np.empty(max(1, n), dtype=np.int32)
+        _lib.check(L.mvamg_gs_levels(n, vp(ip), vp(ix), vp(v), int(mode), ctypes.byref(nlev),
+                                     ctypes.byref(ne), ctypes.byref(mr), ctypes.byref(me), vp(lev_ptr),
+                                     vp(lev_eptr), vp(rows), vp(ents), vp(perm)), "gs_levels")
+        self.n, self.mode = n, mode
+        self.nlev, self.max_rows, self.max_ents = nlev.value, max(1, mr.value), max(1, me.value)
+        self.threads = int(min(1024, max(64, (self.max_rows + 31) // 32 * 32)))
+        self.lev_ptr = to_device(lev_ptr)
+        self.lev_eptr = to_device(lev_eptr)
+        self.rows = to_device(rows.view(np.uint8))
+        self.ents = to_device(ents.view(np.uint8))
+        self.perm = to_device(perm)
+        self.tperm = torch.empty(max(2, n + 2), dtype=torch.float64, device="cuda")
+        self._csr = DeviceCSR(A)
+
+    def smem_bytes(self):
+        xw = (self.n + 1) & ~1
+        buf = self.max_rows * 32 + self.max_ents * 16 + ((self.max_rows + 2) * 8 + 15) // 16 * 16
+        return xw * 8 + 3 * buf
+
+    def args(self):
+        return (self.nlev, self.max_rows, self.max_ents, self.threads, ptr(self.lev_ptr), ptr(self.lev_eptr),
+                ptr(self.rows), ptr(self.ents), ptr(self.perm), ptr(self.tperm))
+
+    def sweep(self, b, x_old, x_new, ws, stream=None):
+        _lib.check(_lib.load().mvamg_gs_level_sweep_f64(
+            0 if self.mode < 2 else 1, self.n, *self._csr.ptrs(), *self.args(), ptr(b), ptr(x_old),
+            ptr(x_new), ptr(ws), stream or stream_handle()), "gs_level_sweep")
+
+
+def level_gs_fits(A, cfg):
+    """Whether the small-level single-CTA sweep is the better schedule for A:
+    small enough for shared memory, and with rows too long for the lean
+    wavefront kernel (the wavefront wins on short-row grid levels)."""
+    n = A.shape[0]
+    if n > cfg.level_gs_max_rows or cfg.generic_gs:
+        return False
+    if cfg.force_level_gs:
+        return True
+    lo, up = _row_counts(as_csr(A))
+    return int(max(lo.max(initial=0), up.max(initial=0))) > 8

@@ -166,6 +166,37 @@ def test_gs_structures_bit_exact(mv, cfg):
             assert np.array_equal(got, want), (name, direction, "zero")
 
 
+def _gs_level_gpu(A, b, x_old, direction, zero):
+    import torch
+    from paper_1907_04417_b200.device import DeviceGsLevels
+
+    A = sp.csr_matrix(A)
+    mode = (0 if direction == "forward" else 2) + (0 if zero else 1)
+    lv = DeviceGsLevels(A, mode)
+    xn = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+    ws = torch.zeros(8, dtype=torch.int32, device="cuda")
+    lv.sweep(_dev(b), None if zero else _dev(x_old), xn, ws)
+    torch.cuda.synchronize()
+    return xn.cpu().numpy()
+
+
+def test_gs_level_kernel_bit_exact(mv, c1):
+    """The single-CTA level-set sweep (small levels) on every structure."""
+    rng = np.random.default_rng(11)
+    mats = c1[1]
+    cases = list(_structures()) + [("c1_l1", mats[1]), ("c1_l2", mats[2]), ("c1_l0", mats[0])]
+    for name, A in cases:
+        n = A.shape[0]
+        b = rng.standard_normal(n)
+        x0 = rng.standard_normal(n)
+        for direction in ("forward", "backward"):
+            for zero in (True, False):
+                want = np.zeros(n) if zero else x0.copy()
+                oracle_gs(A, b, want, direction)
+                got = _gs_level_gpu(A, b, x0, direction, zero)
+                assert np.array_equal(got, want), (name, direction, zero)
+
+
 def test_gs_hand_recurrence(mv):
     # pkg/tests/test_cycles.py:30-38
     A = laplacian_1d(3)
@@ -181,6 +212,15 @@ def test_vcycle_matches_reference(c1):
         assert rel(z, d[key_out]) <= TOL_CYCLE
         assert rel(z, cpu.apply(d[key_in])) <= TOL_CYCLE
     assert rel(op.error_propagation(d["x2"]), d["errprop_x2"]) <= TOL_CYCLE
+
+
+@pytest.mark.parametrize("cfg", [dict(force_level_gs=True), dict(level_gs_max_rows=0),
+                                 dict(generic_gs=True)])
+def test_vcycle_schedules_agree(mv, c1, cfg):
+    """Level-set, wavefront and generic GS schedules give the same cycle."""
+    d, mats, pros, op, _ = c1
+    other = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(**cfg))
+    assert np.array_equal(other.apply(d["b"]), op.apply(d["b"]))
 
 
 def test_vcycle_deterministic(c1):

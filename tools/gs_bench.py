@@ -36,6 +36,33 @@ def main():
     stream = torch.cuda.current_stream()
     for k, lv in enumerate(op.level_dev):
         A = mats[k]
+        if lv.get("levels") is not None:
+            import torch as _t
+            n = A.shape[0]
+            bb = _t.randn(n, dtype=_t.float64, device="cuda")
+            xo = _t.randn(n, dtype=_t.float64, device="cuda")
+            xn = _t.empty(n, dtype=_t.float64, device="cuda")
+            ws = _t.zeros(8, dtype=_t.int32, device="cuda")
+            res = {}
+            for m, s in sorted(lv["levels"].items()):
+                def once():
+                    s.sweep(bb, None if m % 2 == 0 else xo, xn, ws)
+                for _ in range(3):
+                    once()
+                for mode in ("warm", "cold"):
+                    tot = 0.0
+                    for _ in range(20):
+                        if mode == "cold":
+                            flush.fill_(1.0)
+                        e0 = _t.cuda.Event(enable_timing=True); e1 = _t.cuda.Event(enable_timing=True)
+                        e0.record(stream); once(); e1.record(stream); e1.synchronize()
+                        tot += e0.elapsed_time(e1)
+                    res[(m, mode)] = tot / 20 * 1e3
+            desc = " | ".join(f"mode{m} warm {res[(m,'warm')]:.1f}us cold {res[(m,'cold')]:.1f}us" for m in sorted(lv["levels"]))
+            s0 = next(iter(lv["levels"].values()))
+            print(f"level {k}: n={n} nnz={A.nnz} LEVEL-SET nlev={s0.nlev} thr={s0.threads} | {desc} | "
+                  f"{res[(0,'warm')]*1e3/s0.nlev:.0f} ns/level", flush=True)
+            continue
         n = A.shape[0]
         plan = lv["plan"]
         dA = lv["A"]
