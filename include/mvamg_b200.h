@@ -147,6 +147,18 @@ int mvamg_dense_gemv_f64(int n, const double* inv, const double* r, double* z, v
 int mvamg_dot_f64(int n, const double* x, const double* y, double* result, void* ws, void* stream);
 int mvamg_dot_ws_bytes(void);
 
+/* ---- setup helpers (host) --------------------------------------------------- */
+/* Greedy vertex-disjoint acceptance of edges in the given sorted order
+ * (pkg/src/mvamg/_kernels.py:41-61): partner[v] = matched vertex or -1. */
+int mvamg_greedy_match(long long ne, const long long* ei, const long long* ej, int n, long long* partner,
+                       long long* pair_i, long long* pair_j, long long* npairs);
+/* Batched one-sided Jacobi thin SVD of stacked row-major blocks
+ * (pkg/src/mvamg/svd.py:17-55, _kernels.py:64-121): U (same layout as A) and
+ * sigma (nblk x k, descending).  On non-convergence returns MVAMG_E_NOT_SPD
+ * with *failed_block set (SvdConvergenceError in the Python layer). */
+int mvamg_jacobi_svd_batch(int nblk, const int* row_ptr, int k, const double* A, int max_sweeps,
+                           double tol, double* U, double* sigma, int* failed_block);
+
 /* ---- hierarchy (MultigridOperator) ---------------------------------------- */
 typedef struct mvamg_hierarchy mvamg_hierarchy;
 

@@ -18,7 +18,7 @@ SRC = os.path.join(PKG, "csrc", "mvamg_b200.cu")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-shared",
 ]
 
 E_ARG, E_CUDA, E_NOT_SPD, E_TIMEOUT, E_STATE = 1, 2, 3, 4, 5
@@ -47,6 +47,8 @@ SIGNATURES = [
     ("mvamg_gs_levels", _I, [_I, _P, _P, _P, _I, _PI, ctypes.POINTER(_LL), _PI, _PI, _P, _P, _P, _P, _P]),
     ("mvamg_gs_level_sweep_f64", _I, [_I, _I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P,
                                       _P, _P, _P]),
+    ("mvamg_greedy_match", _I, [_LL, _P, _P, _I, _P, _P, _P, ctypes.POINTER(_LL)]),
+    ("mvamg_jacobi_svd_batch", _I, [_I, _P, _I, _P, _I, _D, _P, _P, _PI]),
     ("mvamg_dense_gemv_f64", _I, [_I, _P, _P, _P, _P]),
     ("mvamg_dot_f64", _I, [_I, _P, _P, _P, _P, _P]),
     ("mvamg_dot_ws_bytes", _I, []),

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <string>
@@ -978,6 +979,111 @@ int mvamg_hierarchy_set_gs_levels(mvamg_hierarchy* h, int k, int mode, int nlev,
   g.lev_ptr = lev_ptr; g.lev_eptr = lev_eptr; g.rows = static_cast<const GsLevelRow*>(rows);
   g.ents = static_cast<const GsLevelEntry*>(ents); g.perm = perm; g.tperm = tperm;
   g.nlev = nlev; g.max_rows = max_rows; g.max_ents = max_ents; g.threads = threads;
+  return 0;
+}
+
+// ---- setup helpers (host) ---------------------------------------------------
+int mvamg_greedy_match(long long ne, const long long* ei, const long long* ej, int n, long long* partner,
+                       long long* pair_i, long long* pair_j, long long* npairs) {
+  // Accept vertex-disjoint edges in the given (sorted) order -- the greedy
+  // 1/2-approximate maximum-product matching (pkg/src/mvamg/_kernels.py:41-61).
+  if (n < 0 || ne < 0 || !partner || !npairs) return fail(MVAMG_E_ARG, "greedy_match: bad arguments");
+  for (int v = 0; v < n; ++v) partner[v] = -1;
+  long long np_ = 0;
+  for (long long k = 0; k < ne; ++k) {
+    const long long i = ei[k], j = ej[k];
+    if (i < 0 || j < 0 || i >= n || j >= n) return fail(MVAMG_E_ARG, "greedy_match: vertex out of range");
+    if (partner[i] < 0 && partner[j] < 0) {
+      partner[i] = j;
+      partner[j] = i;
+      if (pair_i) pair_i[np_] = i;
+      if (pair_j) pair_j[np_] = j;
+      ++np_;
+    }
+  }
+  *npairs = np_;
+  return 0;
+}
+
+namespace {
+// One-sided Jacobi column orthogonalisation of B (m x k, row-major) with V
+// (k x k) accumulating the rotations -- the same sweep, pair order, skip rules
+// and roundings as pkg/src/mvamg/_kernels.py:64-121.
+int jacobi_orthogonalize(double* B, double* V, int m, int k, int max_sweeps, double tol) {
+  if (k < 2) return 1;
+  const double rel_tol = std::max(tol, 2.0 * m * 2.220446049250313e-16);
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    double total = 0.0;
+    for (int p = 0; p < k; ++p)
+      for (int r = 0; r < m; ++r) total += B[r * k + p] * B[r * k + p];
+    const double floor_ = tol * total;
+    int rotated = 0;
+    for (int p = 0; p < k - 1; ++p) {
+      for (int q = p + 1; q < k; ++q) {
+        double alpha = 0.0, beta = 0.0, gamma = 0.0;
+        for (int r = 0; r < m; ++r) {
+          alpha += B[r * k + p] * B[r * k + p];
+          beta += B[r * k + q] * B[r * k + q];
+          gamma += B[r * k + p] * B[r * k + q];
+        }
+        if (gamma == 0.0) continue;
+        if (std::fabs(gamma) <= rel_tol * std::sqrt(alpha * beta) || std::fabs(gamma) <= floor_) continue;
+        ++rotated;
+        const double zeta = (beta - alpha) / (2.0 * gamma);
+        const double t = std::copysign(1.0, zeta) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / std::sqrt(1.0 + t * t);
+        const double s = c * t;
+        for (int r = 0; r < m; ++r) {
+          const double bp = B[r * k + p], bq = B[r * k + q];
+          B[r * k + p] = c * bp - s * bq;
+          B[r * k + q] = s * bp + c * bq;
+        }
+        for (int r = 0; r < k; ++r) {
+          const double vp = V[r * k + p], vq = V[r * k + q];
+          V[r * k + p] = c * vp - s * vq;
+          V[r * k + q] = s * vp + c * vq;
+        }
+      }
+    }
+    if (rotated == 0) return 1;
+  }
+  return 0;
+}
+}  // namespace
+
+int mvamg_jacobi_svd_batch(int nblk, const int* row_ptr, int k, const double* A, int max_sweeps,
+                           double tol, double* U, double* sigma, int* failed_block) {
+  // Batched thin SVD of stacked blocks (rows row_ptr[b]..row_ptr[b+1], k
+  // columns, row-major): pkg/src/mvamg/svd.py:17-55 -- Jacobi, column norms,
+  // stable descending sort, U = B / sigma for nonzero sigma.
+  if (nblk < 0 || k < 1 || !row_ptr || !A || !U || !sigma) return fail(MVAMG_E_ARG, "jacobi_svd_batch: bad arguments");
+  if (failed_block) *failed_block = -1;
+  std::vector<double> B, V, s(k);
+  std::vector<int> order(k);
+  for (int b = 0; b < nblk; ++b) {
+    const int r0 = row_ptr[b], m = row_ptr[b + 1] - r0;
+    if (m < 1) return fail(MVAMG_E_ARG, "jacobi_svd_batch: empty block");
+    B.assign(A + (size_t)r0 * k, A + (size_t)(r0 + m) * k);
+    V.assign((size_t)k * k, 0.0);
+    for (int i = 0; i < k; ++i) V[(size_t)i * k + i] = 1.0;
+    if (!jacobi_orthogonalize(B.data(), V.data(), m, k, max_sweeps, tol)) {
+      if (failed_block) *failed_block = b;
+      return fail(MVAMG_E_NOT_SPD, "Jacobi SVD did not converge");
+    }
+    for (int p = 0; p < k; ++p) {
+      double acc = 0.0;
+      for (int r = 0; r < m; ++r) acc += B[(size_t)r * k + p] * B[(size_t)r * k + p];
+      s[p] = std::sqrt(acc);
+    }
+    for (int p = 0; p < k; ++p) order[p] = p;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return -s[x] < -s[y]; });
+    for (int p = 0; p < k; ++p) {
+      const int src = order[p];
+      sigma[(size_t)b * k + p] = s[src];
+      for (int r = 0; r < m; ++r)
+        U[(size_t)(r0 + r) * k + p] = s[src] > 0.0 ? B[(size_t)r * k + src] / s[src] : 0.0;
+    }
+  }
   return 0;
 }
 

@@ -368,3 +368,23 @@ def test_test_phase_matches_reference(mv, c1, c1_comps):
     rep, w = mv.test_phase(comp, mats[0], 15, np.random.default_rng(5))
     assert np.max(np.abs(rep.per_iteration_anorms - d["testphase_anorms"]) / d["testphase_anorms"]) <= 1e-8
     assert rel(w, d["testphase_w"]) <= 1e-8
+
+
+# ------------------------------------------------------------ full setup ----
+def test_fit_c1_end_to_end(mv):
+    """MultiVectorAMG().fit on the GPU (bootstrap test phases on the device)
+    reproduces the reference's hierarchy and iteration count on config 1."""
+    from paper_1907_04417_b200 import problems
+    from paper_1907_04417_b200.estimator import MultiVectorAMG
+
+    d = golden("c1")
+    A = problems.poisson_2d(128)
+    est = MultiVectorAMG().fit(A)
+    assert est.composite_.n_components == int(d["n_comp"])
+    assert est.hierarchy_.sizes() == [16384, 1665, 522, 160]
+    ref = np.asarray(d["smooth_vectors"])
+    for k, v in enumerate(est.smooth_vectors_):
+        assert rel(v, ref[k]) <= 1e-9, k
+    x, rep = est.solve(d["b"], rtol=1e-6)
+    assert abs(rep.iterations - int(d["pcg_nit"])) <= 1
+    assert abs(est.estimate_convergence_factor() - float(d["rho_est"])) <= 1e-6
