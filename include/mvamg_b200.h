@@ -123,23 +123,38 @@ int mvamg_gs_sweep_f64(int direction, int n, const int* indptr, const int* indic
                        int lean_C, int slot_words, int rec_words_max, int ntiles,
                        const int* chain_ptr, const int* tile_ptr, int threads, int window,
                        const double* b, const double* x_old, double* x_new, int* ws, void* stream);
-/* GS level-set schedule for small levels (host).  mode 0 forward from x = 0,
- * 1 forward, 2 backward from x = 0, 3 backward.  Rows are ordered by the
- * level of the sweep's dependency DAG; rows_out receives n 32-byte records
- * {int row, estart, cnt, pad; double diag, RN(1/diag)}, ents_out the entries
- * {double coef; int src, pad} (16 bytes) of every row in CSR order, perm the
- * level-order position of each row.  Query with rows_out == NULL first. */
-int mvamg_gs_levels(int n, const int* indptr, const int* indices, const double* data, int mode,
-                    int* nlev, long long* nents, int* max_rows, int* max_ents, int* lev_ptr,
-                    int* lev_eptr, void* rows_out, void* ents_out, int* perm);
-/* One GS sweep of a small level (n <= ~24k rows) in a single CTA, x resident in
- * shared memory, one barrier per level set.  Bit-identical to the serial loop.
- * tperm: n doubles of device scratch; ws: >= 4 device ints. */
+/* GS level-set schedule for small / mid-size levels (host).  mode 0 forward
+ * from x = 0, 1 forward, 2 backward from x = 0, 3 backward.  Rows are
+ * block-partitioned over a cluster of ncta (1..16) CTAs and, per CTA, ordered
+ * by the level of the sweep's dependency DAG.  rows_out receives n 32-byte
+ * records {int row, estart, cnt, pad; double diag, RN(1/diag)}, ents_out the
+ * entries {double coef; int src (owner CTA << 26 | local row), pad} of every
+ * row in CSR order, lev_ptr / lev_eptr ncta x (nlev+1) offsets, perm the
+ * layout position of each row.  Levels whose per-CTA rows or entries exceed
+ * row_cap / ent_cap (0 = unlimited) are split into cluster-uniform sub-levels
+ * (the staging buffer's capacity).  Query with rows_out == NULL first. */
+int mvamg_gs_levels(int n, const int* indptr, const int* indices, const double* data, int mode, int ncta,
+                    int row_cap, int ent_cap, int* nlev, long long* nents, int* max_rows, int* max_ents,
+                    int* rows_per_cta, int* lev_ptr, int* lev_eptr, void* rows_out, void* ents_out,
+                    int* perm);
+/* One GS sweep of a small / mid-size level on one thread-block cluster: x
+ * resident in (distributed) shared memory, one cluster barrier per level set.
+ * Bit-identical to the serial loop.  tperm: n + 2 doubles of device scratch;
+ * ws: >= 4 device ints. */
 int mvamg_gs_level_sweep_f64(int direction, int n, const int* indptr, const int* indices,
-                             const double* data, int nlev, int max_rows, int max_ents, int threads,
-                             const int* lev_ptr, const int* lev_eptr, const void* rows,
-                             const void* ents, const int* perm, double* tperm, const double* b,
-                             const double* x_old, double* x_new, int* ws, void* stream);
+                             const double* data, int ncta, int rows_per_cta, int nlev, int max_rows,
+                             int max_ents, int threads, const int* lev_ptr, const int* lev_eptr,
+                             const void* rows, const void* ents, const int* perm, double* tperm,
+                             const double* b, const double* x_old, double* x_new, int* ws, void* stream);
+/* Backward GS sweep from x_old with the mode-2 (backward, zero guess) level
+ * schedule: the old upper neighbours are folded into the right-hand side
+ * first (same roundings), so the sweep reads only new values. */
+int mvamg_gs_level_sweep_folded_f64(int n, const int* indptr, const int* indices, const double* data,
+                                    int ncta, int rows_per_cta, int nlev, int max_rows, int max_ents,
+                                    int threads, const int* lev_ptr, const int* lev_eptr,
+                                    const void* rows, const void* ents, const int* perm,
+                                    double* tperm, const double* b, const double* x_old,
+                                    double* x_new, int* ws, void* stream);
 /* z = Inv r, Inv dense row-major n x n (coarsest solve; cycles.py:88-97). */
 int mvamg_dense_gemv_f64(int n, const double* inv, const double* r, double* z, void* stream);
 /* *result = x . y (deterministic two-level reduction; device scalar).
@@ -180,9 +195,10 @@ int mvamg_hierarchy_set_gs_schedule(mvamg_hierarchy* h, int k, int mode, const u
                                     int slot_words, int rec_words_max);
 /* Small-level GS schedule of level k for sweep `mode` (see mvamg_gs_levels);
  * when set it takes precedence over the wavefront schedule. */
-int mvamg_hierarchy_set_gs_levels(mvamg_hierarchy* h, int k, int mode, int nlev, int max_rows,
-                                  int max_ents, int threads, const int* lev_ptr, const int* lev_eptr,
-                                  const void* rows, const void* ents, const int* perm, double* tperm);
+int mvamg_hierarchy_set_gs_levels(mvamg_hierarchy* h, int k, int mode, int ncta, int rows_per_cta,
+                                  int nlev, int max_rows, int max_ents, int threads, const int* lev_ptr,
+                                  const int* lev_eptr, const void* rows, const void* ents,
+                                  const int* perm, double* tperm);
 /* Transfer k: P (n_k x n_{k+1}) and R = P^T (n_{k+1} x n_k), device CSR. */
 int mvamg_hierarchy_set_transfer(mvamg_hierarchy* h, int k, const int* p_indptr,
                                  const int* p_indices, const double* p_data,

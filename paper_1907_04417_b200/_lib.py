@@ -44,11 +44,14 @@ SIGNATURES = [
                                _PI, _P, _P, _P, _P, _P]),
     ("mvamg_gs_sweep_f64", _I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P,
                                 _I, _I, _P, _P, _P, _P, _P]),
-    ("mvamg_gs_levels", _I, [_I, _P, _P, _P, _I, _PI, ctypes.POINTER(_LL), _PI, _PI, _P, _P, _P, _P, _P]),
-    ("mvamg_gs_level_sweep_f64", _I, [_I, _I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P,
-                                      _P, _P, _P]),
+    ("mvamg_gs_levels", _I, [_I, _P, _P, _P, _I, _I, _I, _I, _PI, ctypes.POINTER(_LL), _PI, _PI, _PI, _P, _P,
+                             _P, _P, _P]),
+    ("mvamg_gs_level_sweep_f64", _I, [_I, _I, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P,
+                                      _P, _P, _P, _P]),
     ("mvamg_greedy_match", _I, [_LL, _P, _P, _I, _P, _P, _P, ctypes.POINTER(_LL)]),
     ("mvamg_jacobi_svd_batch", _I, [_I, _P, _I, _P, _I, _D, _P, _P, _PI]),
+    ("mvamg_gs_level_sweep_folded_f64", _I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P,
+                                             _P, _P, _P, _P, _P]),
     ("mvamg_dense_gemv_f64", _I, [_I, _P, _P, _P, _P]),
     ("mvamg_dot_f64", _I, [_I, _P, _P, _P, _P, _P]),
     ("mvamg_dot_ws_bytes", _I, []),
@@ -56,7 +59,7 @@ SIGNATURES = [
     ("mvamg_hierarchy_destroy", _I, [_P]),
     ("mvamg_hierarchy_set_level", _I, [_P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _I]),
     ("mvamg_hierarchy_set_gs_schedule", _I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I]),
-    ("mvamg_hierarchy_set_gs_levels", _I, [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
+    ("mvamg_hierarchy_set_gs_levels", _I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_hierarchy_set_transfer", _I, [_P, _I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_hierarchy_set_coarse", _I, [_P, _P]),
     ("mvamg_hierarchy_workspace_bytes", _I, [_P, ctypes.POINTER(_LL)]),

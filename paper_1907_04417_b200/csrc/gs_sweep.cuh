@@ -559,12 +559,13 @@ struct GsLevelEntry {  // 16 bytes, CSR order within the row
 
 struct GsLevelArgs {
   int n, nlev, zero_init;
-  int max_rows, max_ents;        // per level
-  const int* lev_ptr;            // nlev + 1, level-order row ranges
-  const int* lev_eptr;           // nlev + 1, entry ranges
-  const GsLevelRow* rows;        // n
-  const GsLevelEntry* ents;      // total entries
-  const double* tperm;           // right-hand side in level order
+  int max_rows, max_ents;        // per (CTA, level)
+  int rows_per_cta;              // row block owned by each CTA of the cluster
+  const int* lev_ptr;            // per CTA: nlev + 1 row offsets (global layout), CTA-major
+  const int* lev_eptr;           // per CTA: nlev + 1 entry offsets
+  const GsLevelRow* rows;        // n, CTA-major then level order
+  const GsLevelEntry* ents;      // entries; src = (owner CTA << 26) | local index
+  const double* tperm;           // right-hand side in the rows' layout
   const double* xold;
   double* xnew;
 };
@@ -576,56 +577,92 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_nctas() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned map_rank(unsigned saddr, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ double ld_dsmem_f64(unsigned caddr) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(caddr) : "memory");
+  return v;
+}
+
+// Small and mid-size levels: x resident in (distributed) shared memory, rows in
+// level-set order of the sweep's dependency DAG, one barrier per level (a
+// __syncthreads-equivalent cluster barrier across up to 16 CTAs of a thread
+// block cluster; a cluster of one CTA is the single-CTA case).  Shared x starts
+// from x_old (or zero), so every entry of a row reads x[j] from (distributed)
+// shared memory: lower neighbours were finished in earlier levels, upper
+// neighbours still hold x_old -- exactly what the serial loop reads.  Each
+// (CTA, level) block of rows is contiguous in the host layout and is staged
+// two levels ahead with coalesced cp.async.
+template <bool CLUSTER>
 __global__ void __launch_bounds__(1024, 1) gs_level_kernel(GsLevelArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
+  const unsigned me = CLUSTER ? cluster_rank() : 0u, ncta = CLUSTER ? cluster_nctas() : 1u;
   double* x = reinterpret_cast<double*>(smem);
-  const int xw = (a.n + 1) & ~1;  // doubles, keeps 16-byte alignment
-  // per buffer: rows (32 B each), entries (16 B each), rhs (8 B each + 2 for alignment slack)
+  const int xw = (a.rows_per_cta + 1) & ~1;
   const int rows_b = a.max_rows * 32, ents_b = a.max_ents * 16, rhs_b = (a.max_rows + 2) * 8;
   const int buf_b = rows_b + ents_b + ((rhs_b + 15) & ~15);
   unsigned char* bufs = smem + 8 * xw;
+  const unsigned xs_local = (unsigned)__cvta_generic_to_shared(x);
   const unsigned bufs_s = (unsigned)__cvta_generic_to_shared(bufs);
   const int T = blockDim.x, tid = threadIdx.x;
-  // x <- x_old or 0
-  for (int i = tid; i < a.n; i += T) x[i] = a.zero_init ? 0.0 : __ldg(a.xold + i);
+  const int base = (int)me * a.rows_per_cta;
+  const int nloc = max(0, min(a.rows_per_cta, a.n - base));
+  for (int i = tid; i < nloc; i += T) x[i] = a.zero_init ? 0.0 : __ldg(a.xold + base + i);
+  const int* lp = a.lev_ptr + (size_t)me * (a.nlev + 1);
+  const int* le = a.lev_eptr + (size_t)me * (a.nlev + 1);
   auto stage = [&](int l) {
     if (l < a.nlev) {
       const int b = l % 3;
-      const unsigned base = bufs_s + (unsigned)(b * buf_b);
-      const int r0 = __ldg(a.lev_ptr + l), r1 = __ldg(a.lev_ptr + l + 1);
-      // rows
+      const unsigned dst = bufs_s + (unsigned)(b * buf_b);
+      const int r0 = __ldg(lp + l), r1 = __ldg(lp + l + 1);
+      const int e0 = __ldg(le + l), e1 = __ldg(le + l + 1);
       const char* src = reinterpret_cast<const char*>(a.rows + r0);
-      for (int c = tid; c < (r1 - r0) * 2; c += T) cp_async16(base + 16u * c, src + 16 * c);
-      // entries
-      const int e0 = __ldg(a.lev_eptr + l), e1 = __ldg(a.lev_eptr + l + 1);
+      for (int c = tid; c < (r1 - r0) * 2; c += T) cp_async16(dst + 16u * c, src + 16 * c);
       const char* esrc = reinterpret_cast<const char*>(a.ents + e0);
-      for (int c = tid; c < e1 - e0; c += T) cp_async16(base + rows_b + 16u * c, esrc + 16 * c);
-      // rhs (aligned superset)
+      for (int c = tid; c < e1 - e0; c += T) cp_async16(dst + rows_b + 16u * c, esrc + 16 * c);
       const int t0 = r0 & ~1, t1 = (r1 + 1) & ~1;
       const char* tsrc = reinterpret_cast<const char*>(a.tperm + t0);
-      for (int c = tid; c < (t1 - t0) / 2; c += T) cp_async16(base + rows_b + ents_b + 16u * c, tsrc + 16 * c);
+      for (int c = tid; c < (t1 - t0) / 2; c += T) cp_async16(dst + rows_b + ents_b + 16u * c, tsrc + 16 * c);
     }
     cp_async_commit();
   };
   stage(0);
   stage(1);
+  if (CLUSTER) cluster_sync();  // every CTA's x slice is initialised before anyone reads it
   for (int l = 0; l < a.nlev; ++l) {
-    cp_async_wait<1>();  // this thread's copies of level l have landed
-    __syncthreads();     // ... everyone's; and level l-1's x writes are visible
+    cp_async_wait<1>();
+    __syncthreads();
     stage(l + 2);
     const int b = l % 3;
-    const unsigned char* base = bufs + b * buf_b;
-    const GsLevelRow* rows = reinterpret_cast<const GsLevelRow*>(base);
-    const GsLevelEntry* ents = reinterpret_cast<const GsLevelEntry*>(base + rows_b);
-    const double* rhs = reinterpret_cast<const double*>(base + rows_b + ents_b);
-    const int r0 = __ldg(a.lev_ptr + l), r1 = __ldg(a.lev_ptr + l + 1);
-    const int e0 = __ldg(a.lev_eptr + l), toff = r0 & 1;
+    const unsigned char* bb = bufs + b * buf_b;
+    const GsLevelRow* rows = reinterpret_cast<const GsLevelRow*>(bb);
+    const GsLevelEntry* ents = reinterpret_cast<const GsLevelEntry*>(bb + rows_b);
+    const double* rhs = reinterpret_cast<const double*>(bb + rows_b + ents_b);
+    const int r0 = __ldg(lp + l), r1 = __ldg(lp + l + 1);
+    const int e0 = __ldg(le + l), toff = r0 & 1;
     for (int r = tid; r < r1 - r0; r += T) {
       const GsLevelRow m = rows[r];
       double s = rhs[toff + r];
       const GsLevelEntry* e = ents + (m.estart - e0);
       // chunks of 8: all loads and products first (independent), then the
-      // subtractions in CSR order
+      // subtractions in CSR order, one rounding each (bit-exact)
       for (int k0 = 0; k0 < m.cnt; k0 += 8) {
         double p[8];
 #pragma unroll
@@ -633,19 +670,29 @@ __global__ void __launch_bounds__(1024, 1) gs_level_kernel(GsLevelArgs a) {
           p[u] = 0.0;
           if (k0 + u < m.cnt) {
             const GsLevelEntry en = e[k0 + u];
-            p[u] = __dmul_rn(en.coef, x[en.src]);
+            double xv;
+            if (CLUSTER) {
+              const unsigned owner = (unsigned)en.src >> 26, loc = (unsigned)en.src & ((1u << 26) - 1);
+              xv = ld_dsmem_f64(map_rank(xs_local + 8u * loc, owner));
+            } else {
+              xv = x[en.src];
+            }
+            p[u] = __dmul_rn(en.coef, xv);
           }
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           if (k0 + u < m.cnt) s = __dsub_rn(s, p[u]);
       }
-      x[m.row] = div_rn_markstein(s, m.diag, m.rdiag);
+      x[m.row - base] = div_rn_markstein(s, m.diag, m.rdiag);
     }
+    if (CLUSTER) cluster_sync();  // level l published cluster-wide
   }
   cp_async_wait<0>();
   __syncthreads();
-  for (int i = tid; i < a.n; i += T) a.xnew[i] = x[i];
+  for (int i = tid; i < nloc; i += T) a.xnew[base + i] = x[i];
+  if (CLUSTER) cluster_sync();  // no CTA leaves while others may still read its slice
+  (void)ncta;
 }
 
 }  // namespace mvamg

@@ -129,6 +129,7 @@ struct GsList {
 // Level-set schedule of one sweep mode for the single-CTA small-level kernel
 // (0 forward from x = 0, 1 forward, 2 backward from x = 0, 3 backward).
 struct GsLevels {
+  int ncta = 1, rows_per_cta = 0;
   const int* lev_ptr = nullptr;
   const int* lev_eptr = nullptr;
   const GsLevelRow* rows = nullptr;
@@ -254,15 +255,15 @@ int launch_gs(bool fwd, const Csr& A, const GsList& ls, const GsPlan& p, const d
   return 0;
 }
 
-size_t gs_level_smem(int n, const GsLevels& g) {
-  const size_t xw = (size_t)((n + 1) & ~1);
+size_t gs_level_smem(const GsLevels& g) {
+  const size_t xw = (size_t)((g.rows_per_cta + 1) & ~1);
   const size_t buf = (size_t)g.max_rows * 32 + (size_t)g.max_ents * 16 + (((size_t)(g.max_rows + 2) * 8 + 15) & ~(size_t)15);
   return xw * 8 + 3 * buf;
 }
 
 bool g_level_attr = false;
 int launch_gs_levels(const Csr& A, const GsLevels& g, bool zero, const double* b, const double* xold,
-                     double* xnew, int* ticket, cudaStream_t s) {
+                     double* xnew, int* ticket, cudaStream_t s, bool fold = false) {
   const int n = A.n;
   if (n == 0) return 0;
   if (!g_level_attr) {
@@ -270,19 +271,26 @@ int launch_gs_levels(const Csr& A, const GsLevels& g, bool zero, const double* b
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncSetAttribute(gs_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+    cudaFuncSetAttribute(gs_level_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+    cudaFuncSetAttribute(gs_level_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+    cudaFuncSetAttribute(gs_level_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaGetLastError();
   }
-  const size_t smem = gs_level_smem(n, g);
+  const size_t smem = gs_level_smem(g);
   if (smem > (size_t)g_max_dyn_smem) return fail(MVAMG_E_ARG, "gs levels: shared memory plan too large");
-  // right-hand side in level order (no fold: x_old is read from shared memory)
+  if (g.ncta < 1 || g.ncta > 16) return fail(MVAMG_E_ARG, "gs levels: cluster of 1..16 CTAs");
+  // right-hand side in the schedule's row layout; a backward sweep from a
+  // nonzero guess folds its old upper neighbours here and then runs the
+  // zero-guess schedule (only new values are read during the sweep)
   gs_prepare_kernel<<<grid_for(n), 256, 0, s>>>(n, A.ip, A.ix, A.v, b, xold, g.perm, g.tperm, xnew,
-                                                ticket, 0);
+                                                ticket, fold ? 1 : 0);
   GsLevelArgs a;
   a.n = n;
   a.nlev = g.nlev;
-  a.zero_init = zero ? 1 : 0;
+  a.zero_init = (zero || fold) ? 1 : 0;
   a.max_rows = g.max_rows;
   a.max_ents = g.max_ents;
+  a.rows_per_cta = g.rows_per_cta;
   a.lev_ptr = g.lev_ptr;
   a.lev_eptr = g.lev_eptr;
   a.rows = g.rows;
@@ -290,8 +298,24 @@ int launch_gs_levels(const Csr& A, const GsLevels& g, bool zero, const double* b
   a.tperm = g.tperm;
   a.xold = xold;
   a.xnew = xnew;
-  gs_level_kernel<<<1, g.threads, smem, s>>>(a);
-  CUDA_TRY(cudaGetLastError());
+  if (g.ncta == 1) {
+    gs_level_kernel<false><<<1, g.threads, smem, s>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g.ncta);
+  cfg.blockDim = dim3(g.threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = g.ncta;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_level_kernel<true>, a));
   return 0;
 }
 
@@ -371,7 +395,9 @@ struct mvamg_hierarchy {
       } else {
         bool fwd = sp.kind == MVAMG_GS_FORWARD;
         int lmode = (fwd ? 0 : 2) + (x_cur == nullptr ? 0 : 1);
-        if (l.glv[lmode].rows) {
+        if (!fwd && x_cur != nullptr && l.glv[2].rows) {
+          st = launch_gs_levels(l.A, l.glv[2], false, b, x_cur, out, ticket, s, /*fold=*/true);
+        } else if (l.glv[lmode].rows) {
           st = launch_gs_levels(l.A, l.glv[lmode], x_cur == nullptr, b, x_cur, out, ticket, s);
         } else {
           int mode = fwd ? (x_cur == nullptr ? 0 : 1) : 2;
@@ -878,10 +904,12 @@ int mvamg_gs_sweep_f64(int direction, int n, const int* indptr, const int* indic
   return launch_gs(direction == 0, A, ls, p, b, x_old, x_new, ws, ws + 1, (cudaStream_t)stream);
 }
 
-int mvamg_gs_levels(int n, const int* indptr, const int* indices, const double* data, int mode,
-                    int* nlev, long long* nents, int* max_rows, int* max_ents, int* lev_ptr,
-                    int* lev_eptr, void* rows_out, void* ents_out, int* perm) {
-  if (n < 0 || !indptr || !nlev || !nents || !max_rows || !max_ents || mode < 0 || mode > 3)
+int mvamg_gs_levels(int n, const int* indptr, const int* indices, const double* data, int mode, int ncta,
+                    int row_cap, int ent_cap, int* nlev, long long* nents, int* max_rows, int* max_ents,
+                    int* rows_per_cta, int* lev_ptr, int* lev_eptr, void* rows_out, void* ents_out,
+                    int* perm) {
+  if (n < 0 || !indptr || !nlev || !nents || !max_rows || !max_ents || !rows_per_cta || mode < 0 ||
+      mode > 3 || ncta < 1 || ncta > 16)
     return fail(MVAMG_E_ARG, "gs_levels: bad arguments");
   const bool fwd = mode < 2, zero = (mode % 2) == 0;
   auto keep = [&](int i, int j) {
@@ -889,7 +917,12 @@ int mvamg_gs_levels(int n, const int* indptr, const int* indices, const double* 
     if (!zero) return true;
     return fwd ? j < i : j > i;
   };
-  std::vector<int> lvl(n > 0 ? n : 1, 0);
+  if (row_cap <= 0) row_cap = 1 << 30;
+  if (ent_cap <= 0) ent_cap = 1 << 30;
+  const int rpc = (n + ncta - 1) / ncta;
+  if (rpc >= (1 << 26)) return fail(MVAMG_E_ARG, "gs_levels: too many rows per CTA");
+  // level sets of the sweep's dependency DAG
+  std::vector<int> lvl(n > 0 ? n : 1, 0), rowcnt(n > 0 ? n : 1, 0);
   int nl = 0;
   for (int q = 0; q < n; ++q) {
     const int i = fwd ? q : n - 1 - q;
@@ -901,64 +934,122 @@ int mvamg_gs_levels(int n, const int* indptr, const int* indices, const double* 
     lvl[i] = m;
     nl = std::max(nl, m + 1);
   }
-  std::vector<int> cnt_l(nl + 1, 0), ents_l(nl + 1, 0);
-  std::vector<int> rowcnt(n > 0 ? n : 1, 0);
+  if (n == 0) nl = 0;
   for (int i = 0; i < n; ++i) {
     int c = 0;
     for (int k = indptr[i]; k < indptr[i + 1]; ++k) c += keep(i, indices[k]);
     rowcnt[i] = c;
-    cnt_l[lvl[i] + 1] += 1;
-    ents_l[lvl[i] + 1] += c;
   }
-  int mr = 0, me = 0;
+  // rows of every (cta, level) bucket, ascending
+  std::vector<std::vector<int>> bucket((size_t)ncta * nl);
+  for (int i = 0; i < n; ++i) bucket[(size_t)(i / rpc) * nl + lvl[i]].push_back(i);
+  // split each level into cluster-uniform sub-levels whose (cta) buckets fit the caps
+  std::vector<int> sub(nl > 0 ? nl : 1, 1);
+  std::vector<std::vector<int>> cut((size_t)ncta * nl);  // greedy group boundaries per bucket
   for (int l = 0; l < nl; ++l) {
-    mr = std::max(mr, cnt_l[l + 1]);
-    me = std::max(me, ents_l[l + 1]);
+    int need = 1;
+    for (int c = 0; c < ncta; ++c) {
+      auto& bk = bucket[(size_t)c * nl + l];
+      auto& ct = cut[(size_t)c * nl + l];
+      ct.assign(1, 0);
+      long long ents = 0;
+      int rows = 0;
+      for (int p = 0; p < (int)bk.size(); ++p) {
+        const int rc = rowcnt[bk[p]];
+        if (rows > 0 && (rows + 1 > row_cap || ents + rc > ent_cap)) {
+          ct.push_back(p);
+          ents = 0;
+          rows = 0;
+        }
+        ents += rc;
+        ++rows;
+      }
+      ct.push_back((int)bk.size());
+      need = std::max(need, (int)ct.size() - 1);
+    }
+    sub[l] = need;
   }
-  for (int l = 0; l < nl; ++l) {
-    cnt_l[l + 1] += cnt_l[l];
-    ents_l[l + 1] += ents_l[l];
+  int nsub = 0;
+  for (int l = 0; l < nl; ++l) nsub += sub[l];
+  const size_t L1 = (size_t)nsub + 1;
+  // offsets over (cta, sub-level), CTA-major
+  std::vector<long long> rstart((size_t)ncta * L1), estart((size_t)ncta * L1);
+  long long rofs = 0, eofs = 0, mr = 0, me = 0;
+  for (int c = 0; c < ncta; ++c) {
+    int s = 0;
+    for (int l = 0; l < nl; ++l) {
+      auto& bk = bucket[(size_t)c * nl + l];
+      auto& ct = cut[(size_t)c * nl + l];
+      for (int g = 0; g < sub[l]; ++g, ++s) {
+        rstart[(size_t)c * L1 + s] = rofs;
+        estart[(size_t)c * L1 + s] = eofs;
+        const int p0 = g + 1 < (int)ct.size() ? ct[g] : (int)bk.size();
+        const int p1 = g + 1 < (int)ct.size() ? ct[g + 1] : (int)bk.size();
+        long long e = 0;
+        for (int p = p0; p < p1; ++p) e += rowcnt[bk[p]];
+        rofs += p1 - p0;
+        eofs += e;
+        mr = std::max(mr, (long long)(p1 - p0));
+        me = std::max(me, e);
+      }
+    }
+    rstart[(size_t)c * L1 + nsub] = rofs;
+    estart[(size_t)c * L1 + nsub] = eofs;
   }
-  *nlev = nl;
-  *nents = ents_l[nl];
-  *max_rows = mr;
-  *max_ents = me;
+  if (eofs >= (1LL << 31)) return fail(MVAMG_E_ARG, "gs_levels: more than 2^31 entries");
+  *nlev = nsub;
+  *nents = eofs;
+  *max_rows = (int)mr;
+  *max_ents = (int)me;
+  *rows_per_cta = rpc;
   if (!rows_out) return 0;
-  std::copy(cnt_l.begin(), cnt_l.end(), lev_ptr);
-  std::copy(ents_l.begin(), ents_l.end(), lev_eptr);
+  for (size_t k = 0; k < rstart.size(); ++k) {
+    lev_ptr[k] = (int)rstart[k];
+    lev_eptr[k] = (int)estart[k];
+  }
   GsLevelRow* R = static_cast<GsLevelRow*>(rows_out);
   GsLevelEntry* E = static_cast<GsLevelEntry*>(ents_out);
-  std::vector<int> fillr(cnt_l.begin(), cnt_l.end() - 1), fille(ents_l.begin(), ents_l.end() - 1);
-  for (int i = 0; i < n; ++i) {  // rows of a level in ascending index order
-    const int l = lvl[i];
-    const int pos = fillr[l]++;
-    GsLevelRow& r = R[pos];
-    r.row = i;
-    r.estart = fille[l];
-    r.cnt = rowcnt[i];
-    r.pad = 0;
-    double dg = 0.0;
-    for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
-      const int j = indices[k];
-      if (j == i) dg = data[k];
-      if (!keep(i, j)) continue;
-      GsLevelEntry& e = E[fille[l]++];
-      e.coef = data[k];
-      e.src = j;
-      e.pad = 0;
+  for (int c = 0; c < ncta; ++c) {
+    int s = 0;
+    for (int l = 0; l < nl; ++l) {
+      auto& bk = bucket[(size_t)c * nl + l];
+      auto& ct = cut[(size_t)c * nl + l];
+      for (int g = 0; g < sub[l]; ++g, ++s) {
+        long long pos = rstart[(size_t)c * L1 + s], epos = estart[(size_t)c * L1 + s];
+        const int p0 = g + 1 < (int)ct.size() ? ct[g] : (int)bk.size();
+        const int p1 = g + 1 < (int)ct.size() ? ct[g + 1] : (int)bk.size();
+        for (int p = p0; p < p1; ++p, ++pos) {
+          const int i = bk[p];
+          GsLevelRow& r = R[pos];
+          r.row = i;
+          r.estart = (int)epos;
+          r.cnt = rowcnt[i];
+          r.pad = 0;
+          double dg = 0.0;
+          for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+            const int j = indices[k];
+            if (j == i) dg = data[k];
+            if (!keep(i, j)) continue;
+            GsLevelEntry& e = E[epos++];
+            e.coef = data[k];
+            e.src = ((j / rpc) << 26) | (j % rpc);
+            e.pad = 0;
+          }
+          r.diag = dg;
+          r.rdiag = 1.0 / dg;
+          if (perm) perm[i] = (int)pos;
+        }
+      }
     }
-    r.diag = dg;
-    r.rdiag = 1.0 / dg;
-    if (perm) perm[i] = pos;
   }
   return 0;
 }
 
 int mvamg_gs_level_sweep_f64(int direction, int n, const int* indptr, const int* indices,
-                             const double* data, int nlev, int max_rows, int max_ents, int threads,
-                             const int* lev_ptr, const int* lev_eptr, const void* rows,
-                             const void* ents, const int* perm, double* tperm, const double* b,
-                             const double* x_old, double* x_new, int* ws, void* stream) {
+                             const double* data, int ncta, int rows_per_cta, int nlev, int max_rows,
+                             int max_ents, int threads, const int* lev_ptr, const int* lev_eptr,
+                             const void* rows, const void* ents, const int* perm, double* tperm,
+                             const double* b, const double* x_old, double* x_new, int* ws, void* stream) {
   if (threads < 32 || threads > 1024 || threads % 32) return fail(MVAMG_E_ARG, "gs levels: bad thread count");
   Csr A;
   A.n = n; A.ip = indptr; A.ix = indices; A.v = data;
@@ -966,19 +1057,40 @@ int mvamg_gs_level_sweep_f64(int direction, int n, const int* indptr, const int*
   g.lev_ptr = lev_ptr; g.lev_eptr = lev_eptr; g.rows = static_cast<const GsLevelRow*>(rows);
   g.ents = static_cast<const GsLevelEntry*>(ents); g.perm = perm; g.tperm = tperm;
   g.nlev = nlev; g.max_rows = max_rows; g.max_ents = max_ents; g.threads = threads;
+  g.ncta = ncta; g.rows_per_cta = rows_per_cta;
   (void)direction;  // encoded in the schedule
   set_kernel_attrs();
   return launch_gs_levels(A, g, x_old == nullptr, b, x_old, x_new, ws, (cudaStream_t)stream);
 }
 
-int mvamg_hierarchy_set_gs_levels(mvamg_hierarchy* h, int k, int mode, int nlev, int max_rows,
-                                  int max_ents, int threads, const int* lev_ptr, const int* lev_eptr,
-                                  const void* rows, const void* ents, const int* perm, double* tperm) {
+int mvamg_gs_level_sweep_folded_f64(int n, const int* indptr, const int* indices, const double* data,
+                                    int ncta, int rows_per_cta, int nlev, int max_rows, int max_ents,
+                                    int threads, const int* lev_ptr, const int* lev_eptr,
+                                    const void* rows, const void* ents, const int* perm,
+                                    double* tperm, const double* b, const double* x_old,
+                                    double* x_new, int* ws, void* stream) {
+  if (!x_old) return fail(MVAMG_E_ARG, "gs levels folded: needs x_old");
+  Csr A;
+  A.n = n; A.ip = indptr; A.ix = indices; A.v = data;
+  GsLevels g;
+  g.lev_ptr = lev_ptr; g.lev_eptr = lev_eptr; g.rows = static_cast<const GsLevelRow*>(rows);
+  g.ents = static_cast<const GsLevelEntry*>(ents); g.perm = perm; g.tperm = tperm;
+  g.nlev = nlev; g.max_rows = max_rows; g.max_ents = max_ents; g.threads = threads;
+  g.ncta = ncta; g.rows_per_cta = rows_per_cta;
+  set_kernel_attrs();
+  return launch_gs_levels(A, g, false, b, x_old, x_new, ws, (cudaStream_t)stream, true);
+}
+
+int mvamg_hierarchy_set_gs_levels(mvamg_hierarchy* h, int k, int mode, int ncta, int rows_per_cta,
+                                  int nlev, int max_rows, int max_ents, int threads, const int* lev_ptr,
+                                  const int* lev_eptr, const void* rows, const void* ents,
+                                  const int* perm, double* tperm) {
   if (!h || k < 0 || k >= h->L || mode < 0 || mode > 3) return fail(MVAMG_E_ARG, "set_gs_levels: bad index");
   GsLevels& g = h->lv[k].glv[mode];
   g.lev_ptr = lev_ptr; g.lev_eptr = lev_eptr; g.rows = static_cast<const GsLevelRow*>(rows);
   g.ents = static_cast<const GsLevelEntry*>(ents); g.perm = perm; g.tperm = tperm;
   g.nlev = nlev; g.max_rows = max_rows; g.max_ents = max_ents; g.threads = threads;
+  g.ncta = ncta; g.rows_per_cta = rows_per_cta;
   return 0;
 }
 

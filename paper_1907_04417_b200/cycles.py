@@ -118,13 +118,14 @@ class GpuMultigridOperator:
         for spec, first_zero in ((self.pre_smoother, True), (self.post_smoother, False)):
             if spec.kind == WEIGHTED_JACOBI or spec.sweeps == 0:
                 continue
-            base = 0 if spec.kind == GS_FORWARD else 2
-            if first_zero:
-                modes.add(base)
+            if spec.kind == GS_BACKWARD:
+                modes.add(2)  # from x_old: folded upper neighbours + the zero-guess schedule
+            elif first_zero:
+                modes.add(0)
                 if spec.sweeps > 1:
-                    modes.add(base + 1)
+                    modes.add(1)
             else:
-                modes.add(base + 1)
+                modes.add(1)
         return sorted(modes)
 
     def _init_plain(self, A):
@@ -162,8 +163,9 @@ class GpuMultigridOperator:
                 self._keep.append(dd)
                 small = None
                 if level_gs_fits(A, self.config):
-                    small = {m: DeviceGsLevels(A, m) for m in self._gs_level_modes()}
-                    if any(s.smem_bytes() > self.config.smem_limit for s in small.values()):
+                    try:
+                        small = {m: DeviceGsLevels(A, m, self.config) for m in self._gs_level_modes()}
+                    except ValueError:
                         small = None
                 if small is not None:
                     # single-CTA level-set sweeps; no wavefront schedule needed

@@ -68,7 +68,9 @@ class GpuConfig:
     ring_bytes: int = 48 * 1024     # TMA ring size per warp (D slots of R rounds)
     rounds_in_flight: int = 16      # rounds of records the ring keeps ahead (generic kernel)
     generic_gs: bool = False        # force the generic GS kernel (tests / diagnostics)
-    level_gs_max_rows: int = 24576  # levels up to this size may use the single-CTA level-set sweep
+    level_gs_max_rows: int = 393216 # levels up to this size may use the cluster level-set sweep
+    max_cluster: int = 16           # CTAs per thread-block cluster for level-set sweeps
+    level_stage_bytes: int = 32768  # minimum staging buffer per level (else a larger cluster)
     force_level_gs: bool = False    # use it for every small level (tests / diagnostics)
     smem_limit: int = 227 * 1024 - 1024
 
@@ -301,12 +303,14 @@ LEVEL_ENT_DTYPE = np.dtype([("coef", "<f8"), ("src", "<i4"), ("pad", "<i4")])
 
 
 class DeviceGsLevels:
-    """Single-CTA level-set GS schedule of one small matrix and sweep mode
-    (0 fwd from x=0, 1 fwd, 2 bwd from x=0, 3 bwd), resident on the device."""
+    """Level-set GS schedule of one small / mid-size matrix and sweep mode (0 fwd
+    from x=0, 1 fwd, 2 bwd from x=0, 3 bwd) on one thread-block cluster of 1..16
+    CTAs (the smallest cluster whose shared memory holds x), on the device."""
 
-    def __init__(self, A, mode):
+    def __init__(self, A, mode, cfg=None):
         import torch
 
+        cfg = cfg or GpuConfig()
         A = as_csr(A)
         L = _lib.load()
         n = A.shape[0]
@@ -314,22 +318,40 @@ class DeviceGsLevels:
         ix = np.ascontiguousarray(A.indices, dtype=np.int32)
         v = np.ascontiguousarray(A.data, dtype=np.float64)
         vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
-        nlev, mr, me = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        nlev, mr, me, rpc = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         ne = ctypes.c_longlong()
-        _lib.check(L.mvamg_gs_levels(n, vp(ip), vp(ix), vp(v), int(mode), ctypes.byref(nlev),
-                                     ctypes.byref(ne), ctypes.byref(mr), ctypes.byref(me), None, None,
-                                     None, None, None), "gs_levels")
-        lev_ptr = np.empty(nlev.value + 1, dtype=np.int32)
-        lev_eptr = np.empty(nlev.value + 1, dtype=np.int32)
+        chosen = None
+        for ncta in (1, 2, 4, 8, 16):
+            if ncta > cfg.max_cluster:
+                break
+            rpc_ = -(-n // ncta)
+            room = cfg.smem_limit - 8 * ((rpc_ + 1) & ~1)
+            per_buf = room // 3
+            if per_buf < cfg.level_stage_bytes and not (ncta == cfg.max_cluster or ncta == 16):
+                continue
+            row_cap = min(1024, max(32, per_buf // 160))
+            ent_cap = (per_buf - row_cap * 40 - 32) // 16
+            _lib.check(L.mvamg_gs_levels(n, vp(ip), vp(ix), vp(v), int(mode), ncta, row_cap, ent_cap,
+                                         ctypes.byref(nlev), ctypes.byref(ne), ctypes.byref(mr), ctypes.byref(me),
+                                         ctypes.byref(rpc), None, None, None, None, None), "gs_levels")
+            if self._smem(rpc.value, max(1, mr.value), max(1, me.value)) <= cfg.smem_limit:
+                chosen = (ncta, row_cap, ent_cap)
+                break
+        if chosen is None:
+            raise ValueError("level-set GS schedule does not fit a thread-block cluster")
+        ncta, row_cap, ent_cap = chosen
+        lev_ptr = np.empty(ncta * (nlev.value + 1), dtype=np.int32)
+        lev_eptr = np.empty(ncta * (nlev.value + 1), dtype=np.int32)
         rows = np.zeros(max(1, n), dtype=LEVEL_ROW_DTYPE)
         ents = np.zeros(max(1, ne.value), dtype=LEVEL_ENT_DTYPE)
         perm = np.empty(max(1, n), dtype=np.int32)
-        _lib.check(L.mvamg_gs_levels(n, vp(ip), vp(ix), vp(v), int(mode), ctypes.byref(nlev),
-                                     ctypes.byref(ne), ctypes.byref(mr), ctypes.byref(me), vp(lev_ptr),
-                                     vp(lev_eptr), vp(rows), vp(ents), vp(perm)), "gs_levels")
-        self.n, self.mode = n, mode
+        _lib.check(L.mvamg_gs_levels(n, vp(ip), vp(ix), vp(v), int(mode), ncta, row_cap, ent_cap,
+                                     ctypes.byref(nlev), ctypes.byref(ne), ctypes.byref(mr), ctypes.byref(me),
+                                     ctypes.byref(rpc), vp(lev_ptr), vp(lev_eptr), vp(rows), vp(ents), vp(perm)),
+                   "gs_levels")
+        self.n, self.mode, self.ncta, self.rows_per_cta = n, mode, ncta, rpc.value
         self.nlev, self.max_rows, self.max_ents = nlev.value, max(1, mr.value), max(1, me.value)
-        self.threads = int(min(1024, max(64, (self.max_rows + 31) // 32 * 32)))
+        self.threads = int(min(1024, max(64, (self.max_rows + 31) // 32 * 32)))  # one thread per row
         self.lev_ptr = to_device(lev_ptr)
         self.lev_eptr = to_device(lev_eptr)
         self.rows = to_device(rows.view(np.uint8))
@@ -338,16 +360,26 @@ class DeviceGsLevels:
         self.tperm = torch.empty(max(2, n + 2), dtype=torch.float64, device="cuda")
         self._csr = DeviceCSR(A)
 
-    def smem_bytes(self):
-        xw = (self.n + 1) & ~1
-        buf = self.max_rows * 32 + self.max_ents * 16 + ((self.max_rows + 2) * 8 + 15) // 16 * 16
+    @staticmethod
+    def _smem(rpc, max_rows, max_ents):
+        xw = (rpc + 1) & ~1
+        buf = max_rows * 32 + max_ents * 16 + ((max_rows + 2) * 8 + 15) // 16 * 16
         return xw * 8 + 3 * buf
 
-    def args(self):
-        return (self.nlev, self.max_rows, self.max_ents, self.threads, ptr(self.lev_ptr), ptr(self.lev_eptr),
-                ptr(self.rows), ptr(self.ents), ptr(self.perm), ptr(self.tperm))
+    def smem_bytes(self):
+        return self._smem(self.rows_per_cta, self.max_rows, self.max_ents)
 
-    def sweep(self, b, x_old, x_new, ws, stream=None):
+    def args(self):
+        return (self.ncta, self.rows_per_cta, self.nlev, self.max_rows, self.max_ents, self.threads,
+                ptr(self.lev_ptr), ptr(self.lev_eptr), ptr(self.rows), ptr(self.ents), ptr(self.perm),
+                ptr(self.tperm))
+
+    def sweep(self, b, x_old, x_new, ws, stream=None, fold=False):
+        if fold:  # backward from x_old with this (mode 2) schedule
+            _lib.check(_lib.load().mvamg_gs_level_sweep_folded_f64(
+                self.n, *self._csr.ptrs(), *self.args(), ptr(b), ptr(x_old), ptr(x_new), ptr(ws),
+                stream or stream_handle()), "gs_level_sweep_folded")
+            return
         _lib.check(_lib.load().mvamg_gs_level_sweep_f64(
             0 if self.mode < 2 else 1, self.n, *self._csr.ptrs(), *self.args(), ptr(b), ptr(x_old),
             ptr(x_new), ptr(ws), stream or stream_handle()), "gs_level_sweep")

@@ -166,22 +166,27 @@ def test_gs_structures_bit_exact(mv, cfg):
             assert np.array_equal(got, want), (name, direction, "zero")
 
 
-def _gs_level_gpu(A, b, x_old, direction, zero):
+def _gs_level_gpu(A, b, x_old, direction, zero, cfg=None, fold=False):
     import torch
     from paper_1907_04417_b200.device import DeviceGsLevels
 
     A = sp.csr_matrix(A)
-    mode = (0 if direction == "forward" else 2) + (0 if zero else 1)
-    lv = DeviceGsLevels(A, mode)
+    mode = (0 if direction == "forward" else 2) + (0 if (zero or fold) else 1)
+    lv = DeviceGsLevels(A, mode, cfg)
     xn = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
     ws = torch.zeros(8, dtype=torch.int32, device="cuda")
-    lv.sweep(_dev(b), None if zero else _dev(x_old), xn, ws)
+    lv.sweep(_dev(b), None if zero else _dev(x_old), xn, ws, fold=fold)
     torch.cuda.synchronize()
     return xn.cpu().numpy()
 
 
-def test_gs_level_kernel_bit_exact(mv, c1):
-    """The single-CTA level-set sweep (small levels) on every structure."""
+@pytest.mark.parametrize("cluster", [None, 2, 16])
+def test_gs_level_kernel_bit_exact(mv, c1, cluster):
+    """The level-set sweep (single CTA, or a forced cluster of 2 / 16 CTAs with
+    x in distributed shared memory) on every structure."""
+    cfg = None
+    if cluster:
+        cfg = mv.GpuConfig(smem_limit=8 * 16384 // cluster + 20000, max_cluster=cluster)
     rng = np.random.default_rng(11)
     mats = c1[1]
     cases = list(_structures()) + [("c1_l1", mats[1]), ("c1_l2", mats[2]), ("c1_l0", mats[0])]
@@ -193,8 +198,14 @@ def test_gs_level_kernel_bit_exact(mv, c1):
             for zero in (True, False):
                 want = np.zeros(n) if zero else x0.copy()
                 oracle_gs(A, b, want, direction)
-                got = _gs_level_gpu(A, b, x0, direction, zero)
-                assert np.array_equal(got, want), (name, direction, zero)
+                try:
+                    got = _gs_level_gpu(A, b, x0, direction, zero, cfg)
+                    if direction == "backward" and not zero:
+                        folded = _gs_level_gpu(A, b, x0, direction, zero, cfg, fold=True)
+                        assert np.array_equal(folded, want), (name, "folded", cluster)
+                except ValueError:
+                    continue  # does not fit the forced shared-memory limit
+                assert np.array_equal(got, want), (name, direction, zero, cluster)
 
 
 def test_gs_hand_recurrence(mv):

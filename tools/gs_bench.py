@@ -44,9 +44,12 @@ def main():
             xn = _t.empty(n, dtype=_t.float64, device="cuda")
             ws = _t.zeros(8, dtype=_t.int32, device="cuda")
             res = {}
-            for m, s in sorted(lv["levels"].items()):
+            modes = dict(lv["levels"])
+            if 2 in modes:
+                modes[3] = modes[2]
+            for m, s in sorted(modes.items()):
                 def once():
-                    s.sweep(bb, None if m % 2 == 0 else xo, xn, ws)
+                    s.sweep(bb, None if m % 2 == 0 else xo, xn, ws, fold=(m == 3))
                 for _ in range(3):
                     once()
                 for mode in ("warm", "cold"):
@@ -58,7 +61,7 @@ def main():
                         e0.record(stream); once(); e1.record(stream); e1.synchronize()
                         tot += e0.elapsed_time(e1)
                     res[(m, mode)] = tot / 20 * 1e3
-            desc = " | ".join(f"mode{m} warm {res[(m,'warm')]:.1f}us cold {res[(m,'cold')]:.1f}us" for m in sorted(lv["levels"]))
+            desc = " | ".join(f"mode{m} warm {res[(m,'warm')]:.1f}us cold {res[(m,'cold')]:.1f}us" for m in sorted(modes))
             s0 = next(iter(lv["levels"].values()))
             print(f"level {k}: n={n} nnz={A.nnz} LEVEL-SET nlev={s0.nlev} thr={s0.threads} | {desc} | "
                   f"{res[(0,'warm')]*1e3/s0.nlev:.0f} ns/level", flush=True)
