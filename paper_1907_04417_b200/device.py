@@ -162,20 +162,32 @@ def gs_analyse(A, cfg=None):
     n = A.shape[0]
     C, R, D, slot, S = _gs_ring(A, cfg)
     ring_warp = D * (slot * 8 + 8)
-    T = max(1, min(256, cfg.max_threads))  # chains per tile (block <= 256 threads)
-    while True:
-        Tr = (T + 31) // 32 * 32
-        slots = (cfg.smem_budget - (Tr // 32) * ring_warp) // 8 - 2
-        if slots >= Tr * 16 or T <= 32:
-            break
-        T = max(32, T // 2)
-    if slots < 32:
-        raise ValueError(f"GS ring of {ring_warp} bytes per warp does not fit shared memory")
-    slots = min(slots, cfg.max_window)
-    max_chain = max(1, min(cfg.max_chain, slots // 32))
-    nch, nt, thr, win, dep = (ctypes.c_int() for _ in range(5))
     c_ip = ip.ctypes.data_as(ctypes.c_void_p)
     c_ix = ix.ctypes.data_as(ctypes.c_void_p)
+    nch, nt, thr, win, dep = (ctypes.c_int() for _ in range(5))
+    # natural chain length (longest run of rows coupled to their predecessor,
+    # e.g. a grid line): keep chains whole and pick the widest tile whose
+    # position-major window still fits; split chains only if one warp cannot hold them
+    _lib.check(L.mvamg_gs_analyse(n, c_ip, c_ix, min(cfg.max_chain, 1 << 30), 1, 1 << 30, ctypes.byref(nch),
+                                  ctypes.byref(nt), None, None, None, None, None), "gs_analyse")
+    cp0 = np.empty(nch.value + 1, dtype=np.int32)
+    tp0 = np.empty(nt.value + 1, dtype=np.int32)
+    _lib.check(L.mvamg_gs_analyse(n, c_ip, c_ix, min(cfg.max_chain, 1 << 30), 1, 1 << 30, ctypes.byref(nch),
+                                  ctypes.byref(nt), cp0.ctypes.data_as(ctypes.c_void_p),
+                                  tp0.ctypes.data_as(ctypes.c_void_p), None, None, None), "gs_analyse")
+    lmax = int(np.diff(cp0).max()) if nch.value else 1
+    T, slots, max_chain = 32, 0, 1
+    for T_ in (256, 128, 64, 32):
+        if T_ > max(32, cfg.max_threads):
+            continue
+        s_ = min((cfg.smem_budget - (T_ // 32) * ring_warp) // 8 - 2, cfg.max_window)
+        if s_ >= T_ * lmax or T_ == 32:
+            T, slots = T_, s_
+            break
+    if slots < 32:
+        raise ValueError(f"GS ring of {ring_warp} bytes per warp does not fit shared memory")
+    T = min(T, max(1, cfg.max_threads))
+    max_chain = max(1, min(cfg.max_chain, lmax, slots // max(32, (T + 31) // 32 * 32)))
     _lib.check(L.mvamg_gs_analyse(n, c_ip, c_ix, max_chain, T, slots, ctypes.byref(nch),
                                   ctypes.byref(nt), None, None, None, None, None), "gs_analyse")
     cp = np.empty(nch.value + 1, dtype=np.int32)
