@@ -155,6 +155,35 @@ int mvamg_gs_level_sweep_folded_f64(int n, const int* indptr, const int* indices
                                     const void* rows, const void* ents, const int* perm,
                                     double* tperm, const double* b, const double* x_old,
                                     double* x_new, int* ws, void* stream);
+/* GS dataflow row schedule for mid-size coarse levels (host).  mode as in
+ * mvamg_gs_levels.  Rows are put in topological order of the sweep's DAG
+ * (level, then longest row first); position p holds row rowid[p] with cnt[p]
+ * entries, diagonal dg[p] and RN(1/diag) rdg[p]; perm[row] = p; crit[p] =
+ * e1 | e2 << 16 (0xffff = none): the entry whose input is published last (the
+ * highest DAG level) and the latest one at least two levels earlier -- the
+ * kernel waits on e2, forms every published product, then waits on e1.  Entries
+ * (CSR order; zero-guess modes keep only the DAG direction) are stored per
+ * warp of 32 positions as an ELL slice: entry u of position 32w + l at
+ * (wofs[w] + u) * 32 + l, padded to the warp's longest row; src is the row of
+ * the value, with bit 31 set for an x_old value (modes 1 and 3).  Query with
+ * rowid == NULL first (*nslots = total slice rows, so coef / src hold
+ * 32 * nslots elements; wofs holds ceil(n/32) + 1 ints). */
+int mvamg_gs_rows(int n, const int* indptr, const int* indices, const double* data, int mode,
+                  long long* nslots, int* nlev, int* rowid, int* cnt, int* crit, double* dg, double* rdg,
+                  int* perm, int* wofs, double* coef, int* src);
+/* One GS sweep with a row schedule of `mode` (gs_row_kernel: one thread per
+ * row over the whole GPU, x_new itself as the ready flag, each row's CSR-order
+ * chain advanced as its inputs are published).  A mode-2 schedule with x_old
+ * runs the folded backward sweep.  threads 32..128 per CTA, ctas resident
+ * CTAs (0 = one per SM); max_tile_slots = the largest slice-row count of any
+ * `threads`-position tile (its entries are staged in 384 * max_tile_slots
+ * bytes of shared memory).  Bit-identical to the serial loop.  tperm: n
+ * doubles of scratch; ws: >= 2 device ints (ticket, status). */
+int mvamg_gs_row_sweep_f64(int mode, int n, const int* indptr, const int* indices, const double* data,
+                           const int* rowid, const int* cnt, const int* crit, const double* dg, const double* rdg,
+                           const int* perm, const int* wofs, const double* coef, const int* src,
+                           int threads, int ctas, int max_tile_slots, double* tperm, const double* b,
+                           const double* x_old, double* x_new, int* ws, void* stream);
 /* z = Inv r, Inv dense row-major n x n (coarsest solve; cycles.py:88-97). */
 int mvamg_dense_gemv_f64(int n, const double* inv, const double* r, double* z, void* stream);
 /* *result = x . y (deterministic two-level reduction; device scalar).
@@ -199,6 +228,12 @@ int mvamg_hierarchy_set_gs_levels(mvamg_hierarchy* h, int k, int mode, int ncta,
                                   int nlev, int max_rows, int max_ents, int threads, const int* lev_ptr,
                                   const int* lev_eptr, const void* rows, const void* ents,
                                   const int* perm, double* tperm);
+/* Dataflow row schedule of level k for sweep `mode` (see mvamg_gs_rows);
+ * used when set and no level-set schedule is set for that mode. */
+int mvamg_hierarchy_set_gs_rows(mvamg_hierarchy* h, int k, int mode, const int* rowid, const int* cnt,
+                                const int* crit, const double* dg, const double* rdg, const int* perm, const int* wofs,
+                                const double* coef, const int* src, int threads, int ctas,
+                                int max_tile_slots, double* tperm);
 /* Transfer k: P (n_k x n_{k+1}) and R = P^T (n_{k+1} x n_k), device CSR. */
 int mvamg_hierarchy_set_transfer(mvamg_hierarchy* h, int k, const int* p_indptr,
                                  const int* p_indices, const double* p_data,

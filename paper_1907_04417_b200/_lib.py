@@ -48,6 +48,9 @@ SIGNATURES = [
                              _P, _P, _P]),
     ("mvamg_gs_level_sweep_f64", _I, [_I, _I, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P,
                                       _P, _P, _P, _P]),
+    ("mvamg_gs_rows", _I, [_I, _P, _P, _P, _I, ctypes.POINTER(_LL), _PI, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    ("mvamg_gs_row_sweep_f64", _I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P,
+                                    _P, _P, _P, _P, _P]),
     ("mvamg_greedy_match", _I, [_LL, _P, _P, _I, _P, _P, _P, ctypes.POINTER(_LL)]),
     ("mvamg_jacobi_svd_batch", _I, [_I, _P, _I, _P, _I, _D, _P, _P, _PI]),
     ("mvamg_gs_level_sweep_folded_f64", _I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P,
@@ -60,6 +63,7 @@ SIGNATURES = [
     ("mvamg_hierarchy_set_level", _I, [_P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _I]),
     ("mvamg_hierarchy_set_gs_schedule", _I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I]),
     ("mvamg_hierarchy_set_gs_levels", _I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
+    ("mvamg_hierarchy_set_gs_rows", _I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P]),
     ("mvamg_hierarchy_set_transfer", _I, [_P, _I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_hierarchy_set_coarse", _I, [_P, _P]),
     ("mvamg_hierarchy_workspace_bytes", _I, [_P, ctypes.POINTER(_LL)]),
@@ -81,8 +85,9 @@ _lib = None
 
 def build(force=False, verbose=False):
     """Compile libmvamg_b200.so in-tree for sm_100a (nvcc cross-compiles; no GPU needed)."""
-    srcs = [SRC, os.path.join(PKG, "csrc", "mvamg_kernels.cuh"),
-            os.path.join(REPO, "include", "mvamg_b200.h")]
+    csrc = os.path.join(PKG, "csrc")
+    srcs = [os.path.join(csrc, f) for f in sorted(os.listdir(csrc)) if f.endswith((".cu", ".cuh", ".h"))]
+    srcs.append(os.path.join(REPO, "include", "mvamg_b200.h"))
     if not force and os.path.exists(SO_PATH):
         so_t = os.path.getmtime(SO_PATH)
         if all(os.path.getmtime(s) <= so_t for s in srcs):

@@ -695,4 +695,176 @@ __global__ void __launch_bounds__(1024, 1) gs_level_kernel(GsLevelArgs a) {
   (void)ncta;
 }
 
+
+// ---------------------------------------------------------------------------
+// Mid-size coarse levels (aggregation operators: 20-80 entries per row, DAG
+// depth in the hundreds, no chain structure): dataflow, one thread per row,
+// rows in topological (level, then longest-first) order handed out to CTAs by
+// a ticket so every dependency lies in an earlier or the same ticket (no
+// deadlock).  x_new itself is the ready flag (sentinel-filled by
+// gs_prepare_kernel).  Each lane advances its row's CSR-order chain as far as
+// its inputs are published -- the chain of a row is consumed eagerly while it
+// waits, so when its last input lands only the tail is left -- and the warp
+// loops until all 32 rows are final, which also makes same-warp dependencies
+// safe.  Entries are stored as per-warp ELL slices (entry u of lane l at
+// (wofs[w] + u) * 32 + l) so every load instruction is one coalesced segment.
+struct GsRowArgs {
+  int n, ntiles;
+  const int* rowid;     // position -> row
+  const int* cnt;       // position -> entries
+  const int* crit;      // position -> (c1 | c2 << 16): entry of the latest input, and of one ~2
+                        // levels earlier (0xffff = none); a lane waits on c2 before its first scan
+  const int* wofs;      // warp -> first slice row (nwarps + 1)
+  const double* coef;   // slices
+  const int* src;       // slices: row of the value; bit 31 set = x_old (sweep from a nonzero guess)
+  const double* dg;     // position -> diagonal
+  const double* rdg;    // position -> RN(1 / diagonal)
+  const double* tperm;  // position -> right-hand side (folded for backward sweeps from x_old)
+  const double* xold;
+  double* xnew;
+  int* ticket;
+  int* status;
+  long long* trace;     // diagnostics: per position, %globaltimer when the row was published, then iterations
+  int debug;            // > 0: nanosleep after a failed poll (ns)
+};
+
+__device__ __forceinline__ long long globaltimer_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// Per tile (blockDim.x consecutive positions) the warps' entry slices are
+// staged into shared memory with cp.async.  Each lane then tracks the next 64
+// entries of its row from the chain position kc with a done-mask: every
+// iteration polls the first 8 still-pending entries (one L2 round trip), turns
+// each published one into its product a_k * x_k in place of the coefficient
+// (a product is its own rounding, independent of order), and runs the
+// CSR-order subtraction chain over the done prefix.  Whichever input lands
+// last (the first upper entry of a backward sweep, the last lower entry of a
+// forward one), only the dependent subtractions remain when it does.  An
+// iteration is ~200 instructions, so a lane re-polls every few hundred cycles.
+template <bool OLD>
+__global__ void __launch_bounds__(128) gs_row_kernel(GsRowArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_tile;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int T = blockDim.x, nwb = T >> 5;
+  const int nwarps = (a.n + 31) >> 5;
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1);
+    __syncthreads();
+    const int tk = s_tile;
+    if (tk >= a.ntiles) return;
+    // stage the tile's slices: coef (8 B) then src (4 B) per entry
+    const int w0 = tk * nwb, w1 = min(w0 + nwb, nwarps);
+    const int sl0 = __ldg(a.wofs + w0), sl1 = __ldg(a.wofs + w1);
+    const int nsl = sl1 - sl0;
+    double* s_coef = reinterpret_cast<double*>(smem);
+    int* s_src = reinterpret_cast<int*>(smem + (size_t)nsl * 256);
+    {
+      const char* gc = reinterpret_cast<const char*>(a.coef + (size_t)sl0 * 32);
+      const char* gs = reinterpret_cast<const char*>(a.src + (size_t)sl0 * 32);
+      for (int c = threadIdx.x; c < nsl * 16; c += T) cp_async16(sbase + 16u * c, gc + 16 * c);
+      const unsigned ss = sbase + (unsigned)nsl * 256u;
+      for (int c = threadIdx.x; c < nsl * 8; c += T) cp_async16(ss + 16u * c, gs + 16 * c);
+      cp_async_commit();
+    }
+    const int p = tk * T + threadIdx.x;
+    const bool have = p < a.n;
+    int i = 0, cnt = 0, kc = 0, wsl = 0;
+    double s = 0.0, dg = 1.0, rdg = 1.0;
+    if (have) {
+      i = __ldg(a.rowid + p);
+      cnt = __ldg(a.cnt + p);
+      s = __ldg(a.tperm + p);
+      dg = __ldg(a.dg + p);
+      rdg = __ldg(a.rdg + p);
+    }
+    if (w0 + warp < w1) wsl = __ldg(a.wofs + w0 + warp) - sl0;
+    cp_async_wait<0>();
+    __syncthreads();
+    double* lc = s_coef + (size_t)wsl * 32 + lane;  // entry e of this lane at lc[32 e]
+    const int* ls = s_src + (size_t)wsl * 32 + lane;
+    bool done = !have;
+    unsigned long long mask = 0;  // bit b: entry kc + b holds its product
+    int sc = 1;                   // background cursor (relative to kc)
+    long long spins = 0, progress = 0;
+    for (;;) {
+      if (!done) {
+        // slot 0 polls the chain's head (the entry blocking it, always
+        // pending); slots 1-7 sweep the other pending entries of the 64-entry
+        // window so products are formed while the head is awaited
+        const int lim = min(cnt - kc, 64);
+        int eb[8];
+        double cf[8];
+        unsigned long long xb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int b = u == 0 ? 0 : sc + u - 1;
+          const bool v = b < lim && !((mask >> b) & 1ull);
+          eb[u] = v ? b : -1;
+          int j = 0;
+          cf[u] = 0.0;
+          if (v) {
+            j = ls[32 * (kc + b)];
+            cf[u] = lc[32 * (kc + b)];
+          }
+          const double* src = a.xnew + j;
+          if (OLD && j < 0) src = a.xold + (j & 0x7fffffff);
+          xb[u] = kSentinel;
+          ld_global_if(xb[u], v, src);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (eb[u] >= 0 && xb[u] != kSentinel) {
+            lc[32 * (kc + eb[u])] = __dmul_rn(cf[u], __longlong_as_double((long long)xb[u]));
+            mask |= 1ull << eb[u];
+          }
+        }
+        const int m = min(lim, (~mask) ? __ffsll((long long)~mask) - 1 : 64);  // done prefix
+        for (int t = 0; t < m; t += 4) {
+          double pv[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) pv[q] = (t + q < m) ? lc[32 * (kc + t + q)] : 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (t + q < m) s = __dsub_rn(s, pv[q]);
+        }
+        kc += m;
+        mask = (m >= 64) ? 0ull : (mask >> m);
+        // after progress, look right behind the new head (where the chain goes
+        // next); while blocked, keep sweeping the window
+        progress += m > 0;
+        sc = m > 0 ? 1 : sc + 7;
+        if (sc >= min(cnt - kc, 64)) sc = 1;
+        if (kc == cnt) {
+          st_relaxed_f64(a.xnew + i, div_rn_markstein(s, dg, rdg));
+          if (a.trace) {
+            a.trace[p] = globaltimer_ns();
+            a.trace[a.n + p] = progress;
+          }
+          done = true;
+        }
+      }
+      if (__all_sync(FULL, done)) break;
+      if ((++spins & 1023) == 0) {
+        bool ab = (*reinterpret_cast<volatile int*>(a.status) & ST_GS_TIMEOUT) != 0;
+        if (spins > kGsIdleLimit) {
+          if (lane == 0) atomicOr(a.status, ST_GS_TIMEOUT);
+          ab = true;
+        }
+        if (__any_sync(FULL, ab)) break;
+      }
+    }
+  }
+}
+
 }  // namespace mvamg

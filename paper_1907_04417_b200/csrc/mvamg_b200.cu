@@ -49,6 +49,10 @@ int g_gs_debug = [] {
   const char* e = getenv("MVAMG_GS_DEBUG");
   return e ? atoi(e) : 0;
 }();  // kernels launched by this library (graph nodes counted per replay)
+int g_row_sleep = [] {
+  const char* e = getenv("MVAMG_ROW_SLEEP");
+  return e ? atoi(e) : 0;
+}();
 
 int num_sms() {
   if (g_num_sms == 0) {
@@ -137,6 +141,21 @@ struct GsLevels {
   const int* perm = nullptr;
   double* tperm = nullptr;
   int nlev = 0, max_rows = 0, max_ents = 0, threads = 256;
+};
+
+// Dataflow row schedule (gs_row_kernel) of one sweep mode.
+struct GsRows {
+  int mode = 0, threads = 128, ctas = 0, max_tile_slots = 0;
+  const int* rowid = nullptr;
+  const int* cnt = nullptr;
+  const int* crit = nullptr;
+  const int* wofs = nullptr;
+  const double* coef = nullptr;
+  const int* src = nullptr;
+  const double* dg = nullptr;
+  const double* rdg = nullptr;
+  const int* perm = nullptr;
+  double* tperm = nullptr;
 };
 
 struct Smoother {
@@ -319,6 +338,61 @@ int launch_gs_levels(const Csr& A, const GsLevels& g, bool zero, const double* b
   return 0;
 }
 
+bool g_row_attr = false;
+// Dataflow row sweep: prepare (rhs in position order, fold, sentinel fill,
+// ticket reset), then gs_row_kernel on `ctas` resident CTAs (0 = one per SM).
+int launch_gs_rows(const Csr& A, const GsRows& g, const double* b, const double* xold, double* xnew,
+                   int* ticket, int* status, cudaStream_t s) {
+  const int n = A.n;
+  if (n == 0) return 0;
+  if (!g.rowid) return fail(MVAMG_E_STATE, "gs rows: schedule for this sweep mode was not set");
+  set_kernel_attrs();
+  if (g.threads < 32 || g.threads > 128 || g.threads % 32) return fail(MVAMG_E_ARG, "gs rows: threads must be 32..128");
+  bool fold = false;
+  if (xold) {
+    if (g.mode == 2) fold = true;
+    else if (g.mode == 0) return fail(MVAMG_E_ARG, "gs rows: zero-guess forward schedule with x_old");
+  } else if (g.mode == 1 || g.mode == 3) {
+    return fail(MVAMG_E_ARG, "gs rows: schedule needs x_old");
+  }
+  if (!g_row_attr) {
+    g_row_attr = true;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(gs_row_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+    cudaFuncSetAttribute(gs_row_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+    cudaGetLastError();
+  }
+  const size_t smem = (size_t)g.max_tile_slots * 384;
+  if (smem > (size_t)g_max_dyn_smem) return fail(MVAMG_E_ARG, "gs rows: tile slices exceed shared memory");
+  gs_prepare_kernel<<<grid_for(n), 256, 0, s>>>(n, A.ip, A.ix, A.v, b, xold, g.perm, g.tperm, xnew,
+                                                ticket, fold ? 1 : 0);
+  GsRowArgs a;
+  a.n = n;
+  a.ntiles = (n + g.threads - 1) / g.threads;
+  a.rowid = g.rowid;
+  a.cnt = g.cnt;
+  a.crit = g.crit;
+  a.wofs = g.wofs;
+  a.coef = g.coef;
+  a.src = g.src;
+  a.dg = g.dg;
+  a.rdg = g.rdg;
+  a.tperm = g.tperm;
+  a.xold = xold;
+  a.xnew = xnew;
+  a.ticket = ticket;
+  a.status = status;
+  a.trace = g_gs_trace;
+  a.debug = g_row_sleep;
+  const int grid = std::max(1, std::min(a.ntiles, g.ctas > 0 ? g.ctas : num_sms()));
+  if (g.mode == 1 || g.mode == 3) gs_row_kernel<true><<<grid, g.threads, smem, s>>>(a);
+  else gs_row_kernel<false><<<grid, g.threads, smem, s>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 }  // namespace
 
 // ============================================================================
@@ -331,6 +405,7 @@ struct Level {
   GsPlan plan;
   GsList gl[3];
   GsLevels glv[4];  // small-level single-CTA schedules (used when set)
+  GsRows grw[4];    // dataflow row schedules (used when set and glv is not)
   Csr P, R;  // valid for k < L-1
   double *xa = nullptr, *xb = nullptr, *t = nullptr, *r = nullptr, *z = nullptr;
   double *fr = nullptr, *fx = nullptr, *fp[2] = {nullptr, nullptr}, *fap[2] = {nullptr, nullptr};
@@ -399,6 +474,10 @@ struct mvamg_hierarchy {
           st = launch_gs_levels(l.A, l.glv[2], false, b, x_cur, out, ticket, s, /*fold=*/true);
         } else if (l.glv[lmode].rows) {
           st = launch_gs_levels(l.A, l.glv[lmode], x_cur == nullptr, b, x_cur, out, ticket, s);
+        } else if (!fwd && x_cur != nullptr && l.grw[2].rowid) {
+          st = launch_gs_rows(l.A, l.grw[2], b, x_cur, out, ticket, status_ptr(), s);
+        } else if (l.grw[lmode].rowid) {
+          st = launch_gs_rows(l.A, l.grw[lmode], b, x_cur, out, ticket, status_ptr(), s);
         } else {
           int mode = fwd ? (x_cur == nullptr ? 0 : 1) : 2;
           st = launch_gs(fwd, l.A, l.gl[mode], l.plan, b, x_cur, out, ticket, status_ptr(), s);
@@ -1091,6 +1170,138 @@ int mvamg_hierarchy_set_gs_levels(mvamg_hierarchy* h, int k, int mode, int ncta,
   g.ents = static_cast<const GsLevelEntry*>(ents); g.perm = perm; g.tperm = tperm;
   g.nlev = nlev; g.max_rows = max_rows; g.max_ents = max_ents; g.threads = threads;
   g.ncta = ncta; g.rows_per_cta = rows_per_cta;
+  return 0;
+}
+
+int mvamg_gs_rows(int n, const int* indptr, const int* indices, const double* data, int mode,
+                  long long* nslots, int* nlev, int* rowid, int* cnt, int* crit, double* dg, double* rdg,
+                  int* perm, int* wofs, double* coef, int* src) {
+  if (n < 0 || !indptr || !nslots || !nlev || mode < 0 || mode > 3) return fail(MVAMG_E_ARG, "gs_rows: bad arguments");
+  const bool fwd = mode < 2, zero = (mode % 2) == 0;
+  // level sets of the sweep's dependency DAG
+  std::vector<int> lvl(n > 0 ? n : 1, 0), c(n > 0 ? n : 1, 0);
+  int nl = 0;
+  for (int q = 0; q < n; ++q) {
+    const int i = fwd ? q : n - 1 - q;
+    int m = 0;
+    for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+      const int j = indices[k];
+      if (fwd ? j < i : j > i) m = std::max(m, lvl[j] + 1);
+    }
+    lvl[i] = m;
+    nl = std::max(nl, m + 1);
+  }
+  for (int i = 0; i < n; ++i) {
+    int m = 0;
+    for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+      const int j = indices[k];
+      if (j == i) continue;
+      if (zero && (fwd ? j > i : j < i)) continue;
+      ++m;
+    }
+    c[i] = m;
+  }
+  // topological positions: by level, then longest row first (uniform warps)
+  std::vector<int> order(n > 0 ? n : 1);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.begin() + n, [&](int x, int y) {
+    if (lvl[x] != lvl[y]) return lvl[x] < lvl[y];
+    return c[x] > c[y];
+  });
+  const int nw = (n + 31) / 32;
+  long long tot = 0;
+  for (int w = 0; w < nw; ++w) {
+    int m = 0;
+    for (int l = 0; l < 32 && w * 32 + l < n; ++l) m = std::max(m, c[order[w * 32 + l]]);
+    tot += m;
+  }
+  if (tot * 32 >= (1LL << 31)) return fail(MVAMG_E_ARG, "gs_rows: too many entries");
+  *nslots = tot;
+  *nlev = n > 0 ? nl : 0;
+  if (!rowid) return 0;
+  long long off = 0;
+  for (int w = 0; w < nw; ++w) {
+    int m = 0;
+    for (int l = 0; l < 32 && w * 32 + l < n; ++l) m = std::max(m, c[order[w * 32 + l]]);
+    wofs[w] = (int)off;
+    for (int l = 0; l < 32; ++l) {
+      const int p = w * 32 + l;
+      int u = 0;
+      if (p < n) {
+        const int i = order[p];
+        rowid[p] = i;
+        cnt[p] = c[i];
+        perm[i] = p;
+        double dgv = 0.0;
+        int lmax = -1, e1 = -1;
+        for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+          const int j = indices[k];
+          if (j == i) { dgv = data[k]; continue; }
+          const bool isnew = fwd ? j < i : j > i;
+          if (zero && !isnew) continue;
+          const size_t e = (size_t)(off + u) * 32 + l;
+          coef[e] = data[k];
+          src[e] = isnew ? j : (int)(0x80000000u | (unsigned)j);
+          if (isnew && lvl[j] >= lmax) { lmax = lvl[j]; e1 = u; }
+          ++u;
+        }
+        // wait hints: e1 = the entry of the latest input; e2 = the latest one
+        // at least two levels earlier (the pre-scan trigger)
+        int e2 = -1, l2 = -1;
+        {
+          int uu = 0;
+          for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+            const int j = indices[k];
+            if (j == i) continue;
+            const bool isnew = fwd ? j < i : j > i;
+            if (zero && !isnew) continue;
+            if (isnew && lvl[j] <= lmax - 2 && lvl[j] > l2) { l2 = lvl[j]; e2 = uu; }
+            ++uu;
+          }
+        }
+        if (u >= 0xffff) e1 = e2 = -1;
+        crit[p] = (e1 < 0 ? 0xffff : e1) | ((e2 < 0 ? 0xffff : e2) << 16);
+        dg[p] = dgv;
+        rdg[p] = 1.0 / dgv;
+      }
+      for (; u < m; ++u) {  // padding
+        const size_t e = (size_t)(off + u) * 32 + l;
+        coef[e] = 0.0;
+        src[e] = 0;
+      }
+    }
+    off += m;
+  }
+  wofs[nw] = (int)off;
+  return 0;
+}
+
+int mvamg_gs_row_sweep_f64(int mode, int n, const int* indptr, const int* indices, const double* data,
+                           const int* rowid, const int* cnt, const int* crit, const double* dg, const double* rdg,
+                           const int* perm, const int* wofs, const double* coef, const int* src,
+                           int threads, int ctas, int max_tile_slots, double* tperm, const double* b,
+                           const double* x_old, double* x_new, int* ws, void* stream) {
+  if (mode < 0 || mode > 3) return fail(MVAMG_E_ARG, "gs rows: bad mode");
+  set_kernel_attrs();
+  if (x_old != nullptr && x_old == x_new) return fail(MVAMG_E_ARG, "gs rows: x_new must not alias x_old");
+  Csr A;
+  A.n = n; A.ip = indptr; A.ix = indices; A.v = data;
+  GsRows g;
+  g.mode = mode; g.threads = threads; g.ctas = ctas; g.max_tile_slots = max_tile_slots;
+  g.rowid = rowid; g.cnt = cnt; g.crit = crit; g.wofs = wofs;
+  g.coef = coef; g.src = src; g.dg = dg; g.rdg = rdg; g.perm = perm; g.tperm = tperm;
+  return launch_gs_rows(A, g, b, x_old, x_new, ws, ws + 1, (cudaStream_t)stream);
+}
+
+int mvamg_hierarchy_set_gs_rows(mvamg_hierarchy* h, int k, int mode, const int* rowid, const int* cnt,
+                                const int* crit, const double* dg, const double* rdg, const int* perm, const int* wofs,
+                                const double* coef, const int* src, int threads, int ctas,
+                                int max_tile_slots, double* tperm) {
+  if (!h || k < 0 || k >= h->L || mode < 0 || mode > 3) return fail(MVAMG_E_ARG, "set_gs_rows: bad index");
+  GsRows& g = h->lv[k].grw[mode];
+  g.mode = mode; g.threads = threads; g.ctas = ctas; g.max_tile_slots = max_tile_slots;
+  g.rowid = rowid; g.cnt = cnt; g.crit = crit; g.wofs = wofs;
+  g.coef = coef; g.src = src; g.dg = dg; g.rdg = rdg; g.perm = perm; g.tperm = tperm;
   return 0;
 }
 

@@ -16,7 +16,8 @@ import scipy.linalg
 import scipy.sparse.linalg as spla
 
 from . import _lib
-from .device import (DeviceCSR, DeviceGsLevels, DeviceGsPlan, GpuConfig, as_csr, level_gs_fits, ptr,
+from .device import (DeviceCSR, DeviceGsLevels, DeviceGsPlan, DeviceGsRows, GpuConfig, as_csr,
+                     level_gs_fits, ptr, row_gs_fits,
                      stream_handle, to_device, torch_cuda)
 from .exceptions import NotSpdError
 
@@ -161,6 +162,16 @@ class GpuMultigridOperator:
             if k < nl - 1:
                 dd = to_device(self.diagonals[k], np.float64)
                 self._keep.append(dd)
+                if row_gs_fits(A, k, self.config):
+                    # dataflow row sweeps over the whole GPU; no wavefront schedule needed
+                    rows = {m: DeviceGsRows(A, m, self.config) for m in self._gs_level_modes()}
+                    self.gs_plans.append(None)
+                    self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=None, rows=rows))
+                    _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
+                                                           None, 0, None, None, 32, 0), "set_level")
+                    for m, s in rows.items():
+                        _lib.check(L.mvamg_hierarchy_set_gs_rows(h, k, m, *s.hierarchy_args()), "set_gs_rows")
+                    continue
                 small = None
                 if level_gs_fits(A, self.config):
                     try:

@@ -73,6 +73,11 @@ class GpuConfig:
     level_stage_bytes: int = 32768  # minimum staging buffer per level (else a larger cluster)
     force_level_gs: bool = False    # use it for every small level (tests / diagnostics)
     smem_limit: int = 227 * 1024 - 1024
+    row_gs_min_rows: int = 10000    # coarse levels at least this large use the dataflow row sweep
+    row_gs_threads: int = 128       # threads per CTA of the row sweep
+    row_gs_ctas: int = 0            # resident CTAs of the row sweep (0 = auto)
+    row_gs_smem: int = 96 * 1024    # staged entry slices per row-sweep tile (halve threads above)
+    force_row_gs: bool = False      # use the row sweep for every coarse level (tests / diagnostics)
 
 
 class DeviceCSR:
@@ -395,6 +400,88 @@ class DeviceGsLevels:
         _lib.check(_lib.load().mvamg_gs_level_sweep_f64(
             0 if self.mode < 2 else 1, self.n, *self._csr.ptrs(), *self.args(), ptr(b), ptr(x_old),
             ptr(x_new), ptr(ws), stream or stream_handle()), "gs_level_sweep")
+
+
+class DeviceGsRows:
+    """Dataflow GS row schedule (gs_row_kernel) of one matrix and sweep mode
+    (0 fwd from x=0, 1 fwd, 2 bwd from x=0 -- also the folded backward sweep
+    from x_old --, 3 bwd), on the device."""
+
+    def __init__(self, A, mode, cfg=None):
+        import torch
+
+        cfg = cfg or GpuConfig()
+        A = as_csr(A)
+        L = _lib.load()
+        n = A.shape[0]
+        ip = np.ascontiguousarray(A.indptr, dtype=np.int32)
+        ix = np.ascontiguousarray(A.indices, dtype=np.int32)
+        v = np.ascontiguousarray(A.data, dtype=np.float64)
+        vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        ns, nlev = ctypes.c_longlong(), ctypes.c_int()
+        _lib.check(L.mvamg_gs_rows(n, vp(ip), vp(ix), vp(v), int(mode), ctypes.byref(ns), ctypes.byref(nlev),
+                                   None, None, None, None, None, None, None, None, None), "gs_rows")
+        nw = -(-n // 32)
+        rowid = np.empty(max(1, n), dtype=np.int32)
+        cnt = np.empty(max(1, n), dtype=np.int32)
+        crit = np.empty(max(1, n), dtype=np.int32)
+        dg = np.empty(max(1, n), dtype=np.float64)
+        rdg = np.empty(max(1, n), dtype=np.float64)
+        perm = np.empty(max(1, n), dtype=np.int32)
+        wofs = np.empty(nw + 1, dtype=np.int32)
+        coef = np.empty(max(32, 32 * ns.value), dtype=np.float64)
+        src = np.empty(max(32, 32 * ns.value), dtype=np.int32)
+        _lib.check(L.mvamg_gs_rows(n, vp(ip), vp(ix), vp(v), int(mode), ctypes.byref(ns), ctypes.byref(nlev),
+                                   vp(rowid), vp(cnt), vp(crit), vp(dg), vp(rdg), vp(perm), vp(wofs), vp(coef),
+                                   vp(src)),
+                   "gs_rows")
+        self.n, self.mode, self.nlev, self.nslots = n, mode, nlev.value, ns.value
+        # threads per tile: the configured width, halved while the widest
+        # tile's staged slices (384 B per slice row) exceed the budget
+        T = int(cfg.row_gs_threads)
+        while True:
+            nwb = T // 32
+            ends = np.minimum(np.arange(0, nw + nwb, nwb), nw)
+            mts = int(np.diff(wofs[ends]).max(initial=0))
+            if 384 * mts <= cfg.row_gs_smem or T == 32:
+                break
+            T //= 2
+        if 384 * mts > cfg.smem_limit:
+            raise ValueError("gs rows: a warp's entry slices exceed shared memory")
+        self.threads, self.max_tile_slots = T, mts
+        if cfg.row_gs_ctas > 0:
+            self.ctas = int(cfg.row_gs_ctas)
+        else:  # keep ~16 levels of rows in flight: enough to cover the dependency latency, few idle pollers
+            per_level = n / max(1, self.nlev)
+            self.ctas = int(min(4 * 148, max(8, np.ceil(16 * per_level / self.threads))))
+        self.rowid, self.cnt, self.dg, self.rdg = to_device(rowid), to_device(cnt), to_device(dg), to_device(rdg)
+        self.crit = to_device(crit)
+        self.perm, self.wofs, self.coef, self.src = to_device(perm), to_device(wofs), to_device(coef), to_device(src)
+        self.tperm = torch.empty(max(2, n + 2), dtype=torch.float64, device="cuda")
+        self._csr = DeviceCSR(A)
+
+    def args(self):
+        return (ptr(self.rowid), ptr(self.cnt), ptr(self.crit), ptr(self.dg), ptr(self.rdg), ptr(self.perm),
+                ptr(self.wofs), ptr(self.coef), ptr(self.src), self.threads, self.ctas, self.max_tile_slots,
+                ptr(self.tperm))
+
+    def hierarchy_args(self):
+        return self.args()
+
+    def sweep(self, b, x_old, x_new, ws, stream=None):
+        """One sweep; with x_old a mode-2 schedule runs the folded backward sweep."""
+        _lib.check(_lib.load().mvamg_gs_row_sweep_f64(
+            self.mode, self.n, *self._csr.ptrs(), *self.args(), ptr(b), ptr(x_old), ptr(x_new), ptr(ws),
+            stream or stream_handle()), "gs_row_sweep")
+
+
+def row_gs_fits(A, k, cfg):
+    """Whether a coarse level (k >= 1) should use the dataflow row sweep."""
+    if k == 0 or cfg.generic_gs or cfg.force_level_gs:
+        return False
+    if cfg.force_row_gs:
+        return True
+    return A.shape[0] >= cfg.row_gs_min_rows
 
 
 def level_gs_fits(A, cfg):

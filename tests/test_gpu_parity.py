@@ -208,6 +208,45 @@ def test_gs_level_kernel_bit_exact(mv, c1, cluster):
                 assert np.array_equal(got, want), (name, direction, zero, cluster)
 
 
+def _gs_row_gpu(A, b, x_old, direction, zero, cfg=None, fold=False):
+    import torch
+    from paper_1907_04417_b200.device import DeviceGsRows
+
+    A = sp.csr_matrix(A)
+    mode = (0 if direction == "forward" else 2) + (0 if (zero or fold) else 1)
+    rw = DeviceGsRows(A, mode, cfg)
+    xn = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+    ws = torch.zeros(8, dtype=torch.int32, device="cuda")
+    rw.sweep(_dev(b), None if zero else _dev(x_old), xn, ws)
+    torch.cuda.synchronize()
+    assert int(ws[1].item()) == 0, "gs row sweep timed out"
+    return xn.cpu().numpy()
+
+
+@pytest.mark.parametrize("cfg", [None, dict(row_gs_threads=32, row_gs_ctas=1), dict(row_gs_threads=64, row_gs_ctas=3)])
+def test_gs_row_kernel_bit_exact(mv, c1, cfg):
+    """The dataflow row sweep (one thread per row, eager CSR-order chains,
+    ticketed CTAs; a single resident CTA exercises same-CTA dependencies) in
+    all four modes and folded, on every structure and the C1 levels."""
+    config = mv.GpuConfig(**cfg) if cfg else None
+    rng = np.random.default_rng(13)
+    mats = c1[1]
+    cases = list(_structures()) + [("c1_l1", mats[1]), ("c1_l2", mats[2]), ("c1_l0", mats[0])]
+    for name, A in cases:
+        n = A.shape[0]
+        b = rng.standard_normal(n)
+        x0 = rng.standard_normal(n)
+        for direction in ("forward", "backward"):
+            for zero in (True, False):
+                want = np.zeros(n) if zero else x0.copy()
+                oracle_gs(A, b, want, direction)
+                got = _gs_row_gpu(A, b, x0, direction, zero, config)
+                assert np.array_equal(got, want), (name, direction, zero, cfg)
+                if direction == "backward" and not zero:
+                    folded = _gs_row_gpu(A, b, x0, direction, zero, config, fold=True)
+                    assert np.array_equal(folded, want), (name, "folded", cfg)
+
+
 def test_gs_hand_recurrence(mv):
     # pkg/tests/test_cycles.py:30-38
     A = laplacian_1d(3)
@@ -226,7 +265,7 @@ def test_vcycle_matches_reference(c1):
 
 
 @pytest.mark.parametrize("cfg", [dict(force_level_gs=True), dict(level_gs_max_rows=0),
-                                 dict(generic_gs=True)])
+                                 dict(generic_gs=True), dict(force_row_gs=True)])
 def test_vcycle_schedules_agree(mv, c1, cfg):
     """Level-set, wavefront and generic GS schedules give the same cycle."""
     d, mats, pros, op, _ = c1
