@@ -10,6 +10,7 @@ from .composite import (
     GpuCompositePreconditioner,
     a_norm,
     apply_composite_symmetrized,
+    gpu_composite_of,
     test_phase,
 )
 from .cycles import (
@@ -23,12 +24,13 @@ from .cycles import (
 from .device import DeviceCSR, GpuConfig, as_csr, gs_analyse
 from .exceptions import AmgError, DeviceError, NotSpdError
 from .krylov import SolveReport, pcg
+from .estimator import MultiVectorAMG
 
 MultigridOperator = GpuMultigridOperator
 
 __all__ = [
     "build", "load", "GpuComposite", "GpuCompositePreconditioner", "a_norm",
-    "apply_composite_symmetrized", "test_phase", "GS_BACKWARD", "GS_FORWARD",
+    "apply_composite_symmetrized", "gpu_composite_of", "test_phase", "MultiVectorAMG", "GS_BACKWARD", "GS_FORWARD",
     "WEIGHTED_JACOBI", "CycleSpec", "GpuMultigridOperator", "MultigridOperator",
     "SmootherSpec", "DeviceCSR", "GpuConfig", "as_csr", "gs_analyse", "AmgError",
     "DeviceError", "NotSpdError", "SolveReport", "pcg",
