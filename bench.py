@@ -221,6 +221,20 @@ def run_reference(args, world, rank):
     print(json.dumps(out), flush=True)
 
 
+def measured_traffic(config, kernel):
+    """DRAM bytes (read + write) per launch of the roofline kernel from the
+    committed ncu --set full capture of this configuration, else None."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        table = json.load(open(path))
+    except (OSError, ValueError):
+        return None
+    for key, ent in table.get(config.lower(), {}).items():
+        if kernel.startswith(key):
+            return ent.get("dram_bytes")
+    return None
+
+
 def run_b200(args, world, rank, local):
     import ctypes
 
@@ -232,12 +246,10 @@ def run_b200(args, world, rank, local):
     from paper_1907_04417_b200.roofline import (cycle_bytes, gs_sweep_bytes, measured_peak_gbs,
                                                 pcg_iteration_bytes)
 
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
+    from paper_1907_04417_b200 import replicas
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dist = replicas.init("nccl", torch.device("cuda", local))
     L = _lib.load()
     mats, pros, b, desc, info = load_workload(args.config)
     n = mats[0].shape[0]
@@ -290,11 +302,7 @@ def run_b200(args, world, rank, local):
     torch.cuda.synchronize()
     launches = ctypes.c_longlong()
     L.mvamg_kernel_launches(ctypes.byref(launches), 1)
-    t_solve = tot / steps
-    if dist:
-        tt = torch.tensor([t_solve], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_solve = float(tt.item())
+    t_solve = replicas.max_over_ranks(tot / steps, dist, "cuda")
     n_iters = nit.value
     # ---- e2e: same solve through the C ABI with host buffers ------------------
     b_host = torch.from_numpy(b.copy()).pin_memory()
@@ -321,11 +329,7 @@ def run_b200(args, world, rank, local):
         e1.record(stream)
         e1.synchronize()
         tot += e0.elapsed_time(e1) / 1e3
-    t_e2e = tot / steps
-    if dist:
-        tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_e2e = float(tt.item())
+    t_e2e = replicas.max_over_ranks(tot / steps, dist, "cuda")
     clocks = sampler.stop()
     # ---- one V-cycle and the dominant kernel (fine-level GS sweep) -----------
     reps = 50
@@ -387,7 +391,7 @@ def run_b200(args, world, rank, local):
             "nit": n_iters, "converged": bool(conv.value), "fit_s": info.get("fit_s"),
             "bootstrap_stages": info.get("bootstrap_stages"),
             "l2": "flushed (256 MiB write) before every timed step" if small else "inputs larger than L2",
-            "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (one per GPU)",
+            "parallelism": replicas.parallelism(world),
         },
         "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n + 8 * (n_iters + 1)},
@@ -398,7 +402,8 @@ def run_b200(args, world, rank, local):
                       "frac": it_bytes * n_iters / t_solve / 1e9 / peak},
         "roofline": {"bound": "hbm", "kernel": gs_kernel,
                      "achieved": gs_gbs, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                     "frac": gs_gbs / peak, "traffic": None, "algorithmic_bytes": gs_bytes,
+                     "frac": gs_gbs / peak, "traffic": measured_traffic(args.config, gs_kernel),
+                     "algorithmic_bytes": gs_bytes,
                      "ms": t_gs * 1e3},
         "clocks": clocks,
     }
