@@ -455,18 +455,59 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
       parity ^= 1u << d;
       ++consumed;
       const double* rhs = reinterpret_cast<const double*>(slot + RW) + lane;
+      // Phase A (independent of the sweep's progress): every field of the
+      // chunk's R rounds into registers, and the cross-tile values (code 2)
+      // requested at once -- one L2 round trip per chunk, not per round.
+      int ty[R][C];  // source type per entry (0 chain predecessor, 1 window, 2 other tile, 3 none)
+      unsigned ix[R][C];
+      double av[R][C], rb[R], dgv[R], rdv[R];
+      unsigned long long gv[R][C];
+      bool act[R];
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
         const unsigned long long* rec = slot + rr * 32 * S + lane;
         const int cnt = (int)((unsigned)rec[0] & 0xffffu);
-        const bool active = cnt != (int)kGsNoRow;
-        const int ca = active ? cnt : 0;
-        double av[C], xv[C];
-        bool ready = gs_lean_gather<C>(rec, ca, sbase, a.xnew, xprev, av, xv);
+        act[rr] = cnt != (int)kGsNoRow;
+        const int ca = act[rr] ? cnt : 0;
+        rb[rr] = rhs[rr * 32];
+        dgv[rr] = __longlong_as_double((long long)rec[32]);
+        rdv[rr] = __longlong_as_double((long long)rec[64]);
+#pragma unroll
+        for (int u = 0; u < C; ++u) {
+          const bool in = u < ca;
+          const unsigned code = in ? (unsigned)rec[32 * (4 + 2 * u)] : 0u;
+          av[rr][u] = in ? __longlong_as_double((long long)rec[32 * (3 + 2 * u)]) : 0.0;
+          ty[rr][u] = in ? (int)(code & 3u) : 3;
+          ix[rr][u] = code >> 2;
+          gv[rr][u] = kSentinel;
+          ld_global_if(gv[rr][u], ty[rr][u] == 2, a.xnew + ix[rr][u]);
+        }
+      }
+      // Phase B: per round only the dependent part -- fresh window values,
+      // products, the CSR-order subtraction chain, the division, the stores.
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        double xv[C];
+        bool ready = true;
+#pragma unroll
+        for (int u = 0; u < C; ++u) {
+          unsigned long long v = ty[rr][u] == 2 ? gv[rr][u] : (unsigned long long)__double_as_longlong(xprev);
+          ld_shared_if(v, ty[rr][u] == 1, sbase + 8u * ix[rr][u]);
+          ready &= gs_published(v);
+          xv[u] = __longlong_as_double((long long)v);
+        }
         if (!__all_sync(FULL, ready)) {
           long long spins = 0;
           do {
-            ready = gs_lean_gather<C>(rec, ca, sbase, a.xnew, xprev, av, xv);
+            ready = true;
+#pragma unroll
+            for (int u = 0; u < C; ++u) {
+              unsigned long long v = (unsigned long long)__double_as_longlong(xprev);
+              ld_shared_if(v, ty[rr][u] == 1, sbase + 8u * ix[rr][u]);
+              ld_global_if(v, ty[rr][u] == 2, a.xnew + ix[rr][u]);
+              ready &= gs_published(v);
+              xv[u] = __longlong_as_double((long long)v);
+            }
             if ((++spins & 255) == 0) {
               bool ab = (*reinterpret_cast<volatile int*>(a.status) & ST_GS_TIMEOUT) != 0;
               if (spins > kGsIdleLimit) {
@@ -478,13 +519,12 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
           } while (!__all_sync(FULL, ready));
           if (abort) break;
         }
-        double sacc = rhs[rr * 32];
+        double sacc = rb[rr];
 #pragma unroll
         for (int u = 0; u < C; ++u)
-          if (u < ca) sacc = __dsub_rn(sacc, __dmul_rn(av[u], xv[u]));
-        if (active) {
-          const double xi = div_rn_markstein(sacc, __longlong_as_double((long long)rec[32]),
-                                             __longlong_as_double((long long)rec[64]));
+          if (ty[rr][u] != 3) sacc = __dsub_rn(sacc, __dmul_rn(av[rr][u], xv[u]));
+        if (act[rr]) {
+          const double xi = div_rn_markstein(sacc, dgv[rr], rdv[rr]);
           wslot[q * TS] = (unsigned long long)__double_as_longlong(xi);
           a.xnew[FWD ? cs + q : ce - 1 - q] = xi;
           xprev = xi;
