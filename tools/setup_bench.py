@@ -22,6 +22,9 @@ for k, lv in enumerate(est.operator_.level_dev):
     if lv.get("levels"):
         s0 = next(iter(lv["levels"].values()))
         how = f"level-set cluster={s0.ncta} nlev={s0.nlev} thr={s0.threads}"
+    elif lv.get("rows"):
+        s0 = next(iter(lv["rows"].values()))
+        how = f"row sweep nlev={s0.nlev} thr={s0.threads} ctas={s0.ctas}"
     else:
         pl = lv["plan"]
         how = f"wavefront lean_C={pl.lean_C} tiles={pl.ntiles} thr={pl.threads} depth={pl.depth}"
@@ -38,6 +41,10 @@ for k, lv in enumerate(est.operator_.level_dev):
         fns = {m: (lambda s=s, m=m: s.sweep(bb, None if m % 2 == 0 else xo, xn, ws)) for m, s in lv["levels"].items()}
         if 2 in lv["levels"]:
             fns[3] = lambda s=lv["levels"][2]: s.sweep(bb, xo, xn, ws, fold=True)
+    elif lv.get("rows"):
+        fns = {m: (lambda s=s, m=m: s.sweep(bb, None if m % 2 == 0 else xo, xn, ws)) for m, s in lv["rows"].items()}
+        if 2 in lv["rows"]:
+            fns[3] = lambda s=lv["rows"][2]: s.sweep(bb, xo, xn, ws)
     else:
         gp = lv["gs"]
         fns = {0: lambda: gp.sweep(0, bb, None, xn, ws), 2: lambda: gp.sweep(1, bb, xo, xn, ws)}
