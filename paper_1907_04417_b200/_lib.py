@@ -12,7 +12,8 @@ from .exceptions import DeviceError, NotSpdError
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
-SO_PATH = os.path.join(PKG, "libmvamg_b200.so")
+# MVAMG_LIB: load a diagnostic build instead (e.g. the round-trace build of tools/lean_trace.py)
+SO_PATH = os.environ.get("MVAMG_LIB") or os.path.join(PKG, "libmvamg_b200.so")
 SRC = os.path.join(PKG, "csrc", "mvamg_b200.cu")
 
 NVCC_FLAGS = [

@@ -29,6 +29,9 @@
 #ifndef MVAMG_GS_PHASES
 #define MVAMG_GS_PHASES 0
 #endif
+#ifndef MVAMG_LEAN_TRACE
+#define MVAMG_LEAN_TRACE 0  // diagnostic build: clock64 per round of the first warp into GsArgs::trace
+#endif
 #if MVAMG_GS_PHASES
 #define GS_STAMP(k) do { if (lane == 0) { long long _t = clock64(); ph_acc[k] += _t - ph_last; ph_last = _t; } } while (0)
 #else
@@ -451,50 +454,62 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
     for (int k = 0; k < nch && !abort; ++k) {
       const int d = k % D;
       const unsigned long long* slot = ringp + d * a.slot_words;
+#if MVAMG_LEAN_TRACE
+      if (a.trace && g == 0 && lane == 0 && k < 2048) a.trace[16384 + 4 * k] = clock64();
+#endif
       while (!mbar_try_wait(bars + 8u * d, (parity >> d) & 1u)) {}
       parity ^= 1u << d;
       ++consumed;
+#if MVAMG_LEAN_TRACE
+      if (a.trace && g == 0 && lane == 0 && k < 2048) a.trace[16384 + 4 * k + 1] = clock64();
+#endif
       const double* rhs = reinterpret_cast<const double*>(slot + RW) + lane;
-      // Phase A (independent of the sweep's progress): every field of the
-      // chunk's R rounds into registers, and the cross-tile values (code 2)
+      // Phase A (independent of the sweep's progress): each entry's source
+      // type and index into registers and the cross-tile values (code 2)
       // requested at once -- one L2 round trip per chunk, not per round.
-      int ty[R][C];  // source type per entry (0 chain predecessor, 1 window, 2 other tile, 3 none)
+      // Coefficients, right-hand side and diagonal are loaded in the round
+      // (independent smem loads, off the dependency chain).
+      unsigned tm[R];  // 2 bits per entry: 0 chain predecessor, 1 window, 2 other tile, 3 none
       unsigned ix[R][C];
-      double av[R][C], rb[R], dgv[R], rdv[R];
       unsigned long long gv[R][C];
-      bool act[R];
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
         const unsigned long long* rec = slot + rr * 32 * S + lane;
         const int cnt = (int)((unsigned)rec[0] & 0xffffu);
-        act[rr] = cnt != (int)kGsNoRow;
-        const int ca = act[rr] ? cnt : 0;
-        rb[rr] = rhs[rr * 32];
-        dgv[rr] = __longlong_as_double((long long)rec[32]);
-        rdv[rr] = __longlong_as_double((long long)rec[64]);
+        const int ca = cnt != (int)kGsNoRow ? cnt : 0;
+        tm[rr] = 0u;
 #pragma unroll
         for (int u = 0; u < C; ++u) {
           const bool in = u < ca;
           const unsigned code = in ? (unsigned)rec[32 * (4 + 2 * u)] : 0u;
-          av[rr][u] = in ? __longlong_as_double((long long)rec[32 * (3 + 2 * u)]) : 0.0;
-          ty[rr][u] = in ? (int)(code & 3u) : 3;
+          const unsigned t = in ? (code & 3u) : 3u;
+          tm[rr] |= t << (2 * u);
           ix[rr][u] = code >> 2;
           gv[rr][u] = kSentinel;
-          ld_global_if(gv[rr][u], ty[rr][u] == 2, a.xnew + ix[rr][u]);
+          ld_global_if(gv[rr][u], t == 2u, a.xnew + ix[rr][u]);
         }
       }
+#if MVAMG_LEAN_TRACE
+      if (a.trace && g == 0 && lane == 0 && k * R < 8192) a.trace[2 * (k * R)] = clock64();
+#endif
       // Phase B: per round only the dependent part -- fresh window values,
       // products, the CSR-order subtraction chain, the division, the stores.
+      // Absent entries have a zero coefficient in the uniform record and a
+      // zero value: s - (+0) == s exactly, so the chain needs no selects.
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
-        double xv[C];
+        const unsigned long long* rec = slot + rr * 32 * S + lane;
+        const bool active = ((unsigned)rec[0] & 0xffffu) != kGsNoRow;
+        double av[C], xv[C];
         bool ready = true;
 #pragma unroll
         for (int u = 0; u < C; ++u) {
-          unsigned long long v = ty[rr][u] == 2 ? gv[rr][u] : (unsigned long long)__double_as_longlong(xprev);
-          ld_shared_if(v, ty[rr][u] == 1, sbase + 8u * ix[rr][u]);
-          ready &= gs_published(v);
-          xv[u] = __longlong_as_double((long long)v);
+          const unsigned t = (tm[rr] >> (2 * u)) & 3u;
+          av[u] = __longlong_as_double((long long)rec[32 * (3 + 2 * u)]);
+          unsigned long long v = t == 2u ? gv[rr][u] : (unsigned long long)__double_as_longlong(xprev);
+          ld_shared_if(v, t == 1u, sbase + 8u * ix[rr][u]);
+          ready &= t == 3u || gs_published(v);
+          xv[u] = t == 3u ? 0.0 : __longlong_as_double((long long)v);
         }
         if (!__all_sync(FULL, ready)) {
           long long spins = 0;
@@ -502,11 +517,12 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
             ready = true;
 #pragma unroll
             for (int u = 0; u < C; ++u) {
+              const unsigned t = (tm[rr] >> (2 * u)) & 3u;
               unsigned long long v = (unsigned long long)__double_as_longlong(xprev);
-              ld_shared_if(v, ty[rr][u] == 1, sbase + 8u * ix[rr][u]);
-              ld_global_if(v, ty[rr][u] == 2, a.xnew + ix[rr][u]);
-              ready &= gs_published(v);
-              xv[u] = __longlong_as_double((long long)v);
+              ld_shared_if(v, t == 1u, sbase + 8u * ix[rr][u]);
+              ld_global_if(v, t == 2u, a.xnew + ix[rr][u]);
+              ready &= t == 3u || gs_published(v);
+              xv[u] = t == 3u ? 0.0 : __longlong_as_double((long long)v);
             }
             if ((++spins & 255) == 0) {
               bool ab = (*reinterpret_cast<volatile int*>(a.status) & ST_GS_TIMEOUT) != 0;
@@ -519,24 +535,30 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
           } while (!__all_sync(FULL, ready));
           if (abort) break;
         }
-        double sacc = rb[rr];
+        double sacc = rhs[rr * 32];
 #pragma unroll
-        for (int u = 0; u < C; ++u)
-          if (ty[rr][u] != 3) sacc = __dsub_rn(sacc, __dmul_rn(av[rr][u], xv[u]));
-        if (act[rr]) {
-          const double xi = div_rn_markstein(sacc, dgv[rr], rdv[rr]);
+        for (int u = 0; u < C; ++u) sacc = __dsub_rn(sacc, __dmul_rn(av[u], xv[u]));
+        if (active) {
+          const double xi = div_rn_markstein(sacc, __longlong_as_double((long long)rec[32]),
+                                             __longlong_as_double((long long)rec[64]));
           wslot[q * TS] = (unsigned long long)__double_as_longlong(xi);
           a.xnew[FWD ? cs + q : ce - 1 - q] = xi;
           xprev = xi;
           ++q;
         }
         __syncwarp();
+#if MVAMG_LEAN_TRACE
+        if (a.trace && g == 0 && lane == 0 && k * R + rr < 8192) a.trace[2 * (k * R + rr) + 1] = clock64();
+#endif
       }
       __syncwarp();
       if (!abort && k + D < nch) {
         issue(k + D);
         ++issued;
       }
+#if MVAMG_LEAN_TRACE
+      if (a.trace && g == 0 && lane == 0 && k < 2048) a.trace[16384 + 4 * k + 3] = clock64();
+#endif
     }
     // an aborted sweep leaves copies in flight: land them before reuse / exit
     for (; consumed < issued; ++consumed) {

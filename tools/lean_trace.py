@@ -1,0 +1,70 @@
+"""Per-round clock64 trace of the lean GS kernel's first warp (diagnostics, GPU).
+
+Builds a separate .so with -DMVAMG_LEAN_TRACE=1 (scratch/), runs one forward
+sweep of a Q1 grid and prints the distribution of round durations and the
+share of chunk-start overhead.
+  python tools/lean_trace.py [grid]
+"""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+so = os.path.join(ROOT, "scratch", "libmvamg_trace.so")
+if not os.environ.get("MVAMG_LIB"):
+    sys.path.insert(0, ROOT)
+    from paper_1907_04417_b200 import _lib as L0
+    os.makedirs(os.path.dirname(so), exist_ok=True)
+    subprocess.run(["nvcc", *L0.NVCC_FLAGS, "-DMVAMG_LEAN_TRACE=1", "-o", so, L0.SRC], check=True)
+    os.environ["MVAMG_LIB"] = so
+    os.execv(sys.executable, [sys.executable] + sys.argv)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+sys.path.insert(0, ROOT)
+from paper_1907_04417_b200 import _lib, problems  # noqa: E402
+from paper_1907_04417_b200.device import DeviceGsPlan, ptr  # noqa: E402
+
+g = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+A = problems.anisotropic_q1(g)
+n = A.shape[0]
+gp = DeviceGsPlan(A)
+print(f"plan: tiles={gp.plan.ntiles} thr={gp.plan.threads} lean_C={gp.plan.lean_C} R={gp.plan.R} D={gp.plan.D}")
+b = torch.randn(n, dtype=torch.float64, device="cuda")
+xn = torch.empty(n, dtype=torch.float64, device="cuda")
+ws = torch.zeros(8, dtype=torch.int32, device="cuda")
+tr = torch.zeros(16384 + 4 * 2048, dtype=torch.int64, device="cuda")
+L = _lib.load()
+for _ in range(3):
+    gp.sweep(0, b, None, xn, ws)
+L.mvamg_gs_set_trace(ptr(tr))
+gp.sweep(0, b, None, xn, ws)
+torch.cuda.synchronize()
+L.mvamg_gs_set_trace(None)
+tt = tr.cpu().numpy()
+t = tt[:16384].reshape(-1, 2)
+ck = tt[16384:].reshape(-1, 4)
+nk = int(np.count_nonzero(ck[:, 0]))
+ck = ck[:nk]
+# 0 top of chunk, 1 after mbarrier wait, (round 0 start stamp), 3 after issue
+st0 = t[np.arange(nk) * gp.plan.R, 0]
+print(f"chunk: mbar wait p50 {np.median(ck[:, 1] - ck[:, 0]):.0f}; phase A p50 {np.median(st0 - ck[:, 1]):.0f}; "
+      f"end-of-chunk issue p50 {np.median(ck[:-1, 3] - t[np.arange(nk - 1) * gp.plan.R + gp.plan.R - 1, 1]):.0f}; "
+      f"loop back p50 {np.median(ck[1:, 0] - ck[:-1, 3]):.0f}")
+R = gp.plan.R
+ends = t[:, 1]
+nr = int(np.count_nonzero(ends))
+ends = ends[:nr]
+starts = t[:nr, 0]
+d = np.diff(ends)
+print(f"rounds traced {nr}; round-to-round cycles: p10 {np.percentile(d, 10):.0f} p50 {np.median(d):.0f} "
+      f"p90 {np.percentile(d, 90):.0f} mean {d.mean():.0f}")
+# chunk structure: rounds k*R..k*R+R-1; start stamp at k*R marks the end of phase A
+k0 = np.arange(0, nr - R, R)
+pa = starts[k0[1:]] - ends[k0[1:] - 1]
+r0 = ends[k0] - starts[k0]
+rin = np.concatenate([np.diff(ends[k:k + R]) for k in k0])
+print(f"phase A (chunk start -> first round begins) cycles: p50 {np.median(pa):.0f} mean {pa.mean():.0f}")
+print(f"first round of chunk cycles: p50 {np.median(r0):.0f}; later rounds: p50 {np.median(rin):.0f} mean {rin.mean():.0f}")
+print("first 40 round ends (delta):", np.diff(ends[:41]).tolist())
