@@ -234,6 +234,12 @@ int mvamg_hierarchy_set_gs_rows(mvamg_hierarchy* h, int k, int mode, const int* 
                                 const int* crit, const double* dg, const double* rdg, const int* perm, const int* wofs,
                                 const double* coef, const int* src, int threads, int ctas,
                                 int max_tile_slots, double* tperm);
+/* Run every level >= k0 of the cycle in one thread block (coarse_mega_kernel:
+ * the K-cycle's nested FCG / V recursion, GS sweeps, transfers and coarsest
+ * solve with no kernel launches inside).  Needs the bound workspace, the
+ * default smoothers and single-CTA level-set schedules (modes 0 and 2) on
+ * levels k0..L-2; k0 < 0 turns it off.  A V-cycle is bit-identical either way. */
+int mvamg_hierarchy_set_mega(mvamg_hierarchy* h, int k0);
 /* Transfer k: P (n_k x n_{k+1}) and R = P^T (n_{k+1} x n_k), device CSR. */
 int mvamg_hierarchy_set_transfer(mvamg_hierarchy* h, int k, const int* p_indptr,
                                  const int* p_indices, const double* p_data,

@@ -65,6 +65,7 @@ SIGNATURES = [
     ("mvamg_hierarchy_set_gs_schedule", _I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I]),
     ("mvamg_hierarchy_set_gs_levels", _I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_hierarchy_set_gs_rows", _I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P]),
+    ("mvamg_hierarchy_set_mega", _I, [_P, _I]),
     ("mvamg_hierarchy_set_transfer", _I, [_P, _I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_hierarchy_set_coarse", _I, [_P, _P]),
     ("mvamg_hierarchy_workspace_bytes", _I, [_P, ctypes.POINTER(_LL)]),

@@ -23,6 +23,7 @@
 
 #include "../../include/mvamg_b200.h"
 #include "mvamg_kernels.cuh"
+#include "coarse_mega.cuh"
 
 using namespace mvamg;
 
@@ -428,6 +429,8 @@ struct mvamg_hierarchy {
   DevScalars* host_sc = nullptr;  // pinned mirror
   std::map<std::string, cudaGraphExec_t> graphs;
   std::map<std::string, int> graph_kernels;
+  int mega_k0 = -1;                 // levels >= mega_k0 run in coarse_mega_kernel (-1: off)
+  MegaLevel* mega_dev = nullptr;
 
   ReduceCtx ctx(FcgScalars* fs = nullptr, double* out = nullptr) const {
     ReduceCtx c;
@@ -444,6 +447,27 @@ struct mvamg_hierarchy {
   ~mvamg_hierarchy() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     if (host_sc) cudaFreeHost(host_sc);
+    if (mega_dev) cudaFree(mega_dev);
+  }
+
+  // ---- the small coarse levels in one block (coarse_mega.cuh) --------------
+  // entry: descend(k0, r) or, on an FCG level, fcg(k0, r); result in `out`.
+  int launch_mega(int k0, const double* r, const double*& out, cudaStream_t s) {
+    MegaArgs a;
+    a.k0 = k0;
+    a.L = L;
+    a.entry_fcg = fcg_level(k0) ? 1 : 0;
+    a.kcycle = kind == MVAMG_CYCLE_K ? 1 : 0;
+    a.inner = inner;
+    a.nL = lv[L - 1].A.n;
+    a.lv = mega_dev;
+    a.inv = inv;
+    a.in = r;
+    a.status = status_ptr();
+    coarse_mega_kernel<<<1, kMegaThreads, 0, s>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    out = a.entry_fcg ? lv[k0].fx : (k0 == L - 1 ? lv[k0].z : lv[k0].xa);
+    return 0;
   }
 
   // ---- smoothing (cycles.py:139-148) ----------------------------------------
@@ -510,7 +534,8 @@ struct mvamg_hierarchy {
     if ((st = launch_spmv(1, l.A, x, r, l.t, s))) return st;     // t = r - A x
     if ((st = launch_spmv(0, l.R, l.t, nullptr, c.r, s))) return st;  // rc = R t
     const double* xc = nullptr;
-    if (fcg_level(k + 1)) st = fcg(k + 1, c.r, xc, s);
+    if (mega_k0 == k + 1) st = launch_mega(k + 1, c.r, xc, s);
+    else if (fcg_level(k + 1)) st = fcg(k + 1, c.r, xc, s);
     else st = descend(k + 1, c.r, xc, s);
     if (st) return st;
     if ((st = launch_spmv(2, l.P, xc, nullptr, x, s))) return st;  // x += P xc
@@ -548,6 +573,7 @@ struct mvamg_hierarchy {
   // z = B r for the level-0 cycle.  `r` must stay valid while the sequence runs.
   int cycle(const double* r, const double*& out, cudaStream_t s) {
     if (L == 1) return coarse(r, out, s);
+    if (mega_k0 == 0) return launch_mega(0, r, out, s);
     return descend(0, r, out, s);
   }
 
@@ -1302,6 +1328,47 @@ int mvamg_hierarchy_set_gs_rows(mvamg_hierarchy* h, int k, int mode, const int* 
   g.mode = mode; g.threads = threads; g.ctas = ctas; g.max_tile_slots = max_tile_slots;
   g.rowid = rowid; g.cnt = cnt; g.crit = crit; g.wofs = wofs;
   g.coef = coef; g.src = src; g.dg = dg; g.rdg = rdg; g.perm = perm; g.tperm = tperm;
+  return 0;
+}
+
+int mvamg_hierarchy_set_mega(mvamg_hierarchy* h, int k0) {
+  if (!h) return fail(MVAMG_E_ARG, "set_mega: null handle");
+  if (k0 < 0) {
+    h->mega_k0 = -1;
+    h->graphs.clear();
+    return 0;
+  }
+  if (k0 > h->L - 2) return fail(MVAMG_E_ARG, "set_mega: k0 must leave at least one level above the coarsest");
+  if (h->L > kMegaMaxLevels) return fail(MVAMG_E_ARG, "set_mega: too many levels");
+  if (!h->bound) return fail(MVAMG_E_STATE, "set_mega: bind the workspace first");
+  if (h->pre.kind != MVAMG_GS_FORWARD || h->pre.sweeps != 1 || h->post.kind != MVAMG_GS_BACKWARD ||
+      h->post.sweeps != 1)
+    return fail(MVAMG_E_ARG, "set_mega: needs the default smoothers (1 forward / 1 backward GS sweep)");
+  std::vector<MegaLevel> ml(h->L);
+  for (int k = k0; k < h->L; ++k) {
+    Level& l = h->lv[k];
+    MegaLevel& m = ml[k];
+    std::memset(&m, 0, sizeof(m));
+    m.n = l.A.n;
+    m.ip = l.A.ip; m.ix = l.A.ix; m.v = l.A.v;
+    m.xa = l.xa; m.t = l.t; m.r = l.r; m.z = l.z; m.fr = l.fr; m.fx = l.fx;
+    m.fp0 = l.fp[0]; m.fp1 = l.fp[1]; m.fap0 = l.fap[0]; m.fap1 = l.fap[1];
+    if (k == h->L - 1) continue;
+    const GsLevels& g0 = l.glv[0];
+    const GsLevels& g2 = l.glv[2];
+    if (!g0.rows || !g2.rows || g0.ncta != 1 || g2.ncta != 1)
+      return fail(MVAMG_E_STATE, "set_mega: level " + std::to_string(k) +
+                                     " needs single-CTA level-set schedules for modes 0 and 2");
+    m.nlev0 = g0.nlev; m.lp0 = g0.lev_ptr; m.rows0 = g0.rows; m.ents0 = g0.ents;
+    m.nlev2 = g2.nlev; m.lp2 = g2.lev_ptr; m.rows2 = g2.rows; m.ents2 = g2.ents;
+    m.rip = l.R.ip; m.rix = l.R.ix; m.rv = l.R.v;
+    m.pip = l.P.ip; m.pix = l.P.ix; m.pv = l.P.v;
+  }
+  if (!h->mega_dev) CUDA_TRY(cudaMalloc(&h->mega_dev, sizeof(MegaLevel) * h->L));
+  CUDA_TRY(cudaMemcpy(h->mega_dev, ml.data(), sizeof(MegaLevel) * h->L, cudaMemcpyHostToDevice));
+  h->mega_k0 = k0;
+  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+  h->graphs.clear();  // recapture with the new cycle
   return 0;
 }
 

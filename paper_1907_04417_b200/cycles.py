@@ -9,6 +9,7 @@ HBM; each application runs one V- or K-cycle in libmvamg_b200.so.
 """
 
 import ctypes
+import dataclasses
 from dataclasses import dataclass
 
 import numpy as np
@@ -156,12 +157,32 @@ class GpuMultigridOperator:
         self.gs_plans = []
         self.level_dev = []
         self._dA = []
+        # small coarse levels: one thread block runs them (coarse_mega_kernel)
+        self.mega_k0 = -1
+        cfg = self.config
+        if (cfg.coarse_mega and not plain and nl >= 2 and not cfg.generic_gs
+                and pre.kind == GS_FORWARD and pre.sweeps == 1 and post.kind == GS_BACKWARD
+                and post.sweeps == 1):
+            k = nl - 2
+            while k >= 0 and self.matrices[k].shape[0] <= cfg.mega_max_rows:
+                k -= 1
+            if k + 1 <= nl - 2:
+                self.mega_k0 = k + 1
         for k, A in enumerate(self.matrices):
             dA = DeviceCSR(A)
             self._dA.append(dA)
             if k < nl - 1:
                 dd = to_device(self.diagonals[k], np.float64)
                 self._keep.append(dd)
+                if 0 <= self.mega_k0 <= k:
+                    small = {m: DeviceGsLevels(A, m, dataclasses.replace(cfg, max_cluster=1)) for m in (0, 2)}
+                    self.gs_plans.append(None)
+                    self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=small, mega=True))
+                    _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
+                                                           None, 0, None, None, 32, 0), "set_level")
+                    for m, s in small.items():
+                        _lib.check(L.mvamg_hierarchy_set_gs_levels(h, k, m, *s.args()), "set_gs_levels")
+                    continue
                 if row_gs_fits(A, k, self.config):
                     # dataflow row sweeps over the whole GPU; no wavefront schedule needed
                     rows = {m: DeviceGsRows(A, m, self.config) for m in self._gs_level_modes()}
@@ -223,6 +244,8 @@ class GpuMultigridOperator:
         self._ws = torch.empty(max(8, nbytes.value), dtype=torch.uint8, device="cuda")
         _lib.check(L.mvamg_hierarchy_bind_workspace(h, ptr(self._ws), stream_handle()), "bind_workspace")
         _lib.check(L.mvamg_hierarchy_set_graphs(h, int(bool(self.config.graphs))), "set_graphs")
+        if self.mega_k0 >= 0:
+            _lib.check(L.mvamg_hierarchy_set_mega(h, self.mega_k0), "set_mega")
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -438,3 +438,47 @@ def test_fit_c1_end_to_end(mv):
     x, rep = est.solve(d["b"], rtol=1e-6)
     assert abs(rep.iterations - int(d["pcg_nit"])) <= 1
     assert abs(est.estimate_convergence_factor() - float(d["rho_est"])) <= 1e-6
+
+
+# ------------------------------------------------------- coarse megakernel ----
+def test_mega_vcycle_bit_identical(mv, c1):
+    """V-cycle through the one-block coarse kernel == the multi-kernel path, bit for bit."""
+    d, mats, pros, _, _ = c1
+    op = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(coarse_mega=True))
+    off = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(coarse_mega=False))
+    assert op.mega_k0 == 1 and off.mega_k0 == -1
+    for key in ("b", "r1"):
+        assert np.array_equal(op.apply(d[key]), off.apply(d[key]))
+    assert np.array_equal(op.error_propagation(d["x2"]), off.error_propagation(d["x2"]))
+
+
+@pytest.mark.parametrize("k0_rows", [2000, 600, 200])
+def test_mega_kcycle_matches(mv, c1, k0_rows):
+    """K-cycles with the megakernel entered at different levels agree with the
+    multi-kernel path (FCG dots differ only in summation order) and with the
+    reference golden."""
+    d, mats = c1[0], c1[1]
+    m, p = hierarchy(d, "c0", fine=mats[0])
+    on = mv.GpuMultigridOperator(m, p, cycle=mv.CycleSpec("K", 2),
+                                 config=mv.GpuConfig(coarse_mega=True, mega_max_rows=k0_rows))
+    off = mv.GpuMultigridOperator(m, p, cycle=mv.CycleSpec("K", 2), config=mv.GpuConfig(coarse_mega=False))
+    assert on.mega_k0 >= 1
+    z_on, z_off = on.apply(d["r3"]), off.apply(d["r3"])
+    assert rel(z_on, z_off) <= 1e-12
+    assert rel(z_on, d["kapply_c0_r3"]) <= TOL_CYCLE
+
+
+def test_mega_composite_pcg(mv, c1):
+    """H2 PCG (symmetrized composite of K-cycles) with and without the
+    megakernel: same iteration count, histories within 1e-10."""
+    d, mats = c1[0], c1[1]
+    res = []
+    for cfg in (mv.GpuConfig(coarse_mega=True), mv.GpuConfig(coarse_mega=False)):
+        ops = []
+        for c in range(int(d["n_comp"])):
+            m, p = hierarchy(d, f"c{c}", fine=mats[0])
+            ops.append(mv.GpuMultigridOperator(m, p, cycle=mv.CycleSpec("K", 2), config=cfg))
+        pc = mv.GpuCompositePreconditioner(mv.GpuComposite(ops))
+        res.append(mv.pcg(mats[0], d["b"], precond=pc, rtol=1e-6)[1])
+    assert res[0].iterations == res[1].iterations == int(d["h2pcg_nit"])
+    assert np.max(np.abs(res[0].residual_history - res[1].residual_history) / res[1].residual_history) <= 1e-10
