@@ -45,6 +45,7 @@ def parse_args():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--config", default=os.environ.get("MVAMG_BENCH_CONFIG", "c2"))
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-h2", action="store_true", help="skip the H2 (composite-preconditioned) solve")
     return p.parse_args()
 
 
@@ -66,7 +67,8 @@ def load_workload(name):
         mats, pros = hierarchy(d, "mv")
         desc = ("C1: 2D Poisson 5-point 128x128 (n=16,384), rhs U[-1,1] seed 0, x0=0, rtol 1e-6; "
                 "hierarchy = reference MultiVectorAMG() defaults (golden fixture)")
-        return mats, pros, d["b"], desc, {"fit_s": None}
+        comps = [hierarchy(d, f"c{c}", fine=mats[0]) for c in range(int(d["n_comp"]))]
+        return mats, pros, d["b"], desc, {"fit_s": None, "components": comps}
     from paper_1907_04417_b200 import problems
     from paper_1907_04417_b200.estimator import MultiVectorAMG
 
@@ -82,8 +84,9 @@ def load_workload(name):
     pros = list(est.hierarchy_.prolongator_matrices)
     desc = (spec["desc"] + "; rhs " + ("body load + seeded noise" if name == "c4" else "U[-1,1] seed 0")
             + ", x0=0, rtol 1e-6; hierarchy = MultiVectorAMG() defaults fitted on the box (setup untimed)")
+    comps = [(c.operator.matrices, c.operator.prolongators) for c in est.composite_.components]
     return mats, pros, b, desc, {"fit_s": fit_s, "bootstrap_stages": est.composite_.n_components,
-                                  "operator_complexity": est.operator_complexity_}
+                                  "operator_complexity": est.operator_complexity_, "components": comps}
 
 
 # -------------------------------------------------------------------- clocks --
@@ -407,6 +410,24 @@ def run_b200(args, world, rank, local):
                      "ms": t_gs * 1e3},
         "clocks": clocks,
     }
+    # ---- H2: PCG preconditioned by the symmetrized multiplicative composite
+    # of the bootstrap K-cycles (bootstrap.py:98-113; the paper's solver) ----
+    if info.get("components") and not args.no_h2:
+        comp_ops = [mv.GpuMultigridOperator(m, p, cycle=mv.CycleSpec("K", 2)) for m, p in info["components"]]
+        pc = mv.GpuCompositePreconditioner(mv.GpuComposite(comp_ops))
+        from paper_1907_04417_b200.krylov import pcg as _pcg
+
+        _, rep = _pcg(mats[0], b, precond=pc, rtol=1e-6)  # warm-up (graphs captured)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, rep = _pcg(mats[0], b, precond=pc, rtol=1e-6)
+        e1.record(stream)
+        e1.synchronize()
+        t_h2 = replicas.max_over_ranks(e0.elapsed_time(e1) / 1e3, dist, "cuda")
+        out["h2"] = {"value": t_h2, "unit": "s", "nit": rep.iterations, "components": len(comp_ops),
+                     "converged": bool(rep.converged), "what": "PCG rtol 1e-6 preconditioned by the "
+                     "symmetrized composite of the bootstrap K-cycles (inner FCG 2); one timed solve"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb, cnit = cpu_baseline(mats, pros, b)
         cb["nit"] = cnit
