@@ -114,7 +114,7 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
  * 2, 4, 8), slot_words (>= R*(32*max_S+32), even) and rec_words_max
  * (R*32*max_S) size the per-warp TMA ring.  lean_C > 0 selects the lean
  * kernel: records built with uniform_S = 3 + 2*lean_C, no x_old sources,
- * (R, D) in {(8,2), (4,4), (2,8), (1,8)}.  ws: device
+ * (R, D) in {(8,3), (8,2), (4,4), (2,8), (1,8)}.  ws: device
  * int workspace (>= 4 ints: tile ticket, status word).  Bit-identical to the
  * serial loop. */
 int mvamg_gs_sweep_f64(int direction, int n, const int* indptr, const int* indices, const double* data,

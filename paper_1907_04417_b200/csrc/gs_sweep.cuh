@@ -450,115 +450,175 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
     int q = 0;
     double xprev = 0.0;
     bool abort = false;
-#pragma unroll 1
-    for (int k = 0; k < nch && !abort; ++k) {
+    // One round: only the dependent part -- fresh window values, products,
+    // the CSR-order subtraction chain, the division, the stores.  Absent
+    // entries have a zero coefficient in the uniform record and a zero value:
+    // s - (+0) == s exactly, so the chain needs no selects.  `tmr`, `ixr`,
+    // `gvr` are the round's staged source types / indices / cross-tile values.
+    auto run_round = [&](const unsigned long long* slot, int rr, unsigned tmr, const unsigned* ixr,
+                         const unsigned long long* gvr) {
+      const unsigned long long* rec = slot + rr * 32 * S + lane;
+      const double* rhs = reinterpret_cast<const double*>(slot + RW) + lane;
+      const bool active = ((unsigned)rec[0] & 0xffffu) != kGsNoRow;
+      double av[C], xv[C];
+      bool ready = true;
+#pragma unroll
+      for (int u = 0; u < C; ++u) {
+        const unsigned t = (tmr >> (2 * u)) & 3u;
+        av[u] = __longlong_as_double((long long)rec[32 * (3 + 2 * u)]);
+        unsigned long long v = t == 2u ? gvr[u] : (unsigned long long)__double_as_longlong(xprev);
+        ld_shared_if(v, t == 1u, sbase + 8u * ixr[u]);
+        ready &= t == 3u || gs_published(v);
+        xv[u] = t == 3u ? 0.0 : __longlong_as_double((long long)v);
+      }
+      if (!__all_sync(FULL, ready)) {
+        long long spins = 0;
+        do {
+          ready = true;
+#pragma unroll
+          for (int u = 0; u < C; ++u) {
+            const unsigned t = (tmr >> (2 * u)) & 3u;
+            unsigned long long v = (unsigned long long)__double_as_longlong(xprev);
+            ld_shared_if(v, t == 1u, sbase + 8u * ixr[u]);
+            ld_global_if(v, t == 2u, a.xnew + ixr[u]);
+            ready &= t == 3u || gs_published(v);
+            xv[u] = t == 3u ? 0.0 : __longlong_as_double((long long)v);
+          }
+          if ((++spins & 255) == 0) {
+            bool ab = (*reinterpret_cast<volatile int*>(a.status) & ST_GS_TIMEOUT) != 0;
+            if (spins > kGsIdleLimit) {
+              if (lane == 0) atomicOr(a.status, ST_GS_TIMEOUT);
+              ab = true;
+            }
+            if (__any_sync(FULL, ab)) { abort = true; break; }
+          }
+        } while (!__all_sync(FULL, ready));
+        if (abort) return;
+      }
+      double sacc = rhs[rr * 32];
+#pragma unroll
+      for (int u = 0; u < C; ++u) sacc = __dsub_rn(sacc, __dmul_rn(av[u], xv[u]));
+      if (active) {
+        const double xi = div_rn_markstein(sacc, __longlong_as_double((long long)rec[32]),
+                                           __longlong_as_double((long long)rec[64]));
+        wslot[q * TS] = (unsigned long long)__double_as_longlong(xi);
+        a.xnew[FWD ? cs + q : ce - 1 - q] = xi;
+        xprev = xi;
+        ++q;
+      }
+      __syncwarp();
+    };
+    // Staging of rounds (independent of the sweep's progress): each entry's
+    // source type and index, and the cross-tile values (code 2) requested at
+    // once -- one L2 round trip per group of rounds, not per round.
+    auto load_codes = [&](const unsigned long long* slot, int rr, unsigned* code) {
+      const unsigned long long* rec = slot + rr * 32 * S + lane;
+      const int cnt = (int)((unsigned)rec[0] & 0xffffu);
+      const int ca = cnt != (int)kGsNoRow ? cnt : 0;
+#pragma unroll
+      for (int u = 0; u < C; ++u) code[u] = u < ca ? (unsigned)rec[32 * (4 + 2 * u)] : 3u;
+    };
+    auto decode = [&](const unsigned* code, unsigned& tmr, unsigned* ixr, unsigned long long* gvr) {
+      tmr = 0u;
+#pragma unroll
+      for (int u = 0; u < C; ++u) {
+        const unsigned t = code[u] & 3u;
+        tmr |= t << (2 * u);
+        ixr[u] = code[u] >> 2;
+        gvr[u] = kSentinel;
+        ld_global_if(gvr[u], t == 2u, a.xnew + ixr[u]);
+      }
+    };
+    auto wait_chunk = [&](int k) {
       const int d = k % D;
-      const unsigned long long* slot = ringp + d * a.slot_words;
-#if MVAMG_LEAN_TRACE
-      if (a.trace && g == 0 && lane == 0 && k < 2048) a.trace[16384 + 4 * k] = clock64();
-#endif
       while (!mbar_try_wait(bars + 8u * d, (parity >> d) & 1u)) {}
       parity ^= 1u << d;
       ++consumed;
-#if MVAMG_LEAN_TRACE
-      if (a.trace && g == 0 && lane == 0 && k < 2048) a.trace[16384 + 4 * k + 1] = clock64();
-#endif
-      const double* rhs = reinterpret_cast<const double*>(slot + RW) + lane;
-      // Phase A (independent of the sweep's progress): each entry's source
-      // type and index into registers and the cross-tile values (code 2)
-      // requested at once -- one L2 round trip per chunk, not per round.
-      // Coefficients, right-hand side and diagonal are loaded in the round
-      // (independent smem loads, off the dependency chain).
-      unsigned tm[R];  // 2 bits per entry: 0 chain predecessor, 1 window, 2 other tile, 3 none
-      unsigned ix[R][C];
-      unsigned long long gv[R][C];
+    };
+    if constexpr (R >= 4 && C <= 2) {
+      // Software-pipelined by half chunks (H rounds): while half h runs, the
+      // codes of the next half are loaded (before its first round) and decoded
+      // with their cross-tile prefetches (after it), so staging latency hides
+      // behind the latency-bound rounds.  (Measured: a win for short records,
+      // 5-point grids 339 -> 305 ns/level; for C = 4 the extra live state costs
+      // more than it hides, so those stage whole chunks below.)
+      constexpr int H = R / 2;
+      unsigned tmA[H], ixA[H][C], tmB[H], ixB[H][C], raw[H][C];
+      unsigned long long gvA[H][C], gvB[H][C];
+      if (nch > 0) {
+        wait_chunk(0);
 #pragma unroll
-      for (int rr = 0; rr < R; ++rr) {
-        const unsigned long long* rec = slot + rr * 32 * S + lane;
-        const int cnt = (int)((unsigned)rec[0] & 0xffffu);
-        const int ca = cnt != (int)kGsNoRow ? cnt : 0;
-        tm[rr] = 0u;
-#pragma unroll
-        for (int u = 0; u < C; ++u) {
-          const bool in = u < ca;
-          const unsigned code = in ? (unsigned)rec[32 * (4 + 2 * u)] : 0u;
-          const unsigned t = in ? (code & 3u) : 3u;
-          tm[rr] |= t << (2 * u);
-          ix[rr][u] = code >> 2;
-          gv[rr][u] = kSentinel;
-          ld_global_if(gv[rr][u], t == 2u, a.xnew + ix[rr][u]);
+        for (int h = 0; h < H; ++h) {
+          load_codes(ringp, h, raw[h]);
+          decode(raw[h], tmA[h], ixA[h], gvA[h]);
         }
       }
-#if MVAMG_LEAN_TRACE
-      if (a.trace && g == 0 && lane == 0 && k * R < 8192) a.trace[2 * (k * R)] = clock64();
-#endif
-      // Phase B: per round only the dependent part -- fresh window values,
-      // products, the CSR-order subtraction chain, the division, the stores.
-      // Absent entries have a zero coefficient in the uniform record and a
-      // zero value: s - (+0) == s exactly, so the chain needs no selects.
+#pragma unroll 1
+      for (int k = 0; k < nch && !abort; ++k) {
+        const unsigned long long* slot = ringp + (k % D) * a.slot_words;
+        // half 0 (stage A); stage B = half 1 of this chunk
 #pragma unroll
-      for (int rr = 0; rr < R; ++rr) {
-        const unsigned long long* rec = slot + rr * 32 * S + lane;
-        const bool active = ((unsigned)rec[0] & 0xffffu) != kGsNoRow;
-        double av[C], xv[C];
-        bool ready = true;
+        for (int h = 0; h < H; ++h) load_codes(slot, H + h, raw[h]);
+        run_round(slot, 0, tmA[0], ixA[0], gvA[0]);
+        if (abort) break;
 #pragma unroll
-        for (int u = 0; u < C; ++u) {
-          const unsigned t = (tm[rr] >> (2 * u)) & 3u;
-          av[u] = __longlong_as_double((long long)rec[32 * (3 + 2 * u)]);
-          unsigned long long v = t == 2u ? gv[rr][u] : (unsigned long long)__double_as_longlong(xprev);
-          ld_shared_if(v, t == 1u, sbase + 8u * ix[rr][u]);
-          ready &= t == 3u || gs_published(v);
-          xv[u] = t == 3u ? 0.0 : __longlong_as_double((long long)v);
-        }
-        if (!__all_sync(FULL, ready)) {
-          long long spins = 0;
-          do {
-            ready = true;
+        for (int h = 0; h < H; ++h) decode(raw[h], tmB[h], ixB[h], gvB[h]);
 #pragma unroll
-            for (int u = 0; u < C; ++u) {
-              const unsigned t = (tm[rr] >> (2 * u)) & 3u;
-              unsigned long long v = (unsigned long long)__double_as_longlong(xprev);
-              ld_shared_if(v, t == 1u, sbase + 8u * ix[rr][u]);
-              ld_global_if(v, t == 2u, a.xnew + ix[rr][u]);
-              ready &= t == 3u || gs_published(v);
-              xv[u] = t == 3u ? 0.0 : __longlong_as_double((long long)v);
-            }
-            if ((++spins & 255) == 0) {
-              bool ab = (*reinterpret_cast<volatile int*>(a.status) & ST_GS_TIMEOUT) != 0;
-              if (spins > kGsIdleLimit) {
-                if (lane == 0) atomicOr(a.status, ST_GS_TIMEOUT);
-                ab = true;
-              }
-              if (__any_sync(FULL, ab)) { abort = true; break; }
-            }
-          } while (!__all_sync(FULL, ready));
+        for (int h = 1; h < H; ++h) {
+          run_round(slot, h, tmA[h], ixA[h], gvA[h]);
           if (abort) break;
         }
-        double sacc = rhs[rr * 32];
+        if (abort) break;
+        // half 1 (stage B); stage A = half 0 of the next chunk
+        const bool more = k + 1 < nch;
+        const unsigned long long* nslot = ringp + ((k + 1) % D) * a.slot_words;
+        if (more) {
+          wait_chunk(k + 1);
 #pragma unroll
-        for (int u = 0; u < C; ++u) sacc = __dsub_rn(sacc, __dmul_rn(av[u], xv[u]));
-        if (active) {
-          const double xi = div_rn_markstein(sacc, __longlong_as_double((long long)rec[32]),
-                                             __longlong_as_double((long long)rec[64]));
-          wslot[q * TS] = (unsigned long long)__double_as_longlong(xi);
-          a.xnew[FWD ? cs + q : ce - 1 - q] = xi;
-          xprev = xi;
-          ++q;
+          for (int h = 0; h < H; ++h) load_codes(nslot, h, raw[h]);
         }
+        run_round(slot, H, tmB[0], ixB[0], gvB[0]);
+        if (abort) break;
+        if (more) {
+#pragma unroll
+          for (int h = 0; h < H; ++h) decode(raw[h], tmA[h], ixA[h], gvA[h]);
+        }
+#pragma unroll
+        for (int h = 1; h < H; ++h) {
+          run_round(slot, H + h, tmB[h], ixB[h], gvB[h]);
+          if (abort) break;
+        }
+        if (abort) break;
         __syncwarp();
-#if MVAMG_LEAN_TRACE
-        if (a.trace && g == 0 && lane == 0 && k * R + rr < 8192) a.trace[2 * (k * R + rr) + 1] = clock64();
-#endif
+        if (k + D < nch) {
+          issue(k + D);
+          ++issued;
+        }
       }
-      __syncwarp();
-      if (!abort && k + D < nch) {
-        issue(k + D);
-        ++issued;
+    } else {
+#pragma unroll 1
+      for (int k = 0; k < nch && !abort; ++k) {
+        const unsigned long long* slot = ringp + (k % D) * a.slot_words;
+        wait_chunk(k);
+        unsigned tmr[R], ixr[R][C], code[C];
+        unsigned long long gvr[R][C];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          load_codes(slot, rr, code);
+          decode(code, tmr[rr], ixr[rr], gvr[rr]);
+        }
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          run_round(slot, rr, tmr[rr], ixr[rr], gvr[rr]);
+          if (abort) break;
+        }
+        if (abort) break;
+        __syncwarp();
+        if (k + D < nch) {
+          issue(k + D);
+          ++issued;
+        }
       }
-#if MVAMG_LEAN_TRACE
-      if (a.trace && g == 0 && lane == 0 && k < 2048) a.trace[16384 + 4 * k + 3] = clock64();
-#endif
     }
     // an aborted sweep leaves copies in flight: land them before reuse / exit
     for (; consumed < issued; ++consumed) {

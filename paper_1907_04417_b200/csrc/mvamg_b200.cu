@@ -96,8 +96,8 @@ void set_kernel_attrs() {
 #define MVAMG_LEAN_ATTR(F, CC, RR, DD) \
   ok &= cudaFuncSetAttribute(gs_lean_kernel<F, CC, RR, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) == cudaSuccess;
 #define MVAMG_LEAN_ATTR_C(F, RR, DD) MVAMG_LEAN_ATTR(F, 2, RR, DD) MVAMG_LEAN_ATTR(F, 4, RR, DD) MVAMG_LEAN_ATTR(F, 8, RR, DD)
-  MVAMG_LEAN_ATTR_C(true, 8, 2) MVAMG_LEAN_ATTR_C(true, 4, 4) MVAMG_LEAN_ATTR_C(true, 2, 8) MVAMG_LEAN_ATTR_C(true, 1, 8)
-  MVAMG_LEAN_ATTR_C(false, 8, 2) MVAMG_LEAN_ATTR_C(false, 4, 4) MVAMG_LEAN_ATTR_C(false, 2, 8) MVAMG_LEAN_ATTR_C(false, 1, 8)
+  MVAMG_LEAN_ATTR_C(true, 8, 3) MVAMG_LEAN_ATTR_C(true, 8, 2) MVAMG_LEAN_ATTR_C(true, 4, 4) MVAMG_LEAN_ATTR_C(true, 2, 8) MVAMG_LEAN_ATTR_C(true, 1, 8)
+  MVAMG_LEAN_ATTR_C(false, 8, 3) MVAMG_LEAN_ATTR_C(false, 8, 2) MVAMG_LEAN_ATTR_C(false, 4, 4) MVAMG_LEAN_ATTR_C(false, 2, 8) MVAMG_LEAN_ATTR_C(false, 1, 8)
 #undef MVAMG_LEAN_ATTR_C
 #undef MVAMG_LEAN_ATTR
   g_max_dyn_smem = ok ? maxsm : 48 * 1024;
@@ -243,7 +243,8 @@ int launch_gs(bool fwd, const Csr& A, const GsList& ls, const GsPlan& p, const d
   } while (0)
 #define MVAMG_LEAN_R(F)                                                           \
   do {                                                                            \
-    if (ls.R >= 8) MVAMG_LEAN_C(F, 8, 2);                                         \
+    if (ls.R >= 8 && ls.D >= 3) MVAMG_LEAN_C(F, 8, 3);                            \
+    else if (ls.R >= 8) MVAMG_LEAN_C(F, 8, 2);                                    \
     else if (ls.R >= 4) MVAMG_LEAN_C(F, 4, 4);                                    \
     else if (ls.R >= 2) MVAMG_LEAN_C(F, 2, 8);                                    \
     else MVAMG_LEAN_C(F, 1, 8);                                                   \
@@ -994,7 +995,7 @@ int mvamg_gs_sweep_f64(int direction, int n, const int* indptr, const int* indic
                        const double* b, const double* x_old, double* x_new, int* ws, void* stream) {
   if (threads < 32 || threads > 256 || threads % 32) return fail(MVAMG_E_ARG, "gs: threads must be 32..256, multiple of 32");
   if (R != 1 && R != 2 && R != 4 && R != 8) return fail(MVAMG_E_ARG, "gs: R must be 1, 2, 4 or 8");
-  if (D != 2 && D != 4 && D != 8) return fail(MVAMG_E_ARG, "gs: D must be 2, 4 or 8");
+  if (D != 2 && D != 3 && D != 4 && D != 8) return fail(MVAMG_E_ARG, "gs: D must be 2, 3, 4 or 8");
   if (x_old != nullptr && x_old == x_new) return fail(MVAMG_E_ARG, "gs: x_new must not alias x_old");
   Csr A;
   A.n = n; A.ip = indptr; A.ix = indices; A.v = data;
@@ -1002,8 +1003,8 @@ int mvamg_gs_sweep_f64(int direction, int n, const int* indptr, const int* indic
   ls.rec = rec; ls.round_off = round_off; ls.tbase = tbase; ls.tile_wbase = tile_wbase; ls.perm = perm;
   ls.tperm = tperm; ls.R = R; ls.D = D; ls.slot_words = slot_words; ls.rec_words_max = rec_words_max;
   ls.lean_C = lean_C;
-  if (lean_C > 0 && ((R == 8 && D != 2) || (R == 4 && D != 4) || (R <= 2 && D != 8)))
-    return fail(MVAMG_E_ARG, "gs: lean kernel ring must be (R, D) in {(8,2), (4,4), (2,8), (1,8)}");
+  if (lean_C > 0 && ((R == 8 && D != 2 && D != 3) || (R == 4 && D != 4) || (R <= 2 && D != 8)))
+    return fail(MVAMG_E_ARG, "gs: lean kernel ring must be (R, D) in {(8,3), (8,2), (4,4), (2,8), (1,8)}");
   GsPlan p;
   p.ntiles = ntiles; p.threads = threads; p.window = window; p.chain_ptr = chain_ptr; p.tile_ptr = tile_ptr;
   return launch_gs(direction == 0, A, ls, p, b, x_old, x_new, ws, ws + 1, (cudaStream_t)stream);

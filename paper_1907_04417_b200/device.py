@@ -113,7 +113,7 @@ class GsPlanHost:
     tile_ptr: np.ndarray
 
 
-LEAN_RINGS = ((8, 2), (4, 4), (2, 8), (1, 8))  # (R, D) pairs the lean kernel is built for
+LEAN_RINGS = ((8, 3), (8, 2), (4, 4), (2, 8), (1, 8))  # (R, D) pairs the lean kernel is built for
 
 
 def _row_counts(A):

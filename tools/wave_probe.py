@@ -39,8 +39,7 @@ def run(A, name, **kw):
 
 for g in (256, 1024):
     A = problems.anisotropic_q1(g)
-    for kw in (dict(), dict(max_threads=32), dict(max_threads=64, ring_bytes=24576),
-               dict(max_threads=32, ring_bytes=24576, max_chain=1024)):
+    for kw in (dict(), dict(ring_bytes=80 * 1024), dict(max_threads=64, ring_bytes=24576)):
         run(A, f"q1_{g}", **kw)
 A = problems.poisson_2d(512)
 for kw in (dict(), dict(max_threads=32)):
