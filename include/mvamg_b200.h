@@ -97,13 +97,17 @@ int mvamg_csr_spmv_add_f64(int n, const int* indptr, const int* indices, const d
  * [coefficient][source code] -- the entries still contributing to the serial
  * loop's sum at sweep time, in CSR order.  Rounds of a warp are padded to a
  * multiple of R; uniform_S > 0 pads every round to that many words (the lean
- * kernel's fixed record size).  perm[i] = 32 * (global round of row i) + lane.  Query with
+ * kernel's fixed record size).  rows_per_round = K > 1 (lean records only)
+ * lets a row share its chain predecessor's round (up to K rows of a lane per
+ * round, K slots of S words each, slot-major) when every other intra-warp
+ * input comes from an earlier round.  perm[i] = 32 * (K * global round + slot)
+ * + lane.  Query with
  * rec == NULL for *nwords / *nrounds / *nwarps / *max_S; then round_off holds
  * nrounds+1, tbase nwarps+1, tile_wbase ntiles+1, perm n ints. */
 int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double* data, int ntiles,
                       const int* chain_ptr, const int* tile_ptr, int window, int mode, int R,
-                      int uniform_S, long long* nwords, int* nrounds, int* nwarps, int* max_S,
-                      unsigned long long* rec, int* round_off, int* tbase, int* tile_wbase,
+                      int uniform_S, int rows_per_round, long long* nwords, int* nrounds, int* nwarps,
+                      int* max_S, unsigned long long* rec, int* round_off, int* tbase, int* tile_wbase,
                       int* perm);
 /* One lexicographic GS sweep (_kernels.py:15-38) on device data.  direction
  * 0 = forward, 1 = backward; x_old is the iterate before the sweep (NULL for a
@@ -113,8 +117,10 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
  * 32 * nrounds doubles.  R (rounds per chunk: 1, 2, 4, 8), D (ring slots:
  * 2, 4, 8), slot_words (>= R*(32*max_S+32), even) and rec_words_max
  * (R*32*max_S) size the per-warp TMA ring.  lean_C > 0 selects the lean
- * kernel: records built with uniform_S = 3 + 2*lean_C, no x_old sources,
- * (R, D) in {(8,3), (8,2), (4,4), (2,8), (1,8)}.  ws: device
+ * kernel: records built with uniform_S = 3 + 2*C, no x_old sources,
+ * (R, D) in {(8,3), (8,2), (4,4), (2,8), (1,8)}; lean_C = C | K << 8 with
+ * K > 1 rows per lane per round (C <= 4, (R, D, K) in {(2,2,4), (2,3,4),
+ * (4,2,2)}).  ws: device
  * int workspace (>= 4 ints: tile ticket, status word).  Bit-identical to the
  * serial loop. */
 int mvamg_gs_sweep_f64(int direction, int n, const int* indptr, const int* indices, const double* data,

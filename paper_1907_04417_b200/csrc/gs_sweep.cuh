@@ -389,10 +389,10 @@ __device__ __forceinline__ bool gs_lean_gather(const unsigned long long* rec, in
   return ready;
 }
 
-template <bool FWD, int C, int R, int D>
+template <bool FWD, int C, int R, int D, int K = 1>
 __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
   constexpr int S = 3 + 2 * C;
-  constexpr int RW = R * 32 * S;  // record words of one chunk
+  constexpr int RW = R * K * 32 * S;  // record words of one chunk (R rounds of K row slots)
   extern __shared__ __align__(16) unsigned long long smem_u64[];
   __shared__ int s_tile;
   const unsigned FULL = 0xffffffffu;
@@ -440,9 +440,9 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
         const size_t gr0 = (size_t)gr_base + (size_t)k * R;
         const unsigned dst = ring + 8u * (unsigned)(d * a.slot_words);
         const unsigned bar = bars + 8u * d;
-        mbar_expect_tx(bar, 8u * RW + 8u * 32u * R);
-        bulk_g2s(dst, a.rec + gr0 * 32 * S, 8u * RW, bar);
-        bulk_g2s(dst + 8u * RW, a.tperm + gr0 * 32, 8u * 32u * R, bar);
+        mbar_expect_tx(bar, 8u * RW + 8u * 32u * R * K);
+        bulk_g2s(dst, a.rec + gr0 * 32 * K * S, 8u * RW, bar);
+        bulk_g2s(dst + 8u * RW, a.tperm + gr0 * 32 * K, 8u * 32u * R * K, bar);
       }
     };
     int issued = 0, consumed = 0;
@@ -535,7 +535,127 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
       parity ^= 1u << d;
       ++consumed;
     };
-    if constexpr (R >= 4 && C <= 2) {
+    if constexpr (K > 1) {
+      // K consecutive rows of each lane's chain per round: every slot's
+      // inputs except the chain predecessor come from earlier rounds, so all
+      // of them are gathered at the round's start; the K short chains then
+      // run back to back with the predecessor in a register.  Opt-in
+      // (GpuConfig.lean_rows_per_round): measured slower on Q1 / 5-point
+      // grids -- a row still costs ~420 cycles, and a lane can only start a
+      // round once the lane above finished its whole round, which doubles
+      // the line-to-line skew of the wavefront (tools/lean_trace.py).
+#pragma unroll 1
+      for (int k = 0; k < nch && !abort; ++k) {
+        const unsigned long long* slot = ringp + (k % D) * a.slot_words;
+        const double* rhs = reinterpret_cast<const double*>(slot + RW) + lane;
+        wait_chunk(k);
+        unsigned tmr[R * K], ixr[R * K][C], code[C];
+        unsigned long long gvr[R * K][C];
+#pragma unroll
+        for (int s = 0; s < R * K; ++s) {
+          load_codes(slot, s, code);
+          decode(code, tmr[s], ixr[s], gvr[s]);
+        }
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          double xv[K][C];
+          bool ready = true;
+#pragma unroll
+          for (int kk = 0; kk < K; ++kk) {
+            const int s = rr * K + kk;
+#pragma unroll
+            for (int u = 0; u < C; ++u) {
+              const unsigned t = (tmr[s] >> (2 * u)) & 3u;
+              unsigned long long v = t == 2u ? gvr[s][u] : 0ull;
+              ld_shared_if(v, t == 1u, sbase + 8u * ixr[s][u]);
+              ready &= t == 0u || t == 3u || gs_published(v);
+              xv[kk][u] = __longlong_as_double((long long)v);
+            }
+          }
+#if MVAMG_LEAN_TRACE
+          long long nspin = 0;
+#endif
+          if (!__all_sync(FULL, ready)) {
+            long long spins = 0;
+            do {
+#if MVAMG_LEAN_TRACE
+              ++nspin;
+#endif
+              ready = true;
+#pragma unroll
+              for (int kk = 0; kk < K; ++kk) {
+                const int s = rr * K + kk;
+#pragma unroll
+                for (int u = 0; u < C; ++u) {
+                  const unsigned t = (tmr[s] >> (2 * u)) & 3u;
+                  unsigned long long v = 0ull;
+                  ld_shared_if(v, t == 1u, sbase + 8u * ixr[s][u]);
+                  ld_global_if(v, t == 2u, a.xnew + ixr[s][u]);
+                  ready &= t == 0u || t == 3u || gs_published(v);
+                  xv[kk][u] = __longlong_as_double((long long)v);
+                }
+              }
+              if ((++spins & 255) == 0) {
+                bool ab = (*reinterpret_cast<volatile int*>(a.status) & ST_GS_TIMEOUT) != 0;
+                if (spins > kGsIdleLimit) {
+                  if (lane == 0) atomicOr(a.status, ST_GS_TIMEOUT);
+                  ab = true;
+                }
+                if (__any_sync(FULL, ab)) { abort = true; break; }
+              }
+            } while (!__all_sync(FULL, ready));
+            if (abort) break;
+          }
+          // every slot's record fields before any store: the ring is read
+          // through generic pointers the compiler cannot separate from the
+          // x_new stores, so loads after a store would be serialised behind it
+          double kav[K][C], krb[K], kdg[K], krd[K];
+          bool kact[K];
+#pragma unroll
+          for (int kk = 0; kk < K; ++kk) {
+            const int s = rr * K + kk;
+            const unsigned long long* rec = slot + s * 32 * S + lane;
+            kact[kk] = ((unsigned)rec[0] & 0xffffu) != kGsNoRow;
+            krb[kk] = rhs[s * 32];
+            kdg[kk] = __longlong_as_double((long long)rec[32]);
+            krd[kk] = __longlong_as_double((long long)rec[64]);
+#pragma unroll
+            for (int u = 0; u < C; ++u) kav[kk][u] = __longlong_as_double((long long)rec[32 * (3 + 2 * u)]);
+          }
+#pragma unroll
+          for (int kk = 0; kk < K; ++kk) {
+            const int s = rr * K + kk;
+            double sacc = krb[kk];
+#pragma unroll
+            for (int u = 0; u < C; ++u) {
+              const unsigned t = (tmr[s] >> (2 * u)) & 3u;
+              const double x = t == 0u ? xprev : xv[kk][u];
+              sacc = __dsub_rn(sacc, __dmul_rn(kav[kk][u], x));
+            }
+            if (kact[kk]) {
+              const double xi = div_rn_markstein(sacc, kdg[kk], krd[kk]);
+              wslot[q * TS] = (unsigned long long)__double_as_longlong(xi);
+              a.xnew[FWD ? cs + q : ce - 1 - q] = xi;
+              xprev = xi;
+              ++q;
+            }
+          }
+          __syncwarp();
+#if MVAMG_LEAN_TRACE
+          if (a.trace && g == 0 && lane == 0 && k * R + rr < 8192) {
+            a.trace[2 * (k * R + rr) + 1] = clock64();
+            a.trace[2 * (k * R + rr)] = nspin;
+          }
+#endif
+        }
+        if (abort) break;
+        __syncwarp();
+        if (k + D < nch) {
+          issue(k + D);
+          ++issued;
+        }
+      }
+    } else if constexpr (R >= 4 && C <= 2) {
       // Software-pipelined by half chunks (H rounds): while half h runs, the
       // codes of the next half are loaded (before its first round) and decoded
       // with their cross-tile prefetches (after it), so staging latency hides

@@ -98,6 +98,14 @@ void set_kernel_attrs() {
 #define MVAMG_LEAN_ATTR_C(F, RR, DD) MVAMG_LEAN_ATTR(F, 2, RR, DD) MVAMG_LEAN_ATTR(F, 4, RR, DD) MVAMG_LEAN_ATTR(F, 8, RR, DD)
   MVAMG_LEAN_ATTR_C(true, 8, 3) MVAMG_LEAN_ATTR_C(true, 8, 2) MVAMG_LEAN_ATTR_C(true, 4, 4) MVAMG_LEAN_ATTR_C(true, 2, 8) MVAMG_LEAN_ATTR_C(true, 1, 8)
   MVAMG_LEAN_ATTR_C(false, 8, 3) MVAMG_LEAN_ATTR_C(false, 8, 2) MVAMG_LEAN_ATTR_C(false, 4, 4) MVAMG_LEAN_ATTR_C(false, 2, 8) MVAMG_LEAN_ATTR_C(false, 1, 8)
+#define MVAMG_LEANK_ATTR(F, CC, RR, DD, KK) \
+  ok &= cudaFuncSetAttribute(gs_lean_kernel<F, CC, RR, DD, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) == cudaSuccess;
+#define MVAMG_LEANK_ATTR_F(F)                                                               \
+  MVAMG_LEANK_ATTR(F, 2, 2, 3, 4) MVAMG_LEANK_ATTR(F, 4, 2, 3, 4) MVAMG_LEANK_ATTR(F, 2, 2, 2, 4) \
+  MVAMG_LEANK_ATTR(F, 4, 2, 2, 4) MVAMG_LEANK_ATTR(F, 2, 4, 2, 2) MVAMG_LEANK_ATTR(F, 4, 4, 2, 2)
+  MVAMG_LEANK_ATTR_F(true) MVAMG_LEANK_ATTR_F(false)
+#undef MVAMG_LEANK_ATTR_F
+#undef MVAMG_LEANK_ATTR
 #undef MVAMG_LEAN_ATTR_C
 #undef MVAMG_LEAN_ATTR
   g_max_dyn_smem = ok ? maxsm : 48 * 1024;
@@ -234,11 +242,30 @@ int launch_gs(bool fwd, const Csr& A, const GsList& ls, const GsPlan& p, const d
   a.debug = g_gs_debug;
   const int g = gs_blocks(p, ls);
   if (ls.lean_C > 0) {
+    const int lc = ls.lean_C & 0xff, lk = (ls.lean_C >> 8) & 0xff;
+    if (lk > 1) {  // K rows per lane per round (C <= 4; (R, D, K) in {(2,2,4), (2,3,4), (4,2,2)})
+#define MVAMG_LEANK(F, RR, DD, KK)                                                \
+  do {                                                                            \
+    if (lc <= 2) gs_lean_kernel<F, 2, RR, DD, KK><<<g, p.threads, smem, s>>>(a);  \
+    else gs_lean_kernel<F, 4, RR, DD, KK><<<g, p.threads, smem, s>>>(a);          \
+  } while (0)
+#define MVAMG_LEANK_F(F)                                                          \
+  do {                                                                            \
+    if (lk == 4 && ls.D >= 3) MVAMG_LEANK(F, 2, 3, 4);                            \
+    else if (lk == 4) MVAMG_LEANK(F, 2, 2, 4);                                    \
+    else MVAMG_LEANK(F, 4, 2, 2);                                                 \
+  } while (0)
+      if (fwd) MVAMG_LEANK_F(true); else MVAMG_LEANK_F(false);
+#undef MVAMG_LEANK_F
+#undef MVAMG_LEANK
+      CUDA_TRY(cudaGetLastError());
+      return 0;
+    }
 #define MVAMG_LEAN(F, CC, RR, DD) gs_lean_kernel<F, CC, RR, DD><<<g, p.threads, smem, s>>>(a)
 #define MVAMG_LEAN_C(F, RR, DD)                                                   \
   do {                                                                            \
-    if (ls.lean_C <= 2) MVAMG_LEAN(F, 2, RR, DD);                                 \
-    else if (ls.lean_C <= 4) MVAMG_LEAN(F, 4, RR, DD);                            \
+    if (lc <= 2) MVAMG_LEAN(F, 2, RR, DD);                                        \
+    else if (lc <= 4) MVAMG_LEAN(F, 4, RR, DD);                                   \
     else MVAMG_LEAN(F, 8, RR, DD);                                                \
   } while (0)
 #define MVAMG_LEAN_R(F)                                                           \
@@ -857,13 +884,16 @@ int mvamg_csr_spmv_add_f64(int n, const int* indptr, const int* indices, const d
 
 int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double* data, int ntiles,
                       const int* chain_ptr, const int* tile_ptr, int window, int mode, int R,
-                      int uniform_S, long long* nwords, int* nrounds, int* nwarps, int* max_S,
-                      unsigned long long* rec, int* round_off, int* tbase, int* tile_wbase,
+                      int uniform_S, int rows_per_round, long long* nwords, int* nrounds, int* nwarps,
+                      int* max_S, unsigned long long* rec, int* round_off, int* tbase, int* tile_wbase,
                       int* perm) {
   if (n < 0 || !indptr || !chain_ptr || !tile_ptr || !nwords || !nrounds || !nwarps || mode < 0 ||
       mode > 2 || R < 1 || R > 31)
     return fail(MVAMG_E_ARG, "gs_schedule: bad arguments");
   if (n >= (1 << 29)) return fail(MVAMG_E_ARG, "gs_schedule: n >= 2^29 not encodable");
+  const int K = rows_per_round < 1 ? 1 : rows_per_round;
+  if (K > 8 || (K > 1 && uniform_S <= 0))
+    return fail(MVAMG_E_ARG, "gs_schedule: rows_per_round 1..8, > 1 only with uniform (lean) records");
   const bool fwd = mode < 2, with_old = mode == 1;
   auto dbits = [](double d) {
     unsigned long long u;
@@ -882,7 +912,7 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
     for (int i = chain_ptr[c]; i < chain_ptr[c + 1]; ++i) chain_of[i] = c;
   long long w = 0;
   int gr = 0, gw = 0, smax = 1;
-  std::vector<int> rnd, rows_of_round, cnt_of;
+  std::vector<int> rnd, slot_of, rows_of_round, cnt_of;
   for (int t = 0; t < ntiles; ++t) {
     const int c0 = tile_ptr[t], c1 = tile_ptr[t + 1];
     const int TS = ((c1 - c0 + 31) / 32) * 32;
@@ -891,31 +921,48 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
       const int cB = std::min(cA + 32, c1);
       const int rlo = chain_ptr[cA], rhi = chain_ptr[cB];
       rnd.assign(rhi - rlo, 0);
-      int last[32];
-      for (int L = 0; L < 32; ++L) last[L] = -1;
+      slot_of.assign(rhi - rlo, 0);
+      int last[32], used[32];
+      for (int L = 0; L < 32; ++L) last[L] = -1, used[L] = 0;
       int nr = 0;
       for (int q = 0; q < rhi - rlo; ++q) {
         const int i = fwd ? rlo + q : rhi - 1 - q;
         const int L = chain_of[i] - cA;
-        int r = last[L] + 1;
+        const int c = chain_of[i], pred = fwd ? i - 1 : i + 1;
+        const bool has_pred = fwd ? (i - 1 >= chain_ptr[c]) : (i + 1 < chain_ptr[c + 1]);
+        // every intra-warp input other than the chain predecessor must come
+        // from an earlier round (its value is read from the window at the
+        // round's start); the predecessor may share the round (register)
+        int rmin = 0;
         for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
           const int j = indices[k];
-          if (j != i && lower(i, j) && j >= rlo && j < rhi) r = std::max(r, rnd[j - rlo] + 1);
+          if (j != i && lower(i, j) && j >= rlo && j < rhi && !(has_pred && j == pred))
+            rmin = std::max(rmin, rnd[j - rlo] + 1);
+        }
+        int r;
+        if (last[L] >= 0 && used[L] < K && rmin <= last[L]) {
+          r = last[L];
+          ++used[L];
+        } else {
+          r = std::max(last[L] + 1, rmin);
+          used[L] = 1;
         }
         rnd[i - rlo] = r;
+        slot_of[i - rlo] = used[L] - 1;
         last[L] = r;
         nr = std::max(nr, r + 1);
       }
       nr = ((nr + R - 1) / R) * R;
       if (nr == 0) nr = R;
       if (tbase) tbase[gw] = gr;
-      // rows of each round, one per lane
-      rows_of_round.assign((size_t)nr * 32, -1);
-      for (int i = rlo; i < rhi; ++i) rows_of_round[(size_t)rnd[i - rlo] * 32 + (chain_of[i] - cA)] = i;
+      // rows of each round: K slots per lane
+      rows_of_round.assign((size_t)nr * K * 32, -1);
+      for (int i = rlo; i < rhi; ++i)
+        rows_of_round[((size_t)rnd[i - rlo] * K + slot_of[i - rlo]) * 32 + (chain_of[i] - cA)] = i;
       for (int r = 0; r < nr; ++r, ++gr) {
         int maxcnt = -1;
-        for (int L = 0; L < 32; ++L) {
-          const int i = rows_of_round[(size_t)r * 32 + L];
+        for (int L = 0; L < 32 * K; ++L) {
+          const int i = rows_of_round[(size_t)r * K * 32 + L];
           if (i < 0) continue;
           int cnt = 0;
           for (int k = indptr[i]; k < indptr[i + 1]; ++k) cnt += keep(i, indices[k]);
@@ -928,11 +975,11 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
         }
         smax = std::max(smax, S);
         if (round_off) round_off[gr] = (int)w;
-        if (rec) {
-          unsigned long long* blk = rec + w;
+        if (rec) for (int sl = 0; sl < K; ++sl) {
+          unsigned long long* blk = rec + w + (size_t)sl * 32 * S;
           std::memset(blk, 0, sizeof(unsigned long long) * 32 * S);
           for (int L = 0; L < 32; ++L) {
-            const int i = rows_of_round[(size_t)r * 32 + L];
+            const int i = rows_of_round[((size_t)r * K + sl) * 32 + L];
             if (i < 0) {
               blk[L] = kGsNoRow;
               continue;
@@ -968,12 +1015,12 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
             blk[L] = (unsigned long long)(unsigned)cnt | (fast ? 0x10000ull : 0ull);
             blk[32 + L] = dbits(dg);
             blk[64 + L] = dbits(1.0 / dg);
-            if (perm) perm[i] = gr * 32 + L;
+            if (perm) perm[i] = (gr * K + sl) * 32 + L;
           }
         }
-        w += (long long)32 * S;
+        w += (long long)32 * K * S;
         if (w >= (1LL << 31)) return fail(MVAMG_E_ARG, "gs_schedule: record stream exceeds 2^31 words");
-        if ((long long)gr * 32 >= (1LL << 31)) return fail(MVAMG_E_ARG, "gs_schedule: too many rounds");
+        if ((long long)gr * 32 * K >= (1LL << 31)) return fail(MVAMG_E_ARG, "gs_schedule: too many rounds");
       }
     }
   }
@@ -1003,8 +1050,13 @@ int mvamg_gs_sweep_f64(int direction, int n, const int* indptr, const int* indic
   ls.rec = rec; ls.round_off = round_off; ls.tbase = tbase; ls.tile_wbase = tile_wbase; ls.perm = perm;
   ls.tperm = tperm; ls.R = R; ls.D = D; ls.slot_words = slot_words; ls.rec_words_max = rec_words_max;
   ls.lean_C = lean_C;
-  if (lean_C > 0 && ((R == 8 && D != 2 && D != 3) || (R == 4 && D != 4) || (R <= 2 && D != 8)))
+  const int lean_K = (lean_C >> 8) & 0xff;
+  if (lean_C > 0 && lean_K <= 1 && ((R == 8 && D != 2 && D != 3) || (R == 4 && D != 4) || (R <= 2 && D != 8)))
     return fail(MVAMG_E_ARG, "gs: lean kernel ring must be (R, D) in {(8,3), (8,2), (4,4), (2,8), (1,8)}");
+  if (lean_K > 1 && ((lean_C & 0xff) > 4 ||
+                     !((lean_K == 4 && R == 2 && (D == 2 || D == 3)) || (lean_K == 2 && R == 4 && D == 2))))
+    return fail(MVAMG_E_ARG, "gs: lean kernel with K rows per round needs C <= 4 and (R, D, K) in "
+                             "{(2,2,4), (2,3,4), (4,2,2)}");
   GsPlan p;
   p.ntiles = ntiles; p.threads = threads; p.window = window; p.chain_ptr = chain_ptr; p.tile_ptr = tile_ptr;
   return launch_gs(direction == 0, A, ls, p, b, x_old, x_new, ws, ws + 1, (cudaStream_t)stream);

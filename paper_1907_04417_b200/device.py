@@ -73,6 +73,8 @@ class GpuConfig:
     level_stage_bytes: int = 32768  # minimum staging buffer per level (else a larger cluster)
     force_level_gs: bool = False    # use it for every small level (tests / diagnostics)
     smem_limit: int = 227 * 1024 - 1024
+    lean_rows_per_round: int = 1    # K rows of a lane's chain per round in the lean GS kernel (1 or 4;
+                                    # 4 is bit-exact but slower on grid problems, see gs_sweep.cuh)
     row_gs_min_rows: int = 10000    # coarse levels at least this large use the dataflow row sweep
     row_gs_threads: int = 128       # threads per CTA of the row sweep
     row_gs_ctas: int = 0            # resident CTAs of the row sweep (0 = auto)
@@ -125,6 +127,9 @@ def _row_counts(A):
     return lo, up
 
 
+LEAN_K_RINGS = ((2, 3), (2, 2))  # (R, D) of the K = 4 rows-per-round lean kernel
+
+
 def _gs_ring(A, cfg):
     """Ring plan (lean_C, R, D, slot_words, S) for matrix A.
 
@@ -137,6 +142,14 @@ def _gs_ring(A, cfg):
     if cmax <= 8 and not cfg.generic_gs:
         C = 2 if cmax <= 2 else (4 if cmax <= 4 else 8)
         S = 3 + 2 * C
+        K = int(cfg.lean_rows_per_round)
+        if K == 4 and C <= 4:
+            for R, D in LEAN_K_RINGS:
+                slot = R * 32 * K * (S + 1)
+                if D * slot * 8 <= cfg.ring_bytes:
+                    return C | (K << 8), R, D, slot, S
+            R, D = LEAN_K_RINGS[-1]
+            return C | (K << 8), R, D, R * 32 * K * (S + 1), S
         for R, D in LEAN_RINGS:
             slot = R * 32 * (S + 1)
             if D * slot * 8 <= cfg.ring_bytes:
@@ -221,7 +234,7 @@ class GsScheduleHost:
     max_S: int
 
 
-def gs_schedule(A, plan, mode, R=None, uniform_S=0):
+def gs_schedule(A, plan, mode, R=None, uniform_S=0, K=1):
     """Static round schedule of one GS sweep mode (0 forward from x=0, 1 forward, 2 backward)."""
     A = as_csr(A)
     L = _lib.load()
@@ -234,7 +247,7 @@ def gs_schedule(A, plan, mode, R=None, uniform_S=0):
     vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
     nw, nr, nwarps, smax = ctypes.c_longlong(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
     args = (n, vp(ip), vp(ix), vp(v), plan.ntiles, vp(cp), vp(tp), plan.window, int(mode),
-            int(R or plan.R), int(uniform_S), ctypes.byref(nw), ctypes.byref(nr), ctypes.byref(nwarps),
+            int(R or plan.R), int(uniform_S), int(K), ctypes.byref(nw), ctypes.byref(nr), ctypes.byref(nwarps),
             ctypes.byref(smax))
     _lib.check(L.mvamg_gs_schedule(*args, None, None, None, None, None), "gs_schedule")
     rec = np.zeros(max(2, nw.value), dtype=np.uint64)
@@ -267,11 +280,12 @@ class DeviceGsPlan:
 
             p = self.plan
             if p.lean_C > 0 and m != 1:
-                S = 3 + 2 * p.lean_C
+                C, K = p.lean_C & 0xFF, max(1, p.lean_C >> 8)
+                S = 3 + 2 * C
                 R, D = p.R, p.D
-                h = gs_schedule(self.A, p, m, R=R, uniform_S=S)
-                rec_words_max = R * 32 * S
-                slot_words = rec_words_max + R * 32
+                h = gs_schedule(self.A, p, m, R=R, uniform_S=S, K=K)
+                rec_words_max = R * 32 * K * S
+                slot_words = rec_words_max + R * 32 * K
                 lean = p.lean_C
             else:
                 # generic kernel: pick the deepest ring that fits beside the window
@@ -293,7 +307,8 @@ class DeviceGsPlan:
             self.modes[m] = dict(
                 rec=to_device(h.rec.view(np.int64)), round_off=to_device(h.round_off),
                 tbase=to_device(h.tbase), tile_wbase=to_device(h.tile_wbase), perm=to_device(h.perm),
-                tperm=torch.empty(max(32, 32 * h.nrounds), dtype=torch.float64, device="cuda"),
+                tperm=torch.empty(max(32, 32 * h.nrounds * max(1, lean >> 8)), dtype=torch.float64,
+                                  device="cuda"),
                 R=R, D=D, lean_C=lean, slot_words=slot_words, rec_words_max=rec_words_max,
                 nrounds=h.nrounds, max_S=h.max_S)
         return self.modes[m]

@@ -143,7 +143,7 @@ def _structures():
     yield "dense", random_spd_csr(60, density=0.9, seed=9)
 
 
-@pytest.mark.parametrize("cfg", [None, dict(max_chain=3, max_threads=32, max_window=97),
+@pytest.mark.parametrize("cfg", [None, dict(lean_rows_per_round=4), dict(max_chain=3, max_threads=32, max_window=97),
                                  dict(max_chain=64, max_threads=64, max_window=40),
                                  dict(max_threads=256, ring_bytes=4096),
                                  dict(generic_gs=True), dict(generic_gs=True, max_chain=5, max_threads=40)])

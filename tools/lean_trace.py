@@ -29,12 +29,31 @@ from paper_1907_04417_b200.device import DeviceGsPlan, ptr  # noqa: E402
 g = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 A = problems.anisotropic_q1(g)
 n = A.shape[0]
-gp = DeviceGsPlan(A)
+K = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+from paper_1907_04417_b200.device import GpuConfig  # noqa: E402
+gp = DeviceGsPlan(A, GpuConfig(lean_rows_per_round=K))
 print(f"plan: tiles={gp.plan.ntiles} thr={gp.plan.threads} lean_C={gp.plan.lean_C} R={gp.plan.R} D={gp.plan.D}")
 b = torch.randn(n, dtype=torch.float64, device="cuda")
 xn = torch.empty(n, dtype=torch.float64, device="cuda")
 ws = torch.zeros(8, dtype=torch.int32, device="cuda")
 tr = torch.zeros(16384 + 4 * 2048, dtype=torch.int64, device="cuda")
+if K > 1:
+    L = _lib.load()
+    for _ in range(3):
+        gp.sweep(0, b, None, xn, ws)
+    L.mvamg_gs_set_trace(ptr(tr))
+    gp.sweep(0, b, None, xn, ws)
+    torch.cuda.synchronize()
+    L.mvamg_gs_set_trace(None)
+    t = tr.cpu().numpy()[:16384].reshape(-1, 2)
+    ends = t[:, 1]
+    nr = int(np.count_nonzero(ends))
+    d = np.diff(ends[:nr])
+    print(f"K={K} rounds traced {nr}: round cycles p50 {np.median(d):.0f} mean {d.mean():.0f}; spins per round "
+          f"p50 {np.median(t[:nr, 0]):.0f} mean {t[:nr, 0].mean():.1f}")
+    print("first 30 deltas", d[:30].tolist())
+    print("first 30 spins", t[:30, 0].tolist())
+    sys.exit(0)
 L = _lib.load()
 for _ in range(3):
     gp.sweep(0, b, None, xn, ws)
