@@ -455,6 +455,9 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
     // entries have a zero coefficient in the uniform record and a zero value:
     // s - (+0) == s exactly, so the chain needs no selects.  `tmr`, `ixr`,
     // `gvr` are the round's staged source types / indices / cross-tile values.
+#if MVAMG_LEAN_TRACE
+    int tr_round = 0;
+#endif
     auto run_round = [&](const unsigned long long* slot, int rr, unsigned tmr, const unsigned* ixr,
                          const unsigned long long* gvr) {
       const unsigned long long* rec = slot + rr * 32 * S + lane;
@@ -474,6 +477,9 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
       if (!__all_sync(FULL, ready)) {
         long long spins = 0;
         do {
+#if MVAMG_LEAN_TRACE
+          if (a.trace && g == (a.debug >> 8) && lane == 0) a.trace[16384 + 8192 + (tr_round & 4095)] += 1;
+#endif
           ready = true;
 #pragma unroll
           for (int u = 0; u < C; ++u) {
@@ -507,26 +513,30 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
         ++q;
       }
       __syncwarp();
+#if MVAMG_LEAN_TRACE
+      if (a.trace && g == (a.debug >> 8) && lane == 0 && tr_round < 8192) a.trace[2 * tr_round + 1] = clock64();
+      ++tr_round;
+#endif
     };
     // Staging of rounds (independent of the sweep's progress): each entry's
     // source type and index, and the cross-tile values (code 2) requested at
     // once -- one L2 round trip per group of rounds, not per round.
+    // Lean records come pre-decoded from mvamg_gs_schedule: the header's
+    // bits 16-31 hold every entry's 2-bit source type (absent entries and
+    // rows: 3), so staging is loads, shifts and the prefetches.
     auto load_codes = [&](const unsigned long long* slot, int rr, unsigned* code) {
       const unsigned long long* rec = slot + rr * 32 * S + lane;
-      const int cnt = (int)((unsigned)rec[0] & 0xffffu);
-      const int ca = cnt != (int)kGsNoRow ? cnt : 0;
+      code[C] = (unsigned)(rec[0] >> 16);
 #pragma unroll
-      for (int u = 0; u < C; ++u) code[u] = u < ca ? (unsigned)rec[32 * (4 + 2 * u)] : 3u;
+      for (int u = 0; u < C; ++u) code[u] = (unsigned)rec[32 * (4 + 2 * u)];
     };
     auto decode = [&](const unsigned* code, unsigned& tmr, unsigned* ixr, unsigned long long* gvr) {
-      tmr = 0u;
+      tmr = code[C];
 #pragma unroll
       for (int u = 0; u < C; ++u) {
-        const unsigned t = code[u] & 3u;
-        tmr |= t << (2 * u);
         ixr[u] = code[u] >> 2;
         gvr[u] = kSentinel;
-        ld_global_if(gvr[u], t == 2u, a.xnew + ixr[u]);
+        ld_global_if(gvr[u], ((tmr >> (2 * u)) & 3u) == 2u, a.xnew + ixr[u]);
       }
     };
     auto wait_chunk = [&](int k) {
@@ -549,7 +559,7 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
         const unsigned long long* slot = ringp + (k % D) * a.slot_words;
         const double* rhs = reinterpret_cast<const double*>(slot + RW) + lane;
         wait_chunk(k);
-        unsigned tmr[R * K], ixr[R * K][C], code[C];
+        unsigned tmr[R * K], ixr[R * K][C], code[C + 1];
         unsigned long long gvr[R * K][C];
 #pragma unroll
         for (int s = 0; s < R * K; ++s) {
@@ -642,7 +652,7 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
           }
           __syncwarp();
 #if MVAMG_LEAN_TRACE
-          if (a.trace && g == 0 && lane == 0 && k * R + rr < 8192) {
+          if (a.trace && g == (a.debug >> 8) && lane == 0 && k * R + rr < 8192) {
             a.trace[2 * (k * R + rr) + 1] = clock64();
             a.trace[2 * (k * R + rr)] = nspin;
           }
@@ -663,7 +673,7 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
       // 5-point grids 339 -> 305 ns/level; for C = 4 the extra live state costs
       // more than it hides, so those stage whole chunks below.)
       constexpr int H = R / 2;
-      unsigned tmA[H], ixA[H][C], tmB[H], ixB[H][C], raw[H][C];
+      unsigned tmA[H], ixA[H][C], tmB[H], ixB[H][C], raw[H][C + 1];
       unsigned long long gvA[H][C], gvB[H][C];
       if (nch > 0) {
         wait_chunk(0);
@@ -720,7 +730,7 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
       for (int k = 0; k < nch && !abort; ++k) {
         const unsigned long long* slot = ringp + (k % D) * a.slot_words;
         wait_chunk(k);
-        unsigned tmr[R], ixr[R][C], code[C];
+        unsigned tmr[R], ixr[R][C], code[C + 1];
         unsigned long long gvr[R][C];
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {

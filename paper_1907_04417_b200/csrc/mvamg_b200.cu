@@ -978,10 +978,16 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
         if (rec) for (int sl = 0; sl < K; ++sl) {
           unsigned long long* blk = rec + w + (size_t)sl * 32 * S;
           std::memset(blk, 0, sizeof(unsigned long long) * 32 * S);
+          // lean records: absent entries carry source code 3 ("none") and the
+          // header word's bits 16-31 hold the 2-bit source type of every entry
+          const int nent = uniform_S > 0 ? (S - 3) / 2 : 0;
+          if (uniform_S > 0 && nent > 8) return fail(MVAMG_E_ARG, "gs_schedule: lean records hold <= 8 entries");
+          for (int L = 0; L < 32; ++L)
+            for (int u = 0; u < nent; ++u) blk[(size_t)32 * (4 + 2 * u) + L] = 3ull;
           for (int L = 0; L < 32; ++L) {
             const int i = rows_of_round[((size_t)r * K + sl) * 32 + L];
             if (i < 0) {
-              blk[L] = kGsNoRow;
+              blk[L] = kGsNoRow | (uniform_S > 0 ? 0xffff0000ull : 0ull);
               continue;
             }
             const int c = chain_of[i], cs = chain_ptr[c], ce = chain_ptr[c + 1];
@@ -1012,7 +1018,16 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
               ++cnt;
             }
             if (cnt >= (int)kGsNoRow) return fail(MVAMG_E_ARG, "gs_schedule: row with too many entries");
-            blk[L] = (unsigned long long)(unsigned)cnt | (fast ? 0x10000ull : 0ull);
+            if (uniform_S > 0) {
+              unsigned tb = 0xffffu;  // types of entries >= cnt stay 3
+              for (int u = 0; u < cnt; ++u) {
+                const unsigned t = (unsigned)blk[(size_t)32 * (4 + 2 * u) + L] & 3u;
+                tb = (tb & ~(3u << (2 * u))) | (t << (2 * u));
+              }
+              blk[L] = (unsigned long long)(unsigned)cnt | ((unsigned long long)tb << 16);
+            } else {
+              blk[L] = (unsigned long long)(unsigned)cnt | (fast ? 0x10000ull : 0ull);
+            }
             blk[32 + L] = dbits(dg);
             blk[64 + L] = dbits(1.0 / dg);
             if (perm) perm[i] = (gr * K + sl) * 32 + L;

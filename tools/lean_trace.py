@@ -36,7 +36,7 @@ print(f"plan: tiles={gp.plan.ntiles} thr={gp.plan.threads} lean_C={gp.plan.lean_
 b = torch.randn(n, dtype=torch.float64, device="cuda")
 xn = torch.empty(n, dtype=torch.float64, device="cuda")
 ws = torch.zeros(8, dtype=torch.int32, device="cuda")
-tr = torch.zeros(16384 + 4 * 2048, dtype=torch.int64, device="cuda")
+tr = torch.zeros(16384 + 8192 + 4096, dtype=torch.int64, device="cuda")
 if K > 1:
     L = _lib.load()
     for _ in range(3):
@@ -62,28 +62,13 @@ gp.sweep(0, b, None, xn, ws)
 torch.cuda.synchronize()
 L.mvamg_gs_set_trace(None)
 tt = tr.cpu().numpy()
-t = tt[:16384].reshape(-1, 2)
-ck = tt[16384:].reshape(-1, 4)
-nk = int(np.count_nonzero(ck[:, 0]))
-ck = ck[:nk]
-# 0 top of chunk, 1 after mbarrier wait, (round 0 start stamp), 3 after issue
-st0 = t[np.arange(nk) * gp.plan.R, 0]
-print(f"chunk: mbar wait p50 {np.median(ck[:, 1] - ck[:, 0]):.0f}; phase A p50 {np.median(st0 - ck[:, 1]):.0f}; "
-      f"end-of-chunk issue p50 {np.median(ck[:-1, 3] - t[np.arange(nk - 1) * gp.plan.R + gp.plan.R - 1, 1]):.0f}; "
-      f"loop back p50 {np.median(ck[1:, 0] - ck[:-1, 3]):.0f}")
-R = gp.plan.R
-ends = t[:, 1]
+ends = tt[:16384].reshape(-1, 2)[:, 1]
 nr = int(np.count_nonzero(ends))
 ends = ends[:nr]
-starts = t[:nr, 0]
+spins = tt[16384 + 8192:16384 + 8192 + 4096][:nr]
 d = np.diff(ends)
-print(f"rounds traced {nr}; round-to-round cycles: p10 {np.percentile(d, 10):.0f} p50 {np.median(d):.0f} "
-      f"p90 {np.percentile(d, 90):.0f} mean {d.mean():.0f}")
-# chunk structure: rounds k*R..k*R+R-1; start stamp at k*R marks the end of phase A
-k0 = np.arange(0, nr - R, R)
-pa = starts[k0[1:]] - ends[k0[1:] - 1]
-r0 = ends[k0] - starts[k0]
-rin = np.concatenate([np.diff(ends[k:k + R]) for k in k0])
-print(f"phase A (chunk start -> first round begins) cycles: p50 {np.median(pa):.0f} mean {pa.mean():.0f}")
-print(f"first round of chunk cycles: p50 {np.median(r0):.0f}; later rounds: p50 {np.median(rin):.0f} mean {rin.mean():.0f}")
-print("first 40 round ends (delta):", np.diff(ends[:41]).tolist())
+print(f"warp {os.environ.get('MVAMG_GS_DEBUG', '0')}>>8: rounds {nr}, round cycles p10 {np.percentile(d, 10):.0f} "
+      f"p50 {np.median(d):.0f} p90 {np.percentile(d, 90):.0f} mean {d.mean():.0f}; total {ends[-1] - ends[0]} cycles; "
+      f"rounds with spins {np.count_nonzero(spins)}, spins total {spins.sum()}")
+print("first 40 deltas", d[:40].tolist())
+print("mid 40 deltas", d[nr // 2:nr // 2 + 40].tolist())
