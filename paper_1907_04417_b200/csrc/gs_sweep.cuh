@@ -1047,7 +1047,7 @@ __global__ void __launch_bounds__(128) gs_row_kernel(GsRowArgs a) {
     const int* ls = s_src + (size_t)wsl * 32 + lane;
     bool done = !have;
     unsigned long long mask = 0;  // bit b: entry kc + b holds its product
-    int sc = 1;                   // background cursor (relative to kc)
+    int sc = 4;                   // background cursor (relative to kc), past the fixed slots 1-3
     long long spins = 0, progress = 0;
     for (;;) {
       if (!done) {
@@ -1060,7 +1060,10 @@ __global__ void __launch_bounds__(128) gs_row_kernel(GsRowArgs a) {
         unsigned long long xb[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const int b = u == 0 ? 0 : sc + u - 1;
+          // slot 0: the head; slots 1-3: the entries right behind it (the
+          // last to be published in a backward sweep, the next needed in a
+          // forward one); slots 4-7: a cursor over the rest of the window
+          const int b = u < 4 ? u : sc + u - 4;
           const bool v = b < lim && !((mask >> b) & 1ull);
           eb[u] = v ? b : -1;
           int j = 0;
@@ -1095,8 +1098,8 @@ __global__ void __launch_bounds__(128) gs_row_kernel(GsRowArgs a) {
         // after progress, look right behind the new head (where the chain goes
         // next); while blocked, keep sweeping the window
         progress += m > 0;
-        sc = m > 0 ? 1 : sc + 7;
-        if (sc >= min(cnt - kc, 64)) sc = 1;
+        sc = m > 0 ? 4 : sc + 4;
+        if (sc >= min(cnt - kc, 64)) sc = 4;
         if (kc == cnt) {
           st_relaxed_f64(a.xnew + i, div_rn_markstein(s, dg, rdg));
           if (a.trace) {
