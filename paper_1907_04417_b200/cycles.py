@@ -209,6 +209,17 @@ class GpuMultigridOperator:
                         _lib.check(L.mvamg_hierarchy_set_gs_levels(h, k, m, *s.args()), "set_gs_levels")
                     continue
                 gp = DeviceGsPlan(A, self.config)
+                if (not self.config.generic_gs and gp.plan.nchains > 0
+                        and A.shape[0] / gp.plan.nchains < self.config.min_chain_rows):
+                    # no chain structure for the wavefront: dataflow row sweeps instead
+                    rows = {m: DeviceGsRows(A, m, self.config) for m in self._gs_level_modes()}
+                    self.gs_plans.append(None)
+                    self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=None, rows=rows))
+                    _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
+                                                           None, 0, None, None, 32, 0), "set_level")
+                    for m, s in rows.items():
+                        _lib.check(L.mvamg_hierarchy_set_gs_rows(h, k, m, *s.hierarchy_args()), "set_gs_rows")
+                    continue
                 self.gs_plans.append(gp.plan)
                 self.level_dev.append(dict(A=dA, gs=gp, plan=gp.plan, levels=None))
                 _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),

@@ -80,6 +80,8 @@ class GpuConfig:
     row_gs_ctas: int = 0            # resident CTAs of the row sweep (0 = auto)
     row_gs_smem: int = 96 * 1024    # staged entry slices per row-sweep tile (halve threads above)
     force_row_gs: bool = False      # use the row sweep for every coarse level (tests / diagnostics)
+    min_chain_rows: float = 8.0     # a level whose wavefront chains average fewer rows uses the row sweep
+                                    # (e.g. interleaved multi-dof systems, where row i rarely couples to i-1)
     coarse_mega: bool = False       # run the small coarse levels of a cycle in one thread block (opt-in:
                                     # launch-free but L2-latency bound; slower than the multi-kernel path today)
     mega_max_rows: int = 8192       # levels from the first one with at most this many rows down
