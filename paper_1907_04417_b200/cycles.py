@@ -18,6 +18,7 @@ import scipy.sparse.linalg as spla
 
 from . import _lib
 from .device import (DeviceCSR, DeviceGsLevels, DeviceGsPlan, DeviceGsRows, GpuConfig, as_csr,
+                     autotune_coarse_gs,
                      level_gs_fits, ptr, row_gs_fits,
                      stream_handle, to_device, torch_cuda)
 from .exceptions import NotSpdError
@@ -182,6 +183,26 @@ class GpuMultigridOperator:
                                                            None, 0, None, None, 32, 0), "set_level")
                     for m, s in small.items():
                         _lib.check(L.mvamg_hierarchy_set_gs_levels(h, k, m, *s.args()), "set_gs_levels")
+                    continue
+                if (k >= 1 and self.config.autotune_gs and not self.config.generic_gs
+                        and not self.config.force_level_gs and not self.config.force_row_gs
+                        and A.shape[0] <= self.config.level_gs_max_rows):
+                    # coarse level: the faster of the row and level-set sweeps, per mode
+                    pick = autotune_coarse_gs(A, self._gs_level_modes(), self.config)
+                    self.gs_plans.append(None)
+                    lv = dict(A=dA, gs=None, plan=None, levels=None, rows=None)
+                    _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
+                                                           None, 0, None, None, 32, 0), "set_level")
+                    for m, s in pick.items():
+                        if isinstance(s, DeviceGsRows):
+                            lv["rows"] = lv["rows"] or {}
+                            lv["rows"][m] = s
+                            _lib.check(L.mvamg_hierarchy_set_gs_rows(h, k, m, *s.hierarchy_args()), "set_gs_rows")
+                        else:
+                            lv["levels"] = lv["levels"] or {}
+                            lv["levels"][m] = s
+                            _lib.check(L.mvamg_hierarchy_set_gs_levels(h, k, m, *s.args()), "set_gs_levels")
+                    self.level_dev.append(lv)
                     continue
                 if row_gs_fits(A, k, self.config):
                     # dataflow row sweeps over the whole GPU; no wavefront schedule needed

@@ -80,6 +80,7 @@ class GpuConfig:
     row_gs_ctas: int = 0            # resident CTAs of the row sweep (0 = auto)
     row_gs_smem: int = 96 * 1024    # staged entry slices per row-sweep tile (halve threads above)
     force_row_gs: bool = False      # use the row sweep for every coarse level (tests / diagnostics)
+    autotune_gs: bool = True        # coarse levels: time row and level-set sweeps once, keep the faster per mode
     min_chain_rows: float = 8.0     # a level whose wavefront chains average fewer rows uses the row sweep
                                     # (e.g. interleaved multi-dof systems, where row i rarely couples to i-1)
     coarse_mega: bool = False       # run the small coarse levels of a cycle in one thread block (opt-in:
@@ -493,6 +494,47 @@ class DeviceGsRows:
         _lib.check(_lib.load().mvamg_gs_row_sweep_f64(
             self.mode, self.n, *self._csr.ptrs(), *self.args(), ptr(b), ptr(x_old), ptr(x_new), ptr(ws),
             stream or stream_handle()), "gs_row_sweep")
+
+
+def time_sweep(fn, reps=3):
+    """Device time (s) of fn() -- one GS sweep -- after one warm-up launch."""
+    torch = torch_cuda()
+    fn()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps * 1e-3
+
+
+def autotune_coarse_gs(A, modes, cfg):
+    """For a coarse level: per sweep mode, the faster of the dataflow row sweep
+    and the level-set sweep, timed once on the device ({mode: schedule}).
+    Mode 2 is timed as the folded backward sweep it runs in a cycle."""
+    torch = torch_cuda()
+    n = A.shape[0]
+    rows = {m: DeviceGsRows(A, m, cfg) for m in modes}
+    try:
+        lvls = {m: DeviceGsLevels(A, m, cfg) for m in modes}
+    except ValueError:
+        return dict(rows)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    b = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    xo = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    xn = torch.empty(n, dtype=torch.float64, device="cuda")
+    ws = torch.zeros(8, dtype=torch.int32, device="cuda")
+    out = {}
+    for m in modes:
+        xold = xo if m in (1, 2, 3) else None
+        t_rows = time_sweep(lambda: rows[m].sweep(b, xold, xn, ws))
+        if m == 2:
+            t_lvl = time_sweep(lambda: lvls[m].sweep(b, xo, xn, ws, fold=True))
+        else:
+            t_lvl = time_sweep(lambda: lvls[m].sweep(b, xold, xn, ws))
+        out[m] = rows[m] if t_rows <= t_lvl else lvls[m]
+    return out
 
 
 def row_gs_fits(A, k, cfg):

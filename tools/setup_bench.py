@@ -19,7 +19,10 @@ print(f"fit {time.time() - t:.1f}s stages={est.composite_.n_components} "
       f"opc={est.operator_complexity_:.3f}", flush=True)
 for k, lv in enumerate(est.operator_.level_dev):
     M = est.hierarchy_.matrices[k]
-    if lv.get("levels"):
+    if lv.get("levels") and lv.get("rows"):
+        how = ("autotuned: " + ", ".join(f"mode{m}=level-set(c={s.ncta})" for m, s in lv["levels"].items()) + ", "
+               + ", ".join(f"mode{m}=rows" for m in lv["rows"]))
+    elif lv.get("levels"):
         s0 = next(iter(lv["levels"].values()))
         how = f"level-set cluster={s0.ncta} nlev={s0.nlev} thr={s0.threads}"
     elif lv.get("rows"):
@@ -37,14 +40,16 @@ for k, lv in enumerate(est.operator_.level_dev):
     xo = torch.randn(n, dtype=torch.float64, device="cuda")
     xn = torch.empty(n, dtype=torch.float64, device="cuda")
     ws = torch.zeros(8, dtype=torch.int32, device="cuda")
-    if lv.get("levels"):
-        fns = {m: (lambda s=s, m=m: s.sweep(bb, None if m % 2 == 0 else xo, xn, ws)) for m, s in lv["levels"].items()}
-        if 2 in lv["levels"]:
-            fns[3] = lambda s=lv["levels"][2]: s.sweep(bb, xo, xn, ws, fold=True)
-    elif lv.get("rows"):
-        fns = {m: (lambda s=s, m=m: s.sweep(bb, None if m % 2 == 0 else xo, xn, ws)) for m, s in lv["rows"].items()}
-        if 2 in lv["rows"]:
-            fns[3] = lambda s=lv["rows"][2]: s.sweep(bb, xo, xn, ws)
+    if lv.get("levels") or lv.get("rows"):
+        fns = {}
+        for m, s in (lv.get("levels") or {}).items():
+            fns[m] = lambda s=s, m=m: s.sweep(bb, None if m % 2 == 0 else xo, xn, ws)
+            if m == 2:
+                fns[3] = lambda s=s: s.sweep(bb, xo, xn, ws, fold=True)
+        for m, s in (lv.get("rows") or {}).items():
+            fns[m] = lambda s=s, m=m: s.sweep(bb, None if m % 2 == 0 else xo, xn, ws)
+            if m == 2:
+                fns[3] = lambda s=s: s.sweep(bb, xo, xn, ws)
     else:
         gp = lv["gs"]
         fns = {0: lambda: gp.sweep(0, bb, None, xn, ws), 2: lambda: gp.sweep(1, bb, xo, xn, ws)}
