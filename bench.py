@@ -46,6 +46,7 @@ def parse_args():
     p.add_argument("--config", default=os.environ.get("MVAMG_BENCH_CONFIG", "c2"))
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-h2", action="store_true", help="skip the H2 (composite-preconditioned) solve")
+    p.add_argument("--no-galerkin", action="store_true", help="skip the setup Galerkin-product timing")
     return p.parse_args()
 
 
@@ -428,6 +429,30 @@ def run_b200(args, world, rank, local):
         out["h2"] = {"value": t_h2, "unit": "s", "nit": rep.iterations, "components": len(comp_ops),
                      "converged": bool(rep.converged), "what": "PCG rtol 1e-6 preconditioned by the "
                      "symmetrized composite of the bootstrap K-cycles (inner FCG 2); one timed solve"}
+    # ---- setup: the Galerkin products of this hierarchy on the device
+    # (sparse.py:50-66, bit-identical) against the reference's scipy call ----
+    if rank == 0 and not args.no_galerkin and len(mats) > 1:
+        from paper_1907_04417_b200.device import galerkin_product_device
+        from paper_1907_04417_b200.setup import galerkin_product
+
+        levels = []
+        for k in range(len(pros)):
+            galerkin_product_device(pros[k], mats[k])  # warm-up (module load, allocations)
+            t = {}
+            G = galerkin_product_device(pros[k], mats[k], timing=t)
+            t0 = time.perf_counter()
+            H = galerkin_product(pros[k], mats[k])
+            t_host = time.perf_counter() - t0
+            same = bool(np.array_equal(G.indptr, H.indptr) and np.array_equal(G.indices, H.indices)
+                        and np.array_equal(G.data, H.data))
+            levels.append({"level": k, "n": mats[k].shape[0], "nc": pros[k].shape[1], "nnz_A": int(mats[k].nnz),
+                           "nnz_P": int(pros[k].nnz), "nnz_Ac": int(G.nnz), "device_ms": t["total_ms"],
+                           "phases_ms": {x: round(t[x], 3) for x in ("transpose_ms", "ap_ms", "ptap_ms",
+                                                                     "symmetrize_ms")},
+                           "scipy_ms": t_host * 1e3, "bit_exact": same})
+        out["galerkin"] = {"what": "A_c = (G + G')/2, G = P'(A P) per hierarchy level, device kernels "
+                                   "(csrc/galerkin.cuh) vs the reference's scipy recipe on one host core",
+                           "levels": levels}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb, cnit = cpu_baseline(mats, pros, b)
         cb["nit"] = cnit

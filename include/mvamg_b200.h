@@ -209,6 +209,23 @@ int mvamg_greedy_match(long long ne, const long long* ei, const long long* ej, i
 int mvamg_jacobi_svd_batch(int nblk, const int* row_ptr, int k, const double* A, int max_sweeps,
                            double tol, double* U, double* sigma, int* failed_block);
 
+/* ---- Galerkin product (setup) -------------------------- */
+/* Device CSR owned by the library. */
+typedef struct mvamg_spmat mvamg_spmat;
+/* A_c = galerkin_product(P, A) of pkg/src/mvamg/sparse.py:50-66, bit for bit:
+ * G = P^T (A P) in scipy csr_matmat's summation order (exact zeros dropped),
+ * then (G + G^T) * 0.5 as csr_plus_csr + scalar multiply; canonical (sorted)
+ * CSR.  A: n x n, P: n x nc, all device pointers (int32 / fp64).  On success
+ * *out holds A_c (nc x nc, *nnz_out nonzeros) until mvamg_spmat_destroy;
+ * phase_ms (host, 4 floats, may be NULL) receives the device time of
+ * P^T, A P, P^T (A P) and the symmetrisation.  Synchronises `stream`. */
+int mvamg_galerkin_f64(int n, int nc, const int* a_indptr, const int* a_indices, const double* a_data,
+                       const int* p_indptr, const int* p_indices, const double* p_data, mvamg_spmat** out,
+                       long long* nnz_out, float* phase_ms, void* stream);
+/* Copy a library-owned CSR into caller device buffers (n+1, nnz, nnz). */
+int mvamg_spmat_copy(const mvamg_spmat* m, int* indptr, int* indices, double* data, void* stream);
+int mvamg_spmat_destroy(mvamg_spmat* m);
+
 /* ---- hierarchy (MultigridOperator) ---------------------------------------- */
 typedef struct mvamg_hierarchy mvamg_hierarchy;
 

@@ -302,3 +302,117 @@ int or_pcg_h(or_hier* a_owner, const double* b, int pc_kind, or_hier** ops, int 
              int itmax, double* x, double* hist, int* nit, int* converged, double* work) {
     return or_pcg(&a_owner->A[0], b, pc_kind, ops, nops, rtol, itmax, x, hist, nit, converged, work);
 }
+
+/* ---- Galerkin product (setup) ---------------------------
+ * galerkin_product(P, A) of pkg/src/mvamg/sparse.py:50-66:
+ *   G = (P.T @ (A @ P)).tocsr();  S = ((G + G.T) * 0.5)  (canonical).
+ * scipy's csr_matmat accumulates sums[col] += x_ij * y_jk with sums starting at
+ * 0.0, in the order the products are generated (X row in CSR order, then Y's
+ * row), and drops exact-zero sums; P.T @ AP runs csr_matmat on the transposed
+ * (csc) operands, i.e. G[I,J] = 0.0 + sum over k ascending of AP[k,J]*P[k,I].
+ * csr_plus_csr adds matching entries (one rounding, commutative), keeps a lone
+ * entry as is, drops exact zeros; `* 0.5` scales every stored value. */
+typedef struct { int n, m; int* ip; int* ix; double* v; } or_mat;
+
+static int or_cmp_int(const void* a, const void* b) {
+    int x = *(const int*)a, y = *(const int*)b;
+    return (x > y) - (x < y);
+}
+
+/* C = X @ Y (X: n x k, Y: k x m) in the csr_matmat summation order, sorted columns. */
+static or_mat or_spgemm(int n, int m, const int* xp, const int* xi, const double* xv,
+                        const int* yp, const int* yi, const double* yv) {
+    or_mat C = {n, m, (int*)malloc(sizeof(int) * (size_t)(n + 1)), NULL, NULL};
+    double* sums = (double*)calloc((size_t)m + 1, sizeof(double));
+    char* seen = (char*)calloc((size_t)m + 1, 1);
+    int* cols = (int*)malloc(sizeof(int) * ((size_t)m + 1));
+    size_t cap = 1024, nnz = 0;
+    C.ix = (int*)malloc(sizeof(int) * cap);
+    C.v = (double*)malloc(sizeof(double) * cap);
+    C.ip[0] = 0;
+    for (int i = 0; i < n; ++i) {
+        int nc = 0;
+        for (int jj = xp[i]; jj < xp[i + 1]; ++jj) {
+            const int j = xi[jj];
+            const double a = xv[jj];
+            for (int kk = yp[j]; kk < yp[j + 1]; ++kk) {
+                const int c = yi[kk];
+                sums[c] += a * yv[kk];
+                if (!seen[c]) { seen[c] = 1; cols[nc++] = c; }
+            }
+        }
+        qsort(cols, (size_t)nc, sizeof(int), or_cmp_int);
+        for (int t = 0; t < nc; ++t) {
+            const int c = cols[t];
+            if (sums[c] != 0.0) {
+                if (nnz == cap) {
+                    cap *= 2;
+                    C.ix = (int*)realloc(C.ix, sizeof(int) * cap);
+                    C.v = (double*)realloc(C.v, sizeof(double) * cap);
+                }
+                C.ix[nnz] = c;
+                C.v[nnz] = sums[c];
+                ++nnz;
+            }
+            sums[c] = 0.0;
+            seen[c] = 0;
+        }
+        C.ip[i + 1] = (int)nnz;
+    }
+    free(sums); free(seen); free(cols);
+    return C;
+}
+
+/* Stable transpose: rows of the result list the source rows ascending. */
+static or_mat or_transpose(int n, int m, const int* ip, const int* ix, const double* v) {
+    const int nnz = ip[n];
+    or_mat T = {m, n, (int*)calloc((size_t)m + 1, sizeof(int)), (int*)malloc(sizeof(int) * ((size_t)nnz + 1)),
+                (double*)malloc(sizeof(double) * ((size_t)nnz + 1))};
+    for (int k = 0; k < nnz; ++k) T.ip[ix[k] + 1]++;
+    for (int c = 0; c < m; ++c) T.ip[c + 1] += T.ip[c];
+    int* cur = (int*)malloc(sizeof(int) * ((size_t)m + 1));
+    memcpy(cur, T.ip, sizeof(int) * (size_t)m);
+    for (int i = 0; i < n; ++i)
+        for (int k = ip[i]; k < ip[i + 1]; ++k) {
+            const int p = cur[ix[k]]++;
+            T.ix[p] = i;
+            T.v[p] = v[k];
+        }
+    free(cur);
+    return T;
+}
+
+static void or_mat_free(or_mat* M) { free(M->ip); free(M->ix); free(M->v); }
+
+/* S = (G + G^T) * 0.5 with G = P^T (A P); returns nnz, result owned by *out_*
+ * (free with or_free). */
+int or_galerkin(int n, int nc, const int* aip, const int* aix, const double* av, const int* pip,
+                const int* pix, const double* pv, int** out_ip, int** out_ix, double** out_v) {
+    or_mat AP = or_spgemm(n, nc, aip, aix, av, pip, pix, pv);
+    or_mat R = or_transpose(n, nc, pip, pix, pv);
+    or_mat G = or_spgemm(nc, nc, R.ip, R.ix, R.v, AP.ip, AP.ix, AP.v);
+    or_mat GT = or_transpose(nc, nc, G.ip, G.ix, G.v);
+    int* sip = (int*)malloc(sizeof(int) * ((size_t)nc + 1));
+    const size_t cap = (size_t)G.ip[nc] * 2 + 1;
+    int* six = (int*)malloc(sizeof(int) * cap);
+    double* sv = (double*)malloc(sizeof(double) * cap);
+    int nnz = 0;
+    sip[0] = 0;
+    for (int i = 0; i < nc; ++i) {
+        int a = G.ip[i], ae = G.ip[i + 1], b = GT.ip[i], be = GT.ip[i + 1];
+        while (a < ae || b < be) {
+            int c;
+            double s;
+            if (b >= be || (a < ae && G.ix[a] < GT.ix[b])) { c = G.ix[a]; s = G.v[a] + 0.0; ++a; }
+            else if (a >= ae || GT.ix[b] < G.ix[a]) { c = GT.ix[b]; s = 0.0 + GT.v[b]; ++b; }
+            else { c = G.ix[a]; s = G.v[a] + GT.v[b]; ++a; ++b; }
+            if (s != 0.0) { six[nnz] = c; sv[nnz] = s * 0.5; ++nnz; }
+        }
+        sip[i + 1] = nnz;
+    }
+    or_mat_free(&AP); or_mat_free(&R); or_mat_free(&G); or_mat_free(&GT);
+    *out_ip = sip; *out_ix = six; *out_v = sv;
+    return nnz;
+}
+
+void or_free(void* p) { free(p); }

@@ -177,3 +177,26 @@ def oracle_pcg(owner, b, precond="cycle", ops=None, rtol=1e-6, itmax=1000):
     if st:
         raise ArithmeticError(f"oracle PCG breakdown {st}")
     return x, hist[: nit.value + 1].copy(), nit.value, bool(conv.value)
+
+
+def oracle_galerkin(P, A):
+    """galerkin_product(P, A) (sparse.py:50-66) restated in C: (G + G')/2 with
+    G = P'(A P), scipy csr_matmat summation order, exact zeros dropped."""
+    Am, aip, aix, av = _csr(A)
+    Pm, pip, pix, pv = _csr(P)
+    if Pm.shape[0] != Am.shape[0] or Am.shape[0] != Am.shape[1]:
+        raise ValueError("dimension mismatch")
+    L = lib()
+    L.or_galerkin.restype = _I
+    L.or_galerkin.argtypes = [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]
+    L.or_free.argtypes = [_P]
+    n, nc = Pm.shape
+    oip, oix, ov = _P(), _P(), _P()
+    nnz = L.or_galerkin(n, nc, _ptr(aip), _ptr(aix), _ptr(av), _ptr(pip), _ptr(pix), _ptr(pv),
+                        ctypes.byref(oip), ctypes.byref(oix), ctypes.byref(ov))
+    ip = np.ctypeslib.as_array(ctypes.cast(oip, ctypes.POINTER(_I)), (nc + 1,)).copy()
+    ix = np.ctypeslib.as_array(ctypes.cast(oix, ctypes.POINTER(_I)), (max(nnz, 1),))[:nnz].copy()
+    v = np.ctypeslib.as_array(ctypes.cast(ov, ctypes.POINTER(_D)), (max(nnz, 1),))[:nnz].copy()
+    for p in (oip, oix, ov):
+        L.or_free(p)
+    return sp.csr_matrix((v, ix, ip), shape=(nc, nc))

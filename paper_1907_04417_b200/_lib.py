@@ -80,6 +80,9 @@ SIGNATURES = [
     ("mvamg_composite_destroy", _I, [_P]),
     ("mvamg_composite_apply_symmetrized", _I, [_P, _P, _P]),
     ("mvamg_composite_precond", _I, [_P, _P, _P, _P]),
+    ("mvamg_galerkin_f64", _I, [_I, _I, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_P), ctypes.POINTER(_LL), _P, _P]),
+    ("mvamg_spmat_copy", _I, [_P, _P, _P, _P, _P]),
+    ("mvamg_spmat_destroy", _I, [_P]),
 ]
 
 _lib = None

@@ -24,6 +24,7 @@
 #include "../../include/mvamg_b200.h"
 #include "mvamg_kernels.cuh"
 #include "coarse_mega.cuh"
+#include "galerkin.cuh"
 
 using namespace mvamg;
 
@@ -764,6 +765,223 @@ int pcg_device(mvamg_hierarchy* h, int pc, mvamg_composite* comp, const double* 
   return 0;
 }
 
+
+// ---------------------------------------------------------------------------
+// Galerkin product on the device (galerkin.cuh)
+// ---------------------------------------------------------------------------
+// Device CSR owned by the library (intermediates and the returned A_c).
+struct DevCsr {
+  int n = 0, m = 0;
+  long long nnz = 0;
+  int* ip = nullptr;
+  int* ix = nullptr;
+  double* v = nullptr;
+  void release() {
+    if (ip) cudaFree(ip);
+    if (ix) cudaFree(ix);
+    if (v) cudaFree(v);
+    ip = ix = nullptr;
+    v = nullptr;
+  }
+};
+
+struct DevTmp {  // scoped cudaMalloc
+  void* p = nullptr;
+  ~DevTmp() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* get() const {
+    return static_cast<T*>(p);
+  }
+};
+
+#define GK_LAUNCH_CHECK()                                                         \
+  do {                                                                            \
+    ++g_kernel_launches;                                                          \
+    cudaError_t e_ = cudaGetLastError();                                          \
+    if (e_ != cudaSuccess) return fail(MVAMG_E_CUDA, std::string("galerkin: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+// offsets[0..n] = exclusive scan of cnt[0..n); *total = offsets[n].
+int scan_counts(int n, const int* cnt, long long* offsets, long long* total, cudaStream_t s) {
+  using namespace galerkin;
+  const long long per = (long long)kScanThreads * kScanItems;
+  const int nb = (int)(((long long)n + 1 + per - 1) / per);
+  DevTmp bsum;
+  CUDA_TRY(cudaMalloc(&bsum.p, (size_t)nb * 8));
+  scan_blocks_kernel<<<nb, kScanThreads, 0, s>>>(n, cnt, offsets, bsum.get<long long>());
+  GK_LAUNCH_CHECK();
+  scan_sums_kernel<<<1, kScanThreads, 0, s>>>(nb, bsum.get<long long>());
+  GK_LAUNCH_CHECK();
+  scan_add_kernel<<<grid_for(n + 1), 256, 0, s>>>(n, offsets, bsum.get<long long>());
+  GK_LAUNCH_CHECK();
+  CUDA_TRY(cudaMemcpyAsync(total, offsets + n, 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int alloc_csr(DevCsr& C, int n, int m, long long nnz, const long long* offsets64, cudaStream_t s) {
+  if (nnz >= 0x7fffffffLL) return fail(MVAMG_E_ARG, "galerkin: more than 2^31 - 1 nonzeros");
+  C.n = n;
+  C.m = m;
+  C.nnz = nnz;
+  CUDA_TRY(cudaMalloc(&C.ip, (size_t)(n + 1) * 4));
+  CUDA_TRY(cudaMalloc(&C.ix, (size_t)std::max(nnz, 1LL) * 4));
+  CUDA_TRY(cudaMalloc(&C.v, (size_t)std::max(nnz, 1LL) * 8));
+  galerkin::narrow_offsets_kernel<<<grid_for(n + 1), 256, 0, s>>>(n, offsets64, C.ip);
+  GK_LAUNCH_CHECK();
+  return 0;
+}
+
+// Stable transpose of an n x m CSR (rows of the result list source rows ascending).
+int csr_transpose(int n, int m, const int* ip, const int* ix, const double* v, long long nnz, DevCsr& T,
+                  cudaStream_t s) {
+  using namespace galerkin;
+  DevTmp cnt, off, cur, tix, tv;
+  CUDA_TRY(cudaMalloc(&cnt.p, (size_t)(m + 1) * 4));
+  CUDA_TRY(cudaMalloc(&off.p, (size_t)(m + 1) * 8));
+  CUDA_TRY(cudaMalloc(&cur.p, (size_t)(m + 1) * 4));
+  CUDA_TRY(cudaMalloc(&tix.p, (size_t)std::max(nnz, 1LL) * 4));
+  CUDA_TRY(cudaMalloc(&tv.p, (size_t)std::max(nnz, 1LL) * 8));
+  CUDA_TRY(cudaMemsetAsync(cnt.p, 0, (size_t)(m + 1) * 4, s));
+  CUDA_TRY(cudaMemsetAsync(cur.p, 0, (size_t)(m + 1) * 4, s));
+  if (nnz > 0) {
+    col_count_kernel<<<grid_for((int)std::min(nnz, 1LL << 30)), 256, 0, s>>>(nnz, ix, cnt.get<int>());
+    GK_LAUNCH_CHECK();
+  }
+  long long total = 0;
+  if (int e = scan_counts(m, cnt.get<int>(), off.get<long long>(), &total, s)) return e;
+  if (total != nnz) return fail(MVAMG_E_ARG, "galerkin: column index out of range");
+  if (int e = alloc_csr(T, m, n, nnz, off.get<long long>(), s)) return e;
+  if (nnz > 0) {
+    transpose_scatter_kernel<<<grid_for(n * 32), 256, 0, s>>>(n, ip, ix, v, off.get<long long>(), cur.get<int>(),
+                                                               tix.get<int>(), tv.get<double>());
+    GK_LAUNCH_CHECK();
+    segment_rank_sort_kernel<<<grid_for(m * 32), 256, 0, s>>>(m, off.get<long long>(), tix.get<int>(),
+                                                               tv.get<double>(), T.ix, T.v);
+    GK_LAUNCH_CHECK();
+  }
+  return 0;
+}
+
+// C = X @ Y in csr_matmat's summation order (galerkin.cuh), sorted, zeros dropped.
+int spgemm_ordered(int nrows, int ncols, const int* xp, const int* xi, const double* xv, const int* yp,
+                   const int* yi, const double* yv, DevCsr& C, cudaStream_t s) {
+  using namespace galerkin;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(spgemm_smem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    CUDA_TRY(cudaFuncSetAttribute(spgemm_smem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    attr = true;
+  }
+  DevTmp cnt, flag, rows, ctr, off;
+  CUDA_TRY(cudaMalloc(&cnt.p, (size_t)(nrows + 1) * 4));
+  CUDA_TRY(cudaMalloc(&flag.p, (size_t)nrows + 1));
+  CUDA_TRY(cudaMalloc(&rows.p, (size_t)(nrows + 1) * 4));
+  CUDA_TRY(cudaMalloc(&ctr.p, 16));
+  CUDA_TRY(cudaMalloc(&off.p, (size_t)(nrows + 1) * 8));
+  CUDA_TRY(cudaMemsetAsync(ctr.p, 0, 16, s));
+  CUDA_TRY(cudaMemsetAsync(cnt.p, 0, (size_t)(nrows + 1) * 4, s));
+  int* n_ovf = ctr.get<int>();
+  int* max_ub = n_ovf + 1;
+  const int grid = std::max(1, std::min((nrows + kWarps - 1) / kWarps, num_sms() * 2));
+  if (nrows > 0) {
+    spgemm_smem_kernel<false><<<grid, kWarps * 32, kSmemBytes, s>>>(nrows, xp, xi, xv, yp, yi, yv, cnt.get<int>(),
+                                                                    flag.get<unsigned char>(), rows.get<int>(), n_ovf,
+                                                                    max_ub, nullptr, nullptr, nullptr);
+    GK_LAUNCH_CHECK();
+  }
+  int hctr[2] = {0, 0};
+  CUDA_TRY(cudaMemcpyAsync(hctr, ctr.p, 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  const int novf = hctr[0];
+  int H = 0, ggrid = 0;
+  DevTmp pk, pv;
+  if (novf > 0) {
+    const long long need = std::min<long long>(std::max(hctr[1], 1), std::max(ncols, 1));
+    H = 64;
+    while (H < 2 * need) H <<= 1;
+    long long nw = std::min<long long>(novf, (long long)num_sms() * 2 * kWarps);
+    const long long cap = (1LL << 30) / ((long long)H * 24);  // pool <= 1 GiB
+    nw = std::max(1LL, std::min(nw, cap));
+    ggrid = (int)((nw + kWarps - 1) / kWarps);
+    CUDA_TRY(cudaMalloc(&pk.p, (size_t)ggrid * kWarps * 2 * H * 4));
+    CUDA_TRY(cudaMalloc(&pv.p, (size_t)ggrid * kWarps * 2 * H * 8));
+    spgemm_global_kernel<false><<<ggrid, kWarps * 32, 0, s>>>(novf, rows.get<int>(), xp, xi, xv, yp, yi, yv, H,
+                                                              pk.get<int>(), pv.get<double>(), cnt.get<int>(), nullptr,
+                                                              nullptr, nullptr);
+    GK_LAUNCH_CHECK();
+  }
+  long long total = 0;
+  if (int e = scan_counts(nrows, cnt.get<int>(), off.get<long long>(), &total, s)) return e;
+  if (int e = alloc_csr(C, nrows, ncols, total, off.get<long long>(), s)) return e;
+  if (nrows > 0 && total > 0) {
+    spgemm_smem_kernel<true><<<grid, kWarps * 32, kSmemBytes, s>>>(nrows, xp, xi, xv, yp, yi, yv, nullptr,
+                                                                   flag.get<unsigned char>(), nullptr, nullptr, nullptr,
+                                                                   off.get<long long>(), C.ix, C.v);
+    GK_LAUNCH_CHECK();
+    if (novf > 0) {
+      spgemm_global_kernel<true><<<ggrid, kWarps * 32, 0, s>>>(novf, rows.get<int>(), xp, xi, xv, yp, yi, yv, H,
+                                                               pk.get<int>(), pv.get<double>(), nullptr,
+                                                               off.get<long long>(), C.ix, C.v);
+      GK_LAUNCH_CHECK();
+    }
+  }
+  return 0;
+}
+
+int galerkin_device(int n, int nc, Csr A, Csr P, DevCsr& S, cudaStream_t s, float* phase_ms) {
+  using namespace galerkin;
+  cudaEvent_t ev[5];
+  for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      for (int i = 0; i < 5; ++i) cudaEventDestroy(e[i]);
+    }
+  } guard{ev};
+  DevCsr R, AP, G, GT;
+  struct CsrGuard {
+    DevCsr* m[4];
+    ~CsrGuard() {
+      for (auto* x : m) x->release();
+    }
+  } cg{{&R, &AP, &G, &GT}};
+  CUDA_TRY(cudaEventRecord(ev[0], s));
+  if (int e = csr_transpose(n, nc, P.ip, P.ix, P.v, P.nnz, R, s)) return e;           // R = P^T
+  CUDA_TRY(cudaEventRecord(ev[1], s));
+  if (int e = spgemm_ordered(n, nc, A.ip, A.ix, A.v, P.ip, P.ix, P.v, AP, s)) return e;  // A P
+  CUDA_TRY(cudaEventRecord(ev[2], s));
+  if (int e = spgemm_ordered(nc, nc, R.ip, R.ix, R.v, AP.ip, AP.ix, AP.v, G, s)) return e;  // P^T (A P)
+  CUDA_TRY(cudaEventRecord(ev[3], s));
+  if (int e = csr_transpose(nc, nc, G.ip, G.ix, G.v, G.nnz, GT, s)) return e;
+  DevTmp cnt, off;
+  CUDA_TRY(cudaMalloc(&cnt.p, (size_t)(nc + 1) * 4));
+  CUDA_TRY(cudaMalloc(&off.p, (size_t)(nc + 1) * 8));
+  DevTmp gp, tp;  // int64 row offsets for the merge
+  CUDA_TRY(cudaMalloc(&gp.p, (size_t)(nc + 1) * 8));
+  CUDA_TRY(cudaMalloc(&tp.p, (size_t)(nc + 1) * 8));
+  widen_offsets_kernel<<<grid_for(nc + 1), 256, 0, s>>>(nc, G.ip, gp.get<long long>());
+  GK_LAUNCH_CHECK();
+  widen_offsets_kernel<<<grid_for(nc + 1), 256, 0, s>>>(nc, GT.ip, tp.get<long long>());
+  GK_LAUNCH_CHECK();
+  symmetrize_kernel<false><<<grid_for(nc), 256, 0, s>>>(nc, gp.get<long long>(), G.ix, G.v, tp.get<long long>(),
+                                                        GT.ix, GT.v, cnt.get<int>(), nullptr, nullptr, nullptr);
+  GK_LAUNCH_CHECK();
+  long long total = 0;
+  if (int e = scan_counts(nc, cnt.get<int>(), off.get<long long>(), &total, s)) return e;
+  if (int e = alloc_csr(S, nc, nc, total, off.get<long long>(), s)) return e;
+  symmetrize_kernel<true><<<grid_for(nc), 256, 0, s>>>(nc, gp.get<long long>(), G.ix, G.v, tp.get<long long>(),
+                                                       GT.ix, GT.v, nullptr, off.get<long long>(), S.ix, S.v);
+  GK_LAUNCH_CHECK();
+  CUDA_TRY(cudaEventRecord(ev[4], s));
+  CUDA_TRY(cudaEventSynchronize(ev[4]));
+  if (phase_ms)
+    for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventElapsedTime(&phase_ms[i], ev[i], ev[i + 1]));
+  return 0;
+}
+#undef GK_LAUNCH_CHECK
 }  // namespace
 
 // ============================================================================
@@ -1832,6 +2050,64 @@ int mvamg_composite_precond(mvamg_composite* c, const double* r, double* z, void
   });
   if (st) return st;
   CUDA_TRY(cudaMemcpyAsync(z, h0->pz, (size_t)c->n * 8, cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
+
+struct mvamg_spmat {
+  DevCsr m;
+};
+
+int mvamg_galerkin_f64(int n, int nc, const int* a_indptr, const int* a_indices, const double* a_data,
+                       const int* p_indptr, const int* p_indices, const double* p_data, mvamg_spmat** out,
+                       long long* nnz_out, float* phase_ms, void* stream) {
+  if (!out || n < 0 || nc < 0 || !a_indptr || !p_indptr) return fail(MVAMG_E_ARG, "galerkin: bad arguments");
+  *out = nullptr;
+  cudaStream_t s = (cudaStream_t)stream;
+  int nnz_a = 0, nnz_p = 0;
+  CUDA_TRY(cudaMemcpyAsync(&nnz_a, a_indptr + n, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(&nnz_p, p_indptr + n, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  Csr A, P;
+  A.n = A.m = n;
+  A.nnz = nnz_a;
+  A.ip = a_indptr;
+  A.ix = a_indices;
+  A.v = a_data;
+  P.n = n;
+  P.m = nc;
+  P.nnz = nnz_p;
+  P.ip = p_indptr;
+  P.ix = p_indices;
+  P.v = p_data;
+  auto* h = new mvamg_spmat();
+  int e = galerkin_device(n, nc, A, P, h->m, s, phase_ms);
+  if (e) {
+    h->m.release();
+    delete h;
+    return e;
+  }
+  *out = h;
+  if (nnz_out) *nnz_out = h->m.nnz;
+  return 0;
+}
+
+int mvamg_spmat_copy(const mvamg_spmat* m, int* indptr, int* indices, double* data, void* stream) {
+  if (!m || !indptr) return fail(MVAMG_E_ARG, "spmat_copy: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemcpyAsync(indptr, m->m.ip, (size_t)(m->m.n + 1) * 4, cudaMemcpyDeviceToDevice, s));
+  if (m->m.nnz > 0) {
+    CUDA_TRY(cudaMemcpyAsync(indices, m->m.ix, (size_t)m->m.nnz * 4, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(data, m->m.v, (size_t)m->m.nnz * 8, cudaMemcpyDeviceToDevice, s));
+  }
+  return 0;
+}
+
+int mvamg_spmat_destroy(mvamg_spmat* m) {
+  if (m) {
+    m->m.release();
+    delete m;
+  }
   return 0;
 }
 

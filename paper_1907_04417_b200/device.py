@@ -78,6 +78,7 @@ class GpuConfig:
     row_gs_min_rows: int = 10000    # coarse levels at least this large use the dataflow row sweep
     row_gs_threads: int = 128       # threads per CTA of the row sweep
     row_gs_ctas: int = 0            # resident CTAs of the row sweep (0 = auto)
+    device_galerkin: bool = True    # setup forms P'AP with the device kernel (bit-identical to scipy's)
     row_gs_smem: int = 96 * 1024    # staged entry slices per row-sweep tile (halve threads above)
     force_row_gs: bool = False      # use the row sweep for every coarse level (tests / diagnostics)
     autotune_gs: bool = True        # coarse levels: time row and level-set sweeps once, keep the faster per mode
@@ -557,3 +558,41 @@ def level_gs_fits(A, cfg):
         return True
     lo, up = _row_counts(as_csr(A))
     return int(max(lo.max(initial=0), up.max(initial=0))) > 8
+
+
+def galerkin_product_device(P, A, timing=None):
+    """galerkin_product(P, A) (pkg/src/mvamg/sparse.py:50-66) on the GPU.
+
+    Same arguments, ValueError on a dimension mismatch, and the same canonical
+    CSR bit for bit (csrc/galerkin.cuh restates scipy's summation order).  The
+    operands are uploaded, A_c is formed on the device and returned as a scipy
+    CSR.  ``timing``: optional dict that receives the device milliseconds of the
+    four phases (transpose, A P, P'(A P), symmetrise) and their total."""
+    P = as_csr(P)
+    A = as_csr(A)
+    if P.shape[0] != A.shape[0] or A.shape[0] != A.shape[1]:
+        raise ValueError(f"dimension mismatch: P is {P.shape[0]}x{P.shape[1]}, A is {A.shape[0]}x{A.shape[1]}")
+    torch = torch_cuda()
+    L = _lib.load()
+    n, nc = P.shape
+    dev = [to_device(a) for a in (A.indptr.astype(np.int32), A.indices.astype(np.int32), A.data,
+                                  P.indptr.astype(np.int32), P.indices.astype(np.int32), P.data)]
+    h = ctypes.c_void_p()
+    nnz = ctypes.c_longlong(0)
+    ph = (ctypes.c_float * 4)()
+    _lib.check(L.mvamg_galerkin_f64(n, nc, *[ptr(t) for t in dev], ctypes.byref(h), ctypes.byref(nnz), ph,
+                                    stream_handle()), "galerkin_product")
+    try:
+        ip = torch.empty(nc + 1, dtype=torch.int32, device="cuda")
+        ix = torch.empty(max(nnz.value, 1), dtype=torch.int32, device="cuda")
+        v = torch.empty(max(nnz.value, 1), dtype=torch.float64, device="cuda")
+        _lib.check(L.mvamg_spmat_copy(h, ptr(ip), ptr(ix), ptr(v), stream_handle()), "galerkin_product")
+        torch.cuda.current_stream().synchronize()
+    finally:
+        L.mvamg_spmat_destroy(h)
+    if timing is not None:
+        names = ("transpose_ms", "ap_ms", "ptap_ms", "symmetrize_ms")
+        timing.update({k: float(x) for k, x in zip(names, ph)})
+        timing["total_ms"] = float(sum(ph))
+    k = nnz.value
+    return sp.csr_matrix((v.cpu().numpy()[:k], ix.cpu().numpy()[:k], ip.cpu().numpy()), shape=(nc, nc))

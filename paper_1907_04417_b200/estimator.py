@@ -12,7 +12,7 @@ from .composite import DeviceANorm
 from .cycles import CycleSpec, GpuMultigridOperator
 from .device import to_device
 from .krylov import pcg
-from .setup import (BootstrapParams, CoarseningParams, bootstrap_run, build_multivector_hierarchy,
+from .setup import (BootstrapParams, CoarseningParams, bootstrap_run, build_multivector_hierarchy, coarse_product,
                     build_pairwise_hierarchy, operator_complexity)
 
 
@@ -86,7 +86,7 @@ class MultiVectorAMG:
         A = _check_operator(A)
         w0 = np.ones(A.shape[0])
         if self.nsv == 1:
-            pairwise = build_pairwise_hierarchy(A, w0, self._coarsening())
+            pairwise = build_pairwise_hierarchy(A, w0, self._coarsening(), product=coarse_product(self.config))
             self.composite_ = None
             vectors = [w0]
         else:
@@ -97,7 +97,8 @@ class MultiVectorAMG:
             pairwise = self.composite_.components[n_use - 2].hierarchy
             vectors = self.composite_.smooth_vectors[:n_use]
         self.hierarchy_ = build_multivector_hierarchy(A, pairwise, vectors, merge_levels=self.merge_levels,
-                                                      tol=self.svd_tol, min_coarse_size=self.min_coarse_size)
+                                                      tol=self.svd_tol, min_coarse_size=self.min_coarse_size,
+                                                      product=coarse_product(self.config))
         self.operator_ = GpuMultigridOperator(self.hierarchy_.matrices, self.hierarchy_.prolongator_matrices,
                                               cycle=CycleSpec("V"), config=self.config)
         self.smooth_vectors_ = vectors

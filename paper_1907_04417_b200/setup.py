@@ -207,7 +207,16 @@ class PairwiseHierarchy:
         return [lv.A.shape[0] for lv in self.levels]
 
 
-def pairwise_step(A, w, steps, weight_floor=WEIGHT_FLOOR):
+def coarse_product(config=None):
+    """The Galerkin product the setup uses: the device kernel
+    (device.galerkin_product_device, bit-identical) unless the GpuConfig turns
+    it off, in which case the host scipy recipe."""
+    from .device import GpuConfig, galerkin_product_device
+
+    return galerkin_product_device if (config or GpuConfig()).device_galerkin else galerkin_product
+
+
+def pairwise_step(A, w, steps, weight_floor=WEIGHT_FLOOR, product=galerkin_product):
     """Compose `steps` matching sweeps into one transfer; returns
     (P, A_c, w_c, aggregates, stagnated, steps_done)."""
     if steps < 1:
@@ -223,7 +232,7 @@ def pairwise_step(A, w, steps, weight_floor=WEIGHT_FLOOR):
         Pc, step_aggs = pair_prolongator(Ak, wk, pairs, unmatched)
         aggs = step_aggs if aggs is None else _compose(aggs, step_aggs)
         P = Pc if P is None else (P @ Pc).tocsr()
-        Ak = galerkin_product(Pc, Ak)
+        Ak = product(Pc, Ak)
         wk = Pc.T @ wk
         done += 1
     if P is None:
@@ -231,12 +240,12 @@ def pairwise_step(A, w, steps, weight_floor=WEIGHT_FLOOR):
         signs = np.where(wk >= 0.0, 1.0, -1.0)
         P = sp.csr_matrix((signs, (np.arange(n), np.arange(n))), shape=(n, n))
         aggs = Aggregates(np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int64), n)
-        Ak = galerkin_product(P, A)
+        Ak = product(P, A)
         wk = P.T @ np.asarray(w, dtype=np.float64)
     return P, Ak, wk, aggs, stagnated, done
 
 
-def build_pairwise_hierarchy(A, w, params=None):
+def build_pairwise_hierarchy(A, w, params=None, product=galerkin_product):
     """Coarsen (A, w) until small; a level shrinking by < min_shrink is
     dropped; no pairs at the finest level raises CoarseningStagnationError."""
     params = params or CoarseningParams()
@@ -249,7 +258,7 @@ def build_pairwise_hierarchy(A, w, params=None):
     while levels[-1].A.shape[0] > params.min_coarse_size and len(levels) < params.max_levels:
         cur = levels[-1]
         P, Ac, wc, aggs, stagnated, done = pairwise_step(cur.A, cur.w, params.steps_per_level,
-                                                         params.weight_floor)
+                                                         params.weight_floor, product)
         if done == 0:
             if len(levels) == 1:
                 raise CoarseningStagnationError("matching produced no pairs at the finest level", level=0)
@@ -353,7 +362,8 @@ def block_prolongator(aggs, vectors, n_fine, tol=0.1):
     return BlockProlongator(P, kept, col_off, sig)
 
 
-def build_multivector_hierarchy(A, pairwise, vectors, merge_levels=3, tol=0.1, min_coarse_size=40):
+def build_multivector_hierarchy(A, pairwise, vectors, merge_levels=3, tol=0.1, min_coarse_size=40,
+                                product=galerkin_product):
     """The single multi-vector hierarchy from a pairwise substrate and the
     finest-level smooth vectors (pkg/src/mvamg/multivector.py:262-321)."""
     t0 = time.perf_counter()
@@ -376,7 +386,7 @@ def build_multivector_hierarchy(A, pairwise, vectors, merge_levels=3, tol=0.1, m
             break
         pros.append(bp)
         used.append(aggs)
-        mats.append(galerkin_product(bp.P, mats[-1]))
+        mats.append(product(bp.P, mats[-1]))
         vecs.append([bp.P.T @ v for v in vecs[-1]])
         if idx + 1 < len(sets):  # SVD dofs of an aggregate travel to its parent group
             owner_col = np.repeat(np.arange(bp.kept.shape[0]), bp.kept)
@@ -457,7 +467,8 @@ def bootstrap_run(A, w0=None, params=None, config=None):
     while (rho >= params.rho_des or stage <= params.min_stages) and stage <= params.maxstage:
         t0 = time.perf_counter()
         try:
-            hier = build_pairwise_hierarchy(A, comp.smooth_vectors[-1], params.coarsening)
+            hier = build_pairwise_hierarchy(A, comp.smooth_vectors[-1], params.coarsening,
+                                            product=coarse_product(config))
         except CoarseningStagnationError:
             if stagnated_before or comp.n_components == 0:
                 raise
