@@ -27,21 +27,23 @@ namespace mvamg {
 namespace galerkin {
 
 constexpr int kWarps = 8;           // warps per CTA of the row kernels
-constexpr int kTable = 512;         // shared-memory accumulator slots per warp
-constexpr int kTableFill = 384;     // distinct columns before a row overflows to global memory
-// dynamic shared memory of spgemm_smem_kernel: table + compact list per warp
-constexpr int kSmemBytes = kWarps * (kTable + kTableFill) * (4 + 8);
+constexpr int kTable = 256;         // shared-memory accumulator slots per warp
+constexpr int kTableFill = 192;     // distinct columns before a row overflows to global memory
+// dynamic shared memory of spgemm_smem_kernel per warp: table (key, value),
+// the list of occupied slots, and the compacted (key, value) output list
+constexpr int kSmemBytes = kWarps * (kTable * 12 + kTableFill * 16);
 
 __device__ __forceinline__ unsigned slot_hash(int c) { return (unsigned)c * 2654435761u; }
 
 // Accumulate X row `row` times Y into a (keys, vals) table of H slots
-// (H a power of two, keys -1 = empty, vals 0.0).  Returns false (all lanes)
-// when more than `fill` distinct columns appear; the table is then dirty and
-// must be cleared by the caller with clear_table().
-__device__ __forceinline__ bool accumulate_row(int row, const int* __restrict__ xp, const int* __restrict__ xi,
-                                               const double* __restrict__ xv, const int* __restrict__ yp,
-                                               const int* __restrict__ yi, const double* __restrict__ yv,
-                                               int* keys, double* vals, int H, int fill) {
+// (H a power of two, keys -1 = empty, vals 0.0); every newly occupied slot is
+// appended to `slots`.  Returns the number of distinct columns, or -1 (all
+// lanes) once more than `fill` appear -- the slots listed so far are then
+// still dirty (clear_slots()).
+__device__ __forceinline__ int accumulate_row(int row, const int* __restrict__ xp, const int* __restrict__ xi,
+                                              const double* __restrict__ xv, const int* __restrict__ yp,
+                                              const int* __restrict__ yi, const double* __restrict__ yv,
+                                              int* keys, double* vals, int* slots, int H, int fill) {
   const int lane = threadIdx.x & 31;
   const int j0 = xp[row], j1 = xp[row + 1];
   int distinct = 0;
@@ -51,17 +53,18 @@ __device__ __forceinline__ bool accumulate_row(int row, const int* __restrict__ 
     const int k0 = yp[j], k1 = yp[j + 1];
     for (int base = k0; base < k1; base += 32) {
       const int kk = base + lane;
-      int added = 0;
+      bool added = false;
+      unsigned h = 0;
       if (kk < k1) {
         const int c = yi[kk];
         const double prod = __dmul_rn(a, yv[kk]);
-        unsigned h = slot_hash(c) & (H - 1);
+        h = slot_hash(c) & (H - 1);
         for (int probe = 0; probe < H; ++probe) {
           int key = *(volatile int*)&keys[h];
           if (key == -1) {
             key = atomicCAS(&keys[h], -1, c);
             if (key == -1) {
-              added = 1;
+              added = true;
               key = c;
             }
           }
@@ -72,12 +75,15 @@ __device__ __forceinline__ bool accumulate_row(int row, const int* __restrict__ 
           h = (h + 1) & (H - 1);
         }
       }
-      distinct += __popc(__ballot_sync(0xffffffffu, added));
+      const unsigned m = __ballot_sync(0xffffffffu, added);
+      const int at = distinct + __popc(m & ((1u << lane) - 1u));
+      if (added && at < fill) slots[at] = (int)h;
+      distinct += __popc(m);
       __syncwarp();
-      if (distinct > fill) return false;
+      if (distinct > fill) return -1;
     }
   }
-  return true;
+  return distinct;
 }
 
 __device__ __forceinline__ void clear_table(int* keys, double* vals, int H) {
@@ -88,19 +94,31 @@ __device__ __forceinline__ void clear_table(int* keys, double* vals, int H) {
   __syncwarp();
 }
 
-// Compact the nonzero slots into (lk, lv) while clearing the table, then (FILL)
-// write them sorted by column at ci/cv + ofs.  Exact-zero sums are dropped as
-// csr_matmat does.  Returns the row's nnz.
+// After an overflow: the listed slots plus any slot claimed in the last chunk
+// may be dirty, so clear the whole table.
+__device__ __forceinline__ void clear_slots(int* keys, double* vals, int H) { clear_table(keys, vals, H); }
+
+// Compact the nonzero listed slots into (lk, lv) while clearing them, then
+// (FILL) write them sorted by column at ci/cv + ofs.  Exact-zero sums are
+// dropped as csr_matmat does.  Returns the row's nnz.
 template <bool FILL>
-__device__ __forceinline__ int emit_row(int* keys, double* vals, int H, int* lk, double* lv,
-                                        int* __restrict__ ci, double* __restrict__ cv, long long ofs) {
+__device__ __forceinline__ int emit_row(int distinct, const int* slots, int* keys, double* vals, int* lk,
+                                        double* lv, int* __restrict__ ci, double* __restrict__ cv, long long ofs) {
   const int lane = threadIdx.x & 31;
   int count = 0;
-  for (int s0 = 0; s0 < H; s0 += 32) {
-    const int s = s0 + lane;
-    const int key = keys[s];
-    const double val = vals[s];
-    const bool live = key != -1 && val != 0.0;
+  for (int e0 = 0; e0 < distinct; e0 += 32) {
+    const int e = e0 + lane;
+    bool live = false;
+    int key = 0;
+    double val = 0.0;
+    if (e < distinct) {
+      const int s = slots[e];
+      key = keys[s];
+      val = vals[s];
+      live = val != 0.0;
+      keys[s] = -1;
+      vals[s] = 0.0;
+    }
     const unsigned m = __ballot_sync(0xffffffffu, live);
     if (FILL && live) {
       const int at = count + __popc(m & ((1u << lane) - 1u));
@@ -108,8 +126,6 @@ __device__ __forceinline__ int emit_row(int* keys, double* vals, int H, int* lk,
       lv[at] = val;
     }
     count += __popc(m);
-    keys[s] = -1;
-    vals[s] = 0.0;
   }
   __syncwarp();
   if (FILL) {
@@ -138,14 +154,17 @@ __global__ void __launch_bounds__(kWarps * 32) spgemm_smem_kernel(
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* vals = reinterpret_cast<double*>(g_smem) + w * kTable;
   double* lv = reinterpret_cast<double*>(g_smem) + kWarps * kTable + w * kTableFill;
-  int* keys = reinterpret_cast<int*>(g_smem + kWarps * (kTable + kTableFill) * 8) + w * kTable;
-  int* lk = reinterpret_cast<int*>(g_smem + kWarps * (kTable + kTableFill) * 8) + kWarps * kTable + w * kTableFill;
+  int* ibase = reinterpret_cast<int*>(g_smem + kWarps * (kTable + kTableFill) * 8);
+  int* keys = ibase + w * kTable;
+  int* slots = ibase + kWarps * kTable + w * kTableFill;
+  int* lk = ibase + kWarps * (kTable + kTableFill) + w * kTableFill;
   clear_table(keys, vals, kTable);
   const int warps = gridDim.x * kWarps;
   for (int row = blockIdx.x * kWarps + w; row < nrows; row += warps) {
     if (FILL && ovf_flag[row]) continue;
-    if (!accumulate_row(row, xp, xi, xv, yp, yi, yv, keys, vals, kTable, kTableFill)) {
-      clear_table(keys, vals, kTable);
+    const int distinct = accumulate_row(row, xp, xi, xv, yp, yi, yv, keys, vals, slots, kTable, kTableFill);
+    if (distinct < 0) {
+      clear_slots(keys, vals, kTable);
       if (!FILL && lane == 0) {
         ovf_flag[row] = 1;
         ovf_rows[atomicAdd(n_ovf, 1)] = row;
@@ -155,7 +174,7 @@ __global__ void __launch_bounds__(kWarps * 32) spgemm_smem_kernel(
       }
       continue;
     }
-    const int c = emit_row<FILL>(keys, vals, kTable, lk, lv, ci, cv, FILL ? cp[row] : 0);
+    const int c = emit_row<FILL>(distinct, slots, keys, vals, lk, lv, ci, cv, FILL ? cp[row] : 0);
     if (!FILL && lane == 0) {
       cnt[row] = c;
       ovf_flag[row] = 0;
@@ -173,16 +192,17 @@ __global__ void __launch_bounds__(kWarps * 32) spgemm_global_kernel(
     int* __restrict__ cnt, const long long* __restrict__ cp, int* __restrict__ ci, double* __restrict__ cv) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long gw = (long long)blockIdx.x * kWarps + w;
-  int* keys = pool_keys + gw * 2 * H;
-  int* lk = keys + H;
-  double* vals = pool_vals + gw * 2 * H;
+  int* keys = pool_keys + gw * 3 * (long long)H;
+  int* slots = keys + H;
+  int* lk = keys + 2 * H;
+  double* vals = pool_vals + gw * 2 * (long long)H;
   double* lv = vals + H;
   clear_table(keys, vals, H);
   const int warps = gridDim.x * kWarps;
   for (int t = (int)gw; t < nlist; t += warps) {
     const int row = rows[t];
-    accumulate_row(row, xp, xi, xv, yp, yi, yv, keys, vals, H, H);
-    const int c = emit_row<FILL>(keys, vals, H, lk, lv, ci, cv, FILL ? cp[row] : 0);
+    const int distinct = accumulate_row(row, xp, xi, xv, yp, yi, yv, keys, vals, slots, H, H);
+    const int c = emit_row<FILL>(distinct, slots, keys, vals, lk, lv, ci, cv, FILL ? cp[row] : 0);
     if (!FILL && lane == 0) cnt[row] = c;
   }
 }

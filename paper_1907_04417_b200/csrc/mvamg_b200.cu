@@ -770,25 +770,30 @@ int pcg_device(mvamg_hierarchy* h, int pc, mvamg_composite* comp, const double* 
 // Galerkin product on the device (galerkin.cuh)
 // ---------------------------------------------------------------------------
 // Device CSR owned by the library (intermediates and the returned A_c).
+// Intermediates are stream-ordered allocations (cudaMallocAsync / cudaFreeAsync
+// on the working stream), so freeing them never synchronises the device.
 struct DevCsr {
   int n = 0, m = 0;
   long long nnz = 0;
   int* ip = nullptr;
   int* ix = nullptr;
   double* v = nullptr;
+  cudaStream_t s = nullptr;
   void release() {
-    if (ip) cudaFree(ip);
-    if (ix) cudaFree(ix);
-    if (v) cudaFree(v);
+    for (void* p : {(void*)ip, (void*)ix, (void*)v})
+      if (p) cudaFreeAsync(p, s);
     ip = ix = nullptr;
     v = nullptr;
   }
 };
 
-struct DevTmp {  // scoped cudaMalloc
+struct DevTmp {  // scoped stream-ordered allocation
   void* p = nullptr;
+  cudaStream_t s = nullptr;
+  explicit DevTmp(cudaStream_t st = nullptr) : s(st) {}
+  cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes, s); }
   ~DevTmp() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, s);
   }
   template <class T>
   T* get() const {
@@ -808,8 +813,8 @@ int scan_counts(int n, const int* cnt, long long* offsets, long long* total, cud
   using namespace galerkin;
   const long long per = (long long)kScanThreads * kScanItems;
   const int nb = (int)(((long long)n + 1 + per - 1) / per);
-  DevTmp bsum;
-  CUDA_TRY(cudaMalloc(&bsum.p, (size_t)nb * 8));
+  DevTmp bsum(s);
+  CUDA_TRY(bsum.alloc((size_t)nb * 8));
   scan_blocks_kernel<<<nb, kScanThreads, 0, s>>>(n, cnt, offsets, bsum.get<long long>());
   GK_LAUNCH_CHECK();
   scan_sums_kernel<<<1, kScanThreads, 0, s>>>(nb, bsum.get<long long>());
@@ -826,9 +831,10 @@ int alloc_csr(DevCsr& C, int n, int m, long long nnz, const long long* offsets64
   C.n = n;
   C.m = m;
   C.nnz = nnz;
-  CUDA_TRY(cudaMalloc(&C.ip, (size_t)(n + 1) * 4));
-  CUDA_TRY(cudaMalloc(&C.ix, (size_t)std::max(nnz, 1LL) * 4));
-  CUDA_TRY(cudaMalloc(&C.v, (size_t)std::max(nnz, 1LL) * 8));
+  C.s = s;
+  CUDA_TRY(cudaMallocAsync((void**)&C.ip, (size_t)(n + 1) * 4, s));
+  CUDA_TRY(cudaMallocAsync((void**)&C.ix, (size_t)std::max(nnz, 1LL) * 4, s));
+  CUDA_TRY(cudaMallocAsync((void**)&C.v, (size_t)std::max(nnz, 1LL) * 8, s));
   galerkin::narrow_offsets_kernel<<<grid_for(n + 1), 256, 0, s>>>(n, offsets64, C.ip);
   GK_LAUNCH_CHECK();
   return 0;
@@ -838,12 +844,12 @@ int alloc_csr(DevCsr& C, int n, int m, long long nnz, const long long* offsets64
 int csr_transpose(int n, int m, const int* ip, const int* ix, const double* v, long long nnz, DevCsr& T,
                   cudaStream_t s) {
   using namespace galerkin;
-  DevTmp cnt, off, cur, tix, tv;
-  CUDA_TRY(cudaMalloc(&cnt.p, (size_t)(m + 1) * 4));
-  CUDA_TRY(cudaMalloc(&off.p, (size_t)(m + 1) * 8));
-  CUDA_TRY(cudaMalloc(&cur.p, (size_t)(m + 1) * 4));
-  CUDA_TRY(cudaMalloc(&tix.p, (size_t)std::max(nnz, 1LL) * 4));
-  CUDA_TRY(cudaMalloc(&tv.p, (size_t)std::max(nnz, 1LL) * 8));
+  DevTmp cnt(s), off(s), cur(s), tix(s), tv(s);
+  CUDA_TRY(cnt.alloc((size_t)(m + 1) * 4));
+  CUDA_TRY(off.alloc((size_t)(m + 1) * 8));
+  CUDA_TRY(cur.alloc((size_t)(m + 1) * 4));
+  CUDA_TRY(tix.alloc((size_t)std::max(nnz, 1LL) * 4));
+  CUDA_TRY(tv.alloc((size_t)std::max(nnz, 1LL) * 8));
   CUDA_TRY(cudaMemsetAsync(cnt.p, 0, (size_t)(m + 1) * 4, s));
   CUDA_TRY(cudaMemsetAsync(cur.p, 0, (size_t)(m + 1) * 4, s));
   if (nnz > 0) {
@@ -875,17 +881,17 @@ int spgemm_ordered(int nrows, int ncols, const int* xp, const int* xi, const dou
     CUDA_TRY(cudaFuncSetAttribute(spgemm_smem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
     attr = true;
   }
-  DevTmp cnt, flag, rows, ctr, off;
-  CUDA_TRY(cudaMalloc(&cnt.p, (size_t)(nrows + 1) * 4));
-  CUDA_TRY(cudaMalloc(&flag.p, (size_t)nrows + 1));
-  CUDA_TRY(cudaMalloc(&rows.p, (size_t)(nrows + 1) * 4));
-  CUDA_TRY(cudaMalloc(&ctr.p, 16));
-  CUDA_TRY(cudaMalloc(&off.p, (size_t)(nrows + 1) * 8));
+  DevTmp cnt(s), flag(s), rows(s), ctr(s), off(s);
+  CUDA_TRY(cnt.alloc((size_t)(nrows + 1) * 4));
+  CUDA_TRY(flag.alloc((size_t)nrows + 1));
+  CUDA_TRY(rows.alloc((size_t)(nrows + 1) * 4));
+  CUDA_TRY(ctr.alloc(16));
+  CUDA_TRY(off.alloc((size_t)(nrows + 1) * 8));
   CUDA_TRY(cudaMemsetAsync(ctr.p, 0, 16, s));
   CUDA_TRY(cudaMemsetAsync(cnt.p, 0, (size_t)(nrows + 1) * 4, s));
   int* n_ovf = ctr.get<int>();
   int* max_ub = n_ovf + 1;
-  const int grid = std::max(1, std::min((nrows + kWarps - 1) / kWarps, num_sms() * 2));
+  const int grid = std::max(1, std::min((nrows + kWarps - 1) / kWarps, num_sms() * 4));
   if (nrows > 0) {
     spgemm_smem_kernel<false><<<grid, kWarps * 32, kSmemBytes, s>>>(nrows, xp, xi, xv, yp, yi, yv, cnt.get<int>(),
                                                                     flag.get<unsigned char>(), rows.get<int>(), n_ovf,
@@ -897,17 +903,17 @@ int spgemm_ordered(int nrows, int ncols, const int* xp, const int* xi, const dou
   CUDA_TRY(cudaStreamSynchronize(s));
   const int novf = hctr[0];
   int H = 0, ggrid = 0;
-  DevTmp pk, pv;
+  DevTmp pk(s), pv(s);
   if (novf > 0) {
     const long long need = std::min<long long>(std::max(hctr[1], 1), std::max(ncols, 1));
     H = 64;
     while (H < 2 * need) H <<= 1;
     long long nw = std::min<long long>(novf, (long long)num_sms() * 2 * kWarps);
-    const long long cap = (1LL << 30) / ((long long)H * 24);  // pool <= 1 GiB
-    nw = std::max(1LL, std::min(nw, cap));
+    const long long cap = (1LL << 30) / ((long long)H * 28 * kWarps);  // pool <= 1 GiB
+    nw = std::max<long long>(kWarps, std::min(nw, cap * kWarps));
     ggrid = (int)((nw + kWarps - 1) / kWarps);
-    CUDA_TRY(cudaMalloc(&pk.p, (size_t)ggrid * kWarps * 2 * H * 4));
-    CUDA_TRY(cudaMalloc(&pv.p, (size_t)ggrid * kWarps * 2 * H * 8));
+    CUDA_TRY(pk.alloc((size_t)ggrid * kWarps * 3 * H * 4));
+    CUDA_TRY(pv.alloc((size_t)ggrid * kWarps * 2 * H * 8));
     spgemm_global_kernel<false><<<ggrid, kWarps * 32, 0, s>>>(novf, rows.get<int>(), xp, xi, xv, yp, yi, yv, H,
                                                               pk.get<int>(), pv.get<double>(), cnt.get<int>(), nullptr,
                                                               nullptr, nullptr);
@@ -956,12 +962,12 @@ int galerkin_device(int n, int nc, Csr A, Csr P, DevCsr& S, cudaStream_t s, floa
   if (int e = spgemm_ordered(nc, nc, R.ip, R.ix, R.v, AP.ip, AP.ix, AP.v, G, s)) return e;  // P^T (A P)
   CUDA_TRY(cudaEventRecord(ev[3], s));
   if (int e = csr_transpose(nc, nc, G.ip, G.ix, G.v, G.nnz, GT, s)) return e;
-  DevTmp cnt, off;
-  CUDA_TRY(cudaMalloc(&cnt.p, (size_t)(nc + 1) * 4));
-  CUDA_TRY(cudaMalloc(&off.p, (size_t)(nc + 1) * 8));
-  DevTmp gp, tp;  // int64 row offsets for the merge
-  CUDA_TRY(cudaMalloc(&gp.p, (size_t)(nc + 1) * 8));
-  CUDA_TRY(cudaMalloc(&tp.p, (size_t)(nc + 1) * 8));
+  DevTmp cnt(s), off(s);
+  CUDA_TRY(cnt.alloc((size_t)(nc + 1) * 4));
+  CUDA_TRY(off.alloc((size_t)(nc + 1) * 8));
+  DevTmp gp(s), tp(s);  // int64 row offsets for the merge
+  CUDA_TRY(gp.alloc((size_t)(nc + 1) * 8));
+  CUDA_TRY(tp.alloc((size_t)(nc + 1) * 8));
   widen_offsets_kernel<<<grid_for(nc + 1), 256, 0, s>>>(nc, G.ip, gp.get<long long>());
   GK_LAUNCH_CHECK();
   widen_offsets_kernel<<<grid_for(nc + 1), 256, 0, s>>>(nc, GT.ip, tp.get<long long>());
@@ -2105,7 +2111,8 @@ int mvamg_spmat_copy(const mvamg_spmat* m, int* indptr, int* indices, double* da
 
 int mvamg_spmat_destroy(mvamg_spmat* m) {
   if (m) {
-    m->m.release();
+    for (void* p : {(void*)m->m.ip, (void*)m->m.ix, (void*)m->m.v})
+      if (p) cudaFree(p);  // synchronous: the creating stream may be gone
     delete m;
   }
   return 0;
