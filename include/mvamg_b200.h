@@ -209,6 +209,14 @@ int mvamg_greedy_match(long long ne, const long long* ei, const long long* ej, i
 int mvamg_jacobi_svd_batch(int nblk, const int* row_ptr, int k, const double* A, int max_sweeps,
                            double tol, double* U, double* sigma, int* failed_block);
 
+/* ---- row-partitioned solve: halo packing, Krylov updates -- */
+/* dst[i] = src[idx[i]] (pack a halo message) / dst[idx[i]] = src[i] (unpack). */
+int mvamg_gather_f64(int n, const int* idx, const double* src, double* dst, void* stream);
+int mvamg_scatter_f64(int n, const int* idx, const double* src, double* dst, void* stream);
+/* y = y + (alpha * x)  (krylov.py:57-58) and y = x + (beta * y)  (krylov.py:70). */
+int mvamg_axpy_f64(int n, double alpha, const double* x, double* y, void* stream);
+int mvamg_xpby_f64(int n, const double* x, double beta, double* y, void* stream);
+
 /* ---- Galerkin product (setup) -------------------------- */
 /* Device CSR owned by the library. */
 typedef struct mvamg_spmat mvamg_spmat;

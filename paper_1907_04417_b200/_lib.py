@@ -83,6 +83,10 @@ SIGNATURES = [
     ("mvamg_galerkin_f64", _I, [_I, _I, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_P), ctypes.POINTER(_LL), _P, _P]),
     ("mvamg_spmat_copy", _I, [_P, _P, _P, _P, _P]),
     ("mvamg_spmat_destroy", _I, [_P]),
+    ("mvamg_gather_f64", _I, [_I, _P, _P, _P, _P]),
+    ("mvamg_scatter_f64", _I, [_I, _P, _P, _P, _P]),
+    ("mvamg_axpy_f64", _I, [_I, _D, _P, _P, _P]),
+    ("mvamg_xpby_f64", _I, [_I, _P, _D, _P, _P]),
 ]
 
 _lib = None

@@ -2118,4 +2118,41 @@ int mvamg_spmat_destroy(mvamg_spmat* m) {
   return 0;
 }
 
+
+int mvamg_gather_f64(int n, const int* idx, const double* src, double* dst, void* stream) {
+  if (n < 0) return fail(MVAMG_E_ARG, "gather: n < 0");
+  if (n == 0) return 0;
+  gather_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(n, idx, src, dst);
+  ++g_kernel_launches;
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int mvamg_scatter_f64(int n, const int* idx, const double* src, double* dst, void* stream) {
+  if (n < 0) return fail(MVAMG_E_ARG, "scatter: n < 0");
+  if (n == 0) return 0;
+  scatter_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(n, idx, src, dst);
+  ++g_kernel_launches;
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int mvamg_axpy_f64(int n, double alpha, const double* x, double* y, void* stream) {
+  if (n < 0) return fail(MVAMG_E_ARG, "axpy: n < 0");
+  if (n == 0) return 0;
+  axpy_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(n, alpha, x, y);
+  ++g_kernel_launches;
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int mvamg_xpby_f64(int n, const double* x, double beta, double* y, void* stream) {
+  if (n < 0) return fail(MVAMG_E_ARG, "xpby: n < 0");
+  if (n == 0) return 0;
+  xpby_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(n, x, beta, y);
+  ++g_kernel_launches;
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 }  // extern "C"

@@ -393,4 +393,28 @@ __global__ void pcg_setup_kernel(DevScalars* sc, double rtol, int itmax, double*
   sc->k = 0;
 }
 
+
+// ---- row-partitioned solve: halo packing and Krylov updates ----------------
+__global__ void gather_kernel(int n, const int* __restrict__ idx, const double* __restrict__ src,
+                              double* __restrict__ dst) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[idx[i]];
+}
+
+__global__ void scatter_kernel(int n, const int* __restrict__ idx, const double* __restrict__ src,
+                               double* __restrict__ dst) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[idx[i]] = src[i];
+}
+
+// y_i = y_i + (alpha * x_i)   (krylov.py:57-58: x += alpha p, r -= alpha q)
+__global__ void axpy_kernel(int n, double alpha, const double* __restrict__ x, double* __restrict__ y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[i] = __dadd_rn(y[i], __dmul_rn(alpha, x[i]));
+}
+
+// y_i = x_i + (beta * y_i)   (krylov.py:70: p = z + beta p)
+__global__ void xpby_kernel(int n, const double* __restrict__ x, double beta, double* __restrict__ y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[i] = __dadd_rn(x[i], __dmul_rn(beta, y[i]));
+}
+
 }  // namespace mvamg
