@@ -1,9 +1,7 @@
-"""Multi-GPU plumbing for the benchmark: one process per GPU, independent
-replicas of the solve (DESIGN.md (e): exact-order Gauss-Seidel does not shard
--- row-partitioning a sweep leaves its critical path unchanged -- so N GPUs run
-N independent solves; the only collectives are the barrier around the timed
-region and the max-over-ranks of the device times).  Backend "nccl" on GPUs,
-"gloo" in the CPU tests."""
+"""Multi-GPU plumbing for the benchmark: one process per GPU (torchrun
+environment), process-group set-up, barriers and the max-over-ranks of device
+times.  The row-partitioned solve itself is paper_1907_04417_b200.distributed.
+Backend "nccl" on GPUs, "gloo" in the CPU tests."""
 
 import os
 
