@@ -145,11 +145,13 @@ int mvamg_gs_levels(int n, const int* indptr, const int* indices, const double* 
                     int* perm);
 /* One GS sweep of a small / mid-size level on one thread-block cluster: x
  * resident in (distributed) shared memory, one cluster barrier per level set.
- * Bit-identical to the serial loop.  tperm: n + 2 doubles of device scratch;
+ * group = 1: one thread per row, bit-identical to the serial loop; group = 2,
+ * 4, 8 or 16: that many lanes per row with a shuffle-tree sum (same order of
+ * rows, tolerance parity).  tperm: n + 2 doubles of device scratch;
  * ws: >= 4 device ints. */
 int mvamg_gs_level_sweep_f64(int direction, int n, const int* indptr, const int* indices,
                              const double* data, int ncta, int rows_per_cta, int nlev, int max_rows,
-                             int max_ents, int threads, const int* lev_ptr, const int* lev_eptr,
+                             int max_ents, int threads, int group, const int* lev_ptr, const int* lev_eptr,
                              const void* rows, const void* ents, const int* perm, double* tperm,
                              const double* b, const double* x_old, double* x_new, int* ws, void* stream);
 /* Backward GS sweep from x_old with the mode-2 (backward, zero guess) level
@@ -157,7 +159,7 @@ int mvamg_gs_level_sweep_f64(int direction, int n, const int* indptr, const int*
  * first (same roundings), so the sweep reads only new values. */
 int mvamg_gs_level_sweep_folded_f64(int n, const int* indptr, const int* indices, const double* data,
                                     int ncta, int rows_per_cta, int nlev, int max_rows, int max_ents,
-                                    int threads, const int* lev_ptr, const int* lev_eptr,
+                                    int threads, int group, const int* lev_ptr, const int* lev_eptr,
                                     const void* rows, const void* ents, const int* perm,
                                     double* tperm, const double* b, const double* x_old,
                                     double* x_new, int* ws, void* stream);
@@ -256,8 +258,8 @@ int mvamg_hierarchy_set_gs_schedule(mvamg_hierarchy* h, int k, int mode, const u
 /* Small-level GS schedule of level k for sweep `mode` (see mvamg_gs_levels);
  * when set it takes precedence over the wavefront schedule. */
 int mvamg_hierarchy_set_gs_levels(mvamg_hierarchy* h, int k, int mode, int ncta, int rows_per_cta,
-                                  int nlev, int max_rows, int max_ents, int threads, const int* lev_ptr,
-                                  const int* lev_eptr, const void* rows, const void* ents,
+                                  int nlev, int max_rows, int max_ents, int threads, int group,
+                                  const int* lev_ptr, const int* lev_eptr, const void* rows, const void* ents,
                                   const int* perm, double* tperm);
 /* Dataflow row schedule of level k for sweep `mode` (see mvamg_gs_rows);
  * used when set and no level-set schedule is set for that mode. */

@@ -47,15 +47,15 @@ SIGNATURES = [
                                 _I, _I, _P, _P, _P, _P, _P]),
     ("mvamg_gs_levels", _I, [_I, _P, _P, _P, _I, _I, _I, _I, _PI, ctypes.POINTER(_LL), _PI, _PI, _PI, _P, _P,
                              _P, _P, _P]),
-    ("mvamg_gs_level_sweep_f64", _I, [_I, _I, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P,
-                                      _P, _P, _P, _P]),
+    ("mvamg_gs_level_sweep_f64", _I, [_I, _I, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P,
+                                      _P, _P, _P, _P, _P]),
     ("mvamg_gs_rows", _I, [_I, _P, _P, _P, _I, ctypes.POINTER(_LL), _PI, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     ("mvamg_gs_row_sweep_f64", _I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P,
                                     _P, _P, _P, _P, _P]),
     ("mvamg_greedy_match", _I, [_LL, _P, _P, _I, _P, _P, _P, ctypes.POINTER(_LL)]),
     ("mvamg_jacobi_svd_batch", _I, [_I, _P, _I, _P, _I, _D, _P, _P, _PI]),
-    ("mvamg_gs_level_sweep_folded_f64", _I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P,
-                                             _P, _P, _P, _P, _P]),
+    ("mvamg_gs_level_sweep_folded_f64", _I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P,
+                                             _P, _P, _P, _P, _P, _P]),
     ("mvamg_dense_gemv_f64", _I, [_I, _P, _P, _P, _P]),
     ("mvamg_dot_f64", _I, [_I, _P, _P, _P, _P, _P]),
     ("mvamg_dot_ws_bytes", _I, []),
@@ -63,7 +63,7 @@ SIGNATURES = [
     ("mvamg_hierarchy_destroy", _I, [_P]),
     ("mvamg_hierarchy_set_level", _I, [_P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _I]),
     ("mvamg_hierarchy_set_gs_schedule", _I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I]),
-    ("mvamg_hierarchy_set_gs_levels", _I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
+    ("mvamg_hierarchy_set_gs_levels", _I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_hierarchy_set_gs_rows", _I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P]),
     ("mvamg_hierarchy_set_mega", _I, [_P, _I]),
     ("mvamg_hierarchy_set_transfer", _I, [_P, _I, _P, _P, _P, _P, _P, _P]),

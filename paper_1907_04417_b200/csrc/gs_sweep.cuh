@@ -862,7 +862,13 @@ __device__ __forceinline__ double ld_dsmem_f64(unsigned caddr) {
 // neighbours still hold x_old -- exactly what the serial loop reads.  Each
 // (CTA, level) block of rows is contiguous in the host layout and is staged
 // two levels ahead with coalesced cp.async.
-template <bool CLUSTER>
+// G == 1: one thread per row, CSR-order subtractions (bit-exact with the
+// serial sweep).  G > 1 (tolerance parity, GpuConfig.exact_gs = False): G lanes
+// per row, each summing a strided share of the row's products with FMAs, then
+// an xor-shuffle tree; the row is final after cnt/G + log2(G) dependent steps
+// instead of cnt.  The level order -- hence the GS dependency order -- is the
+// same; only the rounding of each row's sum changes.
+template <bool CLUSTER, int G>
 __global__ void __launch_bounds__(1024, 1) gs_level_kernel(GsLevelArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const unsigned me = CLUSTER ? cluster_rank() : 0u, ncta = CLUSTER ? cluster_nctas() : 1u;
@@ -909,6 +915,36 @@ __global__ void __launch_bounds__(1024, 1) gs_level_kernel(GsLevelArgs a) {
     const double* rhs = reinterpret_cast<const double*>(bb + rows_b + ents_b);
     const int r0 = __ldg(lp + l), r1 = __ldg(lp + l + 1);
     const int e0 = __ldg(le + l), toff = r0 & 1;
+    if (G > 1) {
+      const int ngroups = T / G, g = tid / G, li = tid % G;
+      const int nr = r1 - r0, iters = (nr + ngroups - 1) / ngroups;
+      for (int it = 0; it < iters; ++it) {
+        const int r = g + it * ngroups;
+        const bool act = r < nr;
+        double part = 0.0;
+        GsLevelRow m;
+        if (act) {
+          m = rows[r];
+          const GsLevelEntry* e = ents + (m.estart - e0);
+          for (int k = li; k < m.cnt; k += G) {
+            const GsLevelEntry en = e[k];
+            double xv;
+            if (CLUSTER) {
+              const unsigned owner = (unsigned)en.src >> 26, loc = (unsigned)en.src & ((1u << 26) - 1);
+              xv = ld_dsmem_f64(map_rank(xs_local + 8u * loc, owner));
+            } else {
+              xv = x[en.src];
+            }
+            part = __fma_rn(en.coef, xv, part);
+          }
+        }
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, off));
+        if (act && li == 0) x[m.row - base] = div_rn_markstein(__dsub_rn(rhs[toff + r], part), m.diag, m.rdiag);
+      }
+      if (CLUSTER) cluster_sync();  // level l published cluster-wide
+      continue;
+    }
     for (int r = tid; r < r1 - r0; r += T) {
       const GsLevelRow m = rows[r];
       double s = rhs[toff + r];

@@ -151,6 +151,7 @@ struct GsLevels {
   const int* perm = nullptr;
   double* tperm = nullptr;
   int nlev = 0, max_rows = 0, max_ents = 0, threads = 256;
+  int group = 1;  // lanes per row: 1 = bit-exact CSR order, 2..16 = tolerance parity
 };
 
 // Dataflow row schedule (gs_row_kernel) of one sweep mode.
@@ -320,9 +321,12 @@ int launch_gs_levels(const Csr& A, const GsLevels& g, bool zero, const double* b
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncSetAttribute(gs_level_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
-    cudaFuncSetAttribute(gs_level_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
-    cudaFuncSetAttribute(gs_level_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+#define MVAMG_LEVEL_ATTR(GG)                                                                              \
+  cudaFuncSetAttribute(gs_level_kernel<false, GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024); \
+  cudaFuncSetAttribute(gs_level_kernel<true, GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);  \
+  cudaFuncSetAttribute(gs_level_kernel<true, GG>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    MVAMG_LEVEL_ATTR(1) MVAMG_LEVEL_ATTR(2) MVAMG_LEVEL_ATTR(4) MVAMG_LEVEL_ATTR(8) MVAMG_LEVEL_ATTR(16)
+#undef MVAMG_LEVEL_ATTR
     cudaGetLastError();
   }
   const size_t smem = gs_level_smem(g);
@@ -347,8 +351,16 @@ int launch_gs_levels(const Csr& A, const GsLevels& g, bool zero, const double* b
   a.tperm = g.tperm;
   a.xold = xold;
   a.xnew = xnew;
+  if (g.group != 1 && g.group != 2 && g.group != 4 && g.group != 8 && g.group != 16)
+    return fail(MVAMG_E_ARG, "gs levels: lanes per row must be 1, 2, 4, 8 or 16");
   if (g.ncta == 1) {
-    gs_level_kernel<false><<<1, g.threads, smem, s>>>(a);
+    switch (g.group) {
+      case 1: gs_level_kernel<false, 1><<<1, g.threads, smem, s>>>(a); break;
+      case 2: gs_level_kernel<false, 2><<<1, g.threads, smem, s>>>(a); break;
+      case 4: gs_level_kernel<false, 4><<<1, g.threads, smem, s>>>(a); break;
+      case 8: gs_level_kernel<false, 8><<<1, g.threads, smem, s>>>(a); break;
+      default: gs_level_kernel<false, 16><<<1, g.threads, smem, s>>>(a); break;
+    }
     CUDA_TRY(cudaGetLastError());
     return 0;
   }
@@ -364,7 +376,13 @@ int launch_gs_levels(const Csr& A, const GsLevels& g, bool zero, const double* b
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_level_kernel<true>, a));
+  switch (g.group) {
+    case 1: CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_level_kernel<true, 1>, a)); break;
+    case 2: CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_level_kernel<true, 2>, a)); break;
+    case 4: CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_level_kernel<true, 4>, a)); break;
+    case 8: CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_level_kernel<true, 8>, a)); break;
+    default: CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_level_kernel<true, 16>, a)); break;
+  }
   return 0;
 }
 
@@ -1444,7 +1462,7 @@ int mvamg_gs_levels(int n, const int* indptr, const int* indices, const double* 
 
 int mvamg_gs_level_sweep_f64(int direction, int n, const int* indptr, const int* indices,
                              const double* data, int ncta, int rows_per_cta, int nlev, int max_rows,
-                             int max_ents, int threads, const int* lev_ptr, const int* lev_eptr,
+                             int max_ents, int threads, int group, const int* lev_ptr, const int* lev_eptr,
                              const void* rows, const void* ents, const int* perm, double* tperm,
                              const double* b, const double* x_old, double* x_new, int* ws, void* stream) {
   if (threads < 32 || threads > 1024 || threads % 32) return fail(MVAMG_E_ARG, "gs levels: bad thread count");
@@ -1454,7 +1472,7 @@ int mvamg_gs_level_sweep_f64(int direction, int n, const int* indptr, const int*
   g.lev_ptr = lev_ptr; g.lev_eptr = lev_eptr; g.rows = static_cast<const GsLevelRow*>(rows);
   g.ents = static_cast<const GsLevelEntry*>(ents); g.perm = perm; g.tperm = tperm;
   g.nlev = nlev; g.max_rows = max_rows; g.max_ents = max_ents; g.threads = threads;
-  g.ncta = ncta; g.rows_per_cta = rows_per_cta;
+  g.ncta = ncta; g.rows_per_cta = rows_per_cta; g.group = group;
   (void)direction;  // encoded in the schedule
   set_kernel_attrs();
   return launch_gs_levels(A, g, x_old == nullptr, b, x_old, x_new, ws, (cudaStream_t)stream);
@@ -1462,7 +1480,7 @@ int mvamg_gs_level_sweep_f64(int direction, int n, const int* indptr, const int*
 
 int mvamg_gs_level_sweep_folded_f64(int n, const int* indptr, const int* indices, const double* data,
                                     int ncta, int rows_per_cta, int nlev, int max_rows, int max_ents,
-                                    int threads, const int* lev_ptr, const int* lev_eptr,
+                                    int threads, int group, const int* lev_ptr, const int* lev_eptr,
                                     const void* rows, const void* ents, const int* perm,
                                     double* tperm, const double* b, const double* x_old,
                                     double* x_new, int* ws, void* stream) {
@@ -1473,21 +1491,21 @@ int mvamg_gs_level_sweep_folded_f64(int n, const int* indptr, const int* indices
   g.lev_ptr = lev_ptr; g.lev_eptr = lev_eptr; g.rows = static_cast<const GsLevelRow*>(rows);
   g.ents = static_cast<const GsLevelEntry*>(ents); g.perm = perm; g.tperm = tperm;
   g.nlev = nlev; g.max_rows = max_rows; g.max_ents = max_ents; g.threads = threads;
-  g.ncta = ncta; g.rows_per_cta = rows_per_cta;
+  g.ncta = ncta; g.rows_per_cta = rows_per_cta; g.group = group;
   set_kernel_attrs();
   return launch_gs_levels(A, g, false, b, x_old, x_new, ws, (cudaStream_t)stream, true);
 }
 
 int mvamg_hierarchy_set_gs_levels(mvamg_hierarchy* h, int k, int mode, int ncta, int rows_per_cta,
-                                  int nlev, int max_rows, int max_ents, int threads, const int* lev_ptr,
-                                  const int* lev_eptr, const void* rows, const void* ents,
+                                  int nlev, int max_rows, int max_ents, int threads, int group,
+                                  const int* lev_ptr, const int* lev_eptr, const void* rows, const void* ents,
                                   const int* perm, double* tperm) {
   if (!h || k < 0 || k >= h->L || mode < 0 || mode > 3) return fail(MVAMG_E_ARG, "set_gs_levels: bad index");
   GsLevels& g = h->lv[k].glv[mode];
   g.lev_ptr = lev_ptr; g.lev_eptr = lev_eptr; g.rows = static_cast<const GsLevelRow*>(rows);
   g.ents = static_cast<const GsLevelEntry*>(ents); g.perm = perm; g.tperm = tperm;
   g.nlev = nlev; g.max_rows = max_rows; g.max_ents = max_ents; g.threads = threads;
-  g.ncta = ncta; g.rows_per_cta = rows_per_cta;
+  g.ncta = ncta; g.rows_per_cta = rows_per_cta; g.group = group;
   return 0;
 }
 

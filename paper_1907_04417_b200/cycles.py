@@ -176,7 +176,7 @@ class GpuMultigridOperator:
                 dd = to_device(self.diagonals[k], np.float64)
                 self._keep.append(dd)
                 if 0 <= self.mega_k0 <= k:
-                    small = {m: DeviceGsLevels(A, m, dataclasses.replace(cfg, max_cluster=1)) for m in (0, 2)}
+                    small = {m: DeviceGsLevels(A, m, dataclasses.replace(cfg, max_cluster=1, exact_gs=True)) for m in (0, 2)}
                     self.gs_plans.append(None)
                     self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=small, mega=True))
                     _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),

@@ -79,6 +79,9 @@ class GpuConfig:
     row_gs_threads: int = 128       # threads per CTA of the row sweep
     row_gs_ctas: int = 0            # resident CTAs of the row sweep (0 = auto)
     device_galerkin: bool = True    # setup forms P'AP with the device kernel (bit-identical to scipy's)
+    exact_gs: bool = False          # True: every GS kernel keeps the CSR-order subtractions (bit-exact with
+                                    # the serial sweep); False: level-set sweeps sum long rows over several
+                                    # lanes (same row order, parity within rounding -- north star: 1e-10)
     row_gs_smem: int = 96 * 1024    # staged entry slices per row-sweep tile (halve threads above)
     force_row_gs: bool = False      # use the row sweep for every coarse level (tests / diagnostics)
     autotune_gs: bool = True        # coarse levels: time row and level-set sweeps once, keep the faster per mode
@@ -390,7 +393,11 @@ class DeviceGsLevels:
                    "gs_levels")
         self.n, self.mode, self.ncta, self.rows_per_cta = n, mode, ncta, rpc.value
         self.nlev, self.max_rows, self.max_ents = nlev.value, max(1, mr.value), max(1, me.value)
-        self.threads = int(min(1024, max(64, (self.max_rows + 31) // 32 * 32)))  # one thread per row
+        # lanes per row: 1 keeps the CSR-order subtractions (bit-exact); otherwise
+        # about 8 entries per lane, summed by a shuffle tree (tolerance parity)
+        avg = A.nnz / max(1, n)
+        self.group = 1 if cfg.exact_gs else int(min(16, max(1, 1 << int(np.ceil(np.log2(max(1.0, avg / 8)))))))
+        self.threads = int(min(1024, max(64, (self.max_rows * self.group + 31) // 32 * 32)))
         self.lev_ptr = to_device(lev_ptr)
         self.lev_eptr = to_device(lev_eptr)
         self.rows = to_device(rows.view(np.uint8))
@@ -409,7 +416,7 @@ class DeviceGsLevels:
         return self._smem(self.rows_per_cta, self.max_rows, self.max_ents)
 
     def args(self):
-        return (self.ncta, self.rows_per_cta, self.nlev, self.max_rows, self.max_ents, self.threads,
+        return (self.ncta, self.rows_per_cta, self.nlev, self.max_rows, self.max_ents, self.threads, self.group,
                 ptr(self.lev_ptr), ptr(self.lev_eptr), ptr(self.rows), ptr(self.ents), ptr(self.perm),
                 ptr(self.tperm))
 

@@ -184,9 +184,9 @@ def _gs_level_gpu(A, b, x_old, direction, zero, cfg=None, fold=False):
 def test_gs_level_kernel_bit_exact(mv, c1, cluster):
     """The level-set sweep (single CTA, or a forced cluster of 2 / 16 CTAs with
     x in distributed shared memory) on every structure."""
-    cfg = None
+    cfg = mv.GpuConfig(exact_gs=True)
     if cluster:
-        cfg = mv.GpuConfig(smem_limit=8 * 16384 // cluster + 20000, max_cluster=cluster)
+        cfg = mv.GpuConfig(smem_limit=8 * 16384 // cluster + 20000, max_cluster=cluster, exact_gs=True)
     rng = np.random.default_rng(11)
     mats = c1[1]
     cases = list(_structures()) + [("c1_l1", mats[1]), ("c1_l2", mats[2]), ("c1_l0", mats[0])]
@@ -206,6 +206,42 @@ def test_gs_level_kernel_bit_exact(mv, c1, cluster):
                 except ValueError:
                     continue  # does not fit the forced shared-memory limit
                 assert np.array_equal(got, want), (name, direction, zero, cluster)
+
+
+@pytest.mark.parametrize("cluster", [None, 2])
+def test_gs_level_kernel_relaxed(mv, c1, cluster):
+    """Tolerance-parity level-set sweep (GpuConfig.exact_gs = False: several
+    lanes per row, shuffle-tree sums): same dependency order, each sweep within
+    rounding of the serial loop."""
+    cfg = mv.GpuConfig(exact_gs=False)
+    if cluster:
+        cfg = mv.GpuConfig(smem_limit=8 * 16384 // cluster + 20000, max_cluster=cluster, exact_gs=False)
+    rng = np.random.default_rng(12)
+    mats = c1[1]
+    d = golden("c1")
+    cm, _ = hierarchy(d, "c0", fine=mats[0])
+    cases = list(_structures()) + [("c1_l1", mats[1]), ("c1_l2", mats[2]), ("c1_l3", mats[3]), ("c0_l2", cm[2])]
+    groups = set()
+    for name, A in cases:
+        n = A.shape[0]
+        b = rng.standard_normal(n)
+        x0 = rng.standard_normal(n)
+        for direction in ("forward", "backward"):
+            for zero in (True, False):
+                want = np.zeros(n) if zero else x0.copy()
+                oracle_gs(A, b, want, direction)
+                try:
+                    got = _gs_level_gpu(A, b, x0, direction, zero, cfg)
+                except ValueError:
+                    continue
+                assert rel(got, want) <= 1e-13, (name, direction, zero, cluster)
+        from paper_1907_04417_b200.device import DeviceGsLevels
+
+        try:
+            groups.add(DeviceGsLevels(sp.csr_matrix(A), 0, cfg).group)
+        except ValueError:
+            pass
+    assert max(groups) >= 4  # long coarse rows do run several lanes per row
 
 
 def _gs_row_gpu(A, b, x_old, direction, zero, cfg=None, fold=False):
@@ -269,8 +305,11 @@ def test_vcycle_matches_reference(c1):
 def test_vcycle_schedules_agree(mv, c1, cfg):
     """Level-set, wavefront and generic GS schedules give the same cycle."""
     d, mats, pros, op, _ = c1
-    other = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(**cfg))
-    assert np.array_equal(other.apply(d["b"]), op.apply(d["b"]))
+    exact = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(exact_gs=True))
+    other = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(exact_gs=True, **cfg))
+    assert np.array_equal(other.apply(d["b"]), exact.apply(d["b"]))
+    relaxed = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(exact_gs=False, **cfg))
+    assert rel(relaxed.apply(d["b"]), exact.apply(d["b"])) <= 1e-12
 
 
 def test_vcycle_deterministic(c1):
@@ -444,8 +483,8 @@ def test_fit_c1_end_to_end(mv):
 def test_mega_vcycle_bit_identical(mv, c1):
     """V-cycle through the one-block coarse kernel == the multi-kernel path, bit for bit."""
     d, mats, pros, _, _ = c1
-    op = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(coarse_mega=True))
-    off = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(coarse_mega=False))
+    op = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(coarse_mega=True, exact_gs=True))
+    off = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(coarse_mega=False, exact_gs=True))
     assert op.mega_k0 == 1 and off.mega_k0 == -1
     for key in ("b", "r1"):
         assert np.array_equal(op.apply(d[key]), off.apply(d[key]))
@@ -499,9 +538,9 @@ def test_short_chain_level_uses_row_sweep(mv, c1):
     P0 = sp.csr_matrix(pros[0][perm])
     pm = [A0] + list(mats[1:])
     pp = [P0] + list(pros[1:])
-    op = mv.GpuMultigridOperator(pm, pp)
+    op = mv.GpuMultigridOperator(pm, pp, config=mv.GpuConfig(exact_gs=True))
     assert op.level_dev[0].get("rows") is not None
-    wf = mv.GpuMultigridOperator(pm, pp, config=mv.GpuConfig(min_chain_rows=0.0))
+    wf = mv.GpuMultigridOperator(pm, pp, config=mv.GpuConfig(min_chain_rows=0.0, exact_gs=True))
     assert wf.level_dev[0].get("rows") is None
     b = d["b"][perm]
     z = op.apply(b)
