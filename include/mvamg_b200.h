@@ -170,13 +170,15 @@ int mvamg_gs_level_sweep_folded_f64(int n, const int* indptr, const int* indices
  * e1 | e2 << 16 (0xffff = none): the entry whose input is published last (the
  * highest DAG level) and the latest one at least two levels earlier -- the
  * kernel waits on e2, forms every published product, then waits on e1.  Entries
- * (CSR order; zero-guess modes keep only the DAG direction) are stored per
+ * (entry_order 0: CSR order, bit-exact with the serial sweep; 1: by the DAG
+ * level at which each input becomes final, old values first -- tolerance
+ * parity; zero-guess modes keep only the DAG direction) are stored per
  * warp of 32 positions as an ELL slice: entry u of position 32w + l at
  * (wofs[w] + u) * 32 + l, padded to the warp's longest row; src is the row of
  * the value, with bit 31 set for an x_old value (modes 1 and 3).  Query with
  * rowid == NULL first (*nslots = total slice rows, so coef / src hold
  * 32 * nslots elements; wofs holds ceil(n/32) + 1 ints). */
-int mvamg_gs_rows(int n, const int* indptr, const int* indices, const double* data, int mode,
+int mvamg_gs_rows(int n, const int* indptr, const int* indices, const double* data, int mode, int entry_order,
                   long long* nslots, int* nlev, int* rowid, int* cnt, int* crit, double* dg, double* rdg,
                   int* perm, int* wofs, double* coef, int* src);
 /* One GS sweep with a row schedule of `mode` (gs_row_kernel: one thread per

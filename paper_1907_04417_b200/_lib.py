@@ -49,7 +49,8 @@ SIGNATURES = [
                              _P, _P, _P]),
     ("mvamg_gs_level_sweep_f64", _I, [_I, _I, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P,
                                       _P, _P, _P, _P, _P]),
-    ("mvamg_gs_rows", _I, [_I, _P, _P, _P, _I, ctypes.POINTER(_LL), _PI, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    ("mvamg_gs_rows", _I, [_I, _P, _P, _P, _I, _I, ctypes.POINTER(_LL), _PI, _P, _P, _P, _P, _P, _P, _P, _P,
+                           _P]),
     ("mvamg_gs_row_sweep_f64", _I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P,
                                     _P, _P, _P, _P, _P]),
     ("mvamg_greedy_match", _I, [_LL, _P, _P, _I, _P, _P, _P, ctypes.POINTER(_LL)]),

@@ -1509,7 +1509,7 @@ int mvamg_hierarchy_set_gs_levels(mvamg_hierarchy* h, int k, int mode, int ncta,
   return 0;
 }
 
-int mvamg_gs_rows(int n, const int* indptr, const int* indices, const double* data, int mode,
+int mvamg_gs_rows(int n, const int* indptr, const int* indices, const double* data, int mode, int entry_order,
                   long long* nslots, int* nlev, int* rowid, int* cnt, int* crit, double* dg, double* rdg,
                   int* perm, int* wofs, double* coef, int* src) {
   if (n < 0 || !indptr || !nslots || !nlev || mode < 0 || mode > 3) return fail(MVAMG_E_ARG, "gs_rows: bad arguments");
@@ -1555,6 +1555,9 @@ int mvamg_gs_rows(int n, const int* indptr, const int* indices, const double* da
   *nslots = tot;
   *nlev = n > 0 ? nl : 0;
   if (!rowid) return 0;
+  if (entry_order != 0 && entry_order != 1)
+    return fail(MVAMG_E_ARG, "gs_rows: entry order must be 0 (CSR) or 1 (by input level)");
+  std::vector<int> ents;
   long long off = 0;
   for (int w = 0; w < nw; ++w) {
     int m = 0;
@@ -1570,11 +1573,28 @@ int mvamg_gs_rows(int n, const int* indptr, const int* indices, const double* da
         perm[i] = p;
         double dgv = 0.0;
         int lmax = -1, e1 = -1;
+        // the row's entries in consumption order: CSR order (entry_order = 0, the
+        // reference's rounding), or by the level at which each input becomes
+        // final, old values first, CSR order within a level (entry_order = 1:
+        // tolerance parity -- the chain is consumed as the inputs land, so
+        // only one subtraction is left when the last one arrives)
+        ents.clear();
         for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
           const int j = indices[k];
           if (j == i) { dgv = data[k]; continue; }
           const bool isnew = fwd ? j < i : j > i;
           if (zero && !isnew) continue;
+          ents.push_back(k);
+        }
+        auto avail = [&](int k) {
+          const int j = indices[k];
+          return (fwd ? j < i : j > i) ? lvl[j] : -1;
+        };
+        if (entry_order == 1)
+          std::stable_sort(ents.begin(), ents.end(), [&](int x, int y) { return avail(x) < avail(y); });
+        for (int k : ents) {
+          const int j = indices[k];
+          const bool isnew = fwd ? j < i : j > i;
           const size_t e = (size_t)(off + u) * 32 + l;
           coef[e] = data[k];
           src[e] = isnew ? j : (int)(0x80000000u | (unsigned)j);
@@ -1584,16 +1604,10 @@ int mvamg_gs_rows(int n, const int* indptr, const int* indices, const double* da
         // wait hints: e1 = the entry of the latest input; e2 = the latest one
         // at least two levels earlier (the pre-scan trigger)
         int e2 = -1, l2 = -1;
-        {
-          int uu = 0;
-          for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
-            const int j = indices[k];
-            if (j == i) continue;
-            const bool isnew = fwd ? j < i : j > i;
-            if (zero && !isnew) continue;
-            if (isnew && lvl[j] <= lmax - 2 && lvl[j] > l2) { l2 = lvl[j]; e2 = uu; }
-            ++uu;
-          }
+        for (int uu = 0; uu < (int)ents.size(); ++uu) {
+          const int j = indices[ents[uu]];
+          const bool isnew = fwd ? j < i : j > i;
+          if (isnew && lvl[j] <= lmax - 2 && lvl[j] > l2) { l2 = lvl[j]; e2 = uu; }
         }
         if (u >= 0xffff) e1 = e2 = -1;
         crit[p] = (e1 < 0 ? 0xffff : e1) | ((e2 < 0 ? 0xffff : e2) << 16);

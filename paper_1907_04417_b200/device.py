@@ -448,8 +448,11 @@ class DeviceGsRows:
         v = np.ascontiguousarray(A.data, dtype=np.float64)
         vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
         ns, nlev = ctypes.c_longlong(), ctypes.c_int()
-        _lib.check(L.mvamg_gs_rows(n, vp(ip), vp(ix), vp(v), int(mode), ctypes.byref(ns), ctypes.byref(nlev),
-                                   None, None, None, None, None, None, None, None, None), "gs_rows")
+        order = 0 if cfg.exact_gs else 1  # 1: entries by input level (tolerance parity)
+        self.order = order
+        _lib.check(L.mvamg_gs_rows(n, vp(ip), vp(ix), vp(v), int(mode), order, ctypes.byref(ns),
+                                   ctypes.byref(nlev), None, None, None, None, None, None, None, None, None),
+                   "gs_rows")
         nw = -(-n // 32)
         rowid = np.empty(max(1, n), dtype=np.int32)
         cnt = np.empty(max(1, n), dtype=np.int32)
@@ -460,9 +463,9 @@ class DeviceGsRows:
         wofs = np.empty(nw + 1, dtype=np.int32)
         coef = np.empty(max(32, 32 * ns.value), dtype=np.float64)
         src = np.empty(max(32, 32 * ns.value), dtype=np.int32)
-        _lib.check(L.mvamg_gs_rows(n, vp(ip), vp(ix), vp(v), int(mode), ctypes.byref(ns), ctypes.byref(nlev),
-                                   vp(rowid), vp(cnt), vp(crit), vp(dg), vp(rdg), vp(perm), vp(wofs), vp(coef),
-                                   vp(src)),
+        _lib.check(L.mvamg_gs_rows(n, vp(ip), vp(ix), vp(v), int(mode), order, ctypes.byref(ns),
+                                   ctypes.byref(nlev), vp(rowid), vp(cnt), vp(crit), vp(dg), vp(rdg), vp(perm),
+                                   vp(wofs), vp(coef), vp(src)),
                    "gs_rows")
         self.n, self.mode, self.nlev, self.nslots = n, mode, nlev.value, ns.value
         # threads per tile: the configured width, halved while the widest

@@ -264,7 +264,7 @@ def test_gs_row_kernel_bit_exact(mv, c1, cfg):
     """The dataflow row sweep (one thread per row, eager CSR-order chains,
     ticketed CTAs; a single resident CTA exercises same-CTA dependencies) in
     all four modes and folded, on every structure and the C1 levels."""
-    config = mv.GpuConfig(**cfg) if cfg else None
+    config = mv.GpuConfig(exact_gs=True, **(cfg or {}))
     rng = np.random.default_rng(13)
     mats = c1[1]
     cases = list(_structures()) + [("c1_l1", mats[1]), ("c1_l2", mats[2]), ("c1_l0", mats[0])]
@@ -281,6 +281,29 @@ def test_gs_row_kernel_bit_exact(mv, c1, cfg):
                 if direction == "backward" and not zero:
                     folded = _gs_row_gpu(A, b, x0, direction, zero, config, fold=True)
                     assert np.array_equal(folded, want), (name, "folded", cfg)
+
+
+@pytest.mark.parametrize("cfg", [None, dict(row_gs_threads=32, row_gs_ctas=1)])
+def test_gs_row_kernel_relaxed(mv, c1, cfg):
+    """Row sweep with entries consumed in input-availability order (the
+    default, tolerance parity): same DAG, each sweep within rounding."""
+    config = mv.GpuConfig(exact_gs=False, **(cfg or {}))
+    rng = np.random.default_rng(14)
+    mats = c1[1]
+    cases = list(_structures()) + [("c1_l1", mats[1]), ("c1_l2", mats[2]), ("c1_l0", mats[0])]
+    for name, A in cases:
+        n = A.shape[0]
+        b = rng.standard_normal(n)
+        x0 = rng.standard_normal(n)
+        for direction in ("forward", "backward"):
+            for zero in (True, False):
+                want = np.zeros(n) if zero else x0.copy()
+                oracle_gs(A, b, want, direction)
+                got = _gs_row_gpu(A, b, x0, direction, zero, config)
+                assert rel(got, want) <= 1e-13, (name, direction, zero, cfg)
+                if direction == "backward" and not zero:
+                    folded = _gs_row_gpu(A, b, x0, direction, zero, config, fold=True)
+                    assert rel(folded, want) <= 1e-13, (name, "folded", cfg)
 
 
 def test_gs_hand_recurrence(mv):
