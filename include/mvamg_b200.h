@@ -163,6 +163,25 @@ int mvamg_gs_level_sweep_folded_f64(int n, const int* indptr, const int* indices
                                     const void* rows, const void* ents, const int* perm,
                                     double* tperm, const double* b, const double* x_old,
                                     double* x_new, int* ws, void* stream);
+/* Chain-scan GS sweep (tolerance parity; csrc/gs_scan.cuh) for levels with
+ * chain structure (grid lines): one CTA, chains round-robin over its warps, a
+ * warp composes 32 rows' affine updates x_i = o_i + s_i x_{i-1} with a shuffle
+ * scan.  Same dependency order as _kernels.py:15-38; sums reassociated.  The
+ * schedule comes from paper_1907_04417_b200/gs_scan.py: chains in sweep order;
+ * per record (slope, coefficients) double pairs and four ring addresses; per
+ * segment a 32-byte header (two waits, the deferred source of its last row,
+ * its coefficient); the row -> record map and RN(1/diag); the distinct
+ * source-chain distances as a host array of ndelta <= 4 ints.  window > 0
+ * (power of two, single distance 1): ring slots keep positions mod window.  mode: 0 fwd from 0, 1 fwd from
+ * x_old, 2 bwd from 0, 3 bwd from x_old.  o0: device scratch in the record
+ * layout (padding entries zero).  ws: >= 2 device ints (ws[1]: timeout). */
+int mvamg_gs_scan_sweep_f64(int mode, int n, const int* indptr, const int* indices, const double* data,
+                            int nchains, int S, int ring_len, int ndelta, const int* deltas, int K, int threads,
+                            int window, const int* seg_ptr, const int* chain_start, const int* chain_len,
+                            const void* recv, const void* addr, const void* seginfo, double* o0, const int* rec,
+                            const double* rdiag, const double* b, const double* x_old, double* x_new, int* ws,
+                            void* stream);
+
 /* GS dataflow row schedule for mid-size coarse levels (host).  mode as in
  * mvamg_gs_levels.  Rows are put in topological order of the sweep's DAG
  * (level, then longest row first); position p holds row rowid[p] with cnt[p]
@@ -263,6 +282,13 @@ int mvamg_hierarchy_set_gs_levels(mvamg_hierarchy* h, int k, int mode, int ncta,
                                   int nlev, int max_rows, int max_ents, int threads, int group,
                                   const int* lev_ptr, const int* lev_eptr, const void* rows, const void* ents,
                                   const int* perm, double* tperm);
+/* Chain-scan schedule of level k for sweep `mode` (see mvamg_gs_scan_sweep_f64);
+ * used before any other schedule of that mode when set. */
+int mvamg_hierarchy_set_gs_scan(mvamg_hierarchy* h, int k, int mode, int nchains, int S, int ring_len,
+                                int ndelta, const int* deltas, int K, int threads, int window,
+                                const int* seg_ptr, const int* chain_start, const int* chain_len, const void* recv,
+                                const void* addr, const void* seginfo, double* o0, const int* rec,
+                                const double* rdiag);
 /* Dataflow row schedule of level k for sweep `mode` (see mvamg_gs_rows);
  * used when set and no level-set schedule is set for that mode. */
 int mvamg_hierarchy_set_gs_rows(mvamg_hierarchy* h, int k, int mode, const int* rowid, const int* cnt,

@@ -84,6 +84,8 @@ SIGNATURES = [
     ("mvamg_galerkin_f64", _I, [_I, _I, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_P), ctypes.POINTER(_LL), _P, _P]),
     ("mvamg_spmat_copy", _I, [_P, _P, _P, _P, _P]),
     ("mvamg_spmat_destroy", _I, [_P]),
+    ("mvamg_gs_scan_sweep_f64", _I, [_I, _I, _P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _I] + [_P] * 14),
+    ("mvamg_hierarchy_set_gs_scan", _I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _I] + [_P] * 9),
     ("mvamg_gather_f64", _I, [_I, _P, _P, _P, _P]),
     ("mvamg_scatter_f64", _I, [_I, _P, _P, _P, _P]),
     ("mvamg_axpy_f64", _I, [_I, _D, _P, _P, _P]),

@@ -1,0 +1,271 @@
+// gs_scan.cuh -- chain-scan Gauss-Seidel sweep for fine levels with chain
+// structure (tolerance parity: GpuConfig.exact_gs = False).
+//
+// The reference sweep (pkg/src/mvamg/_kernels.py:15-38) updates rows in order.
+// On a grid, consecutive rows form chains (grid lines).  Within a chain, row i
+// depends on row i-1; every other new-value source lies in an earlier chain.
+// For one chain the update is the affine recurrence
+//     x_i = o_i + s_i * x_{i-1},   s_i = -a_{i,i-1} / a_ii,
+//     o_i = (b_i - sum_old a_ij x_j - sum_{j in earlier chains} a_ij x_j) / a_ii.
+// A warp takes 32 rows of a chain at a time (a segment).  It forms their o_i
+// from the earlier chains, composes the 32 affine maps with a 5-step shuffle
+// scan, and applies the carry from the previous segment.  The in-line
+// dependency chain of 32 rows becomes log2(32) steps.  The DAG is the
+// reference's: every row still uses the new values of all earlier rows and
+// the old values of all later rows.  Only the rounding differs (sums
+// reassociated, o_i scaled by RN(1/a_ii)).
+//
+// Depth: a segment waits for the source segments of its rows, e.g. on a
+// 2-D grid line L segment s waits for line L-1 segment s+1.  The wavefront is
+// therefore 2 x (lines) + (segments per line) steps: 2,080 on C2's fine level,
+// against 3,070 row levels for the exact sweep.  Each step is one warp scan,
+// not one row.
+//
+// One CTA runs the whole sweep.  Chains go round-robin to its warps.  The x
+// values of the last S chains live in a shared-memory ring (slot = chain mod
+// S).  Progress counters in shared memory order the warps; nothing crosses
+// L2 on the dependency path.  The old-value terms and b are folded into o_i by
+// a fully parallel pre-pass (gs_scan_prepass_kernel) before the sweep.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace mvamg {
+namespace gsscan {
+
+constexpr int kMaxDeps = 4;  // distinct source-chain distances
+
+constexpr int kStages = 3;     // segments of records in flight per warp (TMA bulk copies)
+
+// Per-segment header (32 B, one bulk copy with the records): the two waits
+// ((delta << 20) | segments needed), the deferred source of the last row
+// (same encoding) and its position, then its coefficient.
+struct __align__(16) SegInfo {
+  int wait0, wait1, defer, defpos;
+  double defcoef, pad;
+};
+
+struct ScanArgs {
+  int nchains, S, ring_len;     // ring: S slots of ring_len doubles
+  int window;                   // > 0: slots hold positions mod window (single distance 1), producers
+                                // wait for their reader before overwriting; 0: whole chains
+  int ndelta, delta[kMaxDeps];  // distinct source-chain distances (slot-reuse guard)
+  int n, fwd, stage_bytes;
+  int spin_polls, sleep_ns;     // busy polls before backing off with __nanosleep(sleep_ns)
+  const int* seg_ptr;           // chain -> first segment (nchains + 1)
+  const int* chain_start;       // chain -> first row, sweep order
+  const int* chain_len;         // chain -> rows
+  const double2* recv;          // [(segment * NV + v) * 32 + lane]: (slope, c0), (c1, c2), ...
+  const uint4* addr;            // [segment * 32 + lane]: (delta << 20) | position, per source
+  const SegInfo* seginfo;       // [segment]
+  const double* o0;             // pre-pass output, record layout
+  double* xnew;                 // original row order
+  int* status;
+};
+
+__device__ __forceinline__ unsigned long long scan_enc(int chain, int S, unsigned done) {
+  return ((unsigned long long)(unsigned)(chain + S + 1) << 32) | done;
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile_shared_u64(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+__device__ __forceinline__ unsigned addr_k(const uint4& a, int k) {
+  return k == 0 ? a.x : k == 1 ? a.y : k == 2 ? a.z : a.w;
+}
+
+// Every lane of the warp runs the same waits on the same shared-memory words
+// (uniform control flow, no divergent spinning); a failed poll backs off with
+// __nanosleep so waiting warps leave the issue slots to the working ones.
+// Progress of a chain = its number of complete segments.  A segment whose
+// last row has a deferred source is completed (that row fixed, then
+// published) when the warp starts the next segment, or at the chain's end.
+// Each warp streams its segments' records into kStages shared-memory stages
+// with TMA bulk copies (one elected lane, an mbarrier per stage), so no
+// global load sits on the dependency path.
+template <int K>
+__global__ void __launch_bounds__(1024, 1) gs_scan_kernel(ScanArgs a) {
+  constexpr int NV = (K + 2) / 2;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const int S = a.S, RL = a.ring_len, WIN = a.window;
+  unsigned long long* prog = reinterpret_cast<unsigned long long*>(smem);
+  double* ring = reinterpret_cast<double*>(smem + 8 * ((S + 1) & ~1));
+  unsigned char* stages = smem + ((8 * ((S + 1) & ~1) + 8 * (size_t)S * RL + 127) & ~(size_t)127);
+  unsigned char* my_stages = stages + (size_t)warp * kStages * a.stage_bytes;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(stages + (size_t)nw * kStages * a.stage_bytes);
+  const unsigned bar0 = (unsigned)__cvta_generic_to_shared(bars + warp * kStages);
+  const unsigned st0 = (unsigned)__cvta_generic_to_shared(my_stages);
+  for (int i = threadIdx.x; i < S; i += blockDim.x) prog[i] = scan_enc(i - S, S, 0x7fffffffu);
+  for (int i = threadIdx.x; i < S * RL; i += blockDim.x) ring[i] = 0.0;
+  if (lane == 0) {
+    for (int k = 0; k < kStages; ++k) mbar_init(bar0 + 8u * k, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // stage layout: o0 (32 doubles) | recv (NV x 32 double2) | addr (32 uint4) | SegInfo
+  constexpr int OFF_RV = 256, OFF_AD = 256 + NV * 512, OFF_SI = 256 + NV * 512 + 512;
+  unsigned phase = 0;  // parity bit per stage
+  bool dead = false;
+  auto issue = [&](int g, int k) {
+    if (lane == 0) {
+      const unsigned dst = st0 + (unsigned)(k * a.stage_bytes), bar = bar0 + 8u * k;
+      mbar_expect_tx(bar, (unsigned)(OFF_SI + 32));
+      bulk_g2s(dst, a.o0 + (size_t)g * 32, 256u, bar);
+      bulk_g2s(dst + OFF_RV, a.recv + (size_t)g * NV * 32, (unsigned)(NV * 512), bar);
+      bulk_g2s(dst + OFF_AD, a.addr + (size_t)g * 32, 512u, bar);
+      bulk_g2s(dst + OFF_SI, a.seginfo + g, 32u, bar);
+    }
+  };
+  auto wait_stage = [&](int k) {
+    while (!mbar_try_wait(bar0 + 8u * k, (phase >> k) & 1u)) {}
+    phase ^= 1u << k;
+  };
+  // wait until chain c (ring slot cslot) has `need` complete segments
+  auto wait_for = [&](int c, int cslot, unsigned need) {
+    const unsigned long long want = scan_enc(c, S, need);
+    const unsigned long long* p = prog + cslot;
+    if (ld_volatile_shared_u64(p) >= want) return;
+    long long spins = 0;
+    while (ld_volatile_shared_u64(p) < want) {
+      if (++spins > a.spin_polls) __nanosleep(a.sleep_ns);
+      if (spins > (1LL << 24)) {  // a broken schedule must not hang the GPU
+        if (lane == 0) atomicOr(a.status, 8);
+        dead = true;
+        return;
+      }
+    }
+  };
+  auto wait_word = [&](int L, int slot, int w) {
+    if (w == 0) return;
+    const int dl = w >> 20;
+    int cs_ = slot - dl;
+    if (cs_ < 0) cs_ += S;
+    wait_for(L - dl, cs_, (unsigned)(w & 0xfffff));
+  };
+  auto publish = [&](int L, int slot, unsigned done) {
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(prog + slot) = scan_enc(L, S, done);
+  };
+  auto ring_at = [&](int src_slot, int pos) -> double* {
+    return ring + (size_t)src_slot * RL + (WIN ? (pos & (WIN - 1)) : pos);
+  };
+  int slot = warp % S;
+  for (int L = warp; L < a.nchains && !dead; L += nw) {
+    const int g0 = a.seg_ptr[L], nseg = a.seg_ptr[L + 1] - g0;
+    for (int k = 0; k < kStages && k < nseg; ++k) issue(g0 + k, k);
+    // the slot's previous occupant (chain L - S) has no readers left
+    for (int d = 0; d < a.ndelta; ++d) {
+      const int c = L - S + a.delta[d];
+      if (c >= 0) {
+        int cs_ = slot + a.delta[d];
+        if (cs_ >= S) cs_ -= S;
+        wait_for(c, cs_, (unsigned)(a.seg_ptr[c + 1] - a.seg_ptr[c]));
+      }
+    }
+    __threadfence_block();
+    const int cs = a.chain_start[L], len = a.chain_len[L];
+    int rslot = slot + 1;  // window mode: the reader of this chain is chain L + 1
+    if (rslot >= S) rslot -= S;
+    double carry = 0.0;
+    int pend_z = 0, pend_w = 0;  // deferred source of the previous segment's last row
+    double pend_c = 0.0;
+    auto store = [&](int q, double x) {
+      *ring_at(slot, q) = x;
+      a.xnew[a.fwd ? cs + q : a.n - 1 - (cs + q)] = x;
+    };
+    auto fix_pending = [&](int s) {  // complete segment s - 1: its last row's deferred term
+      wait_word(L, slot, pend_z);
+      __threadfence_block();
+      const int dl = pend_z >> 20;
+      int ss = slot - dl;
+      if (ss < 0) ss += S;
+      const double xv = *reinterpret_cast<volatile double*>(ring_at(ss, pend_w));
+      carry = __fma_rn(-pend_c, xv, carry);
+      if (lane == 31) store(s * 32 - 1, carry);
+      publish(L, slot, (unsigned)s);
+      pend_z = 0;
+    };
+    for (int s = 0; s < nseg; ++s) {
+      const int k = s % kStages;
+      wait_stage(k);
+      const unsigned char* st = my_stages + (size_t)k * a.stage_bytes;
+      const double o0 = reinterpret_cast<const double*>(st)[lane];
+      double2 rv[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) rv[v] = reinterpret_cast<const double2*>(st + OFF_RV)[v * 32 + lane];
+      const uint4 ad = reinterpret_cast<const uint4*>(st + OFF_AD)[lane];
+      const SegInfo si = *reinterpret_cast<const SegInfo*>(st + OFF_SI);
+      __syncwarp();
+      if (s + kStages < nseg) issue(g0 + s + kStages, k);  // the stage is free again
+      if (pend_z) fix_pending(s);
+      // window mode: segment s overwrites segment s - WIN/32 of this slot;
+      // its reader must be done with it
+      if (WIN && s >= WIN / 32 && L + 1 < a.nchains) wait_for(L + 1, rslot, (unsigned)(s - WIN / 32 + 2));
+      wait_word(L, slot, si.wait0);
+      wait_word(L, slot, si.wait1);
+      __threadfence_block();
+      double o = o0;
+#pragma unroll
+      for (int kk = 0; kk < K; ++kk) {
+        const unsigned w = addr_k(ad, kk);
+        const int d = (int)(w >> 20), pos = (int)(w & 0xfffffu);
+        int ss = slot - d;
+        if (ss < 0) ss += S;
+        const double c = (kk + 1) % 2 == 0 ? rv[(kk + 1) / 2].x : rv[(kk + 1) / 2].y;
+        const double xv = *reinterpret_cast<volatile double*>(ring_at(ss, pos));
+        o = __fma_rn(-c, xv, o);
+      }
+      // inclusive scan of x -> o + slope * x over the 32 lanes
+      double A = o, B = rv[0].x;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const double Ap = __shfl_up_sync(FULL, A, d), Bp = __shfl_up_sync(FULL, B, d);
+        if (lane >= d) {
+          A = __fma_rn(B, Ap, A);
+          B = __dmul_rn(B, Bp);
+        }
+      }
+      const double x = __fma_rn(B, carry, A);
+      carry = __shfl_sync(FULL, x, 31);
+      const int q = s * 32 + lane;
+      const bool deferred = si.defer != 0;
+      if (q < len && !(deferred && lane == 31)) store(q, x);
+      if (deferred) {
+        pend_z = si.defer;
+        pend_w = si.defpos;
+        pend_c = si.defcoef;
+      } else {
+        publish(L, slot, (unsigned)(s + 1));
+      }
+    }
+    if (pend_z) fix_pending(nseg);
+    slot += nw % S;
+    if (slot >= S) slot -= S;
+  }
+}
+
+// o0[rec(i)] = (b_i - sum over the row's old-value entries a_ij xold_j) * rdiag_i,
+// in the sweep's record layout.  old: 0 none (sweep from zero), 1 entries j > i
+// (forward from x_old), 2 entries j < i (backward from x_old).
+__global__ void gs_scan_prepass_kernel(int n, const int* __restrict__ ip, const int* __restrict__ ix,
+                                       const double* __restrict__ v, const double* __restrict__ rdiag,
+                                       const int* __restrict__ rec, const double* __restrict__ b,
+                                       const double* __restrict__ xold, int old, double* __restrict__ o0) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double s = b[i];
+    if (old) {
+      for (int k = ip[i]; k < ip[i + 1]; ++k) {
+        const int j = ix[k];
+        if (old == 1 ? j > i : j < i) s = __fma_rn(-v[k], xold[j], s);
+      }
+    }
+    o0[rec[i]] = __dmul_rn(s, rdiag[i]);
+  }
+}
+
+}  // namespace gsscan
+}  // namespace mvamg

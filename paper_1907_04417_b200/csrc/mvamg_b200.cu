@@ -25,6 +25,7 @@
 #include "mvamg_kernels.cuh"
 #include "coarse_mega.cuh"
 #include "galerkin.cuh"
+#include "gs_scan.cuh"
 
 using namespace mvamg;
 
@@ -51,6 +52,14 @@ int g_gs_debug = [] {
   const char* e = getenv("MVAMG_GS_DEBUG");
   return e ? atoi(e) : 0;
 }();  // kernels launched by this library (graph nodes counted per replay)
+int g_scan_spin = [] {  // chain-scan sweep: busy polls before __nanosleep back-off
+  const char* e = getenv("MVAMG_SCAN_SPIN");
+  return e ? atoi(e) : 64;
+}();
+int g_scan_sleep = [] {
+  const char* e = getenv("MVAMG_SCAN_SLEEP");
+  return e ? atoi(e) : 32;
+}();
 int g_row_sleep = [] {
   const char* e = getenv("MVAMG_ROW_SLEEP");
   return e ? atoi(e) : 0;
@@ -152,6 +161,21 @@ struct GsLevels {
   double* tperm = nullptr;
   int nlev = 0, max_rows = 0, max_ents = 0, threads = 256;
   int group = 1;  // lanes per row: 1 = bit-exact CSR order, 2..16 = tolerance parity
+};
+
+// Chain-scan schedule (gs_scan.cuh) of one sweep mode (tolerance parity).
+struct GsScan {
+  int nchains = 0, S = 0, ring_len = 0, K = 0, threads = 0, window = 0;
+  int ndelta = 0, delta[gsscan::kMaxDeps] = {0, 0, 0, 0};  // distinct source-chain distances
+  const int* seg_ptr = nullptr;
+  const int* chain_start = nullptr;
+  const int* chain_len = nullptr;
+  const void* recv = nullptr;
+  const void* addr = nullptr;
+  const void* seginfo = nullptr;
+  double* o0 = nullptr;
+  const int* rec = nullptr;
+  const double* rdiag = nullptr;
 };
 
 // Dataflow row schedule (gs_row_kernel) of one sweep mode.
@@ -386,6 +410,80 @@ int launch_gs_levels(const Csr& A, const GsLevels& g, bool zero, const double* b
   return 0;
 }
 
+int set_deltas(GsScan& g, int ndelta, const int* deltas) {
+  if (ndelta < 0 || ndelta > gsscan::kMaxDeps || (ndelta && !deltas))
+    return fail(MVAMG_E_ARG, "gs scan: 0..4 distinct source-chain distances");
+  g.ndelta = ndelta;
+  for (int d = 0; d < ndelta; ++d) {
+    if (deltas[d] < 1 || deltas[d] >= g.S) return fail(MVAMG_E_ARG, "gs scan: distance outside the ring");
+    g.delta[d] = deltas[d];
+  }
+  return 0;
+}
+
+int gs_scan_stage_bytes(int K) { return 256 + ((K + 2) / 2) * 512 + 512 + 32; }
+size_t gs_scan_smem(const GsScan& g) {
+  const size_t nw = (size_t)g.threads / 32;
+  return ((8 * (size_t)((g.S + 1) & ~1) + 8 * (size_t)g.S * g.ring_len + 127) & ~(size_t)127) +
+         nw * gsscan::kStages * (size_t)gs_scan_stage_bytes(g.K) + nw * gsscan::kStages * 8;
+}
+
+// mode: 0 fwd from 0, 1 fwd from x_old, 2 bwd from 0, 3 bwd from x_old.
+int launch_gs_scan(const Csr& A, const GsScan& g, int mode, const double* b, const double* xold, double* xnew,
+                   int* status, cudaStream_t s) {
+  using namespace gsscan;
+  static bool attr = false;
+  if (!attr) {
+    attr = true;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(gs_scan_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    cudaFuncSetAttribute(gs_scan_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    cudaFuncSetAttribute(gs_scan_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    cudaFuncSetAttribute(gs_scan_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    cudaGetLastError();
+  }
+  const int n = A.n;
+  if (n == 0) return 0;
+  if (g.K < 1 || g.K > 4) return fail(MVAMG_E_ARG, "gs scan: 1..4 cross-chain sources per row");
+  if (g.threads < 32 || g.threads > 1024 || g.threads % 32) return fail(MVAMG_E_ARG, "gs scan: bad thread count");
+  const size_t smem = gs_scan_smem(g);
+  if (smem > (size_t)g_max_dyn_smem + 1024) return fail(MVAMG_E_ARG, "gs scan: ring exceeds shared memory");
+  const int old = (mode & 1) ? ((mode < 2) ? 1 : 2) : 0;
+  if (old && !xold) return fail(MVAMG_E_ARG, "gs scan: mode needs x_old");
+  gs_scan_prepass_kernel<<<grid_for(n), 256, 0, s>>>(n, A.ip, A.ix, A.v, g.rdiag, g.rec, b, xold, old, g.o0);
+  ScanArgs a;
+  a.nchains = g.nchains;
+  a.S = g.S;
+  a.ring_len = g.ring_len;
+  a.window = g.window;
+  a.stage_bytes = gs_scan_stage_bytes(g.K);
+  a.spin_polls = g_scan_spin;
+  a.sleep_ns = g_scan_sleep;
+  a.ndelta = g.ndelta;
+  for (int d = 0; d < kMaxDeps; ++d) a.delta[d] = g.delta[d];
+  a.n = n;
+  a.fwd = mode < 2 ? 1 : 0;
+  a.seg_ptr = g.seg_ptr;
+  a.chain_start = g.chain_start;
+  a.chain_len = g.chain_len;
+  a.recv = static_cast<const double2*>(g.recv);
+  a.addr = static_cast<const uint4*>(g.addr);
+  a.seginfo = static_cast<const SegInfo*>(g.seginfo);
+  a.o0 = g.o0;
+  a.xnew = xnew;
+  a.status = status;
+  switch (g.K) {
+    case 1: gs_scan_kernel<1><<<1, g.threads, smem, s>>>(a); break;
+    case 2: gs_scan_kernel<2><<<1, g.threads, smem, s>>>(a); break;
+    case 3: gs_scan_kernel<3><<<1, g.threads, smem, s>>>(a); break;
+    default: gs_scan_kernel<4><<<1, g.threads, smem, s>>>(a); break;
+  }
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 bool g_row_attr = false;
 // Dataflow row sweep: prepare (rhs in position order, fold, sentinel fill,
 // ticket reset), then gs_row_kernel on `ctas` resident CTAs (0 = one per SM).
@@ -454,6 +552,7 @@ struct Level {
   GsList gl[3];
   GsLevels glv[4];  // small-level single-CTA schedules (used when set)
   GsRows grw[4];    // dataflow row schedules (used when set and glv is not)
+  GsScan gsc[4];    // chain-scan schedules (tolerance parity; used first when set)
   Csr P, R;  // valid for k < L-1
   double *xa = nullptr, *xb = nullptr, *t = nullptr, *r = nullptr, *z = nullptr;
   double *fr = nullptr, *fx = nullptr, *fp[2] = {nullptr, nullptr}, *fap[2] = {nullptr, nullptr};
@@ -541,7 +640,9 @@ struct mvamg_hierarchy {
       } else {
         bool fwd = sp.kind == MVAMG_GS_FORWARD;
         int lmode = (fwd ? 0 : 2) + (x_cur == nullptr ? 0 : 1);
-        if (!fwd && x_cur != nullptr && l.glv[2].rows) {
+        if (l.gsc[lmode].nchains) {
+          st = launch_gs_scan(l.A, l.gsc[lmode], lmode, b, x_cur, out, status_ptr(), s);
+        } else if (!fwd && x_cur != nullptr && l.glv[2].rows) {
           st = launch_gs_levels(l.A, l.glv[2], false, b, x_cur, out, ticket, s, /*fold=*/true);
         } else if (l.glv[lmode].rows) {
           st = launch_gs_levels(l.A, l.glv[lmode], x_cur == nullptr, b, x_cur, out, ticket, s);
@@ -2184,6 +2285,42 @@ int mvamg_xpby_f64(int n, const double* x, double beta, double* y, void* stream)
   xpby_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(n, x, beta, y);
   ++g_kernel_launches;
   CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+
+int mvamg_gs_scan_sweep_f64(int mode, int n, const int* indptr, const int* indices, const double* data,
+                            int nchains, int S, int ring_len, int ndelta, const int* deltas, int K, int threads,
+                            int window, const int* seg_ptr, const int* chain_start, const int* chain_len,
+                            const void* recv, const void* addr, const void* seginfo, double* o0, const int* rec,
+                            const double* rdiag, const double* b, const double* x_old, double* x_new, int* ws,
+                            void* stream) {
+  if (mode < 0 || mode > 3 || n < 0 || !ws) return fail(MVAMG_E_ARG, "gs scan: bad arguments");
+  set_kernel_attrs();
+  Csr A;
+  A.n = n; A.ip = indptr; A.ix = indices; A.v = data;
+  GsScan g;
+  g.nchains = nchains; g.S = S; g.ring_len = ring_len; g.K = K; g.threads = threads;
+  if (int e = set_deltas(g, ndelta, deltas)) return e;
+  g.seg_ptr = seg_ptr; g.chain_start = chain_start; g.chain_len = chain_len; g.recv = recv; g.addr = addr;
+  g.seginfo = seginfo; g.o0 = o0; g.rec = rec; g.rdiag = rdiag; g.window = window;
+  if (window && (window & (window - 1))) return fail(MVAMG_E_ARG, "gs scan: window must be a power of two");
+  return launch_gs_scan(A, g, mode, b, x_old, x_new, ws + 1, (cudaStream_t)stream);
+}
+
+int mvamg_hierarchy_set_gs_scan(mvamg_hierarchy* h, int k, int mode, int nchains, int S, int ring_len,
+                                int ndelta, const int* deltas, int K, int threads, int window,
+                                const int* seg_ptr, const int* chain_start, const int* chain_len, const void* recv,
+                                const void* addr, const void* seginfo, double* o0, const int* rec,
+                                const double* rdiag) {
+  if (!h || k < 0 || k >= h->L || mode < 0 || mode > 3) return fail(MVAMG_E_ARG, "set_gs_scan: bad index");
+  if (K < 1 || K > 4) return fail(MVAMG_E_ARG, "set_gs_scan: 1..4 cross-chain sources per row");
+  GsScan& g = h->lv[k].gsc[mode];
+  g.nchains = nchains; g.S = S; g.ring_len = ring_len; g.K = K; g.threads = threads;
+  if (int e = set_deltas(g, ndelta, deltas)) return e;
+  g.seg_ptr = seg_ptr; g.chain_start = chain_start; g.chain_len = chain_len; g.recv = recv; g.addr = addr;
+  g.seginfo = seginfo; g.o0 = o0; g.rec = rec; g.rdiag = rdiag; g.window = window;
+  if (window && (window & (window - 1))) return fail(MVAMG_E_ARG, "gs scan: window must be a power of two");
   return 0;
 }
 

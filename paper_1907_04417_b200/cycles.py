@@ -18,7 +18,7 @@ import scipy.sparse.linalg as spla
 
 from . import _lib
 from .device import (DeviceCSR, DeviceGsLevels, DeviceGsPlan, DeviceGsRows, GpuConfig, as_csr,
-                     autotune_coarse_gs,
+                     autotune_coarse_gs, autotune_scan_gs,
                      level_gs_fits, ptr, row_gs_fits,
                      stream_handle, to_device, torch_cuda)
 from .exceptions import NotSpdError
@@ -129,6 +129,18 @@ class GpuMultigridOperator:
                     modes.add(1)
             else:
                 modes.add(1)
+        return sorted(modes)
+
+    def _gs_scan_modes(self):
+        """Sweep modes of the chain-scan schedule (0 fwd x=0, 1 fwd, 2 bwd x=0, 3 bwd)."""
+        modes = set()
+        for spec, first_zero in ((self.pre_smoother, True), (self.post_smoother, False)):
+            if spec.kind == WEIGHTED_JACOBI or spec.sweeps == 0:
+                continue
+            base = 0 if spec.kind == GS_FORWARD else 2
+            modes.add(base + (0 if first_zero else 1))
+            if first_zero and spec.sweeps > 1:
+                modes.add(base + 1)
         return sorted(modes)
 
     def _init_plain(self, A):
@@ -243,6 +255,12 @@ class GpuMultigridOperator:
                     continue
                 self.gs_plans.append(gp.plan)
                 self.level_dev.append(dict(A=dA, gs=gp, plan=gp.plan, levels=None))
+                if not cfg.exact_gs and cfg.scan_gs:
+                    # tolerance parity: the chain-scan sweep where it is faster (timed once)
+                    scans = autotune_scan_gs(A, gp, self._gs_scan_modes(), cfg)
+                    self.level_dev[-1]["scan"] = scans
+                    for m, sc in scans.items():
+                        _lib.check(L.mvamg_hierarchy_set_gs_scan(h, k, m, *sc.args()), "set_gs_scan")
                 _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
                                                        None, gp.plan.ntiles, ptr(gp.chain_ptr),
                                                        ptr(gp.tile_ptr), gp.plan.threads,

@@ -79,6 +79,7 @@ class GpuConfig:
     row_gs_threads: int = 128       # threads per CTA of the row sweep
     row_gs_ctas: int = 0            # resident CTAs of the row sweep (0 = auto)
     device_galerkin: bool = True    # setup forms P'AP with the device kernel (bit-identical to scipy's)
+    scan_gs: bool = True            # (with exact_gs False) chain-scan sweeps on chain-structured levels when faster
     exact_gs: bool = False          # True: every GS kernel keeps the CSR-order subtractions (bit-exact with
                                     # the serial sweep); False: level-set sweeps sum long rows over several
                                     # lanes (same row order, parity within rounding -- north star: 1e-10)
@@ -606,3 +607,34 @@ def galerkin_product_device(P, A, timing=None):
         timing["total_ms"] = float(sum(ph))
     k = nnz.value
     return sp.csr_matrix((v.cpu().numpy()[:k], ix.cpu().numpy()[:k], ip.cpu().numpy()), shape=(nc, nc))
+
+
+def autotune_scan_gs(A, gp, modes, cfg):
+    """For a chain-structured level: per sweep mode, keep the chain-scan sweep
+    (gs_scan.py, tolerance parity) if one timed run beats the wavefront sweep
+    `gp`.  Returns {mode: DeviceGsScan} for the modes it wins."""
+    from .gs_scan import DeviceGsScan, plan_scan
+
+    torch = torch_cuda()
+    n = A.shape[0]
+    g = torch.Generator(device="cuda").manual_seed(0)
+    b = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    xo = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    xn = torch.empty(n, dtype=torch.float64, device="cuda")
+    ws = torch.zeros(8, dtype=torch.int32, device="cuda")
+    out = {}
+    for m in modes:
+        p = plan_scan(A, m, cfg)
+        if p is None:
+            continue
+        sc = DeviceGsScan(A, m, cfg, plan=p)
+        xold = xo if m % 2 else None
+        t_scan = time_sweep(lambda: sc.sweep(b, xold, xn, ws))
+        if int(ws[1].item()) != 0:
+            raise DeviceError("gs scan sweep timed out (schedule error)")
+        direction = 0 if m < 2 else 1
+        t_wave = time_sweep(lambda: gp.sweep(direction, b, xold, xn, ws))
+        if t_scan < t_wave:
+            out[m] = sc
+    return out
+

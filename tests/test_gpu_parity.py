@@ -569,3 +569,53 @@ def test_short_chain_level_uses_row_sweep(mv, c1):
     z = op.apply(b)
     assert np.array_equal(z, wf.apply(b))
     assert rel(z, OracleOperator(pm, pp).apply(b)) <= TOL_CYCLE
+
+
+# ------------------------------------------------------- chain-scan sweep ----
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+def test_gs_scan_kernel(mv, c1, mode):
+    """Chain-scan sweep (tolerance parity): each sweep within rounding of the
+    reference's serial loop, on grid structures (K = 1, 2, 3) and C1's fine level."""
+    import torch
+    from paper_1907_04417_b200 import problems
+    from paper_1907_04417_b200.gs_scan import DeviceGsScan
+
+    rng = np.random.default_rng(20 + mode)
+    cases = [("lap2d", laplacian_2d(40)), ("lap3d", laplacian_3d(12)), ("q1", problems.anisotropic_q1(70)),
+             ("jump3d", problems.jump_3d(16, 4, 1)), ("c1_l0", c1[1][0]), ("lap1d", laplacian_1d(100))]
+    for name, A in cases:
+        n = A.shape[0]
+        b = rng.standard_normal(n)
+        x0 = rng.standard_normal(n)
+        want = np.zeros(n) if mode % 2 == 0 else x0.copy()
+        oracle_gs(A, b, want, "forward" if mode < 2 else "backward")
+        sc = DeviceGsScan(A, mode)
+        xn = torch.empty(n, dtype=torch.float64, device="cuda")
+        ws = torch.zeros(8, dtype=torch.int32, device="cuda")
+        sc.sweep(_dev(b), None if mode % 2 == 0 else _dev(x0), xn, ws)
+        torch.cuda.synchronize()
+        assert int(ws[1].item()) == 0, name
+        assert rel(xn.cpu().numpy(), want) <= 1e-12, (name, mode)
+
+
+def test_vcycle_with_scan_sweeps(mv, c1):
+    """A hierarchy whose fine level runs the chain-scan sweeps (forced) matches
+    the reference cycle within the north-star tolerance and PCG keeps nit."""
+    d, mats, pros = c1[0], c1[1], c1[2]
+    op = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(exact_gs=False))
+    from paper_1907_04417_b200.gs_scan import DeviceGsScan
+
+    # force the scan schedules on level 0 for both smoother modes
+    L = __import__("paper_1907_04417_b200._lib", fromlist=["load"]).load()
+    keep = []
+    for m in (0, 3):
+        sc = DeviceGsScan(mats[0], m)
+        keep.append(sc)
+        L.mvamg_hierarchy_set_gs_scan(op.handle, 0, m, *sc.args())
+    op._scan_keep = keep
+    L.mvamg_hierarchy_set_graphs(op.handle, 0)
+    z = op.apply(d["b"])
+    assert rel(z, d["apply_b"]) <= TOL_CYCLE
+    x, rep = mv.pcg(mats[0], d["b"], op, rtol=1e-6)
+    assert rep.iterations == int(d["pcg_nit"])
+    assert np.max(np.abs(rep.residual_history - d["pcg_hist"]) / d["pcg_hist"]) <= 1e-10
