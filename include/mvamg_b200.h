@@ -147,7 +147,9 @@ int mvamg_gs_levels(int n, const int* indptr, const int* indices, const double* 
  * resident in (distributed) shared memory, one cluster barrier per level set.
  * group = 1: one thread per row, bit-identical to the serial loop; group = 2,
  * 4, 8 or 16: that many lanes per row with a shuffle-tree sum (same order of
- * rows, tolerance parity).  tperm: n + 2 doubles of device scratch;
+ * rows, tolerance parity); group | 0x100 with ncta = 1: the register-prefetch
+ * variant (only x in shared memory, each level's entries loaded into
+ * registers while the previous level computes; schedules built unsplit).  tperm: n + 2 doubles of device scratch;
  * ws: >= 4 device ints. */
 int mvamg_gs_level_sweep_f64(int direction, int n, const int* indptr, const int* indices,
                              const double* data, int ncta, int rows_per_cta, int nlev, int max_rows,

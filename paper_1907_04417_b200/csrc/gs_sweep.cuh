@@ -984,6 +984,130 @@ __global__ void __launch_bounds__(1024, 1) gs_level_kernel(GsLevelArgs a) {
 }
 
 
+// Single-CTA level-set sweep, tolerance parity (group G > 1), for levels whose
+// x fits in shared memory.  Entries are not staged through shared memory.
+// A level runs in two phases.  (1) Every thread forms the products a_ij * x_j
+// of up to kRegEnts of the level's entries (a level's entries are contiguous,
+// so the loads are coalesced) into a shared product buffer.  Those entries
+// were loaded into registers while the previous level computed, so their L2
+// latency overlaps it.  (2) G lanes per row sum the row's products with a
+// shuffle tree and write x_i.  Sub-levels hold at most blockDim * kRegEnts
+// entries (the host splits larger levels).  The first row of each group's
+// next level is prefetched the same way.
+constexpr int kRegEnts = 8;
+constexpr int kRegThreads = 512;
+
+template <int G>
+struct LevelRegStage {
+  double c[kRegEnts];
+  int s[kRegEnts];
+  GsLevelRow m;
+  double rhs;
+  bool has;
+};
+
+template <int G>
+__device__ __forceinline__ void level_reg_load(const GsLevelArgs& a, const int* lp, const int* le, int l, int tid,
+                                               int g, LevelRegStage<G>& st) {
+#pragma unroll
+  for (int e = 0; e < kRegEnts; ++e) {
+    st.c[e] = 0.0;
+    st.s[e] = 0;
+  }
+  st.has = false;
+  if (l >= a.nlev) return;
+  const int e0 = le[l], e1 = le[l + 1];
+#pragma unroll
+  for (int e = 0; e < kRegEnts; ++e) {
+    const int k = e0 + tid + e * kRegThreads;
+    if (k < e1) {
+      const GsLevelEntry en = a.ents[k];
+      st.c[e] = en.coef;
+      st.s[e] = en.src;
+    }
+  }
+  const int p = lp[l] + g;
+  if (p < lp[l + 1]) {
+    st.m = a.rows[p];
+    st.rhs = __ldg(a.tperm + p);
+    st.has = true;
+  }
+}
+
+template <int G>
+__device__ __forceinline__ void level_reg_run(const GsLevelArgs& a, const int* lp, const int* le, int l, int tid,
+                                              int g, int li, const LevelRegStage<G>& st, double* xsm, double* prod) {
+  constexpr int ngroups = kRegThreads / G;
+  const int e0 = le[l], ne = le[l + 1] - e0;
+  const int r0 = lp[l], r1 = lp[l + 1];
+  // phase 1: products of this level's entries (x of earlier levels is final)
+#pragma unroll
+  for (int e = 0; e < kRegEnts; ++e) {
+    const int k = tid + e * kRegThreads;
+    if (k < ne) prod[k] = __dmul_rn(st.c[e], xsm[st.s[e]]);
+  }
+  __syncthreads();
+  // phase 2: row sums
+  const int iters = (r1 - r0 + ngroups - 1) / ngroups;
+  for (int it = 0; it < iters; ++it) {
+    GsLevelRow mr;
+    double rh = 0.0;
+    bool act;
+    if (it == 0) {
+      mr = st.m;
+      rh = st.rhs;
+      act = st.has;
+    } else {
+      const int p = r0 + g + it * ngroups;
+      act = p < r1;
+      if (act) {
+        mr = a.rows[p];
+        rh = __ldg(a.tperm + p);
+      }
+    }
+    double part = 0.0;
+    if (act)
+      for (int k = li; k < mr.cnt; k += G) part = __dadd_rn(part, prod[mr.estart - e0 + k]);
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, off));
+    if (act && li == 0) xsm[mr.row] = div_rn_markstein(__dsub_rn(rh, part), mr.diag, mr.rdiag);
+  }
+  __syncthreads();
+}
+
+template <int G>
+__global__ void __launch_bounds__(kRegThreads, 1) gs_level_reg_kernel(GsLevelArgs a) {
+  extern __shared__ __align__(16) double xsm[];
+  double* prod = xsm + ((a.n + 1) & ~1);
+  // level offsets in shared memory: no L2 round trip at the head of a level
+  int* lp = reinterpret_cast<int*>(prod + a.max_ents);
+  int* le = lp + a.nlev + 1;
+  const int tid = threadIdx.x;
+  const int g = tid / G, li = tid % G;
+  for (int i = tid; i < a.n; i += kRegThreads) xsm[i] = a.zero_init ? 0.0 : __ldg(a.xold + i);
+  for (int i = tid; i <= a.nlev; i += kRegThreads) {
+    lp[i] = a.lev_ptr[i];
+    le[i] = a.lev_eptr[i];
+  }
+  __syncthreads();
+  // three register stages: level l computes while l + 1 and l + 2 are in flight
+  LevelRegStage<G> A, B, C;
+  level_reg_load(a, lp, le, 0, tid, g, A);
+  level_reg_load(a, lp, le, 1, tid, g, B);
+  for (int l = 0; l < a.nlev; l += 3) {
+    level_reg_load(a, lp, le, l + 2, tid, g, C);
+    level_reg_run(a, lp, le, l, tid, g, li, A, xsm, prod);
+    if (l + 1 >= a.nlev) break;
+    level_reg_load(a, lp, le, l + 3, tid, g, A);
+    level_reg_run(a, lp, le, l + 1, tid, g, li, B, xsm, prod);
+    if (l + 2 >= a.nlev) break;
+    level_reg_load(a, lp, le, l + 4, tid, g, B);
+    level_reg_run(a, lp, le, l + 2, tid, g, li, C, xsm, prod);
+  }
+  for (int i = tid; i < a.n; i += kRegThreads) a.xnew[i] = xsm[i];
+}
+
+
 // ---------------------------------------------------------------------------
 // Mid-size coarse levels (aggregation operators: 20-80 entries per row, DAG
 // depth in the hundreds, no chain structure): dataflow, one thread per row,

@@ -161,6 +161,7 @@ struct GsLevels {
   double* tperm = nullptr;
   int nlev = 0, max_rows = 0, max_ents = 0, threads = 256;
   int group = 1;  // lanes per row: 1 = bit-exact CSR order, 2..16 = tolerance parity
+  int reg = 0;    // single CTA, group > 1: register-prefetch kernel (x only in shared memory)
 };
 
 // Chain-scan schedule (gs_scan.cuh) of one sweep mode (tolerance parity).
@@ -354,7 +355,10 @@ int launch_gs_levels(const Csr& A, const GsLevels& g, bool zero, const double* b
     cudaGetLastError();
   }
   const size_t smem = gs_level_smem(g);
-  if (smem > (size_t)g_max_dyn_smem) return fail(MVAMG_E_ARG, "gs levels: shared memory plan too large");
+  const bool reg_path = g.ncta == 1 && g.group > 1 && g.reg;
+  if (reg_path ? (size_t)(n + 2 + g.max_ents + g.nlev) * 8 > (size_t)g_max_dyn_smem + 1024
+               : smem > (size_t)g_max_dyn_smem)
+    return fail(MVAMG_E_ARG, "gs levels: shared memory plan too large");
   if (g.ncta < 1 || g.ncta > 16) return fail(MVAMG_E_ARG, "gs levels: cluster of 1..16 CTAs");
   // right-hand side in the schedule's row layout; a backward sweep from a
   // nonzero guess folds its old upper neighbours here and then runs the
@@ -377,6 +381,33 @@ int launch_gs_levels(const Csr& A, const GsLevels& g, bool zero, const double* b
   a.xnew = xnew;
   if (g.group != 1 && g.group != 2 && g.group != 4 && g.group != 8 && g.group != 16)
     return fail(MVAMG_E_ARG, "gs levels: lanes per row must be 1, 2, 4, 8 or 16");
+  if (g.ncta == 1 && g.group > 1 && g.reg) {
+    // tolerance parity, x in shared memory, entries prefetched into registers
+    static bool reg_attr = false;
+    if (!reg_attr) {
+      reg_attr = true;
+      int dev = 0, optin = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      cudaFuncSetAttribute(gs_level_reg_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+      cudaFuncSetAttribute(gs_level_reg_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+      cudaFuncSetAttribute(gs_level_reg_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+      cudaFuncSetAttribute(gs_level_reg_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+      cudaGetLastError();
+    }
+    const int T = kRegThreads;
+    if ((long long)g.max_ents > (long long)T * kRegEnts)
+      return fail(MVAMG_E_ARG, "gs levels (register path): a level exceeds 512 * 8 entries");
+    const size_t xs = ((size_t)(n + 1) & ~(size_t)1) * 8 + (size_t)g.max_ents * 8 + (size_t)(g.nlev + 1) * 8;
+    switch (g.group) {
+      case 2: gs_level_reg_kernel<2><<<1, T, xs, s>>>(a); break;
+      case 4: gs_level_reg_kernel<4><<<1, T, xs, s>>>(a); break;
+      case 8: gs_level_reg_kernel<8><<<1, T, xs, s>>>(a); break;
+      default: gs_level_reg_kernel<16><<<1, T, xs, s>>>(a); break;
+    }
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
   if (g.ncta == 1) {
     switch (g.group) {
       case 1: gs_level_kernel<false, 1><<<1, g.threads, smem, s>>>(a); break;
@@ -1573,7 +1604,7 @@ int mvamg_gs_level_sweep_f64(int direction, int n, const int* indptr, const int*
   g.lev_ptr = lev_ptr; g.lev_eptr = lev_eptr; g.rows = static_cast<const GsLevelRow*>(rows);
   g.ents = static_cast<const GsLevelEntry*>(ents); g.perm = perm; g.tperm = tperm;
   g.nlev = nlev; g.max_rows = max_rows; g.max_ents = max_ents; g.threads = threads;
-  g.ncta = ncta; g.rows_per_cta = rows_per_cta; g.group = group;
+  g.ncta = ncta; g.rows_per_cta = rows_per_cta; g.group = group & 0xff; g.reg = (group >> 8) & 1;
   (void)direction;  // encoded in the schedule
   set_kernel_attrs();
   return launch_gs_levels(A, g, x_old == nullptr, b, x_old, x_new, ws, (cudaStream_t)stream);
@@ -1592,7 +1623,7 @@ int mvamg_gs_level_sweep_folded_f64(int n, const int* indptr, const int* indices
   g.lev_ptr = lev_ptr; g.lev_eptr = lev_eptr; g.rows = static_cast<const GsLevelRow*>(rows);
   g.ents = static_cast<const GsLevelEntry*>(ents); g.perm = perm; g.tperm = tperm;
   g.nlev = nlev; g.max_rows = max_rows; g.max_ents = max_ents; g.threads = threads;
-  g.ncta = ncta; g.rows_per_cta = rows_per_cta; g.group = group;
+  g.ncta = ncta; g.rows_per_cta = rows_per_cta; g.group = group & 0xff; g.reg = (group >> 8) & 1;
   set_kernel_attrs();
   return launch_gs_levels(A, g, false, b, x_old, x_new, ws, (cudaStream_t)stream, true);
 }
@@ -1606,7 +1637,7 @@ int mvamg_hierarchy_set_gs_levels(mvamg_hierarchy* h, int k, int mode, int ncta,
   g.lev_ptr = lev_ptr; g.lev_eptr = lev_eptr; g.rows = static_cast<const GsLevelRow*>(rows);
   g.ents = static_cast<const GsLevelEntry*>(ents); g.perm = perm; g.tperm = tperm;
   g.nlev = nlev; g.max_rows = max_rows; g.max_ents = max_ents; g.threads = threads;
-  g.ncta = ncta; g.rows_per_cta = rows_per_cta; g.group = group;
+  g.ncta = ncta; g.rows_per_cta = rows_per_cta; g.group = group & 0xff; g.reg = (group >> 8) & 1;
   return 0;
 }
 

@@ -80,6 +80,8 @@ class GpuConfig:
     row_gs_ctas: int = 0            # resident CTAs of the row sweep (0 = auto)
     device_galerkin: bool = True    # setup forms P'AP with the device kernel (bit-identical to scipy's)
     scan_gs: bool = True            # (with exact_gs False) chain-scan sweeps on chain-structured levels when faster
+    level_reg: bool = False         # (with exact_gs False) single-CTA level sweeps with register-prefetched
+                                    # entries (gs_level_reg_kernel; measured slower than the staged kernel)
     exact_gs: bool = False          # True: every GS kernel keeps the CSR-order subtractions (bit-exact with
                                     # the serial sweep); False: level-set sweeps sum long rows over several
                                     # lanes (same row order, parity within rounding -- north star: 1e-10)
@@ -364,7 +366,21 @@ class DeviceGsLevels:
         nlev, mr, me, rpc = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         ne = ctypes.c_longlong()
         chosen = None
+        # tolerance parity, x fits one CTA: the register-prefetch kernel needs
+        # no staging buffers, so levels are not split (caps 0 = unlimited)
+        reg_ents = 512 * 8  # kRegThreads x kRegEnts of gs_level_reg_kernel: entries per sub-level
+        self.reg = (not cfg.exact_gs and cfg.level_reg and n > 0
+                    and 8 * (n + 2) + 8 * reg_ents + 1024 <= cfg.smem_limit)
+        if self.reg:
+            _lib.check(L.mvamg_gs_levels(n, vp(ip), vp(ix), vp(v), int(mode), 1, 0, reg_ents,
+                                         ctypes.byref(nlev), ctypes.byref(ne), ctypes.byref(mr), ctypes.byref(me),
+                                         ctypes.byref(rpc), None, None, None, None, None), "gs_levels")
+            chosen = (1, 0, reg_ents)
+            if 8 * (n + 2 + me.value + nlev.value) + 1024 > cfg.smem_limit:
+                self.reg, chosen = False, None
         for ncta in (1, 2, 4, 8, 16):
+            if chosen is not None:
+                break
             if ncta > cfg.max_cluster:
                 break
             rpc_ = -(-n // ncta)
@@ -398,7 +414,11 @@ class DeviceGsLevels:
         # about 8 entries per lane, summed by a shuffle tree (tolerance parity)
         avg = A.nnz / max(1, n)
         self.group = 1 if cfg.exact_gs else int(min(16, max(1, 1 << int(np.ceil(np.log2(max(1.0, avg / 8)))))))
+        if self.reg and self.group == 1:
+            self.group = 2
         self.threads = int(min(1024, max(64, (self.max_rows * self.group + 31) // 32 * 32)))
+        if self.reg:  # fixed block (kRegThreads); every thread holds <= 8 of a level's entries
+            self.threads = 512
         self.lev_ptr = to_device(lev_ptr)
         self.lev_eptr = to_device(lev_eptr)
         self.rows = to_device(rows.view(np.uint8))
@@ -417,7 +437,8 @@ class DeviceGsLevels:
         return self._smem(self.rows_per_cta, self.max_rows, self.max_ents)
 
     def args(self):
-        return (self.ncta, self.rows_per_cta, self.nlev, self.max_rows, self.max_ents, self.threads, self.group,
+        return (self.ncta, self.rows_per_cta, self.nlev, self.max_rows, self.max_ents, self.threads,
+                self.group | (0x100 if self.reg else 0),
                 ptr(self.lev_ptr), ptr(self.lev_eptr), ptr(self.rows), ptr(self.ents), ptr(self.perm),
                 ptr(self.tperm))
 
@@ -509,13 +530,36 @@ class DeviceGsRows:
 
 
 def time_sweep(fn, reps=3):
-    """Device time (s) of fn() -- one GS sweep -- after one warm-up launch."""
+    """Device time (s) of fn() -- one GS sweep -- after one warm-up launch.
+
+    The reps calls are captured into one CUDA graph and replayed, so a short
+    sweep is timed on the device (as it runs inside the captured cycle), not
+    at the rate the host can issue it; falls back to direct launches."""
     torch = torch_cuda()
     fn()
+    torch.cuda.synchronize()
+    graph = None
+    try:
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(graph, stream=side):
+                for _ in range(reps):
+                    fn()
+        torch.cuda.current_stream().wait_stream(side)
+        graph.replay()
+        torch.cuda.synchronize()
+    except Exception:  # capture unsupported for this launch sequence
+        graph = None
+        torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(reps):
-        fn()
+    if graph is not None:
+        graph.replay()
+    else:
+        for _ in range(reps):
+            fn()
     e1.record()
     e1.synchronize()
     return e0.elapsed_time(e1) / reps * 1e-3

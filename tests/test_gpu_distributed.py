@@ -21,13 +21,16 @@ def test_distributed_world1_bit_identical():
     import paper_1907_04417_b200 as mv
     from paper_1907_04417_b200.distributed import DistributedSolver
 
+    from paper_1907_04417_b200.distributed import DeviceBackend
+
     d = golden("c1")
     mats, pros = hierarchy(d, "mv")
-    s = DistributedSolver(mats, pros)
+    exact = mv.GpuConfig(exact_gs=True)  # same schedules' bits whatever kernel each level gets
+    s = DistributedSolver(mats, pros, backend=DeviceBackend(exact))
     op = s.op
     z = op.be.vec(op.n_own)
     op.apply(op.be.from_host(d["b"]), z)
-    ref = mv.GpuMultigridOperator(mats, pros).apply(d["b"])
+    ref = mv.GpuMultigridOperator(mats, pros, config=exact).apply(d["b"])
     assert np.array_equal(z.cpu().numpy(), ref)
     x, rep = s.solve(d["b"])
     _, hist, nit, _ = oracle_pcg(OracleOperator(mats, pros), d["b"])

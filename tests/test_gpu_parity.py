@@ -208,13 +208,15 @@ def test_gs_level_kernel_bit_exact(mv, c1, cluster):
                 assert np.array_equal(got, want), (name, direction, zero, cluster)
 
 
-@pytest.mark.parametrize("cluster", [None, 2])
+@pytest.mark.parametrize("cluster", [None, 2, "reg"])
 def test_gs_level_kernel_relaxed(mv, c1, cluster):
     """Tolerance-parity level-set sweep (GpuConfig.exact_gs = False: several
-    lanes per row, shuffle-tree sums): same dependency order, each sweep within
-    rounding of the serial loop."""
+    lanes per row, shuffle-tree sums; "reg": the register-prefetch variant):
+    same dependency order, each sweep within rounding of the serial loop."""
     cfg = mv.GpuConfig(exact_gs=False)
-    if cluster:
+    if cluster == "reg":
+        cfg = mv.GpuConfig(exact_gs=False, level_reg=True)
+    elif cluster:
         cfg = mv.GpuConfig(smem_limit=8 * 16384 // cluster + 20000, max_cluster=cluster, exact_gs=False)
     rng = np.random.default_rng(12)
     mats = c1[1]
