@@ -79,7 +79,9 @@ class GpuConfig:
     row_gs_threads: int = 128       # threads per CTA of the row sweep
     row_gs_ctas: int = 0            # resident CTAs of the row sweep (0 = auto)
     device_galerkin: bool = True    # setup forms P'AP with the device kernel (bit-identical to scipy's)
-    scan_gs: bool = True            # (with exact_gs False) chain-scan sweeps on chain-structured levels when faster
+    scan_gs: bool = False           # (with exact_gs False) time the chain-scan sweep on chain-structured levels
+                                    # at upload and keep it when faster (off: single-SM issue-bound, slower
+                                    # than the wavefront on C2/C3, and the timing costs setup time)
     level_reg: bool = False         # (with exact_gs False) single-CTA level sweeps with register-prefetched
                                     # entries (gs_level_reg_kernel; measured slower than the staged kernel)
     exact_gs: bool = False          # True: every GS kernel keeps the CSR-order subtractions (bit-exact with
