@@ -284,6 +284,9 @@ int mvamg_hierarchy_set_gs_levels(mvamg_hierarchy* h, int k, int mode, int ncta,
                                   int nlev, int max_rows, int max_ents, int threads, int group,
                                   const int* lev_ptr, const int* lev_eptr, const void* rows, const void* ents,
                                   const int* perm, double* tperm);
+/* Diagnostics: 4 x int64 %globaltimer stamps per segment written by the
+ * chain-scan sweeps into trace_dev (NULL turns it off). */
+int mvamg_gs_scan_set_trace(long long* trace_dev);
 /* Chain-scan schedule of level k for sweep `mode` (see mvamg_gs_scan_sweep_f64);
  * used before any other schedule of that mode when set. */
 int mvamg_hierarchy_set_gs_scan(mvamg_hierarchy* h, int k, int mode, int nchains, int S, int ring_len,

@@ -86,6 +86,7 @@ SIGNATURES = [
     ("mvamg_spmat_destroy", _I, [_P]),
     ("mvamg_gs_scan_sweep_f64", _I, [_I, _I, _P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _I] + [_P] * 14),
     ("mvamg_hierarchy_set_gs_scan", _I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _I] + [_P] * 9),
+    ("mvamg_gs_scan_set_trace", _I, [_P]),
     ("mvamg_gather_f64", _I, [_I, _P, _P, _P, _P]),
     ("mvamg_scatter_f64", _I, [_I, _P, _P, _P, _P]),
     ("mvamg_axpy_f64", _I, [_I, _D, _P, _P, _P]),

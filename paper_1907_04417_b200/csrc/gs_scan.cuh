@@ -61,7 +61,14 @@ struct ScanArgs {
   const double* o0;             // pre-pass output, record layout
   double* xnew;                 // original row order
   int* status;
+  long long* trace;             // diagnostics (null): per segment, %globaltimer at 4 points of its step
 };
+
+__device__ __forceinline__ long long scan_clock() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ unsigned long long scan_enc(int chain, int S, unsigned done) {
   return ((unsigned long long)(unsigned)(chain + S + 1) << 32) | done;
@@ -173,10 +180,8 @@ __global__ void __launch_bounds__(1024, 1) gs_scan_kernel(ScanArgs a) {
     double carry = 0.0;
     int pend_z = 0, pend_w = 0;  // deferred source of the previous segment's last row
     double pend_c = 0.0;
-    auto store = [&](int q, double x) {
-      *ring_at(slot, q) = x;
-      a.xnew[a.fwd ? cs + q : a.n - 1 - (cs + q)] = x;
-    };
+    auto store_ring = [&](int q, double x) { *ring_at(slot, q) = x; };
+    auto store_global = [&](int q, double x) { a.xnew[a.fwd ? cs + q : a.n - 1 - (cs + q)] = x; };
     auto fix_pending = [&](int s) {  // complete segment s - 1: its last row's deferred term
       wait_word(L, slot, pend_z);
       __threadfence_block();
@@ -185,8 +190,9 @@ __global__ void __launch_bounds__(1024, 1) gs_scan_kernel(ScanArgs a) {
       if (ss < 0) ss += S;
       const double xv = *reinterpret_cast<volatile double*>(ring_at(ss, pend_w));
       carry = __fma_rn(-pend_c, xv, carry);
-      if (lane == 31) store(s * 32 - 1, carry);
+      if (lane == 31) store_ring(s * 32 - 1, carry);
       publish(L, slot, (unsigned)s);
+      if (lane == 31) store_global(s * 32 - 1, carry);
       pend_z = 0;
     };
     for (int s = 0; s < nseg; ++s) {
@@ -233,7 +239,8 @@ __global__ void __launch_bounds__(1024, 1) gs_scan_kernel(ScanArgs a) {
       carry = __shfl_sync(FULL, x, 31);
       const int q = s * 32 + lane;
       const bool deferred = si.defer != 0;
-      if (q < len && !(deferred && lane == 31)) store(q, x);
+      const bool mine = q < len && !(deferred && lane == 31);
+      if (mine) store_ring(q, x);
       if (deferred) {
         pend_z = si.defer;
         pend_w = si.defpos;
@@ -241,11 +248,227 @@ __global__ void __launch_bounds__(1024, 1) gs_scan_kernel(ScanArgs a) {
       } else {
         publish(L, slot, (unsigned)(s + 1));
       }
+      if (mine) store_global(q, x);
     }
     if (pend_z) fix_pending(nseg);
     slot += nw % S;
     if (slot >= S) slot -= S;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Cluster version (window mode: every source lies in the previous chain).
+// Chain L runs on CTA L mod C of a thread-block cluster, so consecutive lines
+// -- the wavefront -- are spread over C SMs.  Its x values and progress word
+// live in the shared memory of its reader's CTA ((L + 1) mod C): the producer
+// stores them there (st.shared::cluster, then a release store of the progress
+// word) and the reader waits on its own shared memory.  Only the producer's
+// occasional checks (slot reuse, the reader's progress before overwriting a
+// window position) read another CTA's shared memory.
+__device__ __forceinline__ void st_cluster_f64(unsigned caddr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(caddr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_cluster_u64(unsigned caddr, unsigned long long v) {
+  asm volatile("st.release.cluster.shared::cluster.u64 [%0], %1;" ::"r"(caddr), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_cluster_u64(unsigned caddr) {
+  unsigned long long v;
+  asm volatile("ld.acquire.cluster.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(caddr) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_local_u64(unsigned saddr) {
+  // the word is released by a thread of another CTA: acquire at cluster scope
+  unsigned long long v;
+  asm volatile("ld.acquire.cluster.shared::cta.u64 %0, [%1];" : "=l"(v) : "r"(saddr) : "memory");
+  return v;
+}
+
+template <int K>
+__global__ void __launch_bounds__(256, 1) gs_scan_cluster_kernel(ScanArgs a) {
+  constexpr int NV = (K + 2) / 2;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const int C = (int)cluster_nctas(), me = (int)cluster_rank();
+  const int S = a.S, WIN = a.window;  // S slots of WIN doubles per CTA
+  const long long BIAS = (long long)C * S + 1;
+  auto enc = [&](int chain, unsigned done) -> unsigned long long {
+    return ((unsigned long long)(chain + BIAS) << 32) | done;
+  };
+  unsigned long long* prog = reinterpret_cast<unsigned long long*>(smem);
+  double* ring = reinterpret_cast<double*>(smem + 8 * ((S + 1) & ~1));
+  unsigned char* stages = smem + ((8 * ((S + 1) & ~1) + 8 * (size_t)S * WIN + 127) & ~(size_t)127);
+  unsigned char* my_stages = stages + (size_t)warp * kStages * a.stage_bytes;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(stages + (size_t)nw * kStages * a.stage_bytes);
+  const unsigned bar0 = (unsigned)__cvta_generic_to_shared(bars + warp * kStages);
+  const unsigned st0 = (unsigned)__cvta_generic_to_shared(my_stages);
+  const unsigned prog_s = (unsigned)__cvta_generic_to_shared(prog);
+  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
+  // slot k of this CTA first serves chain k*C + (me - 1 mod C): mark its
+  // fictitious predecessor (C*S chains earlier) complete
+  const int first_owner = (me + C - 1) % C;
+  for (int i = threadIdx.x; i < S; i += blockDim.x) prog[i] = enc(i * C + first_owner - C * S, 0x7fffffffu);
+  for (int i = threadIdx.x; i < S * WIN; i += blockDim.x) ring[i] = 0.0;
+  if (lane == 0) {
+    for (int k = 0; k < kStages; ++k) mbar_init(bar0 + 8u * k, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  cluster_sync();  // every CTA's rings and progress words exist before remote stores
+  constexpr int OFF_RV = 256, OFF_AD = 256 + NV * 512, OFF_SI = 256 + NV * 512 + 512;
+  unsigned phase = 0;
+  bool dead = false;
+  auto issue = [&](int g, int k) {
+    if (lane == 0) {
+      const unsigned dst = st0 + (unsigned)(k * a.stage_bytes), bar = bar0 + 8u * k;
+      mbar_expect_tx(bar, (unsigned)(OFF_SI + 32));
+      bulk_g2s(dst, a.o0 + (size_t)g * 32, 256u, bar);
+      bulk_g2s(dst + OFF_RV, a.recv + (size_t)g * NV * 32, (unsigned)(NV * 512), bar);
+      bulk_g2s(dst + OFF_AD, a.addr + (size_t)g * 32, 512u, bar);
+      bulk_g2s(dst + OFF_SI, a.seginfo + g, 32u, bar);
+    }
+  };
+  auto wait_stage = [&](int k) {
+    while (!mbar_try_wait(bar0 + 8u * k, (phase >> k) & 1u)) {}
+    phase ^= 1u << k;
+  };
+  // a chain's progress word: in the shared memory of CTA (c + 1) mod C, slot (c / C) mod S
+  auto prog_addr = [&](int c) -> unsigned {
+    return map_rank(prog_s + 8u * (unsigned)((c / C) % S), (unsigned)((c + 1) % C));
+  };
+  auto wait_remote = [&](int c, unsigned need) {
+    if (c < 0) return;
+    const unsigned long long want = enc(c, need);
+    const unsigned ad = prog_addr(c);
+    long long spins = 0;
+    while (ld_acquire_cluster_u64(ad) < want) {
+      if (++spins > (1LL << 24)) {
+        if (lane == 0) atomicOr(a.status, 8);
+        dead = true;
+        return;
+      }
+      __nanosleep(32);
+    }
+  };
+  auto wait_local = [&](int c, unsigned need) {  // c's word lives here: (c + 1) mod C == me
+    if (c < 0) return;
+    const unsigned long long want = enc(c, need);
+    const unsigned ad = prog_s + 8u * (unsigned)((c / C) % S);
+    long long spins = 0;
+    while (ld_acquire_local_u64(ad) < want) {
+      if (++spins > (1LL << 26)) {
+        if (lane == 0) atomicOr(a.status, 8);
+        dead = true;
+        return;
+      }
+    }
+  };
+  for (int j = warp; !dead; j += nw) {
+    const int L = j * C + me;
+    if (L >= a.nchains) break;
+    const int g0 = a.seg_ptr[L], nseg = a.seg_ptr[L + 1] - g0;
+    for (int k = 0; k < kStages && k < nseg; ++k) issue(g0 + k, k);
+    const int rcta = (L + 1) % C, wslot = (L / C) % S;
+    const unsigned my_ring = map_rank(ring_s + 8u * (unsigned)(wslot * WIN), (unsigned)rcta);
+    const unsigned my_prog = map_rank(prog_s + 8u * (unsigned)wslot, (unsigned)rcta);
+    // the slot's previous occupant (chain L - C*S) has no reader left
+    if (L - C * S >= 0) {
+      const int c = L - C * S + 1;
+      wait_remote(c, (unsigned)(a.seg_ptr[c + 1] - a.seg_ptr[c]));
+    }
+    // source chain L - 1: its ring is in this CTA
+    const int src = L - 1;
+    const double* src_ring = ring + (size_t)(src >= 0 ? (src / C) % S : 0) * WIN;
+    const int cs = a.chain_start[L], len = a.chain_len[L];
+    double carry = 0.0;
+    int pend_z = 0, pend_w = 0;
+    double pend_c = 0.0;
+    // x goes to the reader's ring before the release store of the progress
+    // word, and to x_new (global) after it, so the release never waits on
+    // global-memory stores
+    auto store_ring = [&](int q, double x) { st_cluster_f64(my_ring + 8u * (unsigned)(q & (WIN - 1)), x); };
+    auto store_global = [&](int q, double x) { a.xnew[a.fwd ? cs + q : a.n - 1 - (cs + q)] = x; };
+    auto publish = [&](unsigned done) {
+      __syncwarp();
+      if (lane == 0) st_release_cluster_u64(my_prog, enc(L, done));
+    };
+    auto fix_pending = [&](int s) {
+      wait_local(src, (unsigned)(pend_z & 0xfffff));
+      const double xv = *reinterpret_cast<const volatile double*>(src_ring + (pend_w & (WIN - 1)));
+      carry = __fma_rn(-pend_c, xv, carry);
+      if (lane == 31) store_ring(s * 32 - 1, carry);
+      publish((unsigned)s);
+      if (lane == 31) store_global(s * 32 - 1, carry);
+      pend_z = 0;
+    };
+    unsigned long long reader_seen = 0;  // last observed progress word of chain L + 1 (remote reads are rare)
+    for (int s = 0; s < nseg; ++s) {
+      const int k = s % kStages;
+      long long* tr = a.trace ? a.trace + 4 * (size_t)(g0 + s) : nullptr;
+      if (tr && lane == 0) tr[0] = scan_clock();
+      wait_stage(k);
+      const unsigned char* st = my_stages + (size_t)k * a.stage_bytes;
+      const double o0 = reinterpret_cast<const double*>(st)[lane];
+      double2 rv[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) rv[v] = reinterpret_cast<const double2*>(st + OFF_RV)[v * 32 + lane];
+      const uint4 ad = reinterpret_cast<const uint4*>(st + OFF_AD)[lane];
+      const SegInfo si = *reinterpret_cast<const SegInfo*>(st + OFF_SI);
+      __syncwarp();
+      if (tr && lane == 0) tr[1] = scan_clock();
+      if (s + kStages < nseg) issue(g0 + s + kStages, k);
+      if (pend_z) fix_pending(s);
+      // window: segment s overwrites segment s - WIN/32; the reader (chain L + 1) must be past it
+      if (s >= WIN / 32 && L + 1 < a.nchains) {
+        const unsigned long long want = enc(L + 1, (unsigned)(s - WIN / 32 + 2));
+        if (reader_seen < want) {
+          const unsigned pa = prog_addr(L + 1);
+          reader_seen = ld_acquire_cluster_u64(pa);
+          if (reader_seen < want) {
+            wait_remote(L + 1, (unsigned)(s - WIN / 32 + 2));
+            reader_seen = ld_acquire_cluster_u64(pa);
+          }
+        }
+      }
+      if (si.wait0) wait_local(src, (unsigned)(si.wait0 & 0xfffff));
+      if (tr && lane == 0) tr[2] = scan_clock();
+      double o = o0;
+#pragma unroll
+      for (int kk = 0; kk < K; ++kk) {
+        const unsigned w = addr_k(ad, kk);
+        const int pos = (int)(w & 0xfffffu);
+        const double c = (kk + 1) % 2 == 0 ? rv[(kk + 1) / 2].x : rv[(kk + 1) / 2].y;
+        const double xv = (w >> 20) ? *reinterpret_cast<const volatile double*>(src_ring + (pos & (WIN - 1))) : 0.0;
+        o = __fma_rn(-c, xv, o);
+      }
+      double A = o, B = rv[0].x;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const double Ap = __shfl_up_sync(FULL, A, d), Bp = __shfl_up_sync(FULL, B, d);
+        if (lane >= d) {
+          A = __fma_rn(B, Ap, A);
+          B = __dmul_rn(B, Bp);
+        }
+      }
+      const double x = __fma_rn(B, carry, A);
+      carry = __shfl_sync(FULL, x, 31);
+      const int q = s * 32 + lane;
+      const bool deferred = si.defer != 0;
+      const bool mine = q < len && !(deferred && lane == 31);
+      if (mine) store_ring(q, x);
+      if (deferred) {
+        pend_z = si.defer;
+        pend_w = si.defpos;
+        pend_c = si.defcoef;
+      } else {
+        publish((unsigned)(s + 1));
+      }
+      if (mine) store_global(q, x);
+      if (tr && lane == 0) tr[3] = scan_clock();
+    }
+    if (pend_z) fix_pending(nseg);
+  }
+  cluster_sync();  // nobody leaves while others may still store into its shared memory
 }
 
 // o0[rec(i)] = (b_i - sum over the row's old-value entries a_ij xold_j) * rdiag_i,

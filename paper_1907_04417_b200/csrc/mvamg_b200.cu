@@ -60,6 +60,7 @@ int g_scan_sleep = [] {
   const char* e = getenv("MVAMG_SCAN_SLEEP");
   return e ? atoi(e) : 32;
 }();
+long long* g_scan_trace = nullptr;  // diagnostics: chain-scan per-segment timestamps (mvamg_gs_scan_set_trace)
 int g_row_sleep = [] {
   const char* e = getenv("MVAMG_ROW_SLEEP");
   return e ? atoi(e) : 0;
@@ -167,6 +168,7 @@ struct GsLevels {
 // Chain-scan schedule (gs_scan.cuh) of one sweep mode (tolerance parity).
 struct GsScan {
   int nchains = 0, S = 0, ring_len = 0, K = 0, threads = 0, window = 0;
+  int cluster = 0;  // > 1: chains spread over a cluster of that many CTAs (window mode)
   int ndelta = 0, delta[gsscan::kMaxDeps] = {0, 0, 0, 0};  // distinct source-chain distances
   const int* seg_ptr = nullptr;
   const int* chain_start = nullptr;
@@ -505,6 +507,39 @@ int launch_gs_scan(const Csr& A, const GsScan& g, int mode, const double* b, con
   a.o0 = g.o0;
   a.xnew = xnew;
   a.status = status;
+  a.trace = g_scan_trace;
+  if (g.cluster > 1) {
+    static bool cattr = false;
+    if (!cattr) {
+      cattr = true;
+      cudaFuncSetAttribute(gs_scan_cluster_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(gs_scan_cluster_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(gs_scan_cluster_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(gs_scan_cluster_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaGetLastError();
+    }
+    if (!g.window || g.ndelta != 1 || g.delta[0] != 1)
+      return fail(MVAMG_E_ARG, "gs scan: the cluster sweep needs window mode (sources one chain back)");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g.cluster);
+    cfg.blockDim = dim3(g.threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = g.cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    switch (g.K) {
+      case 1: CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_scan_cluster_kernel<1>, a)); break;
+      case 2: CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_scan_cluster_kernel<2>, a)); break;
+      case 3: CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_scan_cluster_kernel<3>, a)); break;
+      default: CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_scan_cluster_kernel<4>, a)); break;
+    }
+    return 0;
+  }
   switch (g.K) {
     case 1: gs_scan_kernel<1><<<1, g.threads, smem, s>>>(a); break;
     case 2: gs_scan_kernel<2><<<1, g.threads, smem, s>>>(a); break;
@@ -2334,8 +2369,9 @@ int mvamg_gs_scan_sweep_f64(int mode, int n, const int* indptr, const int* indic
   g.nchains = nchains; g.S = S; g.ring_len = ring_len; g.K = K; g.threads = threads;
   if (int e = set_deltas(g, ndelta, deltas)) return e;
   g.seg_ptr = seg_ptr; g.chain_start = chain_start; g.chain_len = chain_len; g.recv = recv; g.addr = addr;
-  g.seginfo = seginfo; g.o0 = o0; g.rec = rec; g.rdiag = rdiag; g.window = window;
-  if (window && (window & (window - 1))) return fail(MVAMG_E_ARG, "gs scan: window must be a power of two");
+  g.seginfo = seginfo; g.o0 = o0; g.rec = rec; g.rdiag = rdiag; g.window = window & 0xffff;
+  g.cluster = window >> 16;
+  if (g.window && (g.window & (g.window - 1))) return fail(MVAMG_E_ARG, "gs scan: window must be a power of two");
   return launch_gs_scan(A, g, mode, b, x_old, x_new, ws + 1, (cudaStream_t)stream);
 }
 
@@ -2350,8 +2386,17 @@ int mvamg_hierarchy_set_gs_scan(mvamg_hierarchy* h, int k, int mode, int nchains
   g.nchains = nchains; g.S = S; g.ring_len = ring_len; g.K = K; g.threads = threads;
   if (int e = set_deltas(g, ndelta, deltas)) return e;
   g.seg_ptr = seg_ptr; g.chain_start = chain_start; g.chain_len = chain_len; g.recv = recv; g.addr = addr;
-  g.seginfo = seginfo; g.o0 = o0; g.rec = rec; g.rdiag = rdiag; g.window = window;
-  if (window && (window & (window - 1))) return fail(MVAMG_E_ARG, "gs scan: window must be a power of two");
+  g.seginfo = seginfo; g.o0 = o0; g.rec = rec; g.rdiag = rdiag; g.window = window & 0xffff;
+  g.cluster = window >> 16;
+  if (g.window && (g.window & (g.window - 1))) return fail(MVAMG_E_ARG, "gs scan: window must be a power of two");
+  return 0;
+}
+
+
+/* Diagnostics: device buffer of 4 int64 per segment that the chain-scan
+ * sweeps fill with %globaltimer stamps (null: off). */
+int mvamg_gs_scan_set_trace(long long* trace_dev) {
+  g_scan_trace = trace_dev;
   return 0;
 }
 

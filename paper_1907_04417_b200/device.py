@@ -82,6 +82,8 @@ class GpuConfig:
     scan_gs: bool = False           # (with exact_gs False) time the chain-scan sweep on chain-structured levels
                                     # at upload and keep it when faster (off: single-SM issue-bound, slower
                                     # than the wavefront on C2/C3, and the timing costs setup time)
+    scan_cluster: int = 0           # CTAs of the cluster chain-scan sweep (window-mode levels; 0/1 = one CTA;
+                                    # 8 measured 2.85 ms vs 2.1 ms one-CTA on C2, tools/scan_trace.py)
     level_reg: bool = False         # (with exact_gs False) single-CTA level sweeps with register-prefetched
                                     # entries (gs_level_reg_kernel; measured slower than the staged kernel)
     exact_gs: bool = False          # True: every GS kernel keeps the CSR-order subtractions (bit-exact with

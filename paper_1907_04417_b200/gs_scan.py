@@ -49,6 +49,7 @@ class ScanPlan:
     addr: np.ndarray      # per (segment, lane): 4 x uint32 (delta << 20 | position), zero cell when unused
     seginfo: np.ndarray   # per segment, 32 B: wait0, wait1, deferred wait, deferred position, its coefficient
     window: int           # > 0: ring slots keep positions mod window (single distance 1)
+    cluster: int          # > 1: chains spread over a thread-block cluster of this many CTAs
     rec: np.ndarray       # original row -> record index
     rdiag: np.ndarray     # original row order
     depth: int            # wavefront steps (segment DAG depth)
@@ -61,8 +62,9 @@ class ScanPlan:
 
 
 MAX_WAITS = 2
-SCAN_WINDOW = 128   # positions per ring slot in window mode (4 segments)
+SCAN_WINDOW = 256   # positions per ring slot in window mode (8 segments)
 STAGES = 3          # staged segments per warp (csrc/gs_scan.cuh kStages)
+SCAN_CLUSTER_WARPS = 8  # warps per CTA of the cluster sweep (gs_scan_cluster_kernel: 256 threads)
 SEGINFO_DTYPE = np.dtype([("wait0", "<i4"), ("wait1", "<i4"), ("defer", "<i4"), ("defpos", "<i4"),
                           ("defcoef", "<f8"), ("pad", "<f8")])
 
@@ -203,6 +205,11 @@ def plan_scan(A, mode, cfg=None):
     if threads == 0:
         return None
     S = threads // 32 + W + 1
+    cluster = 0
+    if window and cfg.scan_cluster > 1:
+        # chain L on CTA L mod C, NW warps each; a CTA's S slots hold its readers' rings
+        cluster, threads = int(cfg.scan_cluster), 32 * SCAN_CLUSTER_WARPS
+        S = SCAN_CLUSTER_WARPS + 2
     rec = np.empty(n, dtype=np.int64)
     if fwd:
         rec[:] = rec_sweep
@@ -210,7 +217,7 @@ def plan_scan(A, mode, cfg=None):
         rec[n - 1 - np.arange(n)] = rec_sweep
     return ScanPlan(n, mode, nch, S, ring_len, W, K, threads, seg_ptr.astype(np.int32),
                     heads.astype(np.int32), clen.astype(np.int32), recv.ravel(), addr.ravel(), seginfo, window,
-                    rec.astype(np.int32), 1.0 / d, depth, deltas, active)
+                    cluster, rec.astype(np.int32), 1.0 / d, depth, deltas, active)
 
 
 def _segment_schedule(nch, seg_ptr, useg, udelta, mneed, is_def):
@@ -272,8 +279,8 @@ class DeviceGsScan:
     def args(self):
         p = self.plan
         return (p.nchains, p.S, p.ring_len, int(p.deltas.shape[0]), self._deltas.ctypes.data_as(ctypes.c_void_p),
-                p.K, p.threads, p.window, ptr(self.seg_ptr), ptr(self.chain_start), ptr(self.chain_len),
-                ptr(self.recv), ptr(self.addr), ptr(self.seginfo), ptr(self.o0), ptr(self.rec), ptr(self.rdiag))
+                p.K, p.threads, p.window | (p.cluster << 16), ptr(self.seg_ptr), ptr(self.chain_start),
+                ptr(self.chain_len), ptr(self.recv), ptr(self.addr), ptr(self.seginfo), ptr(self.o0), ptr(self.rec), ptr(self.rdiag))
 
     def sweep(self, b, x_old, x_new, ws, stream=None):
         mode = self.mode

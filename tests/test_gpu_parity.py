@@ -574,30 +574,39 @@ def test_short_chain_level_uses_row_sweep(mv, c1):
 
 
 # ------------------------------------------------------- chain-scan sweep ----
+@pytest.mark.parametrize("cluster", [8, 0])
 @pytest.mark.parametrize("mode", [0, 1, 2, 3])
-def test_gs_scan_kernel(mv, c1, mode):
+def test_gs_scan_kernel(mv, c1, mode, cluster):
     """Chain-scan sweep (tolerance parity): each sweep within rounding of the
-    reference's serial loop, on grid structures (K = 1, 2, 3) and C1's fine level."""
+    reference's serial loop, on grid structures (K = 1, 2, 3) and C1's fine
+    level; lines longer than the 128-position window run the cluster sweep
+    (cluster = 8) or the one-CTA window sweep (cluster = 0)."""
     import torch
     from paper_1907_04417_b200 import problems
     from paper_1907_04417_b200.gs_scan import DeviceGsScan
 
+    cfg = mv.GpuConfig(scan_cluster=cluster)
     rng = np.random.default_rng(20 + mode)
     cases = [("lap2d", laplacian_2d(40)), ("lap3d", laplacian_3d(12)), ("q1", problems.anisotropic_q1(70)),
-             ("jump3d", problems.jump_3d(16, 4, 1)), ("c1_l0", c1[1][0]), ("lap1d", laplacian_1d(100))]
+             ("jump3d", problems.jump_3d(16, 4, 1)), ("c1_l0", c1[1][0]), ("lap1d", laplacian_1d(100)),
+             ("lap2d_long", laplacian_2d(260)), ("q1_long", problems.anisotropic_q1(300)),
+             ("lap1d_long", laplacian_1d(1000))]
+    seen_cluster = False
     for name, A in cases:
         n = A.shape[0]
         b = rng.standard_normal(n)
         x0 = rng.standard_normal(n)
         want = np.zeros(n) if mode % 2 == 0 else x0.copy()
         oracle_gs(A, b, want, "forward" if mode < 2 else "backward")
-        sc = DeviceGsScan(A, mode)
+        sc = DeviceGsScan(A, mode, cfg)
+        seen_cluster |= sc.plan.cluster > 1
         xn = torch.empty(n, dtype=torch.float64, device="cuda")
         ws = torch.zeros(8, dtype=torch.int32, device="cuda")
         sc.sweep(_dev(b), None if mode % 2 == 0 else _dev(x0), xn, ws)
         torch.cuda.synchronize()
         assert int(ws[1].item()) == 0, name
-        assert rel(xn.cpu().numpy(), want) <= 1e-12, (name, mode)
+        assert rel(xn.cpu().numpy(), want) <= 1e-12, (name, mode, cluster)
+    assert seen_cluster == (cluster > 1)
 
 
 def test_vcycle_with_scan_sweeps(mv, c1):

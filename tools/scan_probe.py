@@ -32,9 +32,15 @@ for m in modes:
         print(f"mode {m}: no scan plan")
         continue
     sc = DeviceGsScan(A, m, plan=p)
+    import os
+    if os.environ.get("SCAN_SINGLE"):
+        p1 = plan_scan(A, m, GpuConfig(scan_cluster=0))
+        sc1 = DeviceGsScan(A, m, plan=p1)
+        t1 = time_sweep(lambda: sc1.sweep(b, xo if m % 2 else None, xn, ws), reps=5)
+        print(f"  single-CTA scan {t1 * 1e6:.0f} us")
     xold = xo if m % 2 else None
     t_scan = time_sweep(lambda: sc.sweep(b, xold, xn, ws), reps=5)
     t_wave = time_sweep(lambda: gp.sweep(0 if m < 2 else 1, b, xold, xn, ws), reps=5)
     print(f"{name} mode {m}: n={n} chains={p.nchains} W={p.W} K={p.K} warps={p.threads // 32} S={p.S} "
-          f"depth={p.depth} plan {tp:.1f}s | scan {t_scan * 1e6:.0f} us ({t_scan * 1e6 / max(1, p.depth):.3f} us/step)"
+          f"cluster={p.cluster} depth={p.depth} plan {tp:.1f}s | scan {t_scan * 1e6:.0f} us ({t_scan * 1e6 / max(1, p.depth):.3f} us/step)"
           f" | wave {t_wave * 1e6:.0f} us | timeout={int(ws[1].item())}", flush=True)
