@@ -458,6 +458,12 @@ def run_b200(args, world, rank, local):
 
         def gs_once():
             small.sweep(r_dev, None, xn, ws, s)
+    elif lv.get("rows"):
+        rows0 = lv["rows"][0]
+        gs_kernel = "gs_row_kernel (dataflow row sweep) level 0, forward from x=0 (+prepare)"
+
+        def gs_once():
+            rows0.sweep(r_dev, None, xn, ws, s)
     else:
         gp = lv["gs"]
         gs_kernel = ("gs_lean_kernel" if gp.plan.lean_C else "gs_sweep_kernel") + \
