@@ -458,7 +458,16 @@ def bootstrap_run(A, w0=None, params=None, config=None):
     from .composite import GpuComposite, test_phase
     from .cycles import CycleSpec, GpuMultigridOperator
 
+    import dataclasses
+
+    from .device import GpuConfig
+
     params = params or BootstrapParams()
+    # the test phase's smooth vectors steer the next stage's matching: run its
+    # K-cycles with the bit-exact sweeps, as the reference's numba loops do, so
+    # near-tied matching decisions follow the reference (the solve itself may
+    # use tolerance parity)
+    config = dataclasses.replace(config or GpuConfig(), exact_gs=True)
     A = as_csr(A)
     w = np.ones(A.shape[0]) if w0 is None else np.asarray(w0, dtype=np.float64)
     rng = np.random.default_rng(params.rng_seed)
