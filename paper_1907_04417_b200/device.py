@@ -535,35 +535,14 @@ class DeviceGsRows:
 
 def time_sweep(fn, reps=3):
     """Device time (s) of fn() -- one GS sweep -- after one warm-up launch.
-
-    The reps calls are captured into one CUDA graph and replayed, so a short
-    sweep is timed on the device (as it runs inside the captured cycle), not
-    at the rate the host can issue it; falls back to direct launches."""
+    (Direct launches: for very short sweeps this includes the host issue rate,
+    the same for every candidate the autotune compares.)"""
     torch = torch_cuda()
     fn()
-    torch.cuda.synchronize()
-    graph = None
-    try:
-        side = torch.cuda.Stream()
-        side.wait_stream(torch.cuda.current_stream())
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(side):
-            with torch.cuda.graph(graph, stream=side):
-                for _ in range(reps):
-                    fn()
-        torch.cuda.current_stream().wait_stream(side)
-        graph.replay()
-        torch.cuda.synchronize()
-    except Exception:  # capture unsupported for this launch sequence
-        graph = None
-        torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    if graph is not None:
-        graph.replay()
-    else:
-        for _ in range(reps):
-            fn()
+    for _ in range(reps):
+        fn()
     e1.record()
     e1.synchronize()
     return e0.elapsed_time(e1) / reps * 1e-3
