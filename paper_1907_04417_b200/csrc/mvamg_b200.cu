@@ -828,10 +828,19 @@ struct mvamg_hierarchy {
   }
 };
 
+// Graphs that replay a composite are cached on its first component's
+// hierarchy, which usually outlives the composite (the bootstrap builds a new
+// composite per stage over the same components).  They are keyed by a serial
+// number, never by the composite's address: a new composite allocated at a
+// freed one's address must not replay the old graph (stale component list and
+// freed buffers -- an intermittent wrong result or illegal address).
+unsigned long long g_composite_serial = 0;
+
 struct mvamg_composite {
   std::vector<mvamg_hierarchy*> ops;
   double *t = nullptr, *acc = nullptr;
   int n = 0;
+  unsigned long long serial = 0;
   std::map<std::string, cudaGraphExec_t> graphs;
   ~mvamg_composite() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
@@ -909,7 +918,8 @@ int pcg_device(mvamg_hierarchy* h, int pc, mvamg_composite* comp, const double* 
   if ((st = sync_flags())) return st;
   if (!h->host_sc->stop) {
     // z = M r ; rz = r'z ; p = z
-    std::string key0 = "pcg0/" + std::to_string(pc) + "/" + std::to_string((size_t)comp);
+    const std::string cid = comp ? std::to_string(comp->serial) : std::string("-");
+    std::string key0 = "pcg0/" + std::to_string(pc) + "/" + cid;
     st = h->run_graph(key0, s, [&](cudaStream_t cs) -> int {
       const double* z = nullptr;
       int e = precond_apply(h, pc, comp, h->pr, z, cs);
@@ -920,7 +930,7 @@ int pcg_device(mvamg_hierarchy* h, int pc, mvamg_composite* comp, const double* 
     });
     if (st) return st;
     if ((st = sync_flags())) return st;
-    std::string keyA = "pcgA", keyB = "pcgB/" + std::to_string(pc) + "/" + std::to_string((size_t)comp);
+    std::string keyA = "pcgA", keyB = "pcgB/" + std::to_string(pc) + "/" + cid;
     while (!h->host_sc->stop) {
       // q = A p ; alpha = rz/p'q ; x += alpha p ; r -= alpha q ; hist ; stop test
       st = h->run_graph(keyA, s, [&](cudaStream_t cs) -> int {
@@ -2216,6 +2226,7 @@ int mvamg_composite_create(mvamg_composite** c, int ncomp, mvamg_hierarchy* cons
   auto* C = new mvamg_composite();
   C->ops.assign(comps, comps + ncomp);
   C->n = n;
+  C->serial = ++g_composite_serial;
   if (cudaMalloc(&C->t, (size_t)n * 8) != cudaSuccess || cudaMalloc(&C->acc, (size_t)n * 8) != cudaSuccess) {
     delete C;
     return fail(MVAMG_E_CUDA, "composite: cudaMalloc failed");
@@ -2234,7 +2245,7 @@ int mvamg_composite_apply_symmetrized(mvamg_composite* c, double* x, void* strea
   cudaStream_t s = (cudaStream_t)stream;
   mvamg_hierarchy* h0 = c->ops[0];
   CUDA_TRY(cudaMemcpyAsync(c->acc, x, (size_t)c->n * 8, cudaMemcpyDeviceToDevice, s));
-  int st = h0->run_graph("composite/" + std::to_string((size_t)c), s,
+  int st = h0->run_graph("composite/" + std::to_string(c->serial), s,
                          [&](cudaStream_t cs) -> int { return c->symmetrized(c->acc, cs); });
   if (st) return st;
   CUDA_TRY(cudaMemcpyAsync(x, c->acc, (size_t)c->n * 8, cudaMemcpyDeviceToDevice, s));
@@ -2247,7 +2258,7 @@ int mvamg_composite_precond(mvamg_composite* c, const double* r, double* z, void
   mvamg_hierarchy* h0 = c->ops[0];
   CUDA_TRY(cudaMemcpyAsync(h0->in, r, (size_t)c->n * 8, cudaMemcpyDeviceToDevice, s));
   const double* out = nullptr;
-  int st = h0->run_graph("compprec/" + std::to_string((size_t)c), s, [&](cudaStream_t cs) -> int {
+  int st = h0->run_graph("compprec/" + std::to_string(c->serial), s, [&](cudaStream_t cs) -> int {
     int e = c->precond(h0->in, out, cs);
     if (e) return e;
     copy_kernel<<<grid_for(c->n), 256, 0, cs>>>(c->n, h0->pz, out);

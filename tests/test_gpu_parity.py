@@ -630,3 +630,20 @@ def test_vcycle_with_scan_sweeps(mv, c1):
     x, rep = mv.pcg(mats[0], d["b"], op, rtol=1e-6)
     assert rep.iterations == int(d["pcg_nit"])
     assert np.max(np.abs(rep.residual_history - d["pcg_hist"]) / d["pcg_hist"]) <= 1e-10
+
+
+def test_composite_graphs_not_reused_across_composites(mv, c1, c1_comps):
+    """A composite created where a destroyed one lived (the bootstrap makes a
+    new composite per stage over the same components) must not replay the old
+    composite's cached graph (keys are serial numbers, not addresses)."""
+    import gc
+
+    d = golden("c1")
+    gpu, cpu = c1_comps
+    x = d["x4"]
+    for ncomp in (1, 2, 3, 4, 2):
+        comp = mv.GpuComposite(gpu[:ncomp])
+        y = comp.apply_symmetrized(x)
+        assert rel(y, oracle_composite(cpu[:ncomp], x)) <= 1e-9, ncomp
+        del comp
+        gc.collect()
