@@ -647,3 +647,25 @@ def test_composite_graphs_not_reused_across_composites(mv, c1, c1_comps):
         assert rel(y, oracle_composite(cpu[:ncomp], x)) <= 1e-9, ncomp
         del comp
         gc.collect()
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_fit_and_solve_medium_matches_oracle(mv, exact):
+    """A fitted mid-size problem (Q1 anisotropic 256^2, 65,536 rows, 4-6
+    levels): the GPU PCG in the default tolerance-parity mode and in the exact
+    mode against the CPU oracle on the same hierarchy -- same iteration count,
+    residual history within 1e-10 per iteration."""
+    from paper_1907_04417_b200 import problems
+
+    A = problems.anisotropic_q1(256)
+    b = problems.rhs_uniform(A.shape[0], 0)
+    est = mv.MultiVectorAMG().fit(A)
+    mats, pros = list(est.hierarchy_.matrices), list(est.hierarchy_.prolongator_matrices)
+    op = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(exact_gs=exact))
+    ref = OracleOperator(mats, pros)
+    z, zr = op.apply(b), ref.apply(b)
+    assert rel(z, zr) <= TOL_CYCLE
+    x, rep = mv.pcg(mats[0], b, op, rtol=1e-6)
+    _, hist, nit, conv = oracle_pcg(ref, b)
+    assert conv and rep.converged and rep.iterations == nit
+    assert np.max(np.abs(rep.residual_history - hist) / hist) <= 1e-10
