@@ -283,6 +283,20 @@ __device__ __forceinline__ unsigned long long ld_acquire_local_u64(unsigned sadd
   return v;
 }
 
+__device__ __forceinline__ void bulk_s2g(void* gdst, unsigned ssrc, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(ssrc), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
 template <int K>
 __global__ void __launch_bounds__(256, 1) gs_scan_cluster_kernel(ScanArgs a) {
   constexpr int NV = (K + 2) / 2;
@@ -302,6 +316,12 @@ __global__ void __launch_bounds__(256, 1) gs_scan_cluster_kernel(ScanArgs a) {
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(stages + (size_t)nw * kStages * a.stage_bytes);
   const unsigned bar0 = (unsigned)__cvta_generic_to_shared(bars + warp * kStages);
   const unsigned st0 = (unsigned)__cvta_generic_to_shared(my_stages);
+  // x_new leaves through TMA bulk stores from two 32-value staging buffers per
+  // warp: asynchronous-proxy stores, so a segment's release store of its
+  // progress word never waits for global memory
+  double* xout = reinterpret_cast<double*>(
+      (reinterpret_cast<size_t>(bars + (size_t)nw * kStages) + 15) & ~(size_t)15) + warp * 64;
+  const unsigned xout_s = (unsigned)__cvta_generic_to_shared(xout);
   const unsigned prog_s = (unsigned)__cvta_generic_to_shared(prog);
   const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
   // slot k of this CTA first serves chain k*C + (me - 1 mod C): mark its
@@ -388,6 +408,18 @@ __global__ void __launch_bounds__(256, 1) gs_scan_cluster_kernel(ScanArgs a) {
     // global-memory stores
     auto store_ring = [&](int q, double x) { st_cluster_f64(my_ring + 8u * (unsigned)(q & (WIN - 1)), x); };
     auto store_global = [&](int q, double x) { a.xnew[a.fwd ? cs + q : a.n - 1 - (cs + q)] = x; };
+    // whole 32-row segments go out by bulk copy when the chain's x_new span is 16-byte aligned
+    const bool bulk = ((a.fwd ? cs : a.n - cs) & 1) == 0;
+    auto stage_out = [&](int seg, int ln, double x) { xout[(seg & 1) * 32 + (a.fwd ? ln : 31 - ln)] = x; };
+    auto flush_out = [&](int seg) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        const size_t start = a.fwd ? (size_t)cs + 32 * seg : (size_t)a.n - 1 - ((size_t)cs + 32 * seg + 31);
+        bulk_s2g(a.xnew + start, xout_s + 256u * (unsigned)(seg & 1), 256u);
+        bulk_commit();
+      }
+    };
     auto publish = [&](unsigned done) {
       __syncwarp();
       if (lane == 0) st_release_cluster_u64(my_prog, enc(L, done));
@@ -398,7 +430,13 @@ __global__ void __launch_bounds__(256, 1) gs_scan_cluster_kernel(ScanArgs a) {
       carry = __fma_rn(-pend_c, xv, carry);
       if (lane == 31) store_ring(s * 32 - 1, carry);
       publish((unsigned)s);
-      if (lane == 31) store_global(s * 32 - 1, carry);
+      const bool full = (s - 1) * 32 + 32 <= len;
+      if (bulk && full) {
+        if (lane == 31) stage_out(s - 1, 31, carry);
+        flush_out(s - 1);
+      } else if (lane == 31) {
+        store_global(s * 32 - 1, carry);
+      }
       pend_z = 0;
     };
     unsigned long long reader_seen = 0;  // last observed progress word of chain L + 1 (remote reads are rare)
@@ -455,19 +493,28 @@ __global__ void __launch_bounds__(256, 1) gs_scan_cluster_kernel(ScanArgs a) {
       const int q = s * 32 + lane;
       const bool deferred = si.defer != 0;
       const bool mine = q < len && !(deferred && lane == 31);
+      const bool full = s * 32 + 32 <= len;
       if (mine) store_ring(q, x);
+      if (bulk && full) {
+        // the staging buffer of segment s last held segment s - 2: its bulk read must be done
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        if (mine) stage_out(s, lane, x);
+      }
       if (deferred) {
         pend_z = si.defer;
         pend_w = si.defpos;
         pend_c = si.defcoef;
       } else {
         publish((unsigned)(s + 1));
+        if (bulk && full) flush_out(s);
       }
-      if (mine) store_global(q, x);
+      if (mine && !(bulk && full)) store_global(q, x);
       if (tr && lane == 0) tr[3] = scan_clock();
     }
     if (pend_z) fix_pending(nseg);
   }
+  if (lane == 0) bulk_wait<0>();  // x_new complete before the kernel ends
   cluster_sync();  // nobody leaves while others may still store into its shared memory
 }
 

@@ -458,7 +458,8 @@ int gs_scan_stage_bytes(int K) { return 256 + ((K + 2) / 2) * 512 + 512 + 32; }
 size_t gs_scan_smem(const GsScan& g) {
   const size_t nw = (size_t)g.threads / 32;
   return ((8 * (size_t)((g.S + 1) & ~1) + 8 * (size_t)g.S * g.ring_len + 127) & ~(size_t)127) +
-         nw * gsscan::kStages * (size_t)gs_scan_stage_bytes(g.K) + nw * gsscan::kStages * 8;
+         nw * gsscan::kStages * (size_t)gs_scan_stage_bytes(g.K) + nw * gsscan::kStages * 8 +
+         (g.cluster > 1 ? 16 + nw * 512 : 0);  // cluster kernel: two 32-value x staging buffers per warp
 }
 
 // mode: 0 fwd from 0, 1 fwd from x_old, 2 bwd from 0, 3 bwd from x_old.
