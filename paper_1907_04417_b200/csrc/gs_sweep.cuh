@@ -389,6 +389,12 @@ __device__ __forceinline__ bool gs_lean_gather(const unsigned long long* rec, in
   return ready;
 }
 
+// Records of at most this many entries per row use the half-chunk software
+// pipeline of the lean kernel (staging of the next half overlaps the rounds).
+#ifndef MVAMG_LEAN_PIPE_C
+#define MVAMG_LEAN_PIPE_C 2
+#endif
+
 template <bool FWD, int C, int R, int D, int K = 1>
 __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
   constexpr int S = 3 + 2 * C;
@@ -665,7 +671,7 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
           ++issued;
         }
       }
-    } else if constexpr (R >= 4 && C <= 2) {
+    } else if constexpr (R >= 4 && C <= MVAMG_LEAN_PIPE_C) {
       // Software-pipelined by half chunks (H rounds): while half h runs, the
       // codes of the next half are loaded (before its first round) and decoded
       // with their cross-tile prefetches (after it), so staging latency hides
