@@ -8,7 +8,6 @@ import socket
 
 import numpy as np
 import pytest
-import scipy.sparse as sp
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
@@ -78,13 +77,11 @@ def _worker(rank, world, port, out):
         d = golden("c1")
         mats, pros = hierarchy(d, "mv")
         s = DistributedSolver(mats, pros, backend=OracleBackend())
-        r_own = s.own_rows(d["apply_b"] if "apply_b" in d else d["b"])
         op = s.op
         z = op.be.vec(op.n_own)
         op.apply(op.be.from_host(s.own_rows(d["b"])), z)
         x, rep = s.solve(d["b"])
         out[rank] = (z.numpy().copy(), x, rep.iterations, rep.residual_history)
-        del r_own
     finally:
         dist.destroy_process_group()
 
