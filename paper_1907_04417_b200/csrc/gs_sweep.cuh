@@ -921,7 +921,7 @@ __global__ void __launch_bounds__(1024, 1) gs_level_kernel(GsLevelArgs a) {
     const double* rhs = reinterpret_cast<const double*>(bb + rows_b + ents_b);
     const int r0 = __ldg(lp + l), r1 = __ldg(lp + l + 1);
     const int e0 = __ldg(le + l), toff = r0 & 1;
-    if (G > 1) {
+    if constexpr (G > 1) {
       const int ngroups = T / G, g = tid / G, li = tid % G;
       const int nr = r1 - r0, iters = (nr + ngroups - 1) / ngroups;
       for (int it = 0; it < iters; ++it) {
@@ -950,7 +950,7 @@ __global__ void __launch_bounds__(1024, 1) gs_level_kernel(GsLevelArgs a) {
       }
       if (CLUSTER) cluster_sync();  // level l published cluster-wide
       continue;
-    }
+    } else {
     for (int r = tid; r < r1 - r0; r += T) {
       const GsLevelRow m = rows[r];
       double s = rhs[toff + r];
@@ -981,6 +981,7 @@ __global__ void __launch_bounds__(1024, 1) gs_level_kernel(GsLevelArgs a) {
       x[m.row - base] = div_rn_markstein(s, m.diag, m.rdiag);
     }
     if (CLUSTER) cluster_sync();  // level l published cluster-wide
+    }
   }
   cp_async_wait<0>();
   __syncthreads();
