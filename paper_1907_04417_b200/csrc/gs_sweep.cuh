@@ -389,13 +389,49 @@ __device__ __forceinline__ bool gs_lean_gather(const unsigned long long* rec, in
   return ready;
 }
 
+// ---- thread-block-cluster tiles (GpuConfig.lean_cluster) ---------------------
+// Consecutive tiles (in processing order) run as the CTAs of one cluster.  A
+// source row in the previous tile of the same cluster is read from that CTA's
+// shared-memory window over DSMEM instead of from x_new through L2; the
+// schedule marks such sources with kGsRemote in the code's index (window slot).
+constexpr unsigned kGsRemote = 1u << 28;
+__device__ __forceinline__ unsigned lean_crank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned lean_cn() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void lean_csync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned lean_cmap(unsigned saddr, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void ld_dsmem_if(unsigned long long& v, bool p, unsigned caddr) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n @q ld.relaxed.cluster.shared::cluster.u64 %0, [%2];\n}"
+               : "+l"(v) : "r"((unsigned)p), "r"(caddr));
+}
+// a cross-tile source: x_new through L2, or the previous tile's window over DSMEM
+__device__ __forceinline__ void ld_cross_if(unsigned long long& v, bool p, unsigned idx, const double* xnew,
+                                            unsigned prev_win) {
+  const bool rem = (idx & kGsRemote) != 0u;
+  ld_global_if(v, p && !rem, xnew + (idx & (kGsRemote - 1u)));
+  ld_dsmem_if(v, p && rem, prev_win + 8u * (idx & (kGsRemote - 1u)));
+}
+
 // Records of at most this many entries per row use the half-chunk software
 // pipeline of the lean kernel (staging of the next half overlaps the rounds).
 #ifndef MVAMG_LEAN_PIPE_C
 #define MVAMG_LEAN_PIPE_C 2
 #endif
 
-template <bool FWD, int C, int R, int D, int K = 1>
+template <bool FWD, int C, int R, int D, int K = 1, bool CLU = false>
 __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
   constexpr int S = 3 + 2 * C;
   constexpr int RW = R * K * 32 * S;  // record words of one chunk (R rounds of K row slots)
@@ -417,17 +453,45 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
   }
   __syncwarp();
   unsigned parity = 0;
+  // CLU: launched as thread-block clusters (a separate instantiation, so the
+  // plain kernel keeps its register budget)
+  const unsigned crank = CLU ? lean_crank() : 0u, cn = CLU ? lean_cn() : 1u;
+  __shared__ int s_blk;
   for (;;) {
     __syncthreads();
-    if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1);
-    __syncthreads();
-    const int tk = s_tile;
-    if (tk >= a.ntiles) return;
-    const int t = FWD ? tk : a.ntiles - 1 - tk;
+    int tk;
+    if (cn > 1) {
+      // cluster mode: a ticket hands out a block of cn consecutive tiles; the
+      // CTA of rank r takes tile block * cn + r.  The barriers also keep every
+      // window alive until its readers in the cluster are done with it.
+      lean_csync();
+      if (threadIdx.x == 0 && crank == 0) s_blk = atomicAdd(a.ticket, 1);
+      lean_csync();
+      if (threadIdx.x == 0) {
+        unsigned v;
+        asm volatile("ld.shared::cluster.u32 %0, [%1];"
+                     : "=r"(v) : "r"(lean_cmap((unsigned)__cvta_generic_to_shared(&s_blk), 0u)) : "memory");
+        s_tile = (int)v * (int)cn + (int)crank;
+      }
+      __syncthreads();
+      tk = s_tile;
+      if (tk - (int)crank >= a.ntiles) return;  // the whole cluster is done
+    } else {
+      if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1);
+      __syncthreads();
+      tk = s_tile;
+      if (tk >= a.ntiles) return;
+    }
+    const bool idle = tk >= a.ntiles;
+    const int t = idle ? 0 : (FWD ? tk : a.ntiles - 1 - tk);
     const int c0 = a.tile_ptr[t], c1 = a.tile_ptr[t + 1];
     const int TS = ((c1 - c0 + 31) / 32) * 32;
     for (int i = threadIdx.x; i < a.window; i += blockDim.x) smem_u64[i] = kSentinel;
     __syncthreads();
+    if (cn > 1) lean_csync();  // every window of the cluster is initialised before remote reads
+    if (idle) continue;
+    const unsigned prev_win = (CLU && cn > 1 && crank > 0) ? lean_cmap(sbase, crank - 1) : 0u;
+    (void)prev_win;
     const int w0 = a.tile_wbase[t], nw = a.tile_wbase[t + 1] - w0;
     if (warp >= nw) continue;
     const int g = w0 + warp;
@@ -492,7 +556,8 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
             const unsigned t = (tmr >> (2 * u)) & 3u;
             unsigned long long v = (unsigned long long)__double_as_longlong(xprev);
             ld_shared_if(v, t == 1u, sbase + 8u * ixr[u]);
-            ld_global_if(v, t == 2u, a.xnew + ixr[u]);
+            if constexpr (CLU) ld_cross_if(v, t == 2u, ixr[u], a.xnew, prev_win);
+            else ld_global_if(v, t == 2u, a.xnew + ixr[u]);
             ready &= t == 3u || gs_published(v);
             xv[u] = t == 3u ? 0.0 : __longlong_as_double((long long)v);
           }
@@ -542,7 +607,8 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
       for (int u = 0; u < C; ++u) {
         ixr[u] = code[u] >> 2;
         gvr[u] = kSentinel;
-        ld_global_if(gvr[u], ((tmr >> (2 * u)) & 3u) == 2u, a.xnew + ixr[u]);
+        if constexpr (CLU) ld_cross_if(gvr[u], ((tmr >> (2 * u)) & 3u) == 2u, ixr[u], a.xnew, prev_win);
+        else ld_global_if(gvr[u], ((tmr >> (2 * u)) & 3u) == 2u, a.xnew + ixr[u]);
       }
     };
     auto wait_chunk = [&](int k) {
@@ -606,7 +672,8 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
                   const unsigned t = (tmr[s] >> (2 * u)) & 3u;
                   unsigned long long v = 0ull;
                   ld_shared_if(v, t == 1u, sbase + 8u * ixr[s][u]);
-                  ld_global_if(v, t == 2u, a.xnew + ixr[s][u]);
+                  if constexpr (CLU) ld_cross_if(v, t == 2u, ixr[s][u], a.xnew, prev_win);
+                  else ld_global_if(v, t == 2u, a.xnew + ixr[s][u]);
                   ready &= t == 0u || t == 3u || gs_published(v);
                   xv[kk][u] = __longlong_as_double((long long)v);
                 }

@@ -104,8 +104,11 @@ void set_kernel_attrs() {
   MVAMG_GS_ATTR_D(false, 1) MVAMG_GS_ATTR_D(false, 2) MVAMG_GS_ATTR_D(false, 4) MVAMG_GS_ATTR_D(false, 8)
 #undef MVAMG_GS_ATTR_D
 #undef MVAMG_GS_ATTR
-#define MVAMG_LEAN_ATTR(F, CC, RR, DD) \
-  ok &= cudaFuncSetAttribute(gs_lean_kernel<F, CC, RR, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) == cudaSuccess;
+#define MVAMG_LEAN_ATTR(F, CC, RR, DD)                                                                   \
+  ok &= cudaFuncSetAttribute(gs_lean_kernel<F, CC, RR, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) == \
+        cudaSuccess;                                                                                     \
+  ok &= cudaFuncSetAttribute(gs_lean_kernel<F, CC, RR, DD, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             maxsm) == cudaSuccess;
 #define MVAMG_LEAN_ATTR_C(F, RR, DD) MVAMG_LEAN_ATTR(F, 2, RR, DD) MVAMG_LEAN_ATTR(F, 4, RR, DD) MVAMG_LEAN_ATTR(F, 8, RR, DD)
   MVAMG_LEAN_ATTR_C(true, 8, 3) MVAMG_LEAN_ATTR_C(true, 8, 2) MVAMG_LEAN_ATTR_C(true, 4, 4) MVAMG_LEAN_ATTR_C(true, 2, 8) MVAMG_LEAN_ATTR_C(true, 1, 8)
   MVAMG_LEAN_ATTR_C(false, 8, 3) MVAMG_LEAN_ATTR_C(false, 8, 2) MVAMG_LEAN_ATTR_C(false, 4, 4) MVAMG_LEAN_ATTR_C(false, 2, 8) MVAMG_LEAN_ATTR_C(false, 1, 8)
@@ -235,6 +238,28 @@ int gs_blocks(const GsPlan& p, const GsList& ls) {
   return std::max(1, std::min(p.ntiles, per_sm * num_sms()));
 }
 
+// Lean-kernel launch, optionally as thread-block clusters of `cluster` CTAs.
+template <class Kern>
+void launch_lean_k(Kern k, int g, int threads, size_t smem, cudaStream_t s, const GsArgs& a, int cluster) {
+  if (cluster <= 1) {
+    k<<<g, threads, smem, s>>>(a);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(std::max(cluster, (g / cluster) * cluster));
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, a);
+}
+
 // One sweep: gs_prepare_kernel writes the right-hand side in (round, lane)
 // order (folding the backward sweep's old upper neighbours), fills x_new with
 // the sentinel and resets the ticket; gs_sweep_kernel then runs the schedule.
@@ -271,12 +296,12 @@ int launch_gs(bool fwd, const Csr& A, const GsList& ls, const GsPlan& p, const d
   a.debug = g_gs_debug;
   const int g = gs_blocks(p, ls);
   if (ls.lean_C > 0) {
-    const int lc = ls.lean_C & 0xff, lk = (ls.lean_C >> 8) & 0xff;
+    const int lc = ls.lean_C & 0xff, lk = (ls.lean_C >> 8) & 0xff, lcl = (ls.lean_C >> 16) & 0xff;
     if (lk > 1) {  // K rows per lane per round (C <= 4; (R, D, K) in {(2,2,4), (2,3,4), (4,2,2)})
 #define MVAMG_LEANK(F, RR, DD, KK)                                                \
   do {                                                                            \
-    if (lc <= 2) gs_lean_kernel<F, 2, RR, DD, KK><<<g, p.threads, smem, s>>>(a);  \
-    else gs_lean_kernel<F, 4, RR, DD, KK><<<g, p.threads, smem, s>>>(a);          \
+    if (lc <= 2) launch_lean_k(gs_lean_kernel<F, 2, RR, DD, KK>, g, p.threads, smem, s, a, 0); \
+    else launch_lean_k(gs_lean_kernel<F, 4, RR, DD, KK>, g, p.threads, smem, s, a, 0);         \
   } while (0)
 #define MVAMG_LEANK_F(F)                                                          \
   do {                                                                            \
@@ -290,7 +315,11 @@ int launch_gs(bool fwd, const Csr& A, const GsList& ls, const GsPlan& p, const d
       CUDA_TRY(cudaGetLastError());
       return 0;
     }
-#define MVAMG_LEAN(F, CC, RR, DD) gs_lean_kernel<F, CC, RR, DD><<<g, p.threads, smem, s>>>(a)
+#define MVAMG_LEAN(F, CC, RR, DD)                                                                   \
+  do {                                                                                             \
+    if (lcl > 1) launch_lean_k(gs_lean_kernel<F, CC, RR, DD, 1, true>, g, p.threads, smem, s, a, lcl); \
+    else launch_lean_k(gs_lean_kernel<F, CC, RR, DD, 1, false>, g, p.threads, smem, s, a, 0);         \
+  } while (0)
 #define MVAMG_LEAN_C(F, RR, DD)                                                   \
   do {                                                                            \
     if (lc <= 2) MVAMG_LEAN(F, 2, RR, DD);                                        \
@@ -1311,6 +1340,10 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
       mode > 2 || R < 1 || R > 31)
     return fail(MVAMG_E_ARG, "gs_schedule: bad arguments");
   if (n >= (1 << 29)) return fail(MVAMG_E_ARG, "gs_schedule: n >= 2^29 not encodable");
+  // rows_per_round: K | (cluster << 8); cluster > 1 marks sources in the previous
+  // tile of the same thread-block cluster (processing order) for DSMEM reads
+  const int cluster = (rows_per_round >> 8) & 0xff;
+  rows_per_round &= 0xff;
   const int K = rows_per_round < 1 ? 1 : rows_per_round;
   if (K > 8 || (K > 1 && uniform_S <= 0))
     return fail(MVAMG_E_ARG, "gs_schedule: rows_per_round 1..8, > 1 only with uniform (lean) records");
@@ -1330,6 +1363,10 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
   std::vector<int> chain_of(n > 0 ? n : 1);
   for (int c = 0; c < nch; ++c)
     for (int i = chain_ptr[c]; i < chain_ptr[c + 1]; ++i) chain_of[i] = c;
+  std::vector<int> tile_of_chain(nch > 0 ? nch : 1);
+  for (int t = 0; t < ntiles; ++t)
+    for (int c = tile_ptr[t]; c < tile_ptr[t + 1]; ++c) tile_of_chain[c] = t;
+  auto ptk = [&](int t) { return fwd ? t : ntiles - 1 - t; };  // processing order of tile t
   long long w = 0;
   int gr = 0, gw = 0, smax = 1;
   std::vector<int> rnd, slot_of, rows_of_round, cnt_of;
@@ -1430,7 +1467,18 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
                 if (slot >= window) return fail(MVAMG_E_ARG, "gs_schedule: window slot out of range");
                 code = (int)(slot << 2) | 1;
               } else {
-                code = (j << 2) | 2;
+                const int cj = chain_of[j], st = tile_of_chain[cj];
+                if (cluster > 1 && ptk(st) == ptk(t) - 1 && ptk(t) % cluster != 0) {
+                  // previous tile of the same cluster: its window slot, read over DSMEM
+                  const int sc0 = tile_ptr[st], sTS = ((tile_ptr[st + 1] - sc0 + 31) / 32) * 32;
+                  const int pos = fwd ? j - chain_ptr[cj] : chain_ptr[cj + 1] - 1 - j;
+                  const long long slot = (long long)pos * sTS + (cj - sc0);
+                  if (slot >= window || slot >= (long long)kGsRemote)
+                    return fail(MVAMG_E_ARG, "gs_schedule: remote window slot out of range");
+                  code = (int)((((unsigned)slot | kGsRemote) << 2) | 2u);
+                } else {
+                  code = (j << 2) | 2;
+                }
               }
               blk[(size_t)32 * (3 + 2 * cnt) + L] = dbits(data[k]);
               blk[(size_t)32 * (4 + 2 * cnt) + L] = (unsigned long long)(unsigned)code;

@@ -84,6 +84,8 @@ class GpuConfig:
                                     # than the wavefront on C2/C3, and the timing costs setup time)
     scan_cluster: int = 0           # CTAs of the cluster chain-scan sweep (window-mode levels; 0/1 = one CTA;
                                     # 8 measured 2.85 ms vs 2.1 ms one-CTA on C2, tools/scan_trace.py)
+    lean_cluster: int = 0           # wavefront tiles as thread-block clusters of this many CTAs (0: off);
+                                    # boundary values of the previous tile come over DSMEM, not L2
     level_reg: bool = False         # (with exact_gs False) single-CTA level sweeps with register-prefetched
                                     # entries (gs_level_reg_kernel; measured slower than the staged kernel)
     exact_gs: bool = False          # True: every GS kernel keeps the CSR-order subtractions (bit-exact with
@@ -297,10 +299,13 @@ class DeviceGsPlan:
                 C, K = p.lean_C & 0xFF, max(1, p.lean_C >> 8)
                 S = 3 + 2 * C
                 R, D = p.R, p.D
-                h = gs_schedule(self.A, p, m, R=R, uniform_S=S, K=K)
+                # thread-block-cluster tiles: sources in the previous tile of the same
+                # cluster are read over DSMEM (GpuConfig.lean_cluster; needs >= 2 tiles)
+                cl = int(self.cfg.lean_cluster) if (self.cfg.lean_cluster > 1 and p.ntiles > 1 and K == 1) else 0
+                h = gs_schedule(self.A, p, m, R=R, uniform_S=S, K=K | (cl << 8))
                 rec_words_max = R * 32 * K * S
                 slot_words = rec_words_max + R * 32 * K
-                lean = p.lean_C
+                lean = p.lean_C | (cl << 16)
             else:
                 # generic kernel: pick the deepest ring that fits beside the window
                 h = gs_schedule(self.A, p, m, R=1)

@@ -669,3 +669,28 @@ def test_fit_and_solve_medium_matches_oracle(mv, exact):
     _, hist, nit, conv = oracle_pcg(ref, b)
     assert conv and rep.converged and rep.iterations == nit
     assert np.max(np.abs(rep.residual_history - hist) / hist) <= 1e-10
+
+
+@pytest.mark.parametrize("cluster", [2, 4, 8])
+def test_gs_lean_cluster_tiles_bit_exact(mv, cluster):
+    """Wavefront tiles launched as thread-block clusters (GpuConfig.lean_cluster):
+    boundary sources in the previous tile of the same cluster come over DSMEM.
+    Still the serial loop bit for bit, forward from zero and backward from x_old,
+    with several tiles (32 chains per tile) on 5- and 9-point grids."""
+    from paper_1907_04417_b200 import problems
+    from paper_1907_04417_b200.device import DeviceGsPlan
+
+    cfg = mv.GpuConfig(max_threads=32, lean_cluster=cluster, exact_gs=True)
+    rng = np.random.default_rng(30 + cluster)
+    for name, A in (("lap2d", laplacian_2d(150)), ("q1", problems.anisotropic_q1(170)),
+                    ("lap2d_odd", laplacian_2d(77))):
+        gp = DeviceGsPlan(sp.csr_matrix(A), cfg)
+        assert gp.plan.ntiles >= 3 and gp.plan.lean_C > 0, name
+        n = A.shape[0]
+        b = rng.standard_normal(n)
+        x0 = rng.standard_normal(n)
+        for direction, zero in (("forward", True), ("backward", False)):
+            want = np.zeros(n) if zero else x0.copy()
+            oracle_gs(A, b, want, direction)
+            got = _gs_gpu(mv, A, b, x0, direction, zero, cfg)
+            assert np.array_equal(got, want), (name, direction, cluster)
