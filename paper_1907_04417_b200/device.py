@@ -84,6 +84,7 @@ class GpuConfig:
                                     # than the wavefront on C2/C3, and the timing costs setup time)
     scan_cluster: int = 0           # CTAs of the cluster chain-scan sweep (window-mode levels; 0/1 = one CTA;
                                     # 8 measured 2.85 ms vs 2.1 ms one-CTA on C2, tools/scan_trace.py)
+    lean_ring: tuple = None         # (R, D) of the lean kernel's record ring, overriding ring_bytes
     lean_cluster: int = 0           # wavefront tiles as thread-block clusters of this many CTAs (0: off);
                                     # boundary values of the previous tile come over DSMEM, not L2
     level_reg: bool = False         # (with exact_gs False) single-CTA level sweeps with register-prefetched
@@ -166,6 +167,9 @@ def _gs_ring(A, cfg):
                     return C | (K << 8), R, D, slot, S
             R, D = LEAN_K_RINGS[-1]
             return C | (K << 8), R, D, R * 32 * K * (S + 1), S
+        if cfg.lean_ring is not None:  # explicit (R, D) (diagnostics / clustered tiles)
+            R, D = cfg.lean_ring
+            return C, R, D, R * 32 * (S + 1), S
         for R, D in LEAN_RINGS:
             slot = R * 32 * (S + 1)
             if D * slot * 8 <= cfg.ring_bytes:
