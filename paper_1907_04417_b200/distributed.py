@@ -216,7 +216,11 @@ class Comm:
     torch.distributed (NCCL: device buffers directly; other backends: staged
     through host memory).  world_size 1 needs no process group."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, direct=None):
+        """direct: hand the arithmetic's tensors to the backend as they are (NCCL
+        with device buffers; default) or stage them through host memory (other
+        backends with device buffers).  The CPU tests use direct=True with gloo
+        and host tensors to run the NCCL code path."""
         import torch.distributed as dist
 
         self.dist = dist if dist.is_available() and dist.is_initialized() else None
@@ -227,9 +231,10 @@ class Comm:
             self.rank = dist.get_rank(group)
             self.size = dist.get_world_size(group)
             self.nccl = dist.get_backend(group) == "nccl"
+        self.direct = self.nccl if direct is None else bool(direct)
 
     def _stage(self, t):
-        return t if self.nccl else t.detach().to("cpu")
+        return t if self.direct else t.detach().to("cpu")
 
     def sendrecv(self, sends, recvs):
         """sends: [(peer, tensor)], recvs: [(peer, tensor)] -- one batch."""
@@ -240,7 +245,7 @@ class Comm:
         for q, t in sends:
             ops.append(dist.P2POp(dist.isend, self._stage(t).contiguous(), q, self.group))
         for q, t in recvs:
-            buf = t if self.nccl else t.new_empty(t.shape, device="cpu")
+            buf = t if self.direct else t.new_empty(t.shape, device="cpu")
             ops.append(dist.P2POp(dist.irecv, buf, q, self.group))
             back.append((t, buf))
         for req in dist.batch_isend_irecv(ops):
@@ -263,7 +268,7 @@ class Comm:
     def broadcast(self, t, root=0):
         if self.size == 1:
             return
-        if self.nccl:
+        if self.direct:
             self.dist.broadcast(t, root, group=self.group)
         else:
             buf = t.detach().to("cpu")

@@ -68,15 +68,16 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, direct=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from _dist_backend import OracleBackend
+        from paper_1907_04417_b200.distributed import Comm
 
         d = golden("c1")
         mats, pros = hierarchy(d, "mv")
-        s = DistributedSolver(mats, pros, backend=OracleBackend())
+        s = DistributedSolver(mats, pros, comm=Comm(direct=direct), backend=OracleBackend())
         op = s.op
         z = op.be.vec(op.n_own)
         op.apply(op.be.from_host(s.own_rows(d["b"])), z)
@@ -86,11 +87,13 @@ def _worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [1, 2, 3])
-def test_distributed_pcg_gloo(world):
+@pytest.mark.parametrize("world,direct", [(1, None), (2, None), (3, None), (2, True), (3, True)])
+def test_distributed_pcg_gloo(world, direct):
+    """direct=True hands the tensors to the backend unstaged -- the NCCL code
+    path (views of the extended vectors as receive buffers), run by gloo."""
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), out, direct), nprocs=world, join=True)
     d = golden("c1")
     mats, pros = hierarchy(d, "mv")
     ref = OracleOperator(mats, pros)
