@@ -560,10 +560,17 @@ def time_sweep(fn, reps=3):
 def autotune_coarse_gs(A, modes, cfg):
     """For a coarse level: per sweep mode, the faster of the dataflow row sweep
     and the level-set sweep, timed once on the device ({mode: schedule}).
-    Mode 2 is timed as the folded backward sweep it runs in a cycle."""
+    Mode 2 is timed as the folded backward sweep it runs in a cycle.
+
+    Only in exact mode: there every schedule gives the same bits.  With
+    tolerance parity the two kernels round differently, so a timing-based pick
+    could make two runs of the same problem differ; the row sweep (the faster
+    one on every C2/C3 coarse level above ~1k rows) is used."""
     torch = torch_cuda()
     n = A.shape[0]
     rows = {m: DeviceGsRows(A, m, cfg) for m in modes}
+    if not cfg.exact_gs:
+        return dict(rows)
     try:
         lvls = {m: DeviceGsLevels(A, m, cfg) for m in modes}
     except ValueError:
