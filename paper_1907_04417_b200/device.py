@@ -84,6 +84,7 @@ class GpuConfig:
                                     # than the wavefront on C2/C3, and the timing costs setup time)
     scan_cluster: int = 0           # CTAs of the cluster chain-scan sweep (window-mode levels; 0/1 = one CTA;
                                     # 8 measured 2.85 ms vs 2.1 ms one-CTA on C2, tools/scan_trace.py)
+    level_gs_small_rows: int = 2000  # tolerance parity: coarse levels up to this size use the level-set sweep
     lean_ring: tuple = None         # (R, D) of the lean kernel's record ring, overriding ring_bytes
     lean_cluster: int = 0           # wavefront tiles as thread-block clusters of this many CTAs (0: off);
                                     # boundary values of the previous tile come over DSMEM, not L2
@@ -564,13 +565,19 @@ def autotune_coarse_gs(A, modes, cfg):
 
     Only in exact mode: there every schedule gives the same bits.  With
     tolerance parity the two kernels round differently, so a timing-based pick
-    could make two runs of the same problem differ; the row sweep (the faster
-    one on every C2/C3 coarse level above ~1k rows) is used."""
+    could make two runs of the same problem differ.  There the choice is by
+    size: the single-CTA level-set sweep up to cfg.level_gs_small_rows rows
+    (faster on every C2/C3/composite level that small), the row sweep above."""
     torch = torch_cuda()
     n = A.shape[0]
-    rows = {m: DeviceGsRows(A, m, cfg) for m in modes}
     if not cfg.exact_gs:
-        return dict(rows)
+        if n <= cfg.level_gs_small_rows:
+            try:
+                return {m: DeviceGsLevels(A, m, cfg) for m in modes}
+            except ValueError:
+                pass
+        return {m: DeviceGsRows(A, m, cfg) for m in modes}
+    rows = {m: DeviceGsRows(A, m, cfg) for m in modes}
     try:
         lvls = {m: DeviceGsLevels(A, m, cfg) for m in modes}
     except ValueError:
