@@ -227,6 +227,15 @@ int mvamg_dot_ws_bytes(void);
  * (pkg/src/mvamg/_kernels.py:41-61): partner[v] = matched vertex or -1. */
 int mvamg_greedy_match(long long ne, const long long* ei, const long long* ej, int n, long long* partner,
                        long long* pair_i, long long* pair_j, long long* npairs);
+/* The same matching on the GPU (device pointers; A symmetric CSR, diag its
+ * diagonal, w the smooth vector): partner[v] = matched vertex or -1.  Rounds of
+ * best-edge picks with mutual picks matched (the locally dominant matching,
+ * equal to the greedy order's result; matching.cuh).  Edge weights are
+ * computed as pkg/src/mvamg/matching.py:99-102 with one rounding per operation.
+ * Synchronises `stream` once per round; *rounds_out = rounds. */
+int mvamg_greedy_match_device(int n, const int* indptr, const int* indices, const double* data,
+                              const double* diag, const double* w, double weight_floor, int* partner,
+                              int* rounds_out, void* stream);
 /* Batched one-sided Jacobi thin SVD of stacked row-major blocks
  * (pkg/src/mvamg/svd.py:17-55, _kernels.py:64-121): U (same layout as A) and
  * sigma (nblk x k, descending).  On non-convergence returns MVAMG_E_NOT_SPD

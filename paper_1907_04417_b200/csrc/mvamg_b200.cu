@@ -26,6 +26,7 @@
 #include "coarse_mega.cuh"
 #include "galerkin.cuh"
 #include "gs_scan.cuh"
+#include "matching.cuh"
 
 using namespace mvamg;
 
@@ -2457,6 +2458,40 @@ int mvamg_hierarchy_set_gs_scan(mvamg_hierarchy* h, int k, int mode, int nchains
  * sweeps fill with %globaltimer stamps (null: off). */
 int mvamg_gs_scan_set_trace(long long* trace_dev) {
   g_scan_trace = trace_dev;
+  return 0;
+}
+
+
+int mvamg_greedy_match_device(int n, const int* indptr, const int* indices, const double* data,
+                              const double* diag, const double* w, double weight_floor, int* partner,
+                              int* rounds_out, void* stream) {
+  using namespace matching;
+  if (n < 0 || (n > 0 && (!indptr || !indices || !data || !diag || !w || !partner)))
+    return fail(MVAMG_E_ARG, "greedy_match_device: bad arguments");
+  if (rounds_out) *rounds_out = 0;
+  if (n == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  DevTmp best(s), flag(s);
+  CUDA_TRY(best.alloc((size_t)n * 4));
+  CUDA_TRY(flag.alloc(16));
+  fill_int_kernel<<<grid_for(n), 256, 0, s>>>(n, partner, -1);
+  ++g_kernel_launches;
+  int rounds = 0;
+  for (;;) {
+    CUDA_TRY(cudaMemsetAsync(flag.p, 0, 4, s));
+    match_best_kernel<<<grid_for(n), 256, 0, s>>>(n, indptr, indices, data, diag, w, weight_floor, partner,
+                                                  best.get<int>());
+    match_pair_kernel<<<grid_for(n), 256, 0, s>>>(n, best.get<int>(), partner, flag.get<int>());
+    g_kernel_launches += 2;
+    CUDA_TRY(cudaGetLastError());
+    int changed = 0;
+    CUDA_TRY(cudaMemcpyAsync(&changed, flag.p, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    ++rounds;
+    if (!changed) break;
+    if (rounds > n + 1) return fail(MVAMG_E_STATE, "greedy_match_device: no progress");
+  }
+  if (rounds_out) *rounds_out = rounds;
   return 0;
 }
 

@@ -86,7 +86,10 @@ class MultiVectorAMG:
         A = _check_operator(A)
         w0 = np.ones(A.shape[0])
         if self.nsv == 1:
-            pairwise = build_pairwise_hierarchy(A, w0, self._coarsening(), product=coarse_product(self.config))
+            from .device import GpuConfig
+
+            pairwise = build_pairwise_hierarchy(A, w0, self._coarsening(), product=coarse_product(self.config),
+                                                device_matching=(self.config or GpuConfig()).device_matching)
             self.composite_ = None
             vectors = [w0]
         else:

@@ -132,6 +132,42 @@ def greedy_matching(i, j, c, n, weight_floor=WEIGHT_FLOOR):
     return pairs, np.flatnonzero(partner[:n] < 0).astype(np.int64)
 
 
+def greedy_matching_device(A, w, weight_floor=WEIGHT_FLOOR):
+    """edge_weights + greedy_matching on the GPU (mvamg_greedy_match_device:
+    locally dominant matching, equal to the greedy order's result).  Same
+    return value: pairs (i < j) in the greedy's acceptance order (weight
+    descending, ties by (i, j)), and the unmatched vertices ascending."""
+    from .device import ptr, stream_handle, to_device, torch_cuda
+
+    torch = torch_cuda()
+    w = np.asarray(w, dtype=np.float64)
+    if A.shape[0] != A.shape[1] or w.shape[0] != A.shape[0]:
+        raise ValueError("A must be square and w of matching length")
+    d = A.diagonal()
+    if np.any(d == 0.0):
+        raise NotSpdError("zero diagonal entry; edge weights are undefined")
+    n = A.shape[0]
+    dev = [to_device(A.indptr, np.int32), to_device(A.indices, np.int32), to_device(A.data, np.float64),
+           to_device(d, np.float64), to_device(w, np.float64)]
+    partner = torch.empty(max(1, n), dtype=torch.int32, device="cuda")
+    rounds = ctypes.c_int()
+    _lib.check(_lib.load().mvamg_greedy_match_device(n, *[ptr(t) for t in dev], float(weight_floor), ptr(partner),
+                                                     ctypes.byref(rounds), stream_handle()), "greedy_match_device")
+    part = partner.cpu().numpy()[:n].astype(np.int64)
+    i = np.flatnonzero(part > np.arange(n))
+    j = part[i]
+    if i.size:
+        # weights of the matched pairs, as edge_weights forms them, for the acceptance order
+        a = np.asarray(A[i, j]).ravel()
+        den = d[i] * w[i] ** 2 + d[j] * w[j] ** 2
+        c = 1.0 - 2.0 * a * w[i] * w[j] / den
+        order = np.lexsort((j, i, -c))
+        pairs = np.stack([i[order], j[order]], axis=1)
+    else:
+        pairs = np.empty((0, 2), dtype=np.int64)
+    return pairs, np.flatnonzero(part < 0).astype(np.int64)
+
+
 def pair_prolongator(A, w, pairs, unmatched):
     """Coarse prolongator of one pairwise step: matched pairs first (matching
     order), then singletons ascending; returns (P_c, aggregates)."""
@@ -216,7 +252,7 @@ def coarse_product(config=None):
     return galerkin_product_device if (config or GpuConfig()).device_galerkin else galerkin_product
 
 
-def pairwise_step(A, w, steps, weight_floor=WEIGHT_FLOOR, product=galerkin_product):
+def pairwise_step(A, w, steps, weight_floor=WEIGHT_FLOOR, product=galerkin_product, device_matching=False):
     """Compose `steps` matching sweeps into one transfer; returns
     (P, A_c, w_c, aggregates, stagnated, steps_done)."""
     if steps < 1:
@@ -224,8 +260,11 @@ def pairwise_step(A, w, steps, weight_floor=WEIGHT_FLOOR, product=galerkin_produ
     Ak, wk = A, np.asarray(w, dtype=np.float64)
     P, aggs, stagnated, done = None, None, False, 0
     for _ in range(steps):
-        i, j, c = edge_weights(Ak, wk)
-        pairs, unmatched = greedy_matching(i, j, c, Ak.shape[0], weight_floor)
+        if device_matching:
+            pairs, unmatched = greedy_matching_device(Ak, wk, weight_floor)
+        else:
+            i, j, c = edge_weights(Ak, wk)
+            pairs, unmatched = greedy_matching(i, j, c, Ak.shape[0], weight_floor)
         if pairs.shape[0] == 0:
             stagnated = True
             break
@@ -245,7 +284,7 @@ def pairwise_step(A, w, steps, weight_floor=WEIGHT_FLOOR, product=galerkin_produ
     return P, Ak, wk, aggs, stagnated, done
 
 
-def build_pairwise_hierarchy(A, w, params=None, product=galerkin_product):
+def build_pairwise_hierarchy(A, w, params=None, product=galerkin_product, device_matching=False):
     """Coarsen (A, w) until small; a level shrinking by < min_shrink is
     dropped; no pairs at the finest level raises CoarseningStagnationError."""
     params = params or CoarseningParams()
@@ -258,7 +297,7 @@ def build_pairwise_hierarchy(A, w, params=None, product=galerkin_product):
     while levels[-1].A.shape[0] > params.min_coarse_size and len(levels) < params.max_levels:
         cur = levels[-1]
         P, Ac, wc, aggs, stagnated, done = pairwise_step(cur.A, cur.w, params.steps_per_level,
-                                                         params.weight_floor, product)
+                                                         params.weight_floor, product, device_matching)
         if done == 0:
             if len(levels) == 1:
                 raise CoarseningStagnationError("matching produced no pairs at the finest level", level=0)
@@ -477,7 +516,8 @@ def bootstrap_run(A, w0=None, params=None, config=None):
         t0 = time.perf_counter()
         try:
             hier = build_pairwise_hierarchy(A, comp.smooth_vectors[-1], params.coarsening,
-                                            product=coarse_product(config))
+                                            product=coarse_product(config),
+                                            device_matching=config.device_matching)
         except CoarseningStagnationError:
             if stagnated_before or comp.n_components == 0:
                 raise

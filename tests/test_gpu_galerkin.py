@@ -71,3 +71,46 @@ def test_galerkin_full_size_c2():
     G = galerkin_product_device(P, A, timing=t)
     assert same_csr(G, galerkin_product(P, A))
     assert t["total_ms"] > 0
+
+
+def _host_matching(A, w):
+    from paper_1907_04417_b200.setup import edge_weights, greedy_matching
+
+    i, j, c = edge_weights(A, w)
+    return greedy_matching(i, j, c, A.shape[0])
+
+
+def test_device_matching_equals_greedy():
+    """The GPU locally dominant matching gives the reference greedy's pairs, in
+    its acceptance order, and its unmatched set (matching.py:78-122), on the
+    golden hierarchies' levels with smooth vectors, random weights, ties
+    (constant weights on a uniform grid) and C2's fine operator."""
+    from _fixtures import laplacian_2d
+    from paper_1907_04417_b200.setup import greedy_matching_device
+
+    rng = np.random.default_rng(5)
+    cases = []
+    for name, P, A, _ in golden_levels():
+        cases.append((name, A, rng.uniform(0.5, 1.5, A.shape[0])))
+    cases.append(("lap2d_ties", laplacian_2d(40), np.ones(1600)))
+    cases.append(("q1_smooth", problems.anisotropic_q1(64), np.cos(np.arange(64 * 64) / 300.0)))
+    cases.append(("c2_fine", problems.anisotropic_q1(1024), rng.standard_normal(1024 * 1024)))
+    for name, A, w in cases:
+        A = sp.csr_matrix(A)
+        p_h, u_h = _host_matching(A, w)
+        p_d, u_d = greedy_matching_device(A, w)
+        assert np.array_equal(p_h, p_d), name
+        assert np.array_equal(u_h, u_d), name
+
+
+def test_fit_with_device_matching_is_identical():
+    """A whole fit with the device matching gives the same hierarchy as with
+    the host greedy (elasticity 64^2: four bootstrap stages)."""
+    import paper_1907_04417_b200 as mv
+
+    A = problems.elasticity_q1(64)
+    e1 = mv.MultiVectorAMG(config=mv.GpuConfig(device_matching=True)).fit(A)
+    e0 = mv.MultiVectorAMG(config=mv.GpuConfig(device_matching=False)).fit(A)
+    for M0, M1 in zip(e0.hierarchy_.matrices, e1.hierarchy_.matrices):
+        assert same_csr(M0, M1)
+    assert len(e0.hierarchy_.matrices) == len(e1.hierarchy_.matrices)
