@@ -86,8 +86,48 @@ def load_workload(name):
     desc = (spec["desc"] + "; rhs " + ("body load + seeded noise" if name == "c4" else "U[-1,1] seed 0")
             + ", x0=0, rtol 1e-6; hierarchy = MultiVectorAMG() defaults fitted on the box (setup untimed)")
     comps = [(c.operator.matrices, c.operator.prolongators) for c in est.composite_.components]
+    svd_case = (est.hierarchy_.aggregate_sets, est.hierarchy_.vectors_per_level)
     return mats, pros, b, desc, {"fit_s": fit_s, "bootstrap_stages": est.composite_.n_components,
-                                  "operator_complexity": est.operator_complexity_, "components": comps}
+                                  "operator_complexity": est.operator_complexity_, "components": comps,
+                                  "svd_case": svd_case}
+
+
+def svd_timing(aggregate_sets, vectors_per_level):
+    """Batched one-sided Jacobi SVD of every multi-vector aggregate block
+    (mvamg_jacobi_svd_batch_device, one thread per aggregate) against the host
+    C++ restatement, on the blocks the fit factored.  Device time includes the
+    blocks' host->device copy and the U/sigma copy back (what the setup pays)."""
+    import ctypes
+
+    import torch
+
+    from paper_1907_04417_b200 import _lib
+    from paper_1907_04417_b200.setup import SVD_MAX_SWEEPS, SVD_PAIR_TOL, _jacobi_svd_device
+
+    levels = []
+    for k, aggs in enumerate(aggregate_sets):
+        V = np.column_stack(vectors_per_level[k])
+        local = np.ascontiguousarray(V[aggs.members])
+        rp = np.ascontiguousarray(aggs.ptr, dtype=np.int32)
+        nv = local.shape[1]
+        _jacobi_svd_device(rp, local, nv)  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        code_d, Ud, sd, _ = _jacobi_svd_device(rp, local, nv)
+        t_dev = time.perf_counter() - t0
+        Uh, sh = np.empty_like(local), np.empty((aggs.n_agg, nv))
+        failed = ctypes.c_int(-1)
+        vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        t0 = time.perf_counter()
+        code_h = _lib.load().mvamg_jacobi_svd_batch(aggs.n_agg, vp(rp), nv, vp(local), SVD_MAX_SWEEPS, SVD_PAIR_TOL,
+                                                    vp(Uh), vp(sh), ctypes.byref(failed))
+        t_host = time.perf_counter() - t0
+        same = bool(code_d == code_h == 0 and np.array_equal(Ud.view(np.int64), Uh.view(np.int64))
+                    and np.array_equal(sd.view(np.int64), sh.view(np.int64)))
+        levels.append({"level": k, "aggregates": int(aggs.n_agg), "rows": int(local.shape[0]), "k": int(nv),
+                       "device_ms": t_dev * 1e3, "host_ms": t_host * 1e3, "bit_exact": same})
+    return {"what": "per-aggregate one-sided Jacobi SVD (csrc/svd.cuh, incl. copies) vs the host C++ "
+                    "restatement on one core", "levels": levels}
 
 
 # -------------------------------------------------------------------- clocks --
@@ -557,6 +597,10 @@ def run_b200(args, world, rank, local):
         out["galerkin"] = {"what": "A_c = (G + G')/2, G = P'(A P) per hierarchy level, device kernels "
                                    "(csrc/galerkin.cuh) vs the reference's scipy recipe on one host core",
                            "levels": levels}
+    # ---- setup: the per-aggregate local SVDs of this hierarchy on the device
+    # (svd.py:17-55, bit-identical) against the host restatement, one core ----
+    if rank == 0 and not args.no_galerkin and info.get("svd_case"):
+        out["svd"] = svd_timing(*info["svd_case"])
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb, cnit = cpu_baseline(mats, pros, b, nit_hint=n_iters)
         cb["nit"] = cnit

@@ -242,6 +242,12 @@ int mvamg_greedy_match_device(int n, const int* indptr, const int* indices, cons
  * with *failed_block set (SvdConvergenceError in the Python layer). */
 int mvamg_jacobi_svd_batch(int nblk, const int* row_ptr, int k, const double* A, int max_sweeps,
                            double tol, double* U, double* sigma, int* failed_block);
+/* The same batched SVD on the GPU (device pointers row_ptr, A, U, sigma; k <= 16;
+ * one thread per block, svd.cuh): U and sigma bit-identical to
+ * mvamg_jacobi_svd_batch.  *failed_block (host) = the smallest non-converged
+ * block, as the host loop reports the first.  Synchronises `stream` once. */
+int mvamg_jacobi_svd_batch_device(int nblk, const int* row_ptr, int k, const double* A, int max_sweeps,
+                                  double tol, double* U, double* sigma, int* failed_block, void* stream);
 
 /* ---- row-partitioned solve: halo packing, Krylov updates -- */
 /* dst[i] = src[idx[i]] (pack a halo message) / dst[idx[i]] = src[i] (unpack). */

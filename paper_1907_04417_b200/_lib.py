@@ -88,6 +88,7 @@ SIGNATURES = [
     ("mvamg_hierarchy_set_gs_scan", _I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _I] + [_P] * 9),
     ("mvamg_gs_scan_set_trace", _I, [_P]),
     ("mvamg_greedy_match_device", _I, [_I, _P, _P, _P, _P, _P, _D, _P, _PI, _P]),
+    ("mvamg_jacobi_svd_batch_device", _I, [_I, _P, _I, _P, _I, _D, _P, _P, _PI, _P]),
     ("mvamg_gather_f64", _I, [_I, _P, _P, _P, _P]),
     ("mvamg_scatter_f64", _I, [_I, _P, _P, _P, _P]),
     ("mvamg_axpy_f64", _I, [_I, _D, _P, _P, _P]),

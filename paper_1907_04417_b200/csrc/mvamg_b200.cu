@@ -27,6 +27,7 @@
 #include "galerkin.cuh"
 #include "gs_scan.cuh"
 #include "matching.cuh"
+#include "svd.cuh"
 
 using namespace mvamg;
 
@@ -2492,6 +2493,32 @@ int mvamg_greedy_match_device(int n, const int* indptr, const int* indices, cons
     if (rounds > n + 1) return fail(MVAMG_E_STATE, "greedy_match_device: no progress");
   }
   if (rounds_out) *rounds_out = rounds;
+  return 0;
+}
+
+int mvamg_jacobi_svd_batch_device(int nblk, const int* row_ptr, int k, const double* A, int max_sweeps,
+                                  double tol, double* U, double* sigma, int* failed_block, void* stream) {
+  // mvamg_jacobi_svd_batch on the GPU (svd.cuh): device pointers, bit-identical U and sigma.
+  if (nblk < 0 || k < 1 || k > svd::kMaxCols || (nblk > 0 && (!row_ptr || !A || !U || !sigma)))
+    return fail(MVAMG_E_ARG, "jacobi_svd_batch_device: bad arguments (k must be 1..16)");
+  if (failed_block) *failed_block = -1;
+  if (nblk == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  DevTmp status(s);
+  CUDA_TRY(status.alloc(8));
+  matching::fill_int_kernel<<<1, 32, 0, s>>>(2, status.get<int>(), 0x7fffffff);
+  svd::jacobi_svd_kernel<<<(nblk + 63) / 64, 64, 0, s>>>(nblk, row_ptr, k, A, max_sweeps, tol, U, sigma,
+                                                         status.get<int>());
+  g_kernel_launches += 2;
+  CUDA_TRY(cudaGetLastError());
+  int st[2];
+  CUDA_TRY(cudaMemcpyAsync(st, status.p, 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (st[1] != 0x7fffffff && st[1] < st[0]) return fail(MVAMG_E_ARG, "jacobi_svd_batch_device: empty block");
+  if (st[0] != 0x7fffffff) {
+    if (failed_block) *failed_block = st[0];
+    return fail(MVAMG_E_NOT_SPD, "Jacobi SVD did not converge");
+  }
   return 0;
 }
 

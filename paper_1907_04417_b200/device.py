@@ -80,6 +80,7 @@ class GpuConfig:
     row_gs_ctas: int = 0            # resident CTAs of the row sweep (0 = auto)
     device_galerkin: bool = True    # setup forms P'AP with the device kernel (bit-identical to scipy's)
     device_matching: bool = True    # setup matches with the device kernel (identical pairs and order)
+    device_svd: bool = True         # setup's local SVDs on the device kernel (bit-identical U, sigma)
     scan_gs: bool = False           # (with exact_gs False) time the chain-scan sweep on chain-structured levels
                                     # at upload and keep it when faster (off: single-SM issue-bound, slower
                                     # than the wavefront on C2/C3, and the timing costs setup time)

@@ -10,7 +10,7 @@ import numpy as np
 
 from .composite import DeviceANorm
 from .cycles import CycleSpec, GpuMultigridOperator
-from .device import to_device
+from .device import GpuConfig, to_device
 from .krylov import pcg
 from .setup import (BootstrapParams, CoarseningParams, bootstrap_run, build_multivector_hierarchy, coarse_product,
                     build_pairwise_hierarchy, operator_complexity)
@@ -43,6 +43,11 @@ def _check_vector(x, n=None, name="vector"):
         raise ValueError(f"{name} contains NaN or Inf entries")
     return x
 
+
+
+def _device_svd(config):
+    """Whether the multi-vector setup runs its local SVDs on the GPU."""
+    return (config or GpuConfig()).device_svd
 
 class MultiVectorAMG:
     """AMG preconditioner folding adaptively generated smooth vectors into one
@@ -101,7 +106,8 @@ class MultiVectorAMG:
             vectors = self.composite_.smooth_vectors[:n_use]
         self.hierarchy_ = build_multivector_hierarchy(A, pairwise, vectors, merge_levels=self.merge_levels,
                                                       tol=self.svd_tol, min_coarse_size=self.min_coarse_size,
-                                                      product=coarse_product(self.config))
+                                                      product=coarse_product(self.config),
+                                                      device_svd=_device_svd(self.config))
         self.operator_ = GpuMultigridOperator(self.hierarchy_.matrices, self.hierarchy_.prolongator_matrices,
                                               cycle=CycleSpec("V"), config=self.config)
         self.smooth_vectors_ = vectors

@@ -359,8 +359,28 @@ def merge_aggregate_levels(hierarchy, merge_levels=3):
     return [merged] + per[merge_levels:]
 
 
-def block_prolongator(aggs, vectors, n_fine, tol=0.1):
-    """Per-aggregate truncated SVD bases (one-sided Jacobi), block diagonal."""
+def _jacobi_svd_device(rp, local, nv):
+    """mvamg_jacobi_svd_batch_device: the batched local SVD on the GPU
+    (csrc/svd.cuh), bit-identical to the host mvamg_jacobi_svd_batch."""
+    from .device import ptr, stream_handle, to_device, torch_cuda
+
+    torch = torch_cuda()
+    n_agg = rp.shape[0] - 1
+    d_rp, d_local = to_device(rp, np.int32), to_device(local, np.float64)
+    d_u = torch.empty(max(1, local.size), dtype=torch.float64, device="cuda")
+    d_sig = torch.empty(max(1, n_agg * nv), dtype=torch.float64, device="cuda")
+    failed = ctypes.c_int(-1)
+    code = _lib.load().mvamg_jacobi_svd_batch_device(n_agg, ptr(d_rp), nv, ptr(d_local), SVD_MAX_SWEEPS,
+                                                     SVD_PAIR_TOL, ptr(d_u), ptr(d_sig), ctypes.byref(failed),
+                                                     stream_handle())
+    U = d_u.cpu().numpy()[:local.size].reshape(local.shape)
+    sig = d_sig.cpu().numpy()[:n_agg * nv].reshape(n_agg, nv)
+    return code, U, sig, failed.value
+
+
+def block_prolongator(aggs, vectors, n_fine, tol=0.1, device_svd=False):
+    """Per-aggregate truncated SVD bases (one-sided Jacobi), block diagonal.
+    device_svd: the SVD runs on the GPU (same U and sigma bit for bit)."""
     V = np.column_stack([np.asarray(v, dtype=np.float64) for v in vectors])
     if V.shape[0] != aggs.n_prev:
         raise ValueError("vector length does not match the aggregate set")
@@ -369,15 +389,19 @@ def block_prolongator(aggs, vectors, n_fine, tol=0.1):
     if np.any(sizes < 1):
         raise ValueError("empty aggregate")
     local = np.ascontiguousarray(V[aggs.members])            # stacked blocks, row-major
-    U = np.empty_like(local)
-    sig = np.empty((aggs.n_agg, nv))
     rp = np.ascontiguousarray(aggs.ptr, dtype=np.int32)
-    failed = ctypes.c_int(-1)
-    vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
-    code = _lib.load().mvamg_jacobi_svd_batch(aggs.n_agg, vp(rp), nv, vp(local), SVD_MAX_SWEEPS, SVD_PAIR_TOL,
-                                              vp(U), vp(sig), ctypes.byref(failed))
+    if device_svd:
+        code, U, sig, failed_id = _jacobi_svd_device(rp, local, nv)
+    else:
+        U = np.empty_like(local)
+        sig = np.empty((aggs.n_agg, nv))
+        failed = ctypes.c_int(-1)
+        vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        code = _lib.load().mvamg_jacobi_svd_batch(aggs.n_agg, vp(rp), nv, vp(local), SVD_MAX_SWEEPS, SVD_PAIR_TOL,
+                                                  vp(U), vp(sig), ctypes.byref(failed))
+        failed_id = failed.value
     if code == _lib.E_NOT_SPD:
-        raise SvdConvergenceError(f"local SVD failed on aggregate {failed.value}", aggregate_id=failed.value)
+        raise SvdConvergenceError(f"local SVD failed on aggregate {failed_id}", aggregate_id=failed_id)
     _lib.check(code, "jacobi_svd_batch")
     tol_a = tol * sizes / n_fine
     floor = sig[:, 0] * 50.0 * np.maximum(sizes, nv) * np.finfo(np.float64).eps
@@ -402,7 +426,7 @@ def block_prolongator(aggs, vectors, n_fine, tol=0.1):
 
 
 def build_multivector_hierarchy(A, pairwise, vectors, merge_levels=3, tol=0.1, min_coarse_size=40,
-                                product=galerkin_product):
+                                product=galerkin_product, device_svd=False):
     """The single multi-vector hierarchy from a pairwise substrate and the
     finest-level smooth vectors (pkg/src/mvamg/multivector.py:262-321)."""
     t0 = time.perf_counter()
@@ -418,7 +442,7 @@ def build_multivector_hierarchy(A, pairwise, vectors, merge_levels=3, tol=0.1, m
         if mats[-1].shape[0] <= min_coarse_size:
             break
         ts = time.perf_counter()
-        bp = block_prolongator(aggs, vecs[-1], n_fine, tol)
+        bp = block_prolongator(aggs, vecs[-1], n_fine, tol, device_svd)
         svd_s += time.perf_counter() - ts
         if bp.P.shape[1] >= mats[-1].shape[0]:
             stalled = True
