@@ -112,3 +112,20 @@ def test_no_cpu_fallback():
     A = laplacian_2d(4)
     with pytest.raises(DeviceError):
         GpuMultigridOperator([A], [])
+
+
+def test_setup_device_kernels_no_cpu_fallback():
+    """The setup's device matching and device SVD fail loudly without a GPU
+    (the host restatements run only when the GpuConfig asks for them)."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1907_04417_b200 import DeviceError
+    from paper_1907_04417_b200.setup import _jacobi_svd_device, greedy_matching_device
+
+    with pytest.raises(DeviceError):
+        _jacobi_svd_device(np.array([0, 2], dtype=np.int32), np.ones((2, 3)), 3)
+    A = laplacian_2d(4)
+    with pytest.raises(DeviceError):
+        greedy_matching_device(A, np.ones(A.shape[0]))
