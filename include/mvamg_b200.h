@@ -88,6 +88,13 @@ int mvamg_csr_residual_f64(int n, const int* indptr, const int* indices, const d
 /* y = y + (A x)  (cycles.py:170, prolongation; sum formed first). */
 int mvamg_csr_spmv_add_f64(int n, const int* indptr, const int* indices, const double* data,
                            const double* x, double* y, void* stream);
+/* The three SpMV forms with the matrix's nnz (mode 0: y = A x, 1: y = b - A x,
+ * 2: y = y + A x; sparse.py:30-40, cycles.py:156,170).  Knowing nnz, small
+ * matrices with long rows (n <= 65,536, >= 4 entries per row on average, the
+ * cycle's coarse levels) run one warp per row: a row's products are formed in
+ * parallel and added in CSR order, bit-identical to the forms above. */
+int mvamg_csr_spmv_mode_f64(int mode, int n, int nnz, const int* indptr, const int* indices, const double* data,
+                            const double* x, const double* b, double* y, void* stream);
 /* GS static round schedule (host).  For sweep `mode` (0 forward from x = 0,
  * 1 forward from a nonzero guess, 2 backward) and the chains / tiles of
  * mvamg_gs_analyse, assigns every row a round inside its warp (one more than

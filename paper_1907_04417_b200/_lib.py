@@ -40,6 +40,7 @@ SIGNATURES = [
     ("mvamg_gs_analyse", _I, [_I, _P, _P, _I, _I, _I, _PI, _PI, _P, _P, _PI, _PI, _PI]),
     ("mvamg_csr_spmv_f64", _I, [_I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_csr_residual_f64", _I, [_I, _P, _P, _P, _P, _P, _P, _P]),
+    ("mvamg_csr_spmv_mode_f64", _I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
     ("mvamg_csr_spmv_add_f64", _I, [_I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_gs_schedule", _I, [_I, _P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _I, ctypes.POINTER(_LL), _PI, _PI,
                                _PI, _P, _P, _P, _P, _P]),

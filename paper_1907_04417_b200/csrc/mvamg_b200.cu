@@ -87,6 +87,8 @@ inline int grid_for(int n, int threads = 256, int per_sm = 8) {
 }
 
 inline int dot_grid(int n) { return std::min(grid_for(n, 256, 8), kDotMaxBlocks); }
+constexpr int kWarpRowMaxRows = 65536;  // levels up to this size with >= kWarpRowMinAvg entries per row
+constexpr int kWarpRowMinAvg = 4;       //   run their SpMVs one warp per row
 
 bool g_attr_done = false;
 int g_max_dyn_smem = 48 * 1024;
@@ -207,8 +209,21 @@ struct Smoother {
 };
 
 // ---- raw launches ----------------------------------------------------------
+// small levels with long rows: one warp per row (bit-identical, see spmv_warp_kernel)
+inline bool warp_rows(const Csr& A) {
+  return A.n > 0 && A.n <= kWarpRowMaxRows && (long long)A.nnz >= (long long)kWarpRowMinAvg * A.n;
+}
+
 int launch_spmv(int mode, const Csr& A, const double* x, const double* b, double* y, cudaStream_t s) {
   if (A.n == 0) return 0;
+  if (warp_rows(A)) {
+    const int gw = std::max(1, std::min((A.n + 7) / 8, num_sms() * 8));
+    if (mode == 0) spmv_warp_kernel<0><<<gw, 256, 0, s>>>(A.n, A.ip, A.ix, A.v, x, b, y);
+    else if (mode == 1) spmv_warp_kernel<1><<<gw, 256, 0, s>>>(A.n, A.ip, A.ix, A.v, x, b, y);
+    else spmv_warp_kernel<2><<<gw, 256, 0, s>>>(A.n, A.ip, A.ix, A.v, x, b, y);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
   int g = grid_for(A.n);
   if (mode == 0) spmv_kernel<0><<<g, 256, 0, s>>>(A.n, A.ip, A.ix, A.v, x, b, y);
   else if (mode == 1) spmv_kernel<1><<<g, 256, 0, s>>>(A.n, A.ip, A.ix, A.v, x, b, y);
@@ -806,8 +821,12 @@ struct mvamg_hierarchy {
                                                 POST_FCG_BETA, ctx(l.fs));
       }
       fcg_p_kernel<<<g, 256, 0, s>>>(n, p, z, l.fp[cur ^ 1], l.fs, it == 0);
-      spmv_dot_kernel<<<dot_grid(n), 256, 0, s>>>(n, l.A.ip, l.A.ix, l.A.v, p, l.fr, ap,
-                                                  POST_FCG_ALPHA, ctx(l.fs));
+      if (warp_rows(l.A))
+        spmv_dot_warp_kernel<<<std::min((n + 7) / 8, kDotMaxBlocks), 256, 0, s>>>(
+            n, l.A.ip, l.A.ix, l.A.v, p, l.fr, ap, POST_FCG_ALPHA, ctx(l.fs));
+      else
+        spmv_dot_kernel<<<dot_grid(n), 256, 0, s>>>(n, l.A.ip, l.A.ix, l.A.v, p, l.fr, ap,
+                                                    POST_FCG_ALPHA, ctx(l.fs));
       fcg_xr_kernel<<<g, 256, 0, s>>>(n, l.fx, l.fr, p, ap, l.fs, it == 0);
       cur ^= 1;
     }
@@ -1317,6 +1336,14 @@ int mvamg_csr_spmv_f64(int n, const int* indptr, const int* indices, const doubl
   Csr A;
   A.n = n; A.ip = indptr; A.ix = indices; A.v = data;
   return launch_spmv(0, A, x, nullptr, y, (cudaStream_t)stream);
+}
+
+int mvamg_csr_spmv_mode_f64(int mode, int n, int nnz, const int* indptr, const int* indices, const double* data,
+                            const double* x, const double* b, double* y, void* stream) {
+  if (mode < 0 || mode > 2 || n < 0 || nnz < 0) return fail(MVAMG_E_ARG, "csr_spmv_mode: bad arguments");
+  Csr A;
+  A.n = n; A.m = n; A.nnz = nnz; A.ip = indptr; A.ix = indices; A.v = data;
+  return launch_spmv(mode, A, x, b, y, (cudaStream_t)stream);
 }
 
 int mvamg_csr_residual_f64(int n, const int* indptr, const int* indices, const double* data,

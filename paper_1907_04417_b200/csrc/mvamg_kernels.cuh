@@ -122,6 +122,46 @@ __global__ void __launch_bounds__(256) spmv_kernel(int n, const int* __restrict_
   }
 }
 
+// The same SpMV family, one warp per row, for small levels with long rows (the
+// K-cycle's coarse levels: a few thousand rows of 10-70 entries).  One thread
+// per row walks its row with ~2 dependent L2 trips per unrolled batch of
+// entries, which dominates there.  Here the lanes load a 32-entry chunk of the
+// row and form the products a_k * x_k (each its own rounding) at once; every
+// lane then adds the chunk's products in CSR order from shuffles, starting
+// from 0.0 as scipy does, so the sum is bit-identical to spmv_kernel's.
+template <int MODE>
+__device__ __forceinline__ double warp_row_sum(int i, const int* __restrict__ ip, const int* __restrict__ ix,
+                                               const double* __restrict__ v, const double* __restrict__ x,
+                                               int lane) {
+  const int k0 = __ldg(ip + i), k1 = __ldg(ip + i + 1);
+  double s = 0.0;
+  for (int c = k0; c < k1; c += 32) {
+    const int k = c + lane, m = min(32, k1 - c);
+    double pr = 0.0;
+    if (k < k1) pr = __dmul_rn(__ldg(v + k), __ldg(x + __ldg(ix + k)));
+    for (int t = 0; t < m; ++t) s = __dadd_rn(s, __shfl_sync(0xffffffffu, pr, t));
+  }
+  return s;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) spmv_warp_kernel(int n, const int* __restrict__ ip,
+                                                        const int* __restrict__ ix,
+                                                        const double* __restrict__ v,
+                                                        const double* __restrict__ x,
+                                                        const double* __restrict__ b, double* y) {
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = w0; i < n; i += nw) {
+    const double s = warp_row_sum<MODE>(i, ip, ix, v, x, lane);
+    if (lane == 0) {
+      if (MODE == 0) y[i] = s;
+      else if (MODE == 1) y[i] = __dsub_rn(__ldg(b + i), s);
+      else y[i] = __dadd_rn(y[i], s);
+    }
+  }
+}
+
 // Weighted Jacobi, out of place: y = x + ((omega*(b - Ax))/d)   (cycles.py:148)
 __global__ void __launch_bounds__(256) jacobi_kernel(int n, const int* __restrict__ ip,
                                                      const int* __restrict__ ix,
@@ -317,6 +357,30 @@ __global__ void __launch_bounds__(256) spmv_dot_kernel(int n, const int* __restr
     double pi = p[i];
     d1 = fma(pi, s, d1);
     if (r) d2 = fma(pi, r[i], d2);
+  }
+  block_sum2(d1, d2);
+  grid_finish(op, d1, d2, c);
+}
+
+// spmv_dot_kernel with one warp per row (spmv_warp_kernel's bit-identical y);
+// lane 0 of each warp accumulates the dots over its rows.
+__global__ void __launch_bounds__(256) spmv_dot_warp_kernel(int n, const int* __restrict__ ip,
+                                                            const int* __restrict__ ix,
+                                                            const double* __restrict__ v,
+                                                            const double* __restrict__ p,
+                                                            const double* __restrict__ r, double* y,
+                                                            int op, ReduceCtx c) {
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  double d1 = 0.0, d2 = 0.0;
+  for (int i = w0; i < n; i += nw) {
+    const double s = warp_row_sum<0>(i, ip, ix, v, p, lane);
+    if (lane == 0) {
+      y[i] = s;
+      const double pi = p[i];
+      d1 = fma(pi, s, d1);
+      if (r) d2 = fma(pi, r[i], d2);
+    }
   }
   block_sum2(d1, d2);
   grid_finish(op, d1, d2, c);

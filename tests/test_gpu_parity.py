@@ -110,6 +110,43 @@ def test_spmv_bit_exact(mv, c1):
         assert np.array_equal(_spmv_gpu(A, x, 2, y=y), y + oracle_spmv(A, x))
 
 
+def _spmv_mode_gpu(A, x, mode, b=None, y=None):
+    import torch
+    from paper_1907_04417_b200 import _lib
+    from paper_1907_04417_b200.device import DeviceCSR, ptr, stream_handle
+
+    dA = DeviceCSR(A)
+    out = _dev(y) if mode == 2 else torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+    bd = _dev(b) if b is not None else _dev(np.zeros(1))
+    _lib.check(_lib.load().mvamg_csr_spmv_mode_f64(mode, A.shape[0], int(A.nnz), *dA.ptrs(), ptr(_dev(x)), ptr(bd),
+                                                   ptr(out), stream_handle()))
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("n,avg", [(300, 9), (5000, 40), (20000, 70), (65536, 12), (70000, 12), (5000, 3)])
+def test_spmv_warp_rows_bit_exact(n, avg):
+    """The one-warp-per-row SpMV (small levels with long rows; rows longer than
+    a warp, empty rows, cancellations to -0.0) equals the sequential CSR-order
+    sum bit for bit in all three forms; sizes on both sides of the cut-over."""
+    rng = np.random.default_rng(n + avg)
+    lens = rng.poisson(avg, n)
+    lens[::97] = 0
+    lens[1::89] = 3 * avg + 40
+    ip = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=ip[1:])
+    ix = np.concatenate([np.sort(rng.choice(n, size=min(k, n), replace=False)) for k in lens]).astype(np.int32)
+    v = rng.standard_normal(ix.shape[0])
+    v[::13] = -0.0
+    A = sp.csr_matrix((v, ix, ip[:len(ip)]), shape=(n, n))
+    x = rng.standard_normal(n)
+    x[::7] = 0.0
+    b, y = rng.standard_normal(n), rng.standard_normal(n)
+    want = oracle_spmv(A, x)
+    assert np.array_equal(_spmv_mode_gpu(A, x, 0).view(np.int64), want.view(np.int64))
+    assert np.array_equal(_spmv_mode_gpu(A, x, 1, b=b), b - want)
+    assert np.array_equal(_spmv_mode_gpu(A, x, 2, y=y), y + want)
+
+
 def test_gs_golden_bit_exact(mv, c1):
     d, mats = c1[0], c1[1]
     A = mats[0]
