@@ -860,6 +860,40 @@ __global__ void __launch_bounds__(256) gs_prepare_kernel(int n, const int* __res
   if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0;
 }
 
+// gs_prepare_kernel's backward fold with one warp per row (small levels with
+// long rows, as spmv_warp_kernel): the lanes form the products of a 32-entry
+// chunk of the row's j < i entries at once, then every lane subtracts them in
+// CSR order from shuffles -- the same roundings in the same order.
+__global__ void __launch_bounds__(256) gs_prepare_fold_warp_kernel(int n, const int* __restrict__ ip,
+                                                                   const int* __restrict__ ix,
+                                                                   const double* __restrict__ v,
+                                                                   const double* __restrict__ b,
+                                                                   const double* __restrict__ xold,
+                                                                   const int* __restrict__ perm, double* tperm,
+                                                                   double* xnew, int* ticket) {
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = w0; i < n; i += nw) {
+    double s = __ldg(b + i);
+    const int k0 = __ldg(ip + i), k1 = __ldg(ip + i + 1);
+    for (int c = k0; c < k1; c += 32) {
+      const int k = c + lane;
+      const int j = k < k1 ? __ldg(ix + k) : 0x7fffffff;
+      const bool lower = j < i;
+      double pr = 0.0;
+      if (lower) pr = __dmul_rn(__ldg(v + k), __ldg(xold + j));
+      const int m = __popc(__ballot_sync(0xffffffffu, lower));  // sorted row: the lower entries lead
+      for (int t = 0; t < m; ++t) s = __dsub_rn(s, __shfl_sync(0xffffffffu, pr, t));
+      if (m < 32) break;
+    }
+    if (lane == 0) {
+      tperm[__ldg(perm + i)] = s;
+      reinterpret_cast<unsigned long long*>(xnew)[i] = kSentinel;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0;
+}
+
 }  // namespace mvamg
 
 namespace mvamg {

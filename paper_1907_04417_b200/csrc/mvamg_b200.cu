@@ -214,6 +214,19 @@ inline bool warp_rows(const Csr& A) {
   return A.n > 0 && A.n <= kWarpRowMaxRows && (long long)A.nnz >= (long long)kWarpRowMinAvg * A.n;
 }
 
+// GS preparation (gs_prepare_kernel); the backward fold of a small long-row
+// level runs one warp per row (bit-identical)
+void launch_prepare(const Csr& A, const double* b, const double* xold, const int* perm, double* tperm,
+                    double* xnew, int* ticket, int fold, cudaStream_t s) {
+  const int n = A.n;
+  if (fold && warp_rows(A)) {
+    const int gw = std::max(1, std::min((n + 7) / 8, num_sms() * 8));
+    gs_prepare_fold_warp_kernel<<<gw, 256, 0, s>>>(n, A.ip, A.ix, A.v, b, xold, perm, tperm, xnew, ticket);
+  } else {
+    gs_prepare_kernel<<<grid_for(n), 256, 0, s>>>(n, A.ip, A.ix, A.v, b, xold, perm, tperm, xnew, ticket, fold);
+  }
+}
+
 int launch_spmv(int mode, const Csr& A, const double* x, const double* b, double* y, cudaStream_t s) {
   if (A.n == 0) return 0;
   if (warp_rows(A)) {
@@ -290,8 +303,7 @@ int launch_gs(bool fwd, const Csr& A, const GsList& ls, const GsPlan& p, const d
   if (smem > (size_t)g_max_dyn_smem)
     return fail(MVAMG_E_ARG, "gs: shared memory plan of " + std::to_string(smem) + " bytes exceeds the limit");
   const int fold = (!fwd && xold != nullptr) ? 1 : 0;
-  gs_prepare_kernel<<<grid_for(n), 256, 0, s>>>(n, A.ip, A.ix, A.v, b, xold, ls.perm, ls.tperm, xnew,
-                                                ticket, fold);
+  launch_prepare(A, b, xold, ls.perm, ls.tperm, xnew, ticket, fold, s);
   GsArgs a;
   a.n = n;
   a.ntiles = p.ntiles;
@@ -411,8 +423,7 @@ int launch_gs_levels(const Csr& A, const GsLevels& g, bool zero, const double* b
   // right-hand side in the schedule's row layout; a backward sweep from a
   // nonzero guess folds its old upper neighbours here and then runs the
   // zero-guess schedule (only new values are read during the sweep)
-  gs_prepare_kernel<<<grid_for(n), 256, 0, s>>>(n, A.ip, A.ix, A.v, b, xold, g.perm, g.tperm, xnew,
-                                                ticket, fold ? 1 : 0);
+  launch_prepare(A, b, xold, g.perm, g.tperm, xnew, ticket, fold ? 1 : 0, s);
   GsLevelArgs a;
   a.n = n;
   a.nlev = g.nlev;
@@ -625,8 +636,7 @@ int launch_gs_rows(const Csr& A, const GsRows& g, const double* b, const double*
   }
   const size_t smem = (size_t)g.max_tile_slots * 384;
   if (smem > (size_t)g_max_dyn_smem) return fail(MVAMG_E_ARG, "gs rows: tile slices exceed shared memory");
-  gs_prepare_kernel<<<grid_for(n), 256, 0, s>>>(n, A.ip, A.ix, A.v, b, xold, g.perm, g.tperm, xnew,
-                                                ticket, fold ? 1 : 0);
+  launch_prepare(A, b, xold, g.perm, g.tperm, xnew, ticket, fold ? 1 : 0, s);
   GsRowArgs a;
   a.n = n;
   a.ntiles = (n + g.threads - 1) / g.threads;
