@@ -2,14 +2,17 @@
 from the committed ncu launch list summary (cold-cache, serialised launches)
 and the fitted hierarchy's sizes in the committed bench line:
 
-  python tools/kernel_gbs.py > profiles/r01c_c2_kernel_gbs.txt
+  python tools/kernel_gbs.py [launch_summary.txt] [bench_line.json] > profiles/r01c_c2_kernel_gbs.txt
 """
 import json
 import os
 import re
+import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-bench = json.load(open(os.path.join(ROOT, "profiles", "r01c_bench_c2.json")))
+SUMMARY = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles", "r01b_c2_launches_summary.txt")
+BENCH = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "profiles", "r01c_bench_c2.json")
+bench = json.loads(open(BENCH).read().strip().splitlines()[-1])
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6518.0
 n = bench["config"]["levels"]
@@ -28,7 +31,7 @@ def ab(nnz, rows):
 B = {
     "gs_lean fwd (level 0, from x=0)": ab(nnzA[0], n[0]) + 24 * n[0],
     "gs_lean bwd (level 0, from x)": ab(nnzA[0], n[0]) + 32 * n[0],
-    "gs_row (levels 1..L-1, both sweeps)": sum(2 * ab(nnzA[k], n[k]) + 56 * n[k] for k in range(1, L)),
+    "coarse sweeps, row + level-set (L1..)": sum(2 * ab(nnzA[k], n[k]) + 56 * n[k] for k in range(1, L)),
     "gs_prepare (all levels, both sweeps)": sum(28 * n[k] * 2 + 6 * nnzA[k] + 8 * n[k] for k in range(L)),
     "spmv<1> residual": sum(ab(nnzA[k], n[k]) + 24 * n[k] for k in range(L)),
     "spmv<0> restriction": sum(ab(nnzP[k], n[k + 1]) + 8 * n[k] + 8 * n[k + 1] for k in range(L)),
@@ -38,26 +41,35 @@ B = {
     "pcg_xr + dot2 + pcg_p": (32 + 16 + 24) * n[0],
 }
 # kernel time per solve from the launch list summary
-summ = open(os.path.join(ROOT, "profiles", "r01b_c2_launches_summary.txt")).read()
+summ = open(SUMMARY).read()
 T = {}
 for line in summ.splitlines():
     m = re.match(r"\s*([\d.]+)%\s+(\d+)\s+([\d.]+)\s+(\S.*)$", line)
     if m:
         T[m.group(4).strip()] = int(m.group(2)) * float(m.group(3)) * 1e-6
+
+
+def tt(*names):
+    return sum(T.get(x, 0.0) for x in names)
+
+
+lean = sorted(x for x in T if x.startswith("gs_lean_kernel"))
 t = {
-    "gs_lean fwd (level 0, from x=0)": T["gs_lean_kernel<0, 4, 8, 2, 1>"],
-    "gs_lean bwd (level 0, from x)": T["gs_lean_kernel<1, 4, 8, 2, 1>"],
-    "gs_row (levels 1..L-1, both sweeps)": T["gs_row_kernel<0>"],
-    "gs_prepare (all levels, both sweeps)": T["gs_prepare_kernel"],
-    "spmv<1> residual": T["spmv_kernel<1>"],
-    "spmv<0> restriction": T["spmv_kernel<0>"],
-    "spmv<2> prolongation": T["spmv_kernel<2>"],
+    "gs_lean fwd (level 0, from x=0)": T[lean[0]],
+    "gs_lean bwd (level 0, from x)": T[lean[1]],
+    "coarse sweeps, row + level-set (L1..)": tt("gs_row_kernel<0>", "gs_row_kernel<false>",
+                                             "gs_level_kernel<0, 1>", "gs_level_kernel<false, 1>",
+                                             "gs_level_kernel<0, 2>", "gs_level_kernel<false, 2>"),
+    "gs_prepare (all levels, both sweeps)": tt("gs_prepare_kernel", "gs_prepare_fold_warp_kernel"),
+    "spmv<1> residual": tt("spmv_kernel<1>", "spmv_warp_kernel<1>"),
+    "spmv<0> restriction": tt("spmv_kernel<0>", "spmv_warp_kernel<0>"),
+    "spmv<2> prolongation": tt("spmv_kernel<2>", "spmv_warp_kernel<2>"),
     "spmv_dot (PCG A p)": T["spmv_dot_kernel"],
     "gemv (coarsest inverse)": T["gemv_kernel"],
-    "pcg_xr + dot2 + pcg_p": T["pcg_xr_kernel"] + T["dot2_kernel"] + T["pcg_p_kernel"],
+    "pcg_xr + dot2 + pcg_p": tt("pcg_xr_kernel", "dot2_kernel", "pcg_p_kernel"),
 }
 print(f"# C2 H1 solve, {nit} PCG iterations; levels {n}; peak {peak:.0f} GB/s (MEASURED_PEAKS.json copy)")
-print("# time: ncu launch list (profiles/r01b_c2_launches_summary.txt, cold cache, serialised);")
+print(f"# time: ncu launch list ({os.path.relpath(SUMMARY, ROOT)}, cold cache, serialised);")
 print("# bytes: SURVEY 8(d) model per kernel family (A_k: 12 nnz + 4 (n+1); vectors 8 B/entry)")
 print(f"{'kernel family':40s} {'MB/iter':>9} {'ms/solve':>9} {'GB/s':>8} {'% peak':>7}")
 tot_b = tot_t = 0.0
