@@ -2145,6 +2145,9 @@ int mvamg_hierarchy_set_transfer(mvamg_hierarchy* h, int k, const int* p_indptr,
   Level& l = h->lv[k];
   l.P.n = l.A.n; l.P.m = h->lv[k + 1].A.n; l.P.ip = p_indptr; l.P.ix = p_indices; l.P.v = p_data;
   l.R.n = h->lv[k + 1].A.n; l.R.m = l.A.n; l.R.ip = r_indptr; l.R.ix = r_indices; l.R.v = r_data;
+  // entry counts (one small read each, at setup): they pick the warp-per-row SpMV on small levels
+  CUDA_TRY(cudaMemcpy(&l.P.nnz, p_indptr + l.P.n, sizeof(int), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(&l.R.nnz, r_indptr + l.R.n, sizeof(int), cudaMemcpyDeviceToHost));
   return 0;
 }
 
