@@ -43,22 +43,52 @@ def parse_args():
     p.add_argument("--steps", type=int, default=None)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--config", default=os.environ.get("MVAMG_BENCH_CONFIG", "c2"))
+    p.add_argument("--config", default=os.environ.get("MVAMG_BENCH_CONFIG", "c3"))
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-h2", action="store_true", help="skip the H2 (composite-preconditioned) solve")
-    p.add_argument("--no-galerkin", action="store_true", help="skip the setup Galerkin-product timing")
+    p.add_argument("--setup-legs", action="store_true", help="also time the setup's device Galerkin products")
     return p.parse_args()
 
 
 # ----------------------------------------------------------------- workloads --
-def load_workload(name):
-    """(matrices, prolongators, b, description, info) for a bench configuration.
+L2_NOTE = {"c1": "flushed (256 MiB write) before every timed step"}
 
-    c1 uses the hierarchy the reference itself built (golden fixture); c2-c4
-    generate the BASELINE.json problem (paper_1907_04417_b200.problems) and
-    fit it with MultiVectorAMG() defaults -- the setup restatement that is
-    bit-exact with the reference's on every configuration it can run here
-    (tests/test_setup.py) -- outside any timed region."""
+
+def workload_config(name):
+    """The `config` both arms print: workload keys only (driver compares them)."""
+    from paper_1907_04417_b200 import problems
+
+    spec = problems.CONFIGS[name]
+    rhs = "body load + seeded noise" if name == "c4" else "U[-1,1] seed 0"
+    desc = (spec["desc"] + f"; rhs {rhs}, x0=0, rtol 1e-6; hierarchy = MultiVectorAMG() defaults "
+            "(bootstrap nsv=5, reference parameters), fitted untimed")
+    if name == "c1":
+        desc = ("C1: 2D Poisson 5-point 128x128 (n=16,384), rhs U[-1,1] seed 0, x0=0, rtol 1e-6; "
+                "hierarchy = the reference's own MultiVectorAMG() fit (golden fixture)")
+    return {"workload": desc, "l2": L2_NOTE.get(name, "inputs larger than L2 (no flush needed)")}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown CPU"
+
+
+def load_workload(name, setup="gpu", log=None):
+    """(matrices, prolongators, b, info) for a bench configuration.
+
+    c1: the hierarchy the reference itself built (golden fixture).  c2-c5: the
+    BASELINE.json problem (paper_1907_04417_b200.problems) fitted with the
+    reference's MultiVectorAMG() defaults.  The fitted hierarchy (plus the
+    bootstrap components for H2) is cached (paper_1907_04417_b200.hcache), so
+    both arms solve the same file when run back to back: the reference arm
+    fits on host cores only (setup="host": oracle/host_setup.py, no GPU
+    library in the process), the B200 arm reads the cache or, absent it, fits
+    with this repo's GPU setup.  Setup is never timed."""
     name = name.lower()
     if name == "c1":
         sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -66,68 +96,43 @@ def load_workload(name):
 
         d = golden("c1")
         mats, pros = hierarchy(d, "mv")
-        desc = ("C1: 2D Poisson 5-point 128x128 (n=16,384), rhs U[-1,1] seed 0, x0=0, rtol 1e-6; "
-                "hierarchy = reference MultiVectorAMG() defaults (golden fixture)")
         comps = [hierarchy(d, f"c{c}", fine=mats[0]) for c in range(int(d["n_comp"]))]
-        return mats, pros, d["b"], desc, {"fit_s": None, "components": comps}
-    from paper_1907_04417_b200 import problems
-    from paper_1907_04417_b200.estimator import MultiVectorAMG
+        return mats, pros, d["b"], {"fit_s": None, "components": comps, "hierarchy": "reference golden fixture"}
+    from paper_1907_04417_b200 import hcache, problems
 
-    if name not in ("c2", "c3", "c4", "c5"):
+    if name not in problems.CONFIGS:
         raise SystemExit(f"unknown --config {name!r}")
-    spec = problems.CONFIGS[name]
-    A = spec["build"]()
+    A = problems.CONFIGS[name]["build"]()
     b = problems.elasticity_rhs(A) if name == "c4" else problems.rhs_uniform(A.shape[0], 0)
+    key = hcache.key(name, A, b, {"estimator": "MultiVectorAMG()"})
+    hit = hcache.load(key)
+    if hit is not None:
+        mats, pros, comps, meta = hit
+        return mats, pros, b, {"fit_s": meta.get("fit_s"), "components": comps, "cache": key,
+                               "hierarchy": f"cache {key} ({meta.get('setup')})",
+                               "bootstrap_stages": len(comps)}
     t0 = time.perf_counter()
-    est = MultiVectorAMG().fit(A)
+    if setup == "host":
+        from oracle.host_setup import fit_host
+
+        mats, pros, info = fit_host(A, log=log)
+        comps = info["components"]
+        how = "CPU-only setup (oracle/host_setup.py, reference algorithm on host cores)"
+    else:
+        from paper_1907_04417_b200.estimator import MultiVectorAMG
+
+        est = MultiVectorAMG().fit(A)
+        mats = list(est.hierarchy_.matrices)
+        pros = list(est.hierarchy_.prolongator_matrices)
+        comps = [(list(c.operator.matrices), list(c.operator.prolongators)) for c in est.composite_.components]
+        how = "GPU setup (MultiVectorAMG.fit)"
     fit_s = time.perf_counter() - t0
-    mats = list(est.hierarchy_.matrices)
-    pros = list(est.hierarchy_.prolongator_matrices)
-    desc = (spec["desc"] + "; rhs " + ("body load + seeded noise" if name == "c4" else "U[-1,1] seed 0")
-            + ", x0=0, rtol 1e-6; hierarchy = MultiVectorAMG() defaults fitted on the box (setup untimed)")
-    comps = [(c.operator.matrices, c.operator.prolongators) for c in est.composite_.components]
-    svd_case = (est.hierarchy_.aggregate_sets, est.hierarchy_.vectors_per_level)
-    return mats, pros, b, desc, {"fit_s": fit_s, "bootstrap_stages": est.composite_.n_components,
-                                  "operator_complexity": est.operator_complexity_, "components": comps,
-                                  "svd_case": svd_case}
-
-
-def svd_timing(aggregate_sets, vectors_per_level):
-    """Batched one-sided Jacobi SVD of every multi-vector aggregate block
-    (mvamg_jacobi_svd_batch_device, one thread per aggregate) against the host
-    C++ restatement, on the blocks the fit factored.  Device time includes the
-    blocks' host->device copy and the U/sigma copy back (what the setup pays)."""
-    import ctypes
-
-    import torch
-
-    from paper_1907_04417_b200 import _lib
-    from paper_1907_04417_b200.setup import SVD_MAX_SWEEPS, SVD_PAIR_TOL, _jacobi_svd_device
-
-    levels = []
-    for k, aggs in enumerate(aggregate_sets):
-        V = np.column_stack(vectors_per_level[k])
-        local = np.ascontiguousarray(V[aggs.members])
-        rp = np.ascontiguousarray(aggs.ptr, dtype=np.int32)
-        nv = local.shape[1]
-        _jacobi_svd_device(rp, local, nv)  # warm-up
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        code_d, Ud, sd, _ = _jacobi_svd_device(rp, local, nv)
-        t_dev = time.perf_counter() - t0
-        Uh, sh = np.empty_like(local), np.empty((aggs.n_agg, nv))
-        failed = ctypes.c_int(-1)
-        vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
-        t0 = time.perf_counter()
-        code_h = _lib.load().mvamg_jacobi_svd_batch(aggs.n_agg, vp(rp), nv, vp(local), SVD_MAX_SWEEPS, SVD_PAIR_TOL,
-                                                    vp(Uh), vp(sh), ctypes.byref(failed))
-        t_host = time.perf_counter() - t0
-        same = bool(code_d == code_h == 0 and np.array_equal(Ud.view(np.int64), Uh.view(np.int64))
-                    and np.array_equal(sd.view(np.int64), sh.view(np.int64)))
-        levels.append({"level": k, "aggregates": int(aggs.n_agg), "rows": int(local.shape[0]), "k": int(nv),
-                       "device_ms": t_dev * 1e3, "host_ms": t_host * 1e3, "bit_exact": same})
-    return {"what": "per-aggregate one-sided Jacobi SVD (csrc/svd.cuh, incl. copies) vs the host C++ "
-                    "restatement on one core", "levels": levels}
+    try:
+        hcache.save(key, mats, pros, comps, {"setup": how, "fit_s": fit_s})
+    except OSError:
+        pass
+    return mats, pros, b, {"fit_s": fit_s, "components": comps, "cache": key, "hierarchy": how,
+                           "bootstrap_stages": len(comps)}
 
 
 # -------------------------------------------------------------------- clocks --
@@ -191,101 +196,105 @@ def dist_setup():
     return world, rank, local
 
 
-def _oracle_rate(op, b, probe_iters=4):
-    """Seconds per PCG iteration of the CPU oracle (a short unconverged run)."""
-    from oracle.oracle import oracle_pcg
-
-    t0 = time.perf_counter()
-    _, _, nit, _ = oracle_pcg(op, b, rtol=1e-300, itmax=probe_iters)
-    return (time.perf_counter() - t0) / max(1, nit)
+def _threads():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
 
 
-def cpu_baseline(mats, pros, b, budget_s=30.0, nit_hint=None):
-    """The CPU oracle (oracle/, plain-C restatement of the reference solve) on
-    one host core: full solves when one fits the budget, one full solve when it
-    takes under ~4 budgets, else a bounded run of PCG iterations scaled to the
-    iteration count of the GPU solve (nit_hint; identical by the parity tests)."""
-    from oracle.oracle import OracleOperator, oracle_pcg
+def cpu_baseline(mats, pros, b, threads, budget_s=30.0, nit_hint=None):
+    """The CPU oracle (oracle/: plain-C restatement of the reference solve) on
+    `threads` host threads (rows / elements / dots split over OpenMP threads,
+    the Gauss-Seidel sweeps serial as in the reference; results independent
+    of the thread count).  Full PCG solves while they fit the budget (at least
+    one); a solve longer than 4 budgets is sampled: the first iterations are
+    timed and scaled to nit_hint (said so in `sample`)."""
+    from oracle.oracle import OracleOperator, oracle_pcg, set_threads
 
+    used = set_threads(threads)
     op = OracleOperator(mats, pros)
-    per_it = _oracle_rate(op, b)
-    if per_it * 200 <= budget_s:
-        times, nit = [], 0
-        while not times or (sum(times) < budget_s / 2 and len(times) < 20):
-            t0 = time.perf_counter()
-            _, _, nit, _ = oracle_pcg(op, b, rtol=1e-6)
-            times.append(time.perf_counter() - t0)
-        return {"value": statistics.median(times), "unit": "s", "cores": 1, "kind": "port",
-                "sample": f"{len(times)} full PCG solves (nit={nit}) of the same workload, median; "
-                          "oracle/mvamg_oracle.c is single-threaded like the reference solve"}, nit
-    if nit_hint and per_it * nit_hint > 4 * budget_s:
-        k = max(2, int(2 * budget_s / per_it))
+    t0 = time.perf_counter()
+    _, _, k, _ = oracle_pcg(op, b, rtol=1e-300, itmax=3)
+    per_it = (time.perf_counter() - t0) / max(1, k)
+    est = per_it * (nit_hint or 100)
+    if est > 4 * budget_s and nit_hint:
+        k = max(3, int(2 * budget_s / per_it))
         t0 = time.perf_counter()
         oracle_pcg(op, b, rtol=1e-300, itmax=k)
         t = (time.perf_counter() - t0) / k * nit_hint
-        return {"value": t, "unit": "s", "cores": 1, "kind": "port",
-                "sample": f"{k} PCG iterations of the same workload timed and scaled to the solve's "
-                          f"nit={nit_hint}; oracle/mvamg_oracle.c is single-threaded like the reference solve"}, nit_hint
-    t0 = time.perf_counter()
-    _, _, nit, conv = oracle_pcg(op, b, rtol=1e-6)
-    t = time.perf_counter() - t0
-    return {"value": t, "unit": "s", "cores": 1, "kind": "port",
-            "sample": f"1 full PCG solve (nit={nit}, converged={conv}) of the same workload; "
-                      "oracle/mvamg_oracle.c is single-threaded like the reference solve"}, nit
+        return {"value": t, "unit": "s", "cores": used, "kind": "port",
+                "sample": f"{k} PCG iterations of the same solve timed and scaled to its nit={nit_hint} "
+                          f"(a full solve would take ~{est:.0f} s); oracle/mvamg_oracle.c on {used} thread(s) "
+                          f"of {cpu_model()}"}, nit_hint
+    times, nit = [], 0
+    while not times or (sum(times) < budget_s and len(times) < 10):
+        t0 = time.perf_counter()
+        _, _, nit, conv = oracle_pcg(op, b, rtol=1e-6)
+        times.append(time.perf_counter() - t0)
+    return {"value": statistics.median(times), "unit": "s", "cores": used, "kind": "port",
+            "sample": f"{len(times)} full PCG solves (nit={nit}) of the same workload on the same hierarchy, "
+                      f"median; oracle/mvamg_oracle.c on {used} thread(s) of {cpu_model()} (SpMV / vector "
+                      "work threaded, Gauss-Seidel serial as in the reference)"}, nit
 
 
 def run_reference(args, world, rank):
-    """The reference's solve path on host cores: the CPU oracle (the reference
-    algorithm restated in C, oracle/), single-threaded like the reference's
-    numba/scipy solve.  Each timed step is a bounded sample -- a fixed number of
-    PCG iterations of the same solve -- and the value is scaled to the full
-    solve's iteration count (measured once, untimed, by one full solve)."""
+    """The reference's solve path on the box's host cores: the CPU oracle (the
+    reference algorithm restated in C, oracle/) with every host thread, on a
+    hierarchy fitted on host cores only (oracle/host_setup.py) -- this process
+    never loads libmvamg_b200.so.  Every timed step is one FULL PCG solve
+    (x0 = 0, rtol 1e-6), wall clock, after W warm-up solves."""
     if rank != 0:
         return
-    mats, pros, b, desc, info = load_workload(args.config)
-    steps = args.steps if args.steps is not None else 10
-    from oracle.oracle import OracleOperator, oracle_pcg
+    from oracle.oracle import OracleOperator, oracle_pcg, set_threads
 
+    threads = set_threads(_threads())
+    name = args.config.lower()
+    mats, pros, b, info = load_workload(name, setup="host")
+    steps = args.steps if args.steps is not None else 10
     op = OracleOperator(mats, pros)
-    t0 = time.perf_counter()
-    _, hist, nit, conv = oracle_pcg(op, b, rtol=1e-6)
-    t_full = time.perf_counter() - t0
-    per_it = t_full / max(1, nit)
-    sample_iters = max(1, min(nit, int(round(3.0 / max(per_it, 1e-9)))))
-    for _ in range(max(0, args.warmup)):
-        oracle_pcg(op, b, rtol=1e-300, itmax=sample_iters)
+    for _ in range(max(1, args.warmup)):
+        _, hist, nit, conv = oracle_pcg(op, b, rtol=1e-6)
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
-        _, _, k, _ = oracle_pcg(op, b, rtol=1e-300, itmax=sample_iters)
-        times.append((time.perf_counter() - t0) / max(1, k))
-    v = statistics.mean(times) * nit
-    sample = (f"each step = the first {sample_iters} PCG iterations of the solve (bounded sample), scaled to the "
-              f"full solve's nit={nit}; one untimed full solve took {t_full:.3f} s")
+        _, hist, nit, conv = oracle_pcg(op, b, rtol=1e-6)
+        times.append(time.perf_counter() - t0)
+    v = statistics.mean(times)
+    try:  # this arm must not have mapped the repo's GPU library
+        mapped = [ln for ln in open("/proc/self/maps") if "libmvamg_b200" in ln]
+    except OSError:
+        mapped = []
+    if mapped:
+        raise SystemExit("reference arm loaded libmvamg_b200.so")
+    sample = (f"each step = one full PCG solve (nit={nit}, converged={conv}) of the workload, wall clock; "
+              f"oracle/mvamg_oracle.c on {threads} thread(s) of {cpu_model()} (SpMV / vector work threaded, "
+              "Gauss-Seidel serial as in the reference)")
     out = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": 0,
-        "steps": steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+        "steps": steps, "warmup": max(1, args.warmup), "ms_per_step": v * 1e3, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "n": mats[0].shape[0], "nit": nit, "converged": bool(conv),
-                   "fit_s": info.get("fit_s")},
-        "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port", "sample": sample},
+        "config": workload_config(name),
+        "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "details": {"nit": nit, "converged": bool(conv), "n": int(mats[0].shape[0]),
+                    "levels": [int(M.shape[0]) for M in mats], "hierarchy": info.get("hierarchy"),
+                    "fit_s": info.get("fit_s"), "min_s": min(times), "max_s": max(times),
+                    "final_relres": float(hist[-1] / hist[0])},
     }
     print(json.dumps(out), flush=True)
 
 
-def measured_traffic(config, kernel):
-    """DRAM bytes (read + write) per launch of the roofline kernel from the
-    committed ncu --set full capture of this configuration, else None."""
+def measured_traffic(config, kernel, level, sweep):
+    """DRAM bytes (read + write) per launch of the roofline kernel, from the
+    committed ncu --set full capture of exactly this kernel on this
+    configuration (profiles/traffic.json, keyed "<kernel>|L<level>|<fwd|bwd>"),
+    else None."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         table = json.load(open(path))
     except (OSError, ValueError):
         return None
-    for key, ent in table.get(config.lower(), {}).items():
-        if kernel.startswith(key):
-            return ent.get("dram_bytes")
-    return None
+    key = f"{kernel}|L{level}|{'fwd' if sweep.startswith('forward') else 'bwd'}"
+    ent = table.get(config.lower(), {}).get(key)
+    return None if ent is None else ent.get("dram_bytes")
 
 
 def run_distributed(args, world, rank, local):
@@ -304,10 +313,10 @@ def run_distributed(args, world, rank, local):
     dist = replicas.init(backend, torch.device("cuda", local))
     obj = [None]
     if rank == 0:
-        mats, pros, b, desc, info = load_workload(args.config)
-        obj[0] = (mats, pros, b, desc, info.get("fit_s"), info.get("bootstrap_stages"))
+        mats, pros, b, info = load_workload(args.config, setup="gpu")
+        obj[0] = (mats, pros, b, info.get("fit_s"), info.get("bootstrap_stages"), info.get("hierarchy"))
     dist.broadcast_object_list(obj, src=0)
-    mats, pros, b, desc, fit_s, stages = obj[0]
+    mats, pros, b, fit_s, stages, hsrc = obj[0]
     n = mats[0].shape[0]
     solver = DistributedSolver(mats, pros, comm=Comm())
     op = solver.op
@@ -355,12 +364,11 @@ def run_distributed(args, world, rank, local):
             "metric": METRIC, "value": t_solve, "unit": "s", "n_gpus": world, "steps": steps, "warmup": warm,
             "ms_per_step": t_solve * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "n": n, "nnz": int(mats[0].nnz), "levels": [M.shape[0] for M in mats],
-                       "nit": rep.iterations, "converged": bool(rep.converged), "true_relres": relres,
-                       "fit_s": fit_s, "bootstrap_stages": stages, "l2": "inputs larger than L2",
-                       "parallelism": f"row-partitioned fine level over {world} GPUs (nnz-balanced blocks, "
-                                      f"halo exchange, exact-order GS relay); coarse levels on GPU 0",
-                       "comm_backend": backend},
+            "config": workload_config(args.config.lower()),
+            "details": {"n": n, "nnz": int(mats[0].nnz), "levels": [M.shape[0] for M in mats],
+                        "nit": rep.iterations, "converged": bool(rep.converged), "true_relres": relres,
+                        "fit_s": fit_s, "bootstrap_stages": stages, "hierarchy": hsrc,
+                        "parallelism": replicas.parallelism(world), "comm_backend": backend},
             "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": 8 * n // world,
                     "d2h_bytes_per_step": 8 * n // world},
             "gpu_launches": int(round(launches.value / steps)),
@@ -377,6 +385,48 @@ def _lib_load():
     return _lib.load()
 
 
+def _level_sweeps(op, k, b_dev, x_old, x_new, ws, s):
+    """(forward-from-zero, backward-from-x_old) sweep callables of level k,
+    whatever schedule the upload picked (lean wavefront / row sweep / level set)."""
+    lv = op.level_dev[k]
+    if lv.get("gs") is not None:
+        gp = lv["gs"]
+        name = "gs_lean_kernel" if gp.plan.lean_C else "gs_sweep_kernel"
+        return ((lambda: gp.sweep(0, b_dev, None, x_new, ws, s)), (lambda: gp.sweep(1, b_dev, x_old, x_new, ws, s)),
+                name, name)
+    fwd = bwd = None
+    names = ["", ""]
+    rows, levels = lv.get("rows") or {}, lv.get("levels") or {}
+    if 0 in rows:
+        fwd, names[0] = (lambda: rows[0].sweep(b_dev, None, x_new, ws, s)), "gs_row_kernel"
+    elif 0 in levels:
+        fwd, names[0] = (lambda: levels[0].sweep(b_dev, None, x_new, ws, s)), "gs_level_kernel"
+    if 2 in rows:
+        bwd, names[1] = (lambda: rows[2].sweep(b_dev, x_old, x_new, ws, s)), "gs_row_kernel"
+    elif 2 in levels:
+        bwd, names[1] = (lambda: levels[2].sweep(b_dev, x_old, x_new, ws, s, fold=True)), "gs_level_kernel"
+    return fwd, bwd, names[0], names[1]
+
+
+def _event_time(fn, reps, stream, flush=None):
+    import torch
+
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    tot = 0.0
+    for _ in range(reps):
+        if flush is not None:
+            flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        e1.synchronize()
+        tot += e0.elapsed_time(e1) / 1e3
+    return tot / reps
+
+
 def run_b200(args, world, rank, local):
     import ctypes
 
@@ -385,20 +435,21 @@ def run_b200(args, world, rank, local):
     import paper_1907_04417_b200 as mv
     from paper_1907_04417_b200 import _lib
     from paper_1907_04417_b200.device import ptr, stream_handle
-    from paper_1907_04417_b200.roofline import (cycle_bytes, gs_sweep_bytes, measured_peak_gbs,
-                                                pcg_iteration_bytes)
+    from paper_1907_04417_b200.roofline import (composite_application_bytes, cycle_bytes, gs_sweep_bytes,
+                                                measured_peak_gbs, pcg_iteration_bytes)
 
     from paper_1907_04417_b200 import replicas
 
     torch.cuda.set_device(local)
     dist = replicas.init("nccl", torch.device("cuda", local))
     L = _lib.load()
-    mats, pros, b, desc, info = load_workload(args.config)
+    name = args.config.lower()
+    mats, pros, b, info = load_workload(name, setup="gpu")
     n = mats[0].shape[0]
     op = mv.GpuMultigridOperator(mats, pros)
     h = op.handle
     s = stream_handle()
-    steps = args.steps if args.steps is not None else (50 if n < 100000 else 10)
+    steps = args.steps if args.steps is not None else (50 if n < 100000 else 20)
     warm = max(3, args.warmup)
 
     b_dev = torch.from_numpy(b).cuda()
@@ -446,6 +497,7 @@ def run_b200(args, world, rank, local):
     L.mvamg_kernel_launches(ctypes.byref(launches), 1)
     t_solve = replicas.max_over_ranks(tot / steps, dist, "cuda")
     n_iters = nit.value
+    hist_gpu = hist_dev[: n_iters + 1].cpu().numpy()
     # ---- e2e: same solve through the C ABI with host buffers ------------------
     b_host = torch.from_numpy(b.copy()).pin_memory()
     x_host = torch.empty(n, dtype=torch.float64).pin_memory()
@@ -473,92 +525,66 @@ def run_b200(args, world, rank, local):
         tot += e0.elapsed_time(e1) / 1e3
     t_e2e = replicas.max_over_ranks(tot / steps, dist, "cuda")
     clocks = sampler.stop()
-    # ---- one V-cycle and the dominant kernel (fine-level GS sweep) -----------
-    reps = 50
+    # ---- one V-cycle, and every level's sweeps timed alone -------------------
+    reps = 20
     r_dev = torch.from_numpy(b).cuda()
-    for _ in range(3):
-        op.apply_device(r_dev)
-    torch.cuda.synchronize()
-    tc = 0.0
-    for _ in range(reps):
-        l2_flush()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        op.apply_device(r_dev)
-        e1.record(stream)
-        e1.synchronize()
-        tc += e0.elapsed_time(e1) / 1e3
-    t_cycle = tc / reps
-    lv = op.level_dev[0]
-    xn = torch.empty(n, dtype=torch.float64, device="cuda")
-    ws = torch.zeros(8, dtype=torch.int32, device="cuda")
-    if lv.get("levels"):
-        small = lv["levels"][0]
-        gs_kernel = "gs_level_kernel (single-CTA level-set sweep) level 0, forward from x=0 (+prepare)"
-
-        def gs_once():
-            small.sweep(r_dev, None, xn, ws, s)
-    elif lv.get("rows"):
-        rows0 = lv["rows"][0]
-        gs_kernel = "gs_row_kernel (dataflow row sweep) level 0, forward from x=0 (+prepare)"
-
-        def gs_once():
-            rows0.sweep(r_dev, None, xn, ws, s)
-    else:
-        gp = lv["gs"]
-        gs_kernel = ("gs_lean_kernel" if gp.plan.lean_C else "gs_sweep_kernel") + \
-            " level 0, forward from x=0 (+prepare)"
-
-        def gs_once():
-            gp.sweep(0, r_dev, None, xn, ws, s)
-
-    for _ in range(3):
-        gs_once()
-    torch.cuda.synchronize()
-    tg = 0.0
-    for _ in range(reps):
-        l2_flush()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        gs_once()
-        e1.record(stream)
-        e1.synchronize()
-        tg += e0.elapsed_time(e1) / 1e3
-    t_gs = tg / reps  # includes the sentinel-fill prep kernel
+    t_cycle = _event_time(lambda: op.apply_device(r_dev), 50, stream, l2_flush)
     peak, peak_src = measured_peak_gbs(ROOT)
-    gs_bytes = gs_sweep_bytes(mats[0], True)
-    gs_gbs = gs_bytes / t_gs / 1e9
+    kernels = []
+    for k in range(len(mats) - 1):
+        nk = mats[k].shape[0]
+        bk = torch.from_numpy(np.random.default_rng(k).uniform(-1, 1, nk)).cuda()
+        xo = torch.from_numpy(np.random.default_rng(100 + k).uniform(-1, 1, nk)).cuda()
+        xn = torch.empty(nk, dtype=torch.float64, device="cuda")
+        ws = torch.zeros(8, dtype=torch.int32, device="cuda")
+        fwd, bwd, fname, bname = _level_sweeps(op, k, bk, xo, xn, ws, s)
+        for fn, nm, zero, what in ((fwd, fname, True, "forward from x=0 (L+D read)"),
+                                   (bwd, bname, False, "backward from x_old (folded)")):
+            if fn is None:
+                continue
+            t = _event_time(fn, reps, stream, l2_flush)
+            by = gs_sweep_bytes(mats[k], zero)
+            kernels.append({"kernel": nm, "level": k, "sweep": what, "rows": int(nk), "ms": t * 1e3,
+                            "algorithmic_bytes": int(by), "gbs": by / t / 1e9, "share_of_cycle": t / t_cycle})
+    dom = max(kernels, key=lambda e: e["ms"]) if kernels else None
     cyc_bytes = cycle_bytes(mats, pros)
     it_bytes = pcg_iteration_bytes(mats, pros)
     out = {
         "metric": METRIC, "value": t_solve, "unit": "s", "n_gpus": world, "steps": steps,
         "warmup": warm, "ms_per_step": t_solve * 1e3, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {
-            "workload": desc, "n": n, "nnz": int(mats[0].nnz), "levels": [M.shape[0] for M in mats],
-            "nit": n_iters, "converged": bool(conv.value), "fit_s": info.get("fit_s"),
-            "bootstrap_stages": info.get("bootstrap_stages"),
-            "l2": "flushed (256 MiB write) before every timed step" if small else "inputs larger than L2",
-            "parallelism": replicas.parallelism(world),
-        },
+        "config": workload_config(name),
         "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n + 8 * (n_iters + 1)},
         "gpu_launches": int(round(launches.value / steps)),
+        "roofline": None,
+        "clocks": clocks,
+        "details": {"n": n, "nnz": int(mats[0].nnz), "levels": [M.shape[0] for M in mats], "nit": n_iters,
+                    "converged": bool(conv.value), "final_relres": float(hist_gpu[-1] / hist_gpu[0]),
+                    "hierarchy": info.get("hierarchy"), "fit_s": info.get("fit_s"),
+                    "bootstrap_stages": info.get("bootstrap_stages"),
+                    "parallelism": replicas.parallelism(world)},
         "cycle": {"ms": t_cycle * 1e3, "model_bytes": cyc_bytes, "gbs": cyc_bytes / t_cycle / 1e9,
                   "frac": cyc_bytes / t_cycle / 1e9 / peak},
         "pcg_model": {"bytes_per_iteration": it_bytes, "gbs": it_bytes * n_iters / t_solve / 1e9,
                       "frac": it_bytes * n_iters / t_solve / 1e9 / peak},
-        "roofline": {"bound": "hbm", "kernel": gs_kernel,
-                     "achieved": gs_gbs, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                     "frac": gs_gbs / peak, "traffic": measured_traffic(args.config, gs_kernel),
-                     "algorithmic_bytes": gs_bytes,
-                     "ms": t_gs * 1e3},
-        "clocks": clocks,
+        "sweeps": kernels,
     }
+    if dom is not None:
+        kname = dom["kernel"]
+        out["roofline"] = {"bound": "hbm", "kernel": f"{kname} level {dom['level']}, {dom['sweep']}",
+                           "achieved": dom["gbs"], "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                           "frac": dom["gbs"] / peak,
+                           "traffic": measured_traffic(name, kname, dom["level"], dom["sweep"]),
+                           "algorithmic_bytes": dom["algorithmic_bytes"], "ms": dom["ms"],
+                           "why": "longest single kernel of the cycle (largest share of one V-cycle, "
+                                  "`sweeps`); the exact-order sweep's bound is its dependency depth x "
+                                  "per-level latency (DESIGN.md)"}
     # ---- H2: PCG preconditioned by the symmetrized multiplicative composite
     # of the bootstrap K-cycles (bootstrap.py:98-113; the paper's solver) ----
-    if info.get("components") and not args.no_h2:
-        comp_ops = [mv.GpuMultigridOperator(m, p, cycle=mv.CycleSpec("K", 2)) for m, p in info["components"]]
+    comps = info.get("components")
+    if comps and not args.no_h2:
+        comp_ops = [mv.GpuMultigridOperator(m, p, cycle=mv.CycleSpec("K", 2)) for m, p in comps]
         pc = mv.GpuCompositePreconditioner(mv.GpuComposite(comp_ops))
         from paper_1907_04417_b200.krylov import pcg as _pcg
 
@@ -570,12 +596,40 @@ def run_b200(args, world, rank, local):
         e1.record(stream)
         e1.synchronize()
         t_h2 = replicas.max_over_ranks(e0.elapsed_time(e1) / 1e3, dist, "cuda")
+        ap_bytes = composite_application_bytes(comps)
+        h2_bytes = (rep.iterations + 1) * ap_bytes + rep.iterations * (12 * mats[0].nnz + 4 * n + 80 * n)
         out["h2"] = {"value": t_h2, "unit": "s", "nit": rep.iterations, "components": len(comp_ops),
-                     "converged": bool(rep.converged), "what": "PCG rtol 1e-6 preconditioned by the "
-                     "symmetrized composite of the bootstrap K-cycles (inner FCG 2); one timed solve"}
-    # ---- setup: the Galerkin products of this hierarchy on the device
-    # (sparse.py:50-66, bit-identical) against the reference's scipy call ----
-    if rank == 0 and not args.no_galerkin and len(mats) > 1:
+                     "converged": bool(rep.converged),
+                     "what": "PCG rtol 1e-6 preconditioned by the symmetrized composite of the bootstrap "
+                             "K-cycles (inner FCG 2); one timed solve",
+                     "model_bytes_per_application": ap_bytes,
+                     "roofline": {"bound": "hbm", "achieved": h2_bytes / t_h2 / 1e9, "peak": peak,
+                                  "unit": "GB/s", "frac": h2_bytes / t_h2 / 1e9 / peak,
+                                  "what": "SURVEY 8(d) composite byte model over the whole H2 solve"}}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            from oracle.oracle import OracleOperator, oracle_composite, oracle_pcg, set_threads
+
+            thr = set_threads(_threads())
+            ops = [OracleOperator(m, p, cycle="K", inner_fcg_iters=2) for m, p in comps]
+            t0 = time.perf_counter()
+            oracle_composite(ops, b)
+            t_app = time.perf_counter() - t0
+            if t_app * (rep.iterations + 1) <= 90.0:
+                t0 = time.perf_counter()
+                _, _, hnit, _ = oracle_pcg(ops[0], b, precond="composite", ops=ops, rtol=1e-6)
+                out["h2"]["cpu_baseline"] = {
+                    "value": time.perf_counter() - t0, "unit": "s", "cores": thr, "kind": "port",
+                    "sample": f"1 full composite-preconditioned PCG solve (nit={hnit}) on the oracle, "
+                              f"{thr} thread(s) of {cpu_model()}"}
+            else:
+                out["h2"]["cpu_baseline"] = {
+                    "value": t_app * (rep.iterations + 1), "unit": "s", "cores": thr, "kind": "port",
+                    "sample": f"one symmetrized application timed ({t_app:.2f} s) x the GPU solve's "
+                              f"{rep.iterations + 1} applications (a full solve would exceed 90 s)"}
+            del ops
+    # ---- setup legs (opt-in): Galerkin products of this hierarchy on the
+    # device (sparse.py:50-66, bit-identical) against scipy ----------------------
+    if rank == 0 and args.setup_legs and len(mats) > 1:
         from paper_1907_04417_b200.device import galerkin_product_device
         from paper_1907_04417_b200.setup import galerkin_product
 
@@ -590,21 +644,22 @@ def run_b200(args, world, rank, local):
             same = bool(np.array_equal(G.indptr, H.indptr) and np.array_equal(G.indices, H.indices)
                         and np.array_equal(G.data, H.data))
             levels.append({"level": k, "n": mats[k].shape[0], "nc": pros[k].shape[1], "nnz_A": int(mats[k].nnz),
-                           "nnz_P": int(pros[k].nnz), "nnz_Ac": int(G.nnz), "device_ms": t["total_ms"],
-                           "phases_ms": {x: round(t[x], 3) for x in ("transpose_ms", "ap_ms", "ptap_ms",
-                                                                     "symmetrize_ms")},
-                           "scipy_ms": t_host * 1e3, "bit_exact": same})
-        out["galerkin"] = {"what": "A_c = (G + G')/2, G = P'(A P) per hierarchy level, device kernels "
-                                   "(csrc/galerkin.cuh) vs the reference's scipy recipe on one host core",
+                           "device_ms": t["total_ms"], "scipy_ms": t_host * 1e3, "bit_exact": same})
+        out["galerkin"] = {"what": "A_c = (G + G')/2, G = P'(A P) per level, device vs scipy (one core)",
                            "levels": levels}
-    # ---- setup: the per-aggregate local SVDs of this hierarchy on the device
-    # (svd.py:17-55, bit-identical) against the host restatement, one core ----
-    if rank == 0 and not args.no_galerkin and info.get("svd_case"):
-        out["svd"] = svd_timing(*info["svd_case"])
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb, cnit = cpu_baseline(mats, pros, b, nit_hint=n_iters)
+        from oracle.oracle import OracleOperator, oracle_pcg
+
+        cb, cnit = cpu_baseline(mats, pros, b, _threads(), nit_hint=n_iters)
         cb["nit"] = cnit
         out["cpu_baseline"] = cb
+        cb1, _ = cpu_baseline(mats, pros, b, 1, budget_s=20.0, nit_hint=n_iters)
+        out["cpu_baseline_1core"] = cb1
+        # parity of the timed GPU solve against the oracle on the same hierarchy
+        _, hist_o, nit_o, _ = oracle_pcg(OracleOperator(mats, pros), b, rtol=1e-6)
+        m = min(len(hist_o), len(hist_gpu))
+        out["details"]["oracle_nit"] = nit_o
+        out["details"]["history_rel_max_vs_oracle"] = float(np.max(np.abs(hist_gpu[:m] - hist_o[:m]) / hist_o[:m]))
     if rank == 0:
         print(json.dumps(out), flush=True)
     if dist:

@@ -328,7 +328,9 @@ int mvamg_hierarchy_set_gs_rows(mvamg_hierarchy* h, int k, int mode, const int* 
  * default smoothers and single-CTA level-set schedules (modes 0 and 2) on
  * levels k0..L-2; k0 < 0 turns it off.  A V-cycle is bit-identical either way. */
 int mvamg_hierarchy_set_mega(mvamg_hierarchy* h, int k0);
-/* Transfer k: P (n_k x n_{k+1}) and R = P^T (n_{k+1} x n_k), device CSR. */
+/* Transfer k: P (n_k x n_{k+1}) and R = P^T (n_{k+1} x n_k), device CSR.
+ * Levels k and k+1 must be set first (their sizes give P's and R's shapes):
+ * otherwise MVAMG_E_STATE.  Synchronises the device once to read nnz(P), nnz(R). */
 int mvamg_hierarchy_set_transfer(mvamg_hierarchy* h, int k, const int* p_indptr,
                                  const int* p_indices, const double* p_data,
                                  const int* r_indptr, const int* r_indices,

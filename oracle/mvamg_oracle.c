@@ -16,11 +16,30 @@
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #define OR_MAXLEV 64
 
+/* Host threads: rows of an SpMV and elements of a vector update are split over
+ * OpenMP threads; every row / element is computed exactly as in the serial
+ * loop, and dots use a fixed blocking (below), so the results do not depend on
+ * the thread count.  The Gauss-Seidel sweeps stay serial (_kernels.py:15-38). */
+#define OR_PAR_MIN 32768
+int or_set_threads(int t) {
+#ifdef _OPENMP
+    if (t > 0) omp_set_num_threads(t);
+    return omp_get_max_threads();
+#else
+    (void)t;
+    return 1;
+#endif
+}
+
 /* scipy csr_matvec: y[i] = 0.0 + sum over row i in CSR order (sparse.py:40). */
 void or_spmv(int n, const int* ip, const int* ix, const double* v, const double* x, double* y) {
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
     for (int i = 0; i < n; ++i) {
         double s = 0.0;
         for (int k = ip[i]; k < ip[i + 1]; ++k) s += v[k] * x[ix[k]];
@@ -42,10 +61,28 @@ void or_gs(int dir, int n, const int* ip, const int* ix, const double* v, const 
     }
 }
 
-/* sequential dot (np.dot is blocked OpenBLAS: parity is by tolerance). */
+/* dot: np.dot is blocked OpenBLAS (FMA, thread-count dependent), so parity is by
+ * tolerance.  Here: sequential within blocks of OR_DOT_BLOCK elements, block
+ * partials added in order -- the same bits for any thread count. */
+#define OR_DOT_BLOCK 8192
 double or_dot(int n, const double* x, const double* y) {
+    if (n <= OR_DOT_BLOCK) {
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) s += x[i] * y[i];
+        return s;
+    }
+    int nb = (n + OR_DOT_BLOCK - 1) / OR_DOT_BLOCK;
+    double* part = (double*)malloc(sizeof(double) * (size_t)nb);
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
+    for (int b = 0; b < nb; ++b) {
+        int i0 = b * OR_DOT_BLOCK, i1 = i0 + OR_DOT_BLOCK < n ? i0 + OR_DOT_BLOCK : n;
+        double s = 0.0;
+        for (int i = i0; i < i1; ++i) s += x[i] * y[i];
+        part[b] = s;
+    }
     double s = 0.0;
-    for (int i = 0; i < n; ++i) s += x[i] * y[i];
+    for (int b = 0; b < nb; ++b) s += part[b];
+    free(part);
     return s;
 }
 
@@ -112,6 +149,7 @@ static void smooth(or_hier* h, int kind, int sweeps, double omega, int k, const 
         } else {
             double* t = h->T[k];
             or_spmv(A->n, A->ip, A->ix, A->v, x, t);
+#pragma omp parallel for schedule(static) if (A->n >= OR_PAR_MIN)
             for (int i = 0; i < A->n; ++i) x[i] += omega * (b[i] - t[i]) / h->diag[k][i];
         }
     }
@@ -141,14 +179,15 @@ static int fcg_level(or_hier* h, int k, const double* b, int iters, double* x) {
             double* pp = h->fp[k][cur ^ 1];
             double* App = h->fap[k][cur ^ 1];
             double beta = or_dot(n, z, App) / pAp_prev;
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
             for (int i = 0; i < n; ++i) p[i] = z[i] - beta * pp[i];
         }
         or_spmv(n, A->ip, A->ix, A->v, p, Ap);
         double pAp = or_dot(n, p, Ap);
         if (!(pAp > 0.0)) return -2;
         double alpha = or_dot(n, p, r) / pAp;
-        for (int i = 0; i < n; ++i) x[i] += alpha * p[i];
-        for (int i = 0; i < n; ++i) r[i] -= alpha * Ap[i];
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
+        for (int i = 0; i < n; ++i) { x[i] += alpha * p[i]; r[i] -= alpha * Ap[i]; }
         pAp_prev = pAp;
         cur ^= 1;
     }
@@ -166,6 +205,7 @@ static int descend(or_hier* h, int k, const double* r, double* out) {
     smooth(h, h->pre_kind, h->pre_sweeps, h->pre_omega, k, r, x);
     double* t = h->T[k];
     or_spmv(n, A->ip, A->ix, A->v, x, t);
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
     for (int i = 0; i < n; ++i) t[i] = r[i] - t[i];
     double* rc = h->RC[k + 1];
     or_spmv(nc, h->R[k].ip, h->R[k].ix, h->R[k].v, t, rc);
@@ -175,6 +215,7 @@ static int descend(or_hier* h, int k, const double* r, double* out) {
     else st = descend(h, k + 1, rc, xc);
     if (st) return st;
     or_spmv(n, h->P[k].ip, h->P[k].ix, h->P[k].v, xc, t);
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
     for (int i = 0; i < n; ++i) x[i] += t[i];
     smooth(h, h->post_kind, h->post_sweeps, h->post_omega, k, r, x);
     if (out != x) memcpy(out, x, sizeof(double) * (size_t)n);
@@ -204,6 +245,7 @@ int or_composite(or_hier** ops, int r, double* x, double* t1, double* t2) {
         or_spmv(n, h->A[0].ip, h->A[0].ix, h->A[0].v, x, t2);
         int st = or_apply(h, t2, t1);
         if (st) return st;
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
         for (int i = 0; i < n; ++i) x[i] = x[i] - t1[i];
     }
     return 0;
@@ -220,9 +262,11 @@ static int composite_precond(or_hier** ops, int nops, const double* r, double* z
     for (int pass = 0; pass < 2 * nops; ++pass) {
         or_hier* h = ops[pass < nops ? pass : 2 * nops - 1 - pass];
         or_spmv(n, A->ip, A->ix, A->v, z, t1);
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
         for (int i = 0; i < n; ++i) t1[i] = r[i] - t1[i];
         int st = or_apply(h, t1, t2);
         if (st) return st;
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
         for (int i = 0; i < n; ++i) z[i] = z[i] + t2[i];
     }
     return 0;
@@ -254,8 +298,8 @@ int or_pcg(const or_csr* A, const double* b, int pc_kind, or_hier** ops, int nop
         double pq = or_dot(n, p, q);
         if (!(pq > 0.0)) { *nit = k; return -2; }
         double alpha = rz / pq;
-        for (int i = 0; i < n; ++i) x[i] += alpha * p[i];
-        for (int i = 0; i < n; ++i) r[i] -= alpha * q[i];
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
+        for (int i = 0; i < n; ++i) { x[i] += alpha * p[i]; r[i] -= alpha * q[i]; }
         ++k;
         hist[k] = sqrt(or_dot(n, r, r));
         if (hist[k] <= rtol * r0) { *converged = 1; break; }
@@ -264,6 +308,7 @@ int or_pcg(const or_csr* A, const double* b, int pc_kind, or_hier** ops, int nop
         double rzn = or_dot(n, r, z);
         if (!(rzn > 0.0)) { *nit = k; return -1; }
         double beta = rzn / rz;
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
         for (int i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
         rz = rzn;
     }
@@ -416,3 +461,109 @@ int or_galerkin(int n, int nc, const int* aip, const int* aix, const double* av,
 }
 
 void or_free(void* p) { free(p); }
+
+
+/* ---- setup natives (test infrastructure: the CPU-only setup of bench.py's
+ * reference arm, oracle/host_setup.py) ------------------------------------- */
+
+/* greedy_accept (_kernels.py:41-61): edges already in the greedy's order
+ * (weight descending, ties by (i, j), matching.py:106-122).  partner[v] = -1
+ * when v stays unmatched.  Returns the number of accepted pairs. */
+long long or_greedy_accept(long long ne, const long long* ei, const long long* ej, int n, long long* partner,
+                           long long* pi, long long* pj) {
+    for (int v = 0; v < n; ++v) partner[v] = -1;
+    long long np = 0;
+    for (long long k = 0; k < ne; ++k) {
+        long long i = ei[k], j = ej[k];
+        if (partner[i] < 0 && partner[j] < 0) {
+            partner[i] = j;
+            partner[j] = i;
+            pi[np] = i;
+            pj[np] = j;
+            ++np;
+        }
+    }
+    return np;
+}
+
+/* One-sided Jacobi on one m x k row-major block in place (_kernels.py:64-121;
+ * the accumulated V is not needed for U and sigma).  Returns 1 if converged. */
+static int or_jacobi(double* B, int m, int k, int max_sweeps, double tol) {
+    if (k < 2) return 1;
+    double rel_tol = tol > 2.0 * m * 2.220446049250313e-16 ? tol : 2.0 * m * 2.220446049250313e-16;
+    for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+        double total = 0.0;
+        for (int p = 0; p < k; ++p)
+            for (int r = 0; r < m; ++r) total += B[(size_t)r * k + p] * B[(size_t)r * k + p];
+        double floor_ = tol * total;
+        int rotated = 0;
+        for (int p = 0; p < k - 1; ++p)
+            for (int q = p + 1; q < k; ++q) {
+                double alpha = 0.0, beta = 0.0, gamma = 0.0;
+                for (int r = 0; r < m; ++r) {
+                    double bp = B[(size_t)r * k + p], bq = B[(size_t)r * k + q];
+                    alpha += bp * bp;
+                    beta += bq * bq;
+                    gamma += bp * bq;
+                }
+                if (gamma == 0.0) continue;
+                if (fabs(gamma) <= rel_tol * sqrt(alpha * beta) || fabs(gamma) <= floor_) continue;
+                ++rotated;
+                double zeta = (beta - alpha) / (2.0 * gamma);
+                double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                double c = 1.0 / sqrt(1.0 + t * t);
+                double s = c * t;
+                for (int r = 0; r < m; ++r) {
+                    double bp = B[(size_t)r * k + p], bq = B[(size_t)r * k + q];
+                    B[(size_t)r * k + p] = c * bp - s * bq;
+                    B[(size_t)r * k + q] = s * bp + c * bq;
+                }
+            }
+        if (rotated == 0) return 1;
+    }
+    return 0;
+}
+
+/* jacobi_svd (svd.py:17-55) of every stacked block rows rp[b]..rp[b+1] (k
+ * columns, row-major): Jacobi, column norms (sequential over rows, as numpy's
+ * axis-0 norm), stable descending sort, U = B / sigma for sigma > 0 else 0.
+ * Blocks are independent (parallel over blocks).  Returns 0, or -1 with
+ * *failed = the first block that did not converge. */
+int or_jacobi_svd_batch(int nblk, const int* rp, int k, const double* A, int max_sweeps, double tol, double* U,
+                        double* sigma, int* failed) {
+    int first_fail = nblk;
+#pragma omp parallel
+    {
+        int cap = 0;
+        double* B = NULL;
+        double s[64];
+        int order[64];
+#pragma omp for schedule(dynamic, 256) reduction(min : first_fail)
+        for (int b = 0; b < nblk; ++b) {
+            int r0 = rp[b], m = rp[b + 1] - r0;
+            if (m * k > cap) { cap = m * k; B = (double*)realloc(B, sizeof(double) * (size_t)cap); }
+            memcpy(B, A + (size_t)r0 * k, sizeof(double) * (size_t)m * k);
+            if (!or_jacobi(B, m, k, max_sweeps, tol)) { if (b < first_fail) first_fail = b; continue; }
+            for (int p = 0; p < k; ++p) {
+                double acc = 0.0;
+                for (int r = 0; r < m; ++r) acc += B[(size_t)r * k + p] * B[(size_t)r * k + p];
+                s[p] = sqrt(acc);
+                order[p] = p;
+            }
+            for (int a = 1; a < k; ++a) {   /* stable insertion sort, descending */
+                int o = order[a], j = a - 1;
+                while (j >= 0 && s[order[j]] < s[o]) { order[j + 1] = order[j]; --j; }
+                order[j + 1] = o;
+            }
+            for (int p = 0; p < k; ++p) {
+                int src = order[p];
+                sigma[(size_t)b * k + p] = s[src];
+                for (int r = 0; r < m; ++r)
+                    U[(size_t)(r0 + r) * k + p] = s[src] > 0.0 ? B[(size_t)r * k + src] / s[src] : 0.0;
+            }
+        }
+        free(B);
+    }
+    if (failed) *failed = first_fail < nblk ? first_fail : -1;
+    return first_fail < nblk ? -1 : 0;
+}

@@ -56,6 +56,12 @@ def lib():
         L.or_gs.argtypes = [_I, _I, _P, _P, _P, _P, _P, _P]
         L.or_dot.argtypes = [_I, _P, _P]
         L.or_dot.restype = _D
+        L.or_set_threads.argtypes = [_I]
+        L.or_set_threads.restype = _I
+        L.or_greedy_accept.argtypes = [ctypes.c_longlong, _P, _P, _I, _P, _P, _P]
+        L.or_greedy_accept.restype = ctypes.c_longlong
+        L.or_jacobi_svd_batch.argtypes = [_I, _P, _I, _P, _I, _D, _P, _P, ctypes.POINTER(_I)]
+        L.or_jacobi_svd_batch.restype = _I
         _LIB = L
     return _LIB
 
@@ -71,6 +77,19 @@ def _csr(M):
     return (M, np.ascontiguousarray(M.indptr, dtype=np.int32),
             np.ascontiguousarray(M.indices, dtype=np.int32),
             np.ascontiguousarray(M.data, dtype=np.float64))
+
+
+def set_threads(t=0):
+    """Host threads for the oracle's SpMVs, vector updates, dots and batched
+    SVDs (0: keep the OpenMP default).  Results do not depend on it; the GS
+    sweeps are serial.  Returns the thread count in effect."""
+    return int(lib().or_set_threads(int(t)))
+
+
+def oracle_dot(x, y):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    return float(lib().or_dot(x.shape[0], _ptr(x), _ptr(y)))
 
 
 def oracle_spmv(A, x):

@@ -88,7 +88,7 @@ inline int grid_for(int n, int threads = 256, int per_sm = 8) {
 
 inline int dot_grid(int n) { return std::min(grid_for(n, 256, 8), kDotMaxBlocks); }
 constexpr int kWarpRowMaxRows = 65536;  // levels up to this size with >= kWarpRowMinAvg entries per row
-constexpr int kWarpRowMinAvg = 4;       //   run their SpMVs one warp per row
+constexpr int kWarpRowMinAvg = 8;       //   run their SpMVs one warp per row
 
 bool g_attr_done = false;
 int g_max_dyn_smem = 48 * 1024;
@@ -1924,6 +1924,7 @@ int mvamg_hierarchy_set_mega(mvamg_hierarchy* h, int k0) {
   if (!h) return fail(MVAMG_E_ARG, "set_mega: null handle");
   if (k0 < 0) {
     h->mega_k0 = -1;
+    for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
     h->graphs.clear();
     return 0;
   }
@@ -2142,10 +2143,18 @@ int mvamg_hierarchy_set_transfer(mvamg_hierarchy* h, int k, const int* p_indptr,
                                  const double* p_data, const int* r_indptr, const int* r_indices,
                                  const double* r_data) {
   if (!h || k < 0 || k >= h->L - 1) return fail(MVAMG_E_ARG, "set_transfer: bad level index");
+  if (!p_indptr || !p_indices || !p_data || !r_indptr || !r_indices || !r_data)
+    return fail(MVAMG_E_ARG, "set_transfer: null operand");
+  // P's and R's shapes come from the levels on both sides: both must be set first
+  if (!h->lv[k].A.ip || !h->lv[k + 1].A.ip)
+    return fail(MVAMG_E_STATE, "set_transfer: levels " + std::to_string(k) + " and " + std::to_string(k + 1) +
+                                   " must be set (mvamg_hierarchy_set_level) before transfer " + std::to_string(k));
   Level& l = h->lv[k];
   l.P.n = l.A.n; l.P.m = h->lv[k + 1].A.n; l.P.ip = p_indptr; l.P.ix = p_indices; l.P.v = p_data;
   l.R.n = h->lv[k + 1].A.n; l.R.m = l.A.n; l.R.ip = r_indptr; l.R.ix = r_indices; l.R.v = r_data;
-  // entry counts (one small read each, at setup): they pick the warp-per-row SpMV on small levels
+  // entry counts (one small read each, at setup): they pick the warp-per-row SpMV on small levels.
+  // The caller's uploads may still be in flight on any stream: wait for the device first.
+  CUDA_TRY(cudaDeviceSynchronize());
   CUDA_TRY(cudaMemcpy(&l.P.nnz, p_indptr + l.P.n, sizeof(int), cudaMemcpyDeviceToHost));
   CUDA_TRY(cudaMemcpy(&l.R.nnz, r_indptr + l.R.n, sizeof(int), cudaMemcpyDeviceToHost));
   return 0;
@@ -2208,6 +2217,13 @@ int mvamg_hierarchy_bind_workspace(mvamg_hierarchy* h, void* ws, void* stream) {
   for (int k = 0; k < h->L; ++k)
     if (!h->lv[k].A.ip) return fail(MVAMG_E_STATE, "bind_workspace: level " + std::to_string(k) + " not set");
   if (!h->inv) return fail(MVAMG_E_STATE, "bind_workspace: coarse inverse not set");
+  for (int k = 0; k < h->L - 1; ++k) {
+    const Level& l = h->lv[k];
+    if (!l.P.ip || !l.R.ip) return fail(MVAMG_E_STATE, "bind_workspace: transfer " + std::to_string(k) + " not set");
+    if (l.P.n != l.A.n || l.P.m != h->lv[k + 1].A.n || l.R.n != h->lv[k + 1].A.n || l.R.m != l.A.n)
+      return fail(MVAMG_E_STATE, "bind_workspace: transfer " + std::to_string(k) +
+                                     " was set before a level it connects changed size");
+  }
   workspace_layout(h, (char*)ws);
   set_kernel_attrs();
   for (int k = 0; k < h->L - 1; ++k)
@@ -2299,7 +2315,10 @@ int mvamg_pcg_solve_host(mvamg_hierarchy* h, int pc_kind, mvamg_composite* comp,
     CUDA_TRY(cudaMallocAsync((void**)&hist_dev, ((size_t)itmax + 1) * 8, s));
   }
   int st = pcg_device(h, pc_kind, comp, h->in, rtol, itmax, hist_dev, nit, converged, status, s);
-  if (st) return st;
+  if (st) {
+    if (hist_dev != h->pt) cudaFreeAsync(hist_dev, s);
+    return st;
+  }
   CUDA_TRY(cudaMemcpyAsync(x_host, h->px, nb, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaMemcpyAsync(hist_host, hist_dev, ((size_t)*nit + 1) * 8, cudaMemcpyDeviceToHost, s));
   if (hist_dev != h->pt) CUDA_TRY(cudaFreeAsync(hist_dev, s));

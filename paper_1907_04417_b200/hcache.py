@@ -1,0 +1,103 @@
+"""Hierarchy serialization.
+
+The reference has no hierarchy format (its only serialization is Matrix
+Market for single matrices, pkg/src/mvamg/mmio.py:18-103), so every run refits:
+minutes on the GPU for C2-C4, hours on one core.  This module stores a fitted
+multi-vector hierarchy plus the bootstrap's K-cycle component hierarchies as
+one uncompressed npz, keyed by the workload (matrix and right-hand-side
+digests), the setup parameters and HCACHE_VERSION (bumped whenever the setup's
+algorithm changes).  bench.py's two arms solve the same file: the reference
+arm fits on host cores and writes it, the B200 arm reads it when present.
+
+Layout: ``A{k}_{indptr,indices,data,shape}``, ``P{k}_...`` for the V-cycle
+hierarchy; ``c{i}_nlev``, ``c{i}_A{k}_...`` (k >= 1), ``c{i}_P{k}_...`` for
+component i (its fine matrix is A0); ``meta`` (JSON text).
+"""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import scipy.sparse as sp
+
+HCACHE_VERSION = 1
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def cache_dir():
+    return os.environ.get("MVAMG_HCACHE", os.path.join(REPO, ".hcache"))
+
+
+def _digest_csr(h, M):
+    M = sp.csr_matrix(M)
+    h.update(np.asarray(M.shape, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(M.indptr, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(M.indices, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(M.data, dtype=np.float64).tobytes())
+
+
+def key(name, A, b, params=None):
+    """Cache key of a workload: name, A, b, setup parameters, format version."""
+    h = hashlib.sha256()
+    h.update(f"{name}|v{HCACHE_VERSION}|{json.dumps(params or {}, sort_keys=True)}".encode())
+    _digest_csr(h, A)
+    h.update(np.ascontiguousarray(b, dtype=np.float64).tobytes())
+    return f"{name}-{h.hexdigest()[:20]}"
+
+
+def path_for(k):
+    return os.path.join(cache_dir(), k + ".npz")
+
+
+def _put(d, pre, M):
+    M = sp.csr_matrix(M)
+    d[pre + "_indptr"] = np.ascontiguousarray(M.indptr, dtype=np.int32)
+    d[pre + "_indices"] = np.ascontiguousarray(M.indices, dtype=np.int32)
+    d[pre + "_data"] = np.ascontiguousarray(M.data, dtype=np.float64)
+    d[pre + "_shape"] = np.asarray(M.shape, dtype=np.int64)
+
+
+def _get(z, pre):
+    return sp.csr_matrix((z[pre + "_data"], z[pre + "_indices"], z[pre + "_indptr"]),
+                         shape=tuple(int(s) for s in z[pre + "_shape"]))
+
+
+def save(k, mats, pros, components=(), meta=None):
+    """Write atomically (a reader never sees a partial file)."""
+    os.makedirs(cache_dir(), exist_ok=True)
+    d = {"nlev": np.int64(len(mats)), "ncomp": np.int64(len(components))}
+    for i, M in enumerate(mats):
+        _put(d, f"A{i}", M)
+    for i, P in enumerate(pros):
+        _put(d, f"P{i}", P)
+    for c, (cm, cp) in enumerate(components):
+        d[f"c{c}_nlev"] = np.int64(len(cm))
+        for i in range(1, len(cm)):
+            _put(d, f"c{c}_A{i}", cm[i])
+        for i, P in enumerate(cp):
+            _put(d, f"c{c}_P{i}", P)
+    d["meta"] = np.asarray(json.dumps(meta or {}))
+    final = path_for(k)
+    tmp = final + f".tmp{os.getpid()}"
+    with open(tmp, "wb") as f:
+        np.savez(f, **d)
+    os.replace(tmp, final)
+    return final
+
+
+def load(k):
+    """(mats, pros, components, meta) or None when the key is not cached."""
+    p = path_for(k)
+    if not os.path.exists(p):
+        return None
+    with np.load(p, allow_pickle=False) as z:
+        mats = [_get(z, f"A{i}") for i in range(int(z["nlev"]))]
+        pros = [_get(z, f"P{i}") for i in range(int(z["nlev"]) - 1)]
+        comps = []
+        for c in range(int(z["ncomp"])):
+            L = int(z[f"c{c}_nlev"])
+            comps.append(([mats[0]] + [_get(z, f"c{c}_A{i}") for i in range(1, L)],
+                          [_get(z, f"c{c}_P{i}") for i in range(L - 1)]))
+        meta = json.loads(str(z["meta"]))
+    return mats, pros, comps, meta

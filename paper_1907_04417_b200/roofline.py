@@ -34,9 +34,50 @@ def pcg_iteration_bytes(matrices, prolongators):
 
 
 def gs_sweep_bytes(A, zero_init):
-    """One GS sweep: A once, b, diag, x_new (+ x_old unless zero-init)."""
+    """One GS sweep.  From x = 0 (forward pre-smoothing) only the lower
+    triangle and the diagonal are read (the upper neighbours are still zero):
+    12 nnz(L+D) + 4 (n+1) + b, diag, x_new.  From x_old: all of A + b, diag,
+    x_old, x_new."""
     n = A.shape[0]
-    return abytes(A) + 8 * n * (3 if zero_init else 4)
+    if zero_init:
+        import scipy.sparse as sp
+
+        nnz_ld = int(sp.tril(A).nnz)
+        return 12 * nnz_ld + 4 * (n + 1) + 8 * n * 3
+    return abytes(A) + 8 * n * 4
+
+
+def kcycle_bytes(matrices, prolongators, inner=2):
+    """SURVEY.md 8(d) composite model: one K-cycle application.  Level k is
+    visited v_k times (v_0 = 1; v_{k+1} = inner * v_k where level k+1 runs an
+    inner FCG, i.e. k + 1 < L - 1, else v_k); each visit costs the V-cycle's
+    per-level terms, each inner FCG step Abytes(A_{k+1}) + 80 n_{k+1}
+    (cycles.py:157-167, krylov.py:75-107)."""
+    L = len(matrices)
+    v = [1] * L
+    for k in range(L - 1):
+        v[k + 1] = inner * v[k] if k + 1 < L - 1 else v[k]
+    B = 0
+    for k in range(L - 1):
+        A, P = matrices[k], prolongators[k]
+        nk, nk1 = A.shape[0], matrices[k + 1].shape[0]
+        per = 2 * abytes(A) + (12 * P.nnz + 4 * (nk + 1)) + (12 * P.nnz + 4 * (nk1 + 1)) + 64 * nk + 16 * nk1
+        B += v[k] * per
+        if k + 1 < L - 1:
+            B += inner * v[k] * (abytes(matrices[k + 1]) + 80 * nk1)
+    nL = matrices[-1].shape[0]
+    return B + v[L - 1] * (8 * nL * nL + 16 * nL)
+
+
+def composite_application_bytes(components, inner=2):
+    """B_H2 = sum_i 2 (Abytes(A_0) + 16 n_0 + B_Kcycle(i)) per symmetrized
+    application (bootstrap.py:98-113; as a preconditioner the residual update
+    replaces the error update, same traffic)."""
+    B = 0
+    for mats, pros in components:
+        A0 = mats[0]
+        B += 2 * (abytes(A0) + 16 * A0.shape[0] + kcycle_bytes(mats, pros, inner))
+    return B
 
 
 def measured_peak_gbs(repo_root):

@@ -252,15 +252,20 @@ def coarse_product(config=None):
     return galerkin_product_device if (config or GpuConfig()).device_galerkin else galerkin_product
 
 
-def pairwise_step(A, w, steps, weight_floor=WEIGHT_FLOOR, product=galerkin_product, device_matching=False):
+def pairwise_step(A, w, steps, weight_floor=WEIGHT_FLOOR, product=galerkin_product, device_matching=False,
+                  matcher=None):
     """Compose `steps` matching sweeps into one transfer; returns
-    (P, A_c, w_c, aggregates, stagnated, steps_done)."""
+    (P, A_c, w_c, aggregates, stagnated, steps_done).  matcher(A, w, floor) ->
+    (pairs, unmatched) replaces the matching (the CPU-only setup of bench.py's
+    reference arm passes the oracle's)."""
     if steps < 1:
         raise ValueError("steps must be >= 1")
     Ak, wk = A, np.asarray(w, dtype=np.float64)
     P, aggs, stagnated, done = None, None, False, 0
     for _ in range(steps):
-        if device_matching:
+        if matcher is not None:
+            pairs, unmatched = matcher(Ak, wk, weight_floor)
+        elif device_matching:
             pairs, unmatched = greedy_matching_device(Ak, wk, weight_floor)
         else:
             i, j, c = edge_weights(Ak, wk)
@@ -284,7 +289,7 @@ def pairwise_step(A, w, steps, weight_floor=WEIGHT_FLOOR, product=galerkin_produ
     return P, Ak, wk, aggs, stagnated, done
 
 
-def build_pairwise_hierarchy(A, w, params=None, product=galerkin_product, device_matching=False):
+def build_pairwise_hierarchy(A, w, params=None, product=galerkin_product, device_matching=False, matcher=None):
     """Coarsen (A, w) until small; a level shrinking by < min_shrink is
     dropped; no pairs at the finest level raises CoarseningStagnationError."""
     params = params or CoarseningParams()
@@ -297,7 +302,7 @@ def build_pairwise_hierarchy(A, w, params=None, product=galerkin_product, device
     while levels[-1].A.shape[0] > params.min_coarse_size and len(levels) < params.max_levels:
         cur = levels[-1]
         P, Ac, wc, aggs, stagnated, done = pairwise_step(cur.A, cur.w, params.steps_per_level,
-                                                         params.weight_floor, product, device_matching)
+                                                         params.weight_floor, product, device_matching, matcher)
         if done == 0:
             if len(levels) == 1:
                 raise CoarseningStagnationError("matching produced no pairs at the finest level", level=0)
@@ -378,9 +383,10 @@ def _jacobi_svd_device(rp, local, nv):
     return code, U, sig, failed.value
 
 
-def block_prolongator(aggs, vectors, n_fine, tol=0.1, device_svd=False):
+def block_prolongator(aggs, vectors, n_fine, tol=0.1, device_svd=False, svd=None):
     """Per-aggregate truncated SVD bases (one-sided Jacobi), block diagonal.
-    device_svd: the SVD runs on the GPU (same U and sigma bit for bit)."""
+    device_svd: the SVD runs on the GPU (same U and sigma bit for bit);
+    svd(rp, local, nv) -> (code, U, sigma, failed) replaces it (CPU-only setup)."""
     V = np.column_stack([np.asarray(v, dtype=np.float64) for v in vectors])
     if V.shape[0] != aggs.n_prev:
         raise ValueError("vector length does not match the aggregate set")
@@ -390,7 +396,9 @@ def block_prolongator(aggs, vectors, n_fine, tol=0.1, device_svd=False):
         raise ValueError("empty aggregate")
     local = np.ascontiguousarray(V[aggs.members])            # stacked blocks, row-major
     rp = np.ascontiguousarray(aggs.ptr, dtype=np.int32)
-    if device_svd:
+    if svd is not None:
+        code, U, sig, failed_id = svd(rp, local, nv)
+    elif device_svd:
         code, U, sig, failed_id = _jacobi_svd_device(rp, local, nv)
     else:
         U = np.empty_like(local)
@@ -426,7 +434,7 @@ def block_prolongator(aggs, vectors, n_fine, tol=0.1, device_svd=False):
 
 
 def build_multivector_hierarchy(A, pairwise, vectors, merge_levels=3, tol=0.1, min_coarse_size=40,
-                                product=galerkin_product, device_svd=False):
+                                product=galerkin_product, device_svd=False, svd=None):
     """The single multi-vector hierarchy from a pairwise substrate and the
     finest-level smooth vectors (pkg/src/mvamg/multivector.py:262-321)."""
     t0 = time.perf_counter()
@@ -442,7 +450,7 @@ def build_multivector_hierarchy(A, pairwise, vectors, merge_levels=3, tol=0.1, m
         if mats[-1].shape[0] <= min_coarse_size:
             break
         ts = time.perf_counter()
-        bp = block_prolongator(aggs, vecs[-1], n_fine, tol, device_svd)
+        bp = block_prolongator(aggs, vecs[-1], n_fine, tol, device_svd, svd)
         svd_s += time.perf_counter() - ts
         if bp.P.shape[1] >= mats[-1].shape[0]:
             stalled = True
