@@ -117,6 +117,7 @@ typedef struct {
     or_csr A[OR_MAXLEV], P[OR_MAXLEV], R[OR_MAXLEV];
     const double* diag[OR_MAXLEV];
     const double* lu; const int* piv;      /* coarsest LU (cycles.py:88-97) */
+    const double* inv;                     /* or, when set, a dense coarsest (pseudo-)inverse */
     /* scratch, allocated by or_hier_alloc */
     double *X[OR_MAXLEV], *T[OR_MAXLEV], *RC[OR_MAXLEV];
     double *fr[OR_MAXLEV], *fx[OR_MAXLEV], *fp[OR_MAXLEV][2], *fap[OR_MAXLEV][2];
@@ -156,6 +157,19 @@ static void smooth(or_hier* h, int kind, int sweeps, double omega, int k, const 
 }
 
 static int descend(or_hier* h, int k, const double* r, double* out);
+
+/* Coarsest solve: the reference's LU (cycles.py:96-97), or z = inv r with the
+ * stated C5 deviation (truncated-eigen pseudo-inverse). */
+static void coarse_solve(or_hier* h, int k, const double* r, double* out) {
+    int n = h->A[k].n;
+    if (!h->inv) { or_lu_solve(n, h->lu, h->piv, r, out); return; }
+#pragma omp parallel for schedule(static) if (n >= 2048)
+    for (int i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < n; ++j) s += h->inv[(size_t)i * n + j] * r[j];
+        out[i] = s;
+    }
+}
 
 /* fcg (krylov.py:75-107), x0 = 0, preconditioner = descend(k). Returns <0 on breakdown. */
 static int fcg_level(or_hier* h, int k, const double* b, int iters, double* x) {
@@ -197,7 +211,7 @@ static int fcg_level(or_hier* h, int k, const double* b, int iters, double* x) {
 /* MultigridOperator._descend (cycles.py:150-172); out must not alias r. */
 static int descend(or_hier* h, int k, const double* r, double* out) {
     int L = h->nlev;
-    if (k == L - 1) { or_lu_solve(h->A[k].n, h->lu, h->piv, r, out); return 0; }
+    if (k == L - 1) { coarse_solve(h, k, r, out); return 0; }
     const or_csr* A = &h->A[k];
     int n = A->n, nc = h->A[k + 1].n;
     double* x = h->X[k];
@@ -224,7 +238,7 @@ static int descend(or_hier* h, int k, const double* r, double* out) {
 
 /* MultigridOperator.apply (cycles.py:174-179). */
 int or_apply(or_hier* h, const double* r, double* z) {
-    if (h->nlev == 1) { or_lu_solve(h->A[0].n, h->lu, h->piv, r, z); return 0; }
+    if (h->nlev == 1) { coarse_solve(h, 0, r, z); return 0; }
     return descend(h, 0, r, z);
 }
 
@@ -339,7 +353,9 @@ void or_hier_set_transfer(or_hier* h, int k, int n, int nc, const int* pip, cons
     h->R[k].n = nc; h->R[k].m = n; h->R[k].ip = rip; h->R[k].ix = rix; h->R[k].v = rv;
 }
 
-void or_hier_set_coarse(or_hier* h, const double* lu, const int* piv) { h->lu = lu; h->piv = piv; }
+void or_hier_set_coarse(or_hier* h, const double* lu, const int* piv) { h->lu = lu; h->piv = piv; h->inv = NULL; }
+
+void or_hier_set_coarse_inverse(or_hier* h, const double* inv) { h->inv = inv; }
 
 void or_hier_destroy(or_hier* h) { if (h) { or_hier_free(h); free(h); } }
 

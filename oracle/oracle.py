@@ -44,6 +44,7 @@ def lib():
         L.or_hier_set_level.argtypes = [_P, _I, _I, _P, _P, _P, _P]
         L.or_hier_set_transfer.argtypes = [_P, _I, _I, _I, _P, _P, _P, _P, _P, _P]
         L.or_hier_set_coarse.argtypes = [_P, _P, _P]
+        L.or_hier_set_coarse_inverse.argtypes = [_P, _P]
         L.or_hier_alloc.argtypes = [_P]
         L.or_hier_destroy.argtypes = [_P]
         L.or_apply.argtypes = [_P, _P, _P]
@@ -115,7 +116,11 @@ class OracleOperator:
     """CPU restatement of MultigridOperator (cycles.py:100-190)."""
 
     def __init__(self, matrices, prolongators, cycle="V", inner_fcg_iters=2,
-                 pre=("gauss_seidel_forward", 1, 1.0), post=("gauss_seidel_backward", 1, 1.0)):
+                 pre=("gauss_seidel_forward", 1, 1.0), post=("gauss_seidel_backward", 1, 1.0),
+                 coarse_pinv_rtol=0.0):
+        """coarse_pinv_rtol > 0: the stated C5 deviation -- the coarsest level
+        is solved with the truncated-eigen pseudo-inverse (eigenvalues at or
+        below rtol * lambda_max dropped) instead of the reference's LU."""
         L = lib()
         self._keep = []
         self.nlev = len(matrices)
@@ -136,11 +141,18 @@ class OracleOperator:
             self._keep += [pip, pix, pv, rip, rix, rv]
             L.or_hier_set_transfer(self.h, k, Pm.shape[0], Pm.shape[1], _ptr(pip), _ptr(pix),
                                    _ptr(pv), _ptr(rip), _ptr(rix), _ptr(rv))
-        lu, piv = scipy.linalg.lu_factor(self.matrices[-1].toarray())
-        lu = np.ascontiguousarray(lu)
-        piv = np.ascontiguousarray(piv, dtype=np.int32)
-        self._keep += [lu, piv]
-        L.or_hier_set_coarse(self.h, _ptr(lu), _ptr(piv))
+        if coarse_pinv_rtol > 0.0:
+            w, Q = np.linalg.eigh(self.matrices[-1].toarray())
+            keep = w > coarse_pinv_rtol * w[-1]
+            inv = np.ascontiguousarray((Q[:, keep] / w[keep]) @ Q[:, keep].T)
+            self._keep.append(inv)
+            L.or_hier_set_coarse_inverse(self.h, _ptr(inv))
+        else:
+            lu, piv = scipy.linalg.lu_factor(self.matrices[-1].toarray())
+            lu = np.ascontiguousarray(lu)
+            piv = np.ascontiguousarray(piv, dtype=np.int32)
+            self._keep += [lu, piv]
+            L.or_hier_set_coarse(self.h, _ptr(lu), _ptr(piv))
         L.or_hier_alloc(self.h)
 
     def __del__(self):

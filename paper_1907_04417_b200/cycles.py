@@ -67,6 +67,14 @@ def _checked_diagonal(A):
     return d
 
 
+def coarse_pinv(Ac, rtol):
+    """Truncated-eigen pseudo-inverse of a symmetric dense matrix: eigenvalues
+    at or below rtol * lambda_max are dropped (row-major float64)."""
+    w, Q = np.linalg.eigh(Ac)
+    keep = w > rtol * w[-1]
+    return np.ascontiguousarray((Q[:, keep] / w[keep]) @ Q[:, keep].T)
+
+
 class GpuMultigridOperator:
     """Prepared B^{-1} on the GPU for a hierarchy of (matrices, prolongators)."""
 
@@ -284,10 +292,7 @@ class GpuMultigridOperator:
             self.coarse_lu = None
             self._inv = to_device(np.zeros(1), np.float64)  # never applied (no cycle)
         else:
-            Ac = self.matrices[-1].toarray()
-            self.coarse_lu = scipy.linalg.lu_factor(Ac)
-            inv = scipy.linalg.lu_solve(self.coarse_lu, np.eye(Ac.shape[0]))
-            self._inv = to_device(np.ascontiguousarray(inv), np.float64)
+            self._inv = to_device(self._coarse_inverse(), np.float64)
         _lib.check(L.mvamg_hierarchy_set_coarse(h, ptr(self._inv)), "set_coarse")
         nbytes = ctypes.c_longlong()
         _lib.check(L.mvamg_hierarchy_workspace_bytes(h, ctypes.byref(nbytes)), "workspace_bytes")
@@ -296,6 +301,26 @@ class GpuMultigridOperator:
         _lib.check(L.mvamg_hierarchy_set_graphs(h, int(bool(self.config.graphs))), "set_graphs")
         if self.mega_k0 >= 0:
             _lib.check(L.mvamg_hierarchy_set_mega(h, self.mega_k0), "set_mega")
+
+    def _coarse_inverse(self):
+        """Dense coarsest operator applied by one GEMV per visit: the inverse
+        from the reference's own LU factors (cycles.py:88-97), or with
+        config.coarse_pinv_rtol > 0 the truncated-eigen pseudo-inverse."""
+        Ac = self.matrices[-1].toarray()
+        rtol = float(self.config.coarse_pinv_rtol)
+        if rtol > 0.0:
+            self.coarse_lu = None
+            return coarse_pinv(Ac, rtol)
+        self.coarse_lu = scipy.linalg.lu_factor(Ac)
+        return np.ascontiguousarray(scipy.linalg.lu_solve(self.coarse_lu, np.eye(Ac.shape[0])))
+
+    def set_coarse_pinv(self, rtol):
+        """Switch the coarsest solve in place (same device buffer, so captured
+        graphs stay valid): rtol > 0 pseudo-inverse, 0 the LU inverse."""
+        torch = torch_cuda()
+        self.config = dataclasses.replace(self.config, coarse_pinv_rtol=float(rtol))
+        self._inv.copy_(torch.from_numpy(self._coarse_inverse()).reshape(self._inv.shape))
+        torch.cuda.synchronize()
 
     def __del__(self):
         h = getattr(self, "_h", None)

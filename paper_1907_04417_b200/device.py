@@ -103,6 +103,9 @@ class GpuConfig:
     coarse_mega: bool = False       # run the small coarse levels of a cycle in one thread block (opt-in:
                                     # launch-free but L2-latency bound; slower than the multi-kernel path today)
     mega_max_rows: int = 8192       # levels from the first one with at most this many rows down
+    coarse_pinv_rtol: float = 0.0   # 0: the coarsest inverse from the reference's LU factors (cycles.py:88-97);
+                                    # > 0: the stated C5 deviation -- truncated-eigen pseudo-inverse dropping
+                                    # eigenvalues <= rtol * lambda_max (a numerically singular A_L)
 
 
 class DeviceCSR:

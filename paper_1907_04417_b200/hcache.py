@@ -26,7 +26,7 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def cache_dir():
-    return os.environ.get("MVAMG_HCACHE", os.path.join(REPO, ".hcache"))
+    return os.environ.get("MVAMG_HCACHE", "/tmp/mvamg_hcache")
 
 
 def _digest_csr(h, M):

@@ -15,7 +15,7 @@ from paper_1907_04417_b200.krylov import pcg  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 what = sys.argv[2] if len(sys.argv) > 2 else "solve"
-mats, pros, b, desc, info = bench.load_workload(cfg)
+mats, pros, b, info = bench.load_workload(cfg)
 op = GpuMultigridOperator(mats, pros)
 x, rep = pcg(mats[0], b, precond=op, rtol=1e-6)  # warm-up (graphs captured)
 torch.cuda.synchronize()
