@@ -396,6 +396,15 @@ def _level_sweeps(op, k, b_dev, x_old, x_new, ws, s):
                 name, name)
     fwd = bwd = None
     names = ["", ""]
+    st = lv.get("stream") or {}
+    if 0 in st:
+        fwd, names[0] = (lambda: st[0].sweep(b_dev, None, x_new, ws, s)), "gs_stream_kernel"
+    if 3 in st:
+        bwd, names[1] = (lambda: st[3].sweep(b_dev, x_old, x_new, ws, s)), "gs_stream_kernel"
+    elif 2 in st:
+        bwd, names[1] = (lambda: st[2].sweep(b_dev, x_old, x_new, ws, s, fold=True)), "gs_stream_kernel+fold"
+    if st:
+        return fwd, bwd, names[0], names[1]
     rows, levels = lv.get("rows") or {}, lv.get("levels") or {}
     if 0 in rows:
         fwd, names[0] = (lambda: rows[0].sweep(b_dev, None, x_new, ws, s)), "gs_row_kernel"

@@ -70,13 +70,17 @@ int mvamg_gs_set_trace(long long* trace_dev);
  * position-major shared window (threads x longest chain slots) fits
  * max_window slots.  Call first with the out arrays
  * NULL to get counts, then with arrays of nchains+1 / ntiles+1 ints.
+ * chain_order (nchains ints, or NULL for the natural order): the processing
+ * order of the chains -- tiles (and warps) are ranges of it, e.g. 2-D blocks
+ * of the grid lines of a 3-D problem, so that most line-to-line dependences
+ * stay inside a tile's shared window.
  * Replaces nothing in the reference (numba runs rows serially,
  * _kernels.py:15-38); the schedule preserves that order's dependency DAG, so
  * the sweep result is bit-identical.                                          */
 int mvamg_gs_analyse(int n, const int* indptr, const int* indices, int max_chain,
                      int max_threads, int max_window, int* nchains, int* ntiles,
                      int* chain_ptr, int* tile_ptr, int* threads_out, int* window_out,
-                     int* depth_out);
+                     int* depth_out, const int* chain_order);
 
 /* ---- stream-level kernels (device pointers) ------------------------------- */
 /* y = A x  (sparse.py:30-40; scipy csr_matvec order, bit-exact). */
@@ -110,12 +114,14 @@ int mvamg_csr_spmv_mode_f64(int mode, int n, int nnz, const int* indptr, const i
  * input comes from an earlier round.  perm[i] = 32 * (K * global round + slot)
  * + lane.  Query with
  * rec == NULL for *nwords / *nrounds / *nwarps / *max_S; then round_off holds
- * nrounds+1, tbase nwarps+1, tile_wbase ntiles+1, perm n ints. */
+ * nrounds+1, tbase nwarps+1, tile_wbase ntiles+1, perm n ints.  chain_order:
+ * as in mvamg_gs_analyse (every inter-warp input must lie in an earlier warp
+ * of that order; MVAMG_E_ARG otherwise). */
 int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double* data, int ntiles,
                       const int* chain_ptr, const int* tile_ptr, int window, int mode, int R,
                       int uniform_S, int rows_per_round, long long* nwords, int* nrounds, int* nwarps,
                       int* max_S, unsigned long long* rec, int* round_off, int* tbase, int* tile_wbase,
-                      int* perm);
+                      int* perm, const int* chain_order);
 /* One lexicographic GS sweep (_kernels.py:15-38) on device data.  direction
  * 0 = forward, 1 = backward; x_old is the iterate before the sweep (NULL for a
  * zero guess); x_new receives the result and must not alias x_old.  The CSR
@@ -134,8 +140,8 @@ int mvamg_gs_sweep_f64(int direction, int n, const int* indptr, const int* indic
                        const unsigned long long* rec, const int* round_off, const int* tbase,
                        const int* tile_wbase, const int* perm, double* tperm, int R, int D,
                        int lean_C, int slot_words, int rec_words_max, int ntiles,
-                       const int* chain_ptr, const int* tile_ptr, int threads, int window,
-                       const double* b, const double* x_old, double* x_new, int* ws, void* stream);
+                       const int* chain_ptr, const int* tile_ptr, const int* chain_order, int threads,
+                       int window, const double* b, const double* x_old, double* x_new, int* ws, void* stream);
 /* GS level-set schedule for small / mid-size levels (host).  mode 0 forward
  * from x = 0, 1 forward, 2 backward from x = 0, 3 backward.  Rows are
  * block-partitioned over a cluster of ncta (1..16) CTAs and, per CTA, ordered
@@ -163,6 +169,36 @@ int mvamg_gs_level_sweep_f64(int direction, int n, const int* indptr, const int*
                              int max_ents, int threads, int group, const int* lev_ptr, const int* lev_eptr,
                              const void* rows, const void* ents, const int* perm, double* tperm,
                              const double* b, const double* x_old, double* x_new, int* ws, void* stream);
+/* Streamed level-set GS plan for one SM (csrc/gs_stream.cuh) -- replaces the
+ * serial gs_forward / gs_backward loops of pkg/src/mvamg/_kernels.py:15-38 on
+ * coarse levels whose x (and, for a sweep from x_old, b) fit in shared memory.
+ * mode: 0 forward from x = 0, 1 forward from x_old, 2 backward from x = 0,
+ * 3 backward from x_old.  Rows are batched by their level in the sweep's
+ * dependency DAG and the batches packed, in sweep order, into stages of at
+ * most slot_bytes per CTA.  ncta > 1 (zero-guess modes 0 and 2 only): a
+ * thread-block cluster of that many CTAs, CTA c holding rows [c R, (c+1) R),
+ * R = ceil(n / ncta), and reading the others' x over DSMEM.  Call with blob ==
+ * NULL to get *blob_bytes and *nstages, then with a host blob of that size and
+ * stage_off of nstages * ncta + 1 entries. */
+int mvamg_gs_stream_plan(int n, const int* indptr, const int* indices, const double* data, int mode,
+                         int slot_bytes, int ncta, long long* blob_bytes, int* nstages, int* nlevels,
+                         unsigned char* blob, long long* stage_off);
+/* One GS sweep with a stream plan (device blob and stage offsets): ncta CTAs
+ * of 256 threads (one, or a cluster), x in shared memory, nslots stages of the plan in flight by TMA
+ * bulk copies.  group = 1: one thread per row, bit-identical to the serial
+ * loop; 2, 4, 8, 16: lanes per row with an FMA / shuffle-tree sum (tolerance
+ * parity).  x_old is read only by modes 1 and 3. */
+int mvamg_gs_stream_sweep_f64(int n, int mode, int nstages, int nslots, int slot_bytes, int group, int ncta,
+                              const void* blob, const long long* stage_off, const double* b,
+                              const double* x_old, double* x_new, void* stream);
+/* Backward GS sweep from x_old with a mode-2 (backward, zero guess) stream
+ * plan: t = b - (old lower neighbours) in CSR order into tfold (n doubles),
+ * then the zero-guess sweep on t -- bit-identical to the serial loop with
+ * group 1.  ws: >= 4 device ints. */
+int mvamg_gs_stream_sweep_folded_f64(int n, const int* indptr, const int* indices, const double* data, int nstages,
+                                     int nslots, int slot_bytes, int group, int ncta, const void* blob,
+                                     const long long* stage_off, double* tfold, const double* b,
+                                     const double* x_old, double* x_new, int* ws, void* stream);
 /* Backward GS sweep from x_old with the mode-2 (backward, zero guess) level
  * schedule: the old upper neighbours are folded into the right-hand side
  * first (same roundings), so the sweep reads only new values. */
@@ -294,7 +330,7 @@ int mvamg_hierarchy_destroy(mvamg_hierarchy* h);
 int mvamg_hierarchy_set_level(mvamg_hierarchy* h, int k, int n, int nnz, const int* indptr,
                               const int* indices, const double* data, const double* diag,
                               const double* rdiag, int ntiles, const int* chain_ptr,
-                              const int* tile_ptr, int gs_threads, int gs_window);
+                              const int* tile_ptr, const int* chain_order, int gs_threads, int gs_window);
 /* GS schedule of level k for sweep `mode` (see mvamg_gs_schedule), device. */
 int mvamg_hierarchy_set_gs_schedule(mvamg_hierarchy* h, int k, int mode, const unsigned long long* rec,
                                     const int* round_off, const int* tbase, const int* tile_wbase,
@@ -306,6 +342,16 @@ int mvamg_hierarchy_set_gs_levels(mvamg_hierarchy* h, int k, int mode, int ncta,
                                   int nlev, int max_rows, int max_ents, int threads, int group,
                                   const int* lev_ptr, const int* lev_eptr, const void* rows, const void* ents,
                                   const int* perm, double* tperm);
+/* Diagnostics: CTA 0 of every streamed sweep writes (tag, clock64) pairs --
+ * tag -2 before a stage's wait, -3 after it, the batch's rows after its
+ * barrier -- into trace_dev (cap int64s; [0] = entries used).  NULL: off. */
+int mvamg_gs_stream_set_trace(long long* trace_dev, int cap);
+/* Stream plan of level k for sweep `mode` (see mvamg_gs_stream_plan); used
+ * before every other schedule of that mode.  A mode-2 plan with tfold (n
+ * device doubles) also serves backward sweeps from x_old: the old lower
+ * neighbours are folded into the right-hand side first (same roundings). */
+int mvamg_hierarchy_set_gs_stream(mvamg_hierarchy* h, int k, int mode, int nstages, int nslots, int slot_bytes,
+                                  int group, int ncta, const void* blob, const long long* stage_off, double* tfold);
 /* Diagnostics: 4 x int64 %globaltimer stamps per segment written by the
  * chain-scan sweeps into trace_dev (NULL turns it off). */
 int mvamg_gs_scan_set_trace(long long* trace_dev);

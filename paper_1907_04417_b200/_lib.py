@@ -37,15 +37,15 @@ SIGNATURES = [
     ("mvamg_last_error", ctypes.c_char_p, []),
     ("mvamg_kernel_launches", _I, [ctypes.POINTER(_LL), _I]),
     ("mvamg_gs_set_trace", _I, [_P]),
-    ("mvamg_gs_analyse", _I, [_I, _P, _P, _I, _I, _I, _PI, _PI, _P, _P, _PI, _PI, _PI]),
+    ("mvamg_gs_analyse", _I, [_I, _P, _P, _I, _I, _I, _PI, _PI, _P, _P, _PI, _PI, _PI, _P]),
     ("mvamg_csr_spmv_f64", _I, [_I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_csr_residual_f64", _I, [_I, _P, _P, _P, _P, _P, _P, _P]),
     ("mvamg_csr_spmv_mode_f64", _I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
     ("mvamg_csr_spmv_add_f64", _I, [_I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_gs_schedule", _I, [_I, _P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _I, ctypes.POINTER(_LL), _PI, _PI,
-                               _PI, _P, _P, _P, _P, _P]),
+                               _PI, _P, _P, _P, _P, _P, _P]),
     ("mvamg_gs_sweep_f64", _I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P,
-                                _I, _I, _P, _P, _P, _P, _P]),
+                                _P, _I, _I, _P, _P, _P, _P, _P]),
     ("mvamg_gs_levels", _I, [_I, _P, _P, _P, _I, _I, _I, _I, _PI, ctypes.POINTER(_LL), _PI, _PI, _PI, _P, _P,
                              _P, _P, _P]),
     ("mvamg_gs_level_sweep_f64", _I, [_I, _I, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P,
@@ -54,6 +54,11 @@ SIGNATURES = [
                            _P]),
     ("mvamg_gs_row_sweep_f64", _I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P,
                                     _P, _P, _P, _P, _P]),
+    ("mvamg_gs_stream_plan", _I, [_I, _P, _P, _P, _I, _I, _I, ctypes.POINTER(_LL), _PI, _PI, _P, _P]),
+    ("mvamg_gs_stream_sweep_f64", _I, [_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
+    ("mvamg_gs_stream_sweep_folded_f64", _I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    ("mvamg_gs_stream_set_trace", _I, [_P, _I]),
+    ("mvamg_hierarchy_set_gs_stream", _I, [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P]),
     ("mvamg_greedy_match", _I, [_LL, _P, _P, _I, _P, _P, _P, ctypes.POINTER(_LL)]),
     ("mvamg_jacobi_svd_batch", _I, [_I, _P, _I, _P, _I, _D, _P, _P, _PI]),
     ("mvamg_gs_level_sweep_folded_f64", _I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P,
@@ -63,7 +68,7 @@ SIGNATURES = [
     ("mvamg_dot_ws_bytes", _I, []),
     ("mvamg_hierarchy_create", _I, [ctypes.POINTER(_P), _I, _I, _I, _I, _I, _D, _I, _I, _D]),
     ("mvamg_hierarchy_destroy", _I, [_P]),
-    ("mvamg_hierarchy_set_level", _I, [_P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _I, _I]),
+    ("mvamg_hierarchy_set_level", _I, [_P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _I, _I]),
     ("mvamg_hierarchy_set_gs_schedule", _I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I]),
     ("mvamg_hierarchy_set_gs_levels", _I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_hierarchy_set_gs_rows", _I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P]),

@@ -65,7 +65,8 @@ struct GsArgs {
   const int* tbase;              // first global round of each warp (nwarps + 1)
   const int* tile_wbase;         // first warp of each tile (ntiles + 1)
   const int* chain_ptr;
-  const int* tile_ptr;
+  const int* tile_ptr;           // tiles: ranges of the chain order
+  const int* chain_order;        // processing order of the chains (nullptr: natural order)
   const double* tperm;           // right-hand side in (round, lane) order
   const double* xold;
   double* xnew;
@@ -201,14 +202,15 @@ __global__ void __launch_bounds__(256, 1) gs_sweep_kernel(GsArgs a) {
     if (warp < nw) {
       const int g = w0 + warp;
       const int gr_base = a.tbase[g], nr = a.tbase[g + 1] - gr_base, nch = nr / R;
-      const int c = c0 + warp * 32 + lane;
+      const int cl = c0 + warp * 32 + lane;  // position in the chain order
       int cs = 0, len = 0;
-      if (c < c1) {
+      if (cl < c1) {
+        const int c = a.chain_order ? a.chain_order[cl] : cl;
         cs = a.chain_ptr[c];
         len = a.chain_ptr[c + 1] - cs;
       }
       const int ce = cs + len;
-      volatile unsigned long long* wslot = win + (c - c0);  // + q * TS: this lane's published rows
+      volatile unsigned long long* wslot = win + (cl - c0);  // + q * TS: this lane's published rows
       // chunk k (rounds [kR, kR+R)) -> slot k % D.  `ko` holds the chunk's round
       // offsets (lane j: round j), loaded a full ring cycle earlier, so issuing
       // never waits on memory.
@@ -496,14 +498,15 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
     if (warp >= nw) continue;
     const int g = w0 + warp;
     const int gr_base = a.tbase[g], nch = (a.tbase[g + 1] - gr_base) / R;
-    const int c = c0 + warp * 32 + lane;
+    const int cl = c0 + warp * 32 + lane;  // position in the chain order
     int cs = 0, len = 0;
-    if (c < c1) {
+    if (cl < c1) {
+      const int c = a.chain_order ? a.chain_order[cl] : cl;
       cs = a.chain_ptr[c];
       len = a.chain_ptr[c + 1] - cs;
     }
     const int ce = cs + len;
-    volatile unsigned long long* wslot = win + (c - c0);
+    volatile unsigned long long* wslot = win + (cl - c0);
     auto issue = [&](int k) {
       if (lane == 0) {
         const int d = k % D;
@@ -854,7 +857,7 @@ __global__ void __launch_bounds__(256) gs_prepare_kernel(int n, const int* __res
         s = __dsub_rn(s, __dmul_rn(__ldg(v + k), __ldg(xold + j)));
       }
     }
-    tperm[__ldg(perm + i)] = s;
+    tperm[perm ? __ldg(perm + i) : i] = s;
     reinterpret_cast<unsigned long long*>(xnew)[i] = kSentinel;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0;
@@ -887,7 +890,7 @@ __global__ void __launch_bounds__(256) gs_prepare_fold_warp_kernel(int n, const 
       if (m < 32) break;
     }
     if (lane == 0) {
-      tperm[__ldg(perm + i)] = s;
+      tperm[perm ? __ldg(perm + i) : i] = s;
       reinterpret_cast<unsigned long long*>(xnew)[i] = kSentinel;
     }
   }

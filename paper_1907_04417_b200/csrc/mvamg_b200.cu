@@ -26,6 +26,7 @@
 #include "coarse_mega.cuh"
 #include "galerkin.cuh"
 #include "gs_scan.cuh"
+#include "gs_stream.cuh"
 #include "matching.cuh"
 #include "svd.cuh"
 
@@ -140,7 +141,8 @@ struct Csr {
 struct GsPlan {
   int ntiles = 0, threads = 32, window = 0;
   const int* chain_ptr = nullptr;
-  const int* tile_ptr = nullptr;
+  const int* tile_ptr = nullptr;     // tiles: ranges of the chain order
+  const int* chain_order = nullptr;  // processing order of the chains (nullptr: natural)
 };
 
 // Static round schedule of one sweep mode (0 forward from x = 0, 1 forward,
@@ -170,6 +172,15 @@ struct GsLevels {
   int nlev = 0, max_rows = 0, max_ents = 0, threads = 256;
   int group = 1;  // lanes per row: 1 = bit-exact CSR order, 2..16 = tolerance parity
   int reg = 0;    // single CTA, group > 1: register-prefetch kernel (x only in shared memory)
+};
+
+// Streamed level-set schedule (gs_stream.cuh) of one sweep mode: one SM, x (and
+// b) in shared memory, level packets through a TMA ring.
+struct GsStream {
+  int nstages = 0, nslots = 0, slot_bytes = 0, group = 1, ncta = 1;
+  const unsigned char* blob = nullptr;
+  const long long* stage_off = nullptr;
+  double* tfold = nullptr;  // n doubles: folded right-hand side (mode-2 plan used from x_old)
 };
 
 // Chain-scan schedule (gs_scan.cuh) of one sweep mode (tolerance parity).
@@ -316,6 +327,7 @@ int launch_gs(bool fwd, const Csr& A, const GsList& ls, const GsPlan& p, const d
   a.tile_wbase = ls.tile_wbase;
   a.chain_ptr = p.chain_ptr;
   a.tile_ptr = p.tile_ptr;
+  a.chain_order = p.chain_order;
   a.tperm = ls.tperm;
   a.xold = xold;
   a.xnew = xnew;
@@ -394,6 +406,87 @@ size_t gs_level_smem(const GsLevels& g) {
   const size_t xw = (size_t)((g.rows_per_cta + 1) & ~1);
   const size_t buf = (size_t)g.max_rows * 32 + (size_t)g.max_ents * 16 + (((size_t)(g.max_rows + 2) * 8 + 15) & ~(size_t)15);
   return xw * 8 + 3 * buf;
+}
+
+// gs_stream_kernel on one SM.  with_old: x starts at x_old and b is kept in
+// shared memory too (every off-diagonal entry is in the plan); otherwise x
+// starts at b (a sweep from x = 0).
+long long* g_stream_trace = nullptr;  // diagnostics: mvamg_gs_stream_set_trace
+int g_stream_trace_cap = 0;
+
+size_t gs_stream_smem(int n, int with_old, const GsStream& g) {
+  const int R = g.ncta > 1 ? (n + g.ncta - 1) / g.ncta : n;
+  const size_t xw = (size_t)((R + 1) & ~1);
+  return xw * 8 * (with_old ? 2 : 1) + (size_t)g.nslots * (size_t)g.slot_bytes;
+}
+
+int launch_gs_stream(int n, const GsStream& g, int with_old, const double* b, const double* xold, double* xnew,
+                     cudaStream_t s) {
+  if (n == 0) return 0;
+  static bool attr = false;
+  if (!attr) {
+    attr = true;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+#define MVAMG_STREAM_ATTR(GG)                                                                                 \
+  cudaFuncSetAttribute(gs_stream_kernel<GG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024); \
+  cudaFuncSetAttribute(gs_stream_kernel<GG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);  \
+  cudaFuncSetAttribute(gs_stream_kernel<GG, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    MVAMG_STREAM_ATTR(1) MVAMG_STREAM_ATTR(2) MVAMG_STREAM_ATTR(4) MVAMG_STREAM_ATTR(8) MVAMG_STREAM_ATTR(16)
+#undef MVAMG_STREAM_ATTR
+    cudaGetLastError();
+  }
+  if (g.nslots < 1 || g.nslots > 8 || g.slot_bytes < 64 || (g.slot_bytes & 127))
+    return fail(MVAMG_E_ARG, "gs stream: 1..8 slots of a multiple of 128 bytes");
+  if (g.ncta < 1 || g.ncta > 16 || (g.ncta > 1 && with_old))
+    return fail(MVAMG_E_ARG, "gs stream: clusters of 1..16 CTAs, zero-guess plans only");
+  if (with_old && !xold) return fail(MVAMG_E_ARG, "gs stream: sweep from x_old without x_old");
+  const size_t smem = gs_stream_smem(n, with_old, g);
+  if (smem > (size_t)g_max_dyn_smem) return fail(MVAMG_E_ARG, "gs stream: x, b and the ring exceed shared memory");
+  GsStreamArgs a;
+  a.n = n;
+  a.with_old = with_old;
+  a.nstages = g.nstages;
+  a.nslots = g.nslots;
+  a.slot_bytes = g.slot_bytes;
+  a.blob = g.blob;
+  a.stage_off = g.stage_off;
+  a.b = b;
+  a.xold = xold;
+  a.xnew = xnew;
+  a.rows_per_cta = g.ncta > 1 ? (n + g.ncta - 1) / g.ncta : n;
+  a.trace = g_stream_trace;
+  a.trace_cap = g_stream_trace_cap;
+  void (*kern)(GsStreamArgs) = nullptr;
+  const bool clu = g.ncta > 1;
+  switch (g.group) {
+    case 1: kern = clu ? gs_stream_kernel<1, true> : gs_stream_kernel<1, false>; break;
+    case 2: kern = clu ? gs_stream_kernel<2, true> : gs_stream_kernel<2, false>; break;
+    case 4: kern = clu ? gs_stream_kernel<4, true> : gs_stream_kernel<4, false>; break;
+    case 8: kern = clu ? gs_stream_kernel<8, true> : gs_stream_kernel<8, false>; break;
+    case 16: kern = clu ? gs_stream_kernel<16, true> : gs_stream_kernel<16, false>; break;
+    default: return fail(MVAMG_E_ARG, "gs stream: lanes per row must be 1, 2, 4, 8 or 16");
+  }
+  if (!clu) {
+    kern<<<1, kStreamThreads, smem, s>>>(a);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)g.ncta);
+    cfg.blockDim = dim3(kStreamThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)g.ncta;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a));
+  }
+  CUDA_TRY(cudaGetLastError());
+  return 0;
 }
 
 bool g_level_attr = false;
@@ -673,6 +766,7 @@ struct Level {
   const double* rdiag = nullptr;
   GsPlan plan;
   GsList gl[3];
+  GsStream gss[4];  // streamed single-SM schedules (used first when set)
   GsLevels glv[4];  // small-level single-CTA schedules (used when set)
   GsRows grw[4];    // dataflow row schedules (used when set and glv is not)
   GsScan gsc[4];    // chain-scan schedules (tolerance parity; used first when set)
@@ -763,7 +857,14 @@ struct mvamg_hierarchy {
       } else {
         bool fwd = sp.kind == MVAMG_GS_FORWARD;
         int lmode = (fwd ? 0 : 2) + (x_cur == nullptr ? 0 : 1);
-        if (l.gsc[lmode].nchains) {
+        if (l.gss[lmode].nstages) {
+          st = launch_gs_stream(l.A.n, l.gss[lmode], x_cur != nullptr, b, x_cur, out, s);
+        } else if (!fwd && x_cur != nullptr && l.gss[2].nstages && l.gss[2].tfold) {
+          // backward from x_old with the zero-guess plan: fold the old lower
+          // neighbours into the right-hand side first (same roundings, CSR order)
+          launch_prepare(l.A, b, x_cur, nullptr, l.gss[2].tfold, out, ticket, 1, s);
+          st = launch_gs_stream(l.A.n, l.gss[2], 0, l.gss[2].tfold, nullptr, out, s);
+        } else if (l.gsc[lmode].nchains) {
           st = launch_gs_scan(l.A, l.gsc[lmode], lmode, b, x_cur, out, status_ptr(), s);
         } else if (!fwd && x_cur != nullptr && l.glv[2].rows) {
           st = launch_gs_levels(l.A, l.glv[2], false, b, x_cur, out, ticket, s, /*fold=*/true);
@@ -1267,7 +1368,7 @@ const char* mvamg_last_error(void) { return g_err.c_str(); }
 
 int mvamg_gs_analyse(int n, const int* indptr, const int* indices, int max_chain, int max_threads,
                      int max_window, int* nchains, int* ntiles, int* chain_ptr, int* tile_ptr,
-                     int* threads_out, int* window_out, int* depth_out) {
+                     int* threads_out, int* window_out, int* depth_out, const int* chain_order) {
   if (n < 0 || !indptr || (n > 0 && !indices) || !nchains || !ntiles)
     return fail(MVAMG_E_ARG, "gs_analyse: bad arguments");
   if (max_chain < 1) max_chain = 1;
@@ -1300,7 +1401,9 @@ int mvamg_gs_analyse(int n, const int* indptr, const int* indices, int max_chain
   tp.push_back(0);
   int cnt = 0, maxlen = 0, maxcnt = 1, maxslots = 1;
   for (int c = 0; c < nc; ++c) {
-    int cl = cp[c + 1] - cp[c];
+    const int oc = chain_order ? chain_order[c] : c;  // tiles are ranges of the chain order
+    if (oc < 0 || oc >= nc) return fail(MVAMG_E_ARG, "gs_analyse: chain order out of range");
+    int cl = cp[oc + 1] - cp[oc];
     if (cnt > 0 && (cnt + 1 > max_threads || (long long)r32(cnt + 1) * std::max(maxlen, cl) > max_window)) {
       tp.push_back(c);
       maxcnt = std::max(maxcnt, cnt);
@@ -1374,7 +1477,7 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
                       const int* chain_ptr, const int* tile_ptr, int window, int mode, int R,
                       int uniform_S, int rows_per_round, long long* nwords, int* nrounds, int* nwarps,
                       int* max_S, unsigned long long* rec, int* round_off, int* tbase, int* tile_wbase,
-                      int* perm) {
+                      int* perm, const int* chain_order) {
   if (n < 0 || !indptr || !chain_ptr || !tile_ptr || !nwords || !nrounds || !nwarps || mode < 0 ||
       mode > 2 || R < 1 || R > 31)
     return fail(MVAMG_E_ARG, "gs_schedule: bad arguments");
@@ -1399,12 +1502,38 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
   };
   auto lower = [&](int i, int j) { return fwd ? (j < i) : (j > i); };
   const int nch = tile_ptr[ntiles];
-  std::vector<int> chain_of(n > 0 ? n : 1);
+  if (chain_order && cluster > 1) return fail(MVAMG_E_ARG, "gs_schedule: chain order and cluster tiles exclude each other");
+  // chains are ranges of rows; warps / tiles are ranges of the chain order
+  // (position cl holds chain ord(cl)); `pos_of` inverts it
+  auto ord = [&](int cl) { return chain_order ? chain_order[cl] : cl; };
+  std::vector<int> chain_of(n > 0 ? n : 1), pos_of(nch > 0 ? nch : 1), lidx(n > 0 ? n : 1, 0);
   for (int c = 0; c < nch; ++c)
     for (int i = chain_ptr[c]; i < chain_ptr[c + 1]; ++i) chain_of[i] = c;
-  std::vector<int> tile_of_chain(nch > 0 ? nch : 1);
+  for (int cl = 0; cl < nch; ++cl) {
+    const int c = ord(cl);
+    if (c < 0 || c >= nch) return fail(MVAMG_E_ARG, "gs_schedule: chain order out of range");
+    pos_of[c] = cl;
+  }
+  std::vector<int> tile_of_chain(nch > 0 ? nch : 1), warp_of_chain(nch > 0 ? nch : 1);
   for (int t = 0; t < ntiles; ++t)
-    for (int c = tile_ptr[t]; c < tile_ptr[t + 1]; ++c) tile_of_chain[c] = t;
+    for (int cl = tile_ptr[t]; cl < tile_ptr[t + 1]; ++cl) tile_of_chain[ord(cl)] = t;
+  {
+    int w = 0;
+    for (int t = 0; t < ntiles; ++t)
+      for (int cA = tile_ptr[t]; cA < tile_ptr[t + 1]; cA += 32, ++w)
+        for (int cl = cA; cl < std::min(cA + 32, tile_ptr[t + 1]); ++cl) warp_of_chain[ord(cl)] = w;
+  }
+  // an inter-warp input must come from a warp earlier in processing order, or
+  // warps could wait on each other (the natural order of grid lines has it)
+  for (int i = 0; i < n; ++i)
+    for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+      const int j = indices[k];
+      if (j == i || !lower(i, j)) continue;
+      const int wi = warp_of_chain[chain_of[i]], wj = warp_of_chain[chain_of[j]];
+      if (wi != wj && (fwd ? wj > wi : wj < wi))
+        return fail(MVAMG_E_ARG, "gs_schedule: the chain order puts an input in a later warp");
+    }
+  std::vector<int> wrows;
   auto ptk = [&](int t) { return fwd ? t : ntiles - 1 - t; };  // processing order of tile t
   long long w = 0;
   int gr = 0, gw = 0, smax = 1;
@@ -1415,15 +1544,22 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
     if (tile_wbase) tile_wbase[t] = gw;
     for (int cA = c0; cA < c1; cA += 32, ++gw) {
       const int cB = std::min(cA + 32, c1);
-      const int rlo = chain_ptr[cA], rhi = chain_ptr[cB];
-      rnd.assign(rhi - rlo, 0);
-      slot_of.assign(rhi - rlo, 0);
+      // the warp's rows in sweep order (its chains need not be consecutive)
+      wrows.clear();
+      for (int cl = cA; cl < cB; ++cl)
+        for (int i = chain_ptr[ord(cl)]; i < chain_ptr[ord(cl) + 1]; ++i) wrows.push_back(i);
+      std::sort(wrows.begin(), wrows.end());
+      if (!fwd) std::reverse(wrows.begin(), wrows.end());
+      const int nwr = (int)wrows.size();
+      for (int q = 0; q < nwr; ++q) lidx[wrows[q]] = q;
+      rnd.assign(nwr, 0);
+      slot_of.assign(nwr, 0);
       int last[32], used[32];
       for (int L = 0; L < 32; ++L) last[L] = -1, used[L] = 0;
       int nr = 0;
-      for (int q = 0; q < rhi - rlo; ++q) {
-        const int i = fwd ? rlo + q : rhi - 1 - q;
-        const int L = chain_of[i] - cA;
+      for (int q = 0; q < nwr; ++q) {
+        const int i = wrows[q];
+        const int L = pos_of[chain_of[i]] - cA;
         const int c = chain_of[i], pred = fwd ? i - 1 : i + 1;
         const bool has_pred = fwd ? (i - 1 >= chain_ptr[c]) : (i + 1 < chain_ptr[c + 1]);
         // every intra-warp input other than the chain predecessor must come
@@ -1432,8 +1568,8 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
         int rmin = 0;
         for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
           const int j = indices[k];
-          if (j != i && lower(i, j) && j >= rlo && j < rhi && !(has_pred && j == pred))
-            rmin = std::max(rmin, rnd[j - rlo] + 1);
+          if (j != i && lower(i, j) && warp_of_chain[chain_of[j]] == gw && !(has_pred && j == pred))
+            rmin = std::max(rmin, rnd[lidx[j]] + 1);
         }
         int r;
         if (last[L] >= 0 && used[L] < K && rmin <= last[L]) {
@@ -1443,8 +1579,8 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
           r = std::max(last[L] + 1, rmin);
           used[L] = 1;
         }
-        rnd[i - rlo] = r;
-        slot_of[i - rlo] = used[L] - 1;
+        rnd[q] = r;
+        slot_of[q] = used[L] - 1;
         last[L] = r;
         nr = std::max(nr, r + 1);
       }
@@ -1453,8 +1589,8 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
       if (tbase) tbase[gw] = gr;
       // rows of each round: K slots per lane
       rows_of_round.assign((size_t)nr * K * 32, -1);
-      for (int i = rlo; i < rhi; ++i)
-        rows_of_round[((size_t)rnd[i - rlo] * K + slot_of[i - rlo]) * 32 + (chain_of[i] - cA)] = i;
+      for (int q = 0; q < nwr; ++q)
+        rows_of_round[((size_t)rnd[q] * K + slot_of[q]) * 32 + (pos_of[chain_of[wrows[q]]] - cA)] = wrows[q];
       for (int r = 0; r < nr; ++r, ++gr) {
         int maxcnt = -1;
         for (int L = 0; L < 32 * K; ++L) {
@@ -1499,10 +1635,10 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
                 code = (j << 2) | 3;
               } else if ((fwd && j == i - 1 && j >= cs) || (!fwd && j == i + 1 && j < ce)) {
                 code = 0;
-              } else if (chain_of[j] >= c0 && chain_of[j] < c1) {
+              } else if (tile_of_chain[chain_of[j]] == t) {
                 const int cj = chain_of[j];
                 const int pos = fwd ? j - chain_ptr[cj] : chain_ptr[cj + 1] - 1 - j;
-                const long long slot = (long long)pos * TS + (cj - c0);
+                const long long slot = (long long)pos * TS + (pos_of[cj] - c0);
                 if (slot >= window) return fail(MVAMG_E_ARG, "gs_schedule: window slot out of range");
                 code = (int)(slot << 2) | 1;
               } else {
@@ -1560,8 +1696,8 @@ int mvamg_gs_sweep_f64(int direction, int n, const int* indptr, const int* indic
                        const unsigned long long* rec, const int* round_off, const int* tbase,
                        const int* tile_wbase, const int* perm, double* tperm, int R, int D,
                        int lean_C, int slot_words, int rec_words_max, int ntiles,
-                       const int* chain_ptr, const int* tile_ptr, int threads, int window,
-                       const double* b, const double* x_old, double* x_new, int* ws, void* stream) {
+                       const int* chain_ptr, const int* tile_ptr, const int* chain_order, int threads,
+                       int window, const double* b, const double* x_old, double* x_new, int* ws, void* stream) {
   if (threads < 32 || threads > 256 || threads % 32) return fail(MVAMG_E_ARG, "gs: threads must be 32..256, multiple of 32");
   if (R != 1 && R != 2 && R != 4 && R != 8) return fail(MVAMG_E_ARG, "gs: R must be 1, 2, 4 or 8");
   if (D != 2 && D != 3 && D != 4 && D != 8) return fail(MVAMG_E_ARG, "gs: D must be 2, 3, 4 or 8");
@@ -1581,6 +1717,7 @@ int mvamg_gs_sweep_f64(int direction, int n, const int* indptr, const int* indic
                              "{(2,2,4), (2,3,4), (4,2,2)}");
   GsPlan p;
   p.ntiles = ntiles; p.threads = threads; p.window = window; p.chain_ptr = chain_ptr; p.tile_ptr = tile_ptr;
+  p.chain_order = chain_order;
   return launch_gs(direction == 0, A, ls, p, b, x_old, x_new, ws, ws + 1, (cudaStream_t)stream);
 }
 
@@ -1771,6 +1908,236 @@ int mvamg_hierarchy_set_gs_levels(mvamg_hierarchy* h, int k, int mode, int ncta,
   g.ents = static_cast<const GsLevelEntry*>(ents); g.perm = perm; g.tperm = tperm;
   g.nlev = nlev; g.max_rows = max_rows; g.max_ents = max_ents; g.threads = threads;
   g.ncta = ncta; g.rows_per_cta = rows_per_cta; g.group = group & 0xff; g.reg = (group >> 8) & 1;
+  return 0;
+}
+
+// Streamed level-set plan (gs_stream.cuh).  Call with blob == nullptr to size
+// it (*blob_bytes, *nstages), then with buffers of those sizes.  Rows go into
+// batches by their level in the sweep's dependency DAG -- for a sweep from
+// x_old also after every row whose old value they read on the other side
+// (anti-dependence through the transposed pattern) -- in sweep order within a
+// level.  With ncta > 1 CTA c owns rows [c R, (c+1) R), R = ceil(n / ncta),
+// and its blob of stage s holds its rows of that stage's batches; a level
+// whose part on some CTA exceeds a slot is split into several batches on all.
+int mvamg_gs_stream_plan(int n, const int* indptr, const int* indices, const double* data, int mode,
+                         int slot_bytes, int ncta, long long* blob_bytes, int* nstages, int* nlevels,
+                         unsigned char* blob, long long* stage_off) {
+  if (n < 0 || !indptr || (n > 0 && (!indices || !data)) || mode < 0 || mode > 3 || slot_bytes < 256 ||
+      !blob_bytes || !nstages || ncta < 1 || ncta > 16 || (ncta > 1 && (mode & 1)))
+    return fail(MVAMG_E_ARG, "gs_stream_plan: bad arguments (clusters: zero-guess modes only)");
+  const bool fwd = mode < 2, old = (mode & 1) != 0;
+  const int R = ncta > 1 ? (n + ncta - 1) / ncta : std::max(n, 1);
+  if (ncta > 1 && R >= (1 << 24)) return fail(MVAMG_E_ARG, "gs_stream_plan: slice too large to encode");
+  auto dep = [&](int i, int j) { return fwd ? j < i : j > i; };
+  auto keep = [&](int i, int j) { return j != i && (old || dep(i, j)); };
+  std::vector<int> lvl(n > 0 ? n : 1, 0), cnt(n > 0 ? n : 1, 0);
+  std::vector<double> dg(n > 0 ? n : 1, 0.0);
+  // transposed pattern (anti-dependences of a sweep from x_old)
+  std::vector<int> tp, tix;
+  if (old) {
+    tp.assign(n + 1, 0);
+    for (int i = 0; i < n; ++i)
+      for (int k = indptr[i]; k < indptr[i + 1]; ++k) tp[indices[k] + 1]++;
+    for (int i = 0; i < n; ++i) tp[i + 1] += tp[i];
+    tix.resize(tp[n] > 0 ? tp[n] : 1);
+    std::vector<int> cur(tp.begin(), tp.end() - 1);
+    for (int i = 0; i < n; ++i)
+      for (int k = indptr[i]; k < indptr[i + 1]; ++k) tix[cur[indices[k]]++] = i;
+  }
+  int nl = 0;
+  for (int q = 0; q < n; ++q) {
+    const int i = fwd ? q : n - 1 - q;
+    int m = 0;
+    for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+      const int j = indices[k];
+      if (j == i) dg[i] = data[k];
+      if (keep(i, j)) ++cnt[i];
+      if (j != i && dep(i, j)) m = std::max(m, lvl[j] + 1);
+    }
+    if (old)  // row r read x_old[i] on its other side: i must run after r
+      for (int k = tp[i]; k < tp[i + 1]; ++k) {
+        const int r = tix[k];
+        if (r != i && dep(i, r)) m = std::max(m, lvl[r] + 1);
+      }
+    lvl[i] = m;
+    nl = std::max(nl, m + 1);
+  }
+  if (n > 0 && *std::min_element(dg.begin(), dg.begin() + n) == 0.0)
+    return fail(MVAMG_E_NOT_SPD, "gs_stream_plan: zero diagonal");
+  // rows by (level, CTA), sweep order within
+  const int NC = ncta;
+  std::vector<int> lp((size_t)nl * NC + 1, 0), order(n > 0 ? n : 1);
+  for (int i = 0; i < n; ++i) lp[(size_t)lvl[i] * NC + i / R + 1]++;
+  for (size_t t = 0; t + 1 < lp.size(); ++t) lp[t + 1] += lp[t];
+  {
+    std::vector<int> cur(lp.begin(), lp.end() - 1);
+    for (int q = 0; q < n; ++q) {
+      const int i = fwd ? q : n - 1 - q;
+      order[cur[(size_t)lvl[i] * NC + i / R]++] = i;
+    }
+  }
+  auto a16 = [](long long v) { return (v + 15) & ~15LL; };
+  auto stage_size = [&](long long nb, long long nr, long long ne) {
+    return a16(a16(a16(16 + 8 * nb) + 32 * nr + 8 * ne) + 4 * ne);
+  };
+  // batches: per CTA a (first position, rows) range of `order`; a level split
+  // where one CTA's part does not fit a slot (same split count on every CTA)
+  struct Part { int p, r; long long e; };
+  std::vector<std::vector<Part>> batches;  // batch -> NC parts
+  for (int l = 0; l < nl; ++l) {
+    int parts = 1;
+    std::vector<std::vector<Part>> chunks(NC);
+    for (int c = 0; c < NC; ++c) {
+      const int b0 = lp[(size_t)l * NC + c], b1 = lp[(size_t)l * NC + c + 1];
+      int p = b0;
+      while (p < b1) {
+        int q = p;
+        long long ne = 0;
+        while (q < b1 && stage_size(1, q - p + 1, ne + cnt[order[q]]) <= slot_bytes) ne += cnt[order[q++]];
+        if (q == p) return fail(MVAMG_E_ARG, "gs_stream_plan: a row does not fit one slot");
+        chunks[c].push_back({p, q - p, ne});
+        p = q;
+      }
+      parts = std::max(parts, (int)chunks[c].size());
+    }
+    for (int k = 0; k < parts; ++k) {
+      std::vector<Part> bt(NC);
+      for (int c = 0; c < NC; ++c) bt[c] = k < (int)chunks[c].size() ? chunks[c][k] : Part{0, 0, 0};
+      batches.push_back(bt);
+    }
+  }
+  // stages: consecutive batches while every CTA's part of the stage fits a slot
+  std::vector<std::pair<int, int>> stages;  // (first batch, batches)
+  {
+    size_t bi = 0;
+    while (bi < batches.size()) {
+      size_t bj = bi;
+      std::vector<long long> nr(NC, 0), ne(NC, 0);
+      while (bj < batches.size()) {
+        bool fits = true;
+        for (int c = 0; c < NC && fits; ++c)
+          fits = stage_size((long long)(bj - bi + 1), nr[c] + batches[bj][c].r, ne[c] + batches[bj][c].e) <=
+                 slot_bytes;
+        if (!fits) break;
+        for (int c = 0; c < NC; ++c) {
+          nr[c] += batches[bj][c].r;
+          ne[c] += batches[bj][c].e;
+        }
+        ++bj;
+      }
+      stages.push_back({(int)bi, (int)(bj - bi)});
+      bi = bj;
+    }
+  }
+  const size_t NS = stages.size();
+  std::vector<long long> off(NS * NC + 1, 0);
+  long long total = 0;
+  for (size_t s = 0; s < NS; ++s)
+    for (int c = 0; c < NC; ++c) {
+      long long nr = 0, ne = 0;
+      for (int b = stages[s].first; b < stages[s].first + stages[s].second; ++b) {
+        nr += batches[b][c].r;
+        ne += batches[b][c].e;
+      }
+      total += stage_size(stages[s].second, nr, ne);
+      off[s * NC + c + 1] = total;
+    }
+  *blob_bytes = total;
+  *nstages = (int)NS;
+  if (nlevels) *nlevels = nl;
+  if (!blob) return 0;
+  if (!stage_off) return fail(MVAMG_E_ARG, "gs_stream_plan: stage offsets buffer missing");
+  std::memset(blob, 0, (size_t)total);
+  for (size_t s = 0; s < NS; ++s)
+    for (int c = 0; c < NC; ++c) {
+      unsigned char* st = blob + off[s * NC + c];
+      const int b0 = stages[s].first, nb = stages[s].second;
+      unsigned nr = 0, ne = 0;
+      for (int b = b0; b < b0 + nb; ++b) {
+        nr += (unsigned)batches[b][c].r;
+        ne += (unsigned)batches[b][c].e;
+      }
+      unsigned* hdr = reinterpret_cast<unsigned*>(st);
+      hdr[0] = (unsigned)nb;
+      hdr[1] = nr;
+      hdr[2] = ne;
+      const long long rows_off = a16(16 + 8LL * nb), coef_off = rows_off + 32LL * nr;
+      const long long src_off = a16(coef_off + 8LL * ne);
+      GsStreamRow* rows = reinterpret_cast<GsStreamRow*>(st + rows_off);
+      double* coef = reinterpret_cast<double*>(st + coef_off);
+      unsigned* src = reinterpret_cast<unsigned*>(st + src_off);
+      unsigned r = 0, e = 0;
+      for (int b = b0; b < b0 + nb; ++b) {
+        hdr[4 + 2 * (b - b0)] = r;
+        hdr[5 + 2 * (b - b0)] = (unsigned)batches[b][c].r;
+        for (int t = 0; t < batches[b][c].r; ++t, ++r) {
+          const int i = order[batches[b][c].p + t];
+          GsStreamRow& m = rows[r];
+          m.row = (unsigned)(i - c * (NC > 1 ? R : 0));
+          m.cnt = (unsigned)cnt[i];
+          m.ebeg = e;
+          m.pad = 0;
+          m.diag = dg[i];
+          m.rdiag = 1.0 / dg[i];
+          for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+            const int j = indices[k];
+            if (!keep(i, j)) continue;
+            coef[e] = data[k];
+            src[e] = NC > 1 ? ((unsigned)(j / R) << 24) | (unsigned)(j % R) : (unsigned)j;
+            ++e;
+          }
+        }
+      }
+    }
+  std::copy(off.begin(), off.end(), stage_off);
+  return 0;
+}
+
+int mvamg_gs_stream_sweep_f64(int n, int mode, int nstages, int nslots, int slot_bytes, int group, int ncta,
+                              const void* blob, const long long* stage_off, const double* b, const double* x_old,
+                              double* x_new, void* stream) {
+  if (n < 0 || mode < 0 || mode > 3 || (n > 0 && (!blob || !stage_off || !b || !x_new)))
+    return fail(MVAMG_E_ARG, "gs_stream_sweep: bad arguments");
+  GsStream g;
+  g.nstages = nstages; g.nslots = nslots; g.slot_bytes = slot_bytes; g.group = group; g.ncta = ncta;
+  g.blob = static_cast<const unsigned char*>(blob);
+  g.stage_off = stage_off;
+  return launch_gs_stream(n, g, mode & 1, b, x_old, x_new, (cudaStream_t)stream);
+}
+
+int mvamg_gs_stream_sweep_folded_f64(int n, const int* indptr, const int* indices, const double* data, int nstages,
+                                     int nslots, int slot_bytes, int group, int ncta, const void* blob,
+                                     const long long* stage_off, double* tfold, const double* b,
+                                     const double* x_old, double* x_new, int* ws, void* stream) {
+  if (n < 0 || (n > 0 && (!indptr || !indices || !data || !blob || !stage_off || !tfold || !b || !x_old || !x_new ||
+                          !ws)))
+    return fail(MVAMG_E_ARG, "gs_stream_sweep_folded: bad arguments");
+  Csr A;
+  A.n = n; A.m = n; A.ip = indptr; A.ix = indices; A.v = data;
+  A.nnz = 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  GsStream g;
+  g.nstages = nstages; g.nslots = nslots; g.slot_bytes = slot_bytes; g.group = group; g.ncta = ncta;
+  g.blob = static_cast<const unsigned char*>(blob);
+  g.stage_off = stage_off;
+  launch_prepare(A, b, x_old, nullptr, tfold, x_new, ws, 1, s);
+  return launch_gs_stream(n, g, 0, tfold, nullptr, x_new, s);
+}
+
+int mvamg_gs_stream_set_trace(long long* trace_dev, int cap) {
+  g_stream_trace = trace_dev;
+  g_stream_trace_cap = trace_dev ? cap : 0;
+  return 0;
+}
+
+int mvamg_hierarchy_set_gs_stream(mvamg_hierarchy* h, int k, int mode, int nstages, int nslots, int slot_bytes,
+                                  int group, int ncta, const void* blob, const long long* stage_off, double* tfold) {
+  if (!h || k < 0 || k >= h->L || mode < 0 || mode > 3) return fail(MVAMG_E_ARG, "set_gs_stream: bad index");
+  GsStream& g = h->lv[k].gss[mode];
+  g.nstages = nstages; g.nslots = nslots; g.slot_bytes = slot_bytes; g.group = group; g.ncta = ncta;
+  g.blob = static_cast<const unsigned char*>(blob);
+  g.stage_off = stage_off;
+  g.tfold = tfold;
   return 0;
 }
 
@@ -2113,7 +2480,7 @@ int mvamg_hierarchy_destroy(mvamg_hierarchy* h) {
 int mvamg_hierarchy_set_level(mvamg_hierarchy* h, int k, int n, int nnz, const int* indptr,
                               const int* indices, const double* data, const double* diag,
                               const double* rdiag, int ntiles, const int* chain_ptr,
-                              const int* tile_ptr, int gs_threads, int gs_window) {
+                              const int* tile_ptr, const int* chain_order, int gs_threads, int gs_window) {
   if (!h || k < 0 || k >= h->L) return fail(MVAMG_E_ARG, "set_level: bad level index");
   Level& l = h->lv[k];
   l.A.n = n; l.A.m = n; l.A.nnz = nnz; l.A.ip = indptr; l.A.ix = indices; l.A.v = data;
@@ -2122,6 +2489,7 @@ int mvamg_hierarchy_set_level(mvamg_hierarchy* h, int k, int n, int nnz, const i
   l.plan.ntiles = ntiles;
   l.plan.chain_ptr = chain_ptr;
   l.plan.tile_ptr = tile_ptr;
+  l.plan.chain_order = chain_order;
   l.plan.threads = gs_threads;
   l.plan.window = gs_window;
   return 0;

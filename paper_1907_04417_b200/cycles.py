@@ -17,7 +17,8 @@ import scipy.linalg
 import scipy.sparse.linalg as spla
 
 from . import _lib
-from .device import (DeviceCSR, DeviceGsLevels, DeviceGsPlan, DeviceGsRows, GpuConfig, as_csr,
+from .device import (DeviceCSR, DeviceGsLevels, DeviceGsPlan, DeviceGsRows, DeviceGsStream, GpuConfig, as_csr,
+                     stream_ctas,
                      autotune_coarse_gs, autotune_scan_gs,
                      level_gs_fits, ptr, row_gs_fits,
                      stream_handle, to_device, torch_cuda)
@@ -139,6 +140,24 @@ class GpuMultigridOperator:
                 modes.add(1)
         return sorted(modes)
 
+    def _gs_stream_modes(self, A):
+        """Stream plans the cycle needs for level matrix A: {mode: plan mode}
+        (a backward sweep from x_old that does not fit with b in shared memory
+        runs the folded mode-2 plan); None when a needed mode cannot stream."""
+        need = {}
+        for spec, first_zero in ((self.pre_smoother, True), (self.post_smoother, False)):
+            if spec.kind == WEIGHTED_JACOBI or spec.sweeps == 0:
+                continue
+            base = 0 if spec.kind == GS_FORWARD else 2
+            for m in ({base + (0 if first_zero else 1)} | ({base + 1} if spec.sweeps > 1 else set())):
+                if stream_ctas(A, m, self.config):
+                    need[m] = m
+                elif m == 3 and stream_ctas(A, 2, self.config):
+                    need[m] = 2
+                else:
+                    return None
+        return need
+
     def _gs_scan_modes(self):
         """Sweep modes of the chain-scan schedule (0 fwd x=0, 1 fwd, 2 bwd x=0, 3 bwd)."""
         modes = set()
@@ -200,9 +219,21 @@ class GpuMultigridOperator:
                     self.gs_plans.append(None)
                     self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=small, mega=True))
                     _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
-                                                           None, 0, None, None, 32, 0), "set_level")
+                                                           None, 0, None, None, None, 32, 0), "set_level")
                     for m, s in small.items():
                         _lib.check(L.mvamg_hierarchy_set_gs_levels(h, k, m, *s.args()), "set_gs_levels")
+                    continue
+                smodes = (self._gs_stream_modes(A) if cfg.stream_gs and not cfg.generic_gs
+                          and not cfg.force_level_gs and not cfg.force_row_gs else None)
+                if smodes:
+                    # streamed level-set sweeps on one SM (x, b in shared memory)
+                    plans = {pm: DeviceGsStream(A, pm, cfg) for pm in set(smodes.values())}
+                    self.gs_plans.append(None)
+                    self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=None, rows=None, stream=plans))
+                    _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
+                                                           None, 0, None, None, None, 32, 0), "set_level")
+                    for pm, sp in plans.items():
+                        _lib.check(L.mvamg_hierarchy_set_gs_stream(h, k, pm, *sp.args()), "set_gs_stream")
                     continue
                 if (k >= 1 and self.config.autotune_gs and not self.config.generic_gs
                         and not self.config.force_level_gs and not self.config.force_row_gs
@@ -212,7 +243,7 @@ class GpuMultigridOperator:
                     self.gs_plans.append(None)
                     lv = dict(A=dA, gs=None, plan=None, levels=None, rows=None)
                     _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
-                                                           None, 0, None, None, 32, 0), "set_level")
+                                                           None, 0, None, None, None, 32, 0), "set_level")
                     for m, s in pick.items():
                         if isinstance(s, DeviceGsRows):
                             lv["rows"] = lv["rows"] or {}
@@ -230,7 +261,7 @@ class GpuMultigridOperator:
                     self.gs_plans.append(None)
                     self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=None, rows=rows))
                     _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
-                                                           None, 0, None, None, 32, 0), "set_level")
+                                                           None, 0, None, None, None, 32, 0), "set_level")
                     for m, s in rows.items():
                         _lib.check(L.mvamg_hierarchy_set_gs_rows(h, k, m, *s.hierarchy_args()), "set_gs_rows")
                     continue
@@ -245,7 +276,7 @@ class GpuMultigridOperator:
                     self.gs_plans.append(None)
                     self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=small))
                     _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
-                                                           None, 0, None, None, 32, 0), "set_level")
+                                                           None, 0, None, None, None, 32, 0), "set_level")
                     for m, s in small.items():
                         _lib.check(L.mvamg_hierarchy_set_gs_levels(h, k, m, *s.args()), "set_gs_levels")
                     continue
@@ -257,7 +288,7 @@ class GpuMultigridOperator:
                     self.gs_plans.append(None)
                     self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=None, rows=rows))
                     _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
-                                                           None, 0, None, None, 32, 0), "set_level")
+                                                           None, 0, None, None, None, 32, 0), "set_level")
                     for m, s in rows.items():
                         _lib.check(L.mvamg_hierarchy_set_gs_rows(h, k, m, *s.hierarchy_args()), "set_gs_rows")
                     continue
@@ -271,7 +302,7 @@ class GpuMultigridOperator:
                         _lib.check(L.mvamg_hierarchy_set_gs_scan(h, k, m, *sc.args()), "set_gs_scan")
                 _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
                                                        None, gp.plan.ntiles, ptr(gp.chain_ptr),
-                                                       ptr(gp.tile_ptr), gp.plan.threads,
+                                                       ptr(gp.tile_ptr), ptr(gp.chain_order), gp.plan.threads,
                                                        gp.plan.window), "set_level")
                 for m in self._gs_modes():
                     sch = gp.mode(m)
@@ -281,7 +312,7 @@ class GpuMultigridOperator:
                         sch["lean_C"], sch["slot_words"], sch["rec_words_max"]), "set_gs_schedule")
             else:
                 _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), None, None, 0,
-                                                       None, None, 32, 0), "set_level")
+                                                       None, None, None, 32, 0), "set_level")
         for k, (P, R) in enumerate(zip(self.prolongators, self.restrictions)):
             dP, dR = DeviceCSR(P), DeviceCSR(R)
             self._keep += [dP, dR]

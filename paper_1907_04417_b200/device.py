@@ -103,6 +103,15 @@ class GpuConfig:
     coarse_mega: bool = False       # run the small coarse levels of a cycle in one thread block (opt-in:
                                     # launch-free but L2-latency bound; slower than the multi-kernel path today)
     mega_max_rows: int = 8192       # levels from the first one with at most this many rows down
+    block_chains: bool = True       # 3-D grid lines: tiles of 2-D blocks of lines (chain_block_order), so a
+                                    # line's z-neighbour is mostly in the same tile's shared window
+    stream_gs: bool = True          # levels whose x (and b) fit one SM's shared memory: the streamed level-set
+                                    # sweep (gs_stream.cuh: TMA ring of level packets), before any other schedule
+    stream_slot_bytes: int = 65536  # largest ring slot of the streamed sweep (four slots fill the free smem)
+    stream_entries_per_cta: int = 1 << 30  # entries a sweep streams per SM before it spreads over a cluster
+                                    # (clusters measured slower than the row sweep on C3: off by default)
+    stream_max_rows: int = 4096     # levels up to this size stream (C3: 1.3-1.9x the level-set / row sweeps
+                                    # at <= 1.8k rows, equal at 5k)
     coarse_pinv_rtol: float = 0.0   # 0: the coarsest inverse from the reference's LU factors (cycles.py:88-97);
                                     # > 0: the stated C5 deviation -- truncated-eigen pseudo-inverse dropping
                                     # eigenvalues <= rtol * lambda_max (a numerically singular A_L)
@@ -196,6 +205,50 @@ def _gs_ring(A, cfg):
     return 0, R, D, R * (32 * S + 32), S
 
 
+def chain_block_order(A, chain_ptr, T):
+    """Processing order of the chains for 2-D blocked tiles, or None.
+
+    The chains of a natural ordering of a 3-D grid problem are its x-lines,
+    numbered c = y + G z; line (y, z) depends on lines (y-1, z) and (y, z-1).
+    Consecutive chains per tile (the natural order) put every z-neighbour in
+    another tile, so the sweep's critical path crosses ~G tiles through L2.
+    Blocks of by x bz lines per tile (T = by * bz chains; within a tile z-major
+    pairs of y-runs per warp) keep both neighbours in the tile's shared window
+    for all but the block faces: ~G/by + G/bz cross-tile hops.  Detected from
+    the chain-to-chain dependence offsets (1 and a dominant G > 1); every
+    input still lies in an earlier block (tiles run in order), which
+    mvamg_gs_schedule verifies.  None when there is no such structure."""
+    nch = chain_ptr.shape[0] - 1
+    if nch < 4 * T or T < 32:
+        return None
+    n = A.shape[0]
+    chain_of = np.repeat(np.arange(nch, dtype=np.int64), np.diff(chain_ptr))
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(A.indptr))
+    lo = A.indices < rows
+    d = chain_of[rows[lo]] - chain_of[A.indices[lo]]
+    d = d[d > 1]
+    if d.size == 0:
+        return None
+    vals, cnt = np.unique(d, return_counts=True)
+    G = int(vals[np.argmax(cnt)])
+    if cnt.max() < 0.9 * d.size or nch % G or G < 8:
+        return None
+    Z = nch // G
+    bz = 1
+    while bz * bz * 2 <= T:
+        bz *= 2
+    by = T // bz
+    if by < 8 or Z < 2 * bz:
+        return None
+    order = []
+    for z0 in range(0, Z, bz):
+        for y0 in range(0, G, by):
+            zz = np.arange(z0, min(z0 + bz, Z))
+            yy = np.arange(y0, min(y0 + by, G))
+            order.append((yy[None, :] + G * zz[:, None]).ravel())
+    return np.ascontiguousarray(np.concatenate(order), dtype=np.int32)
+
+
 def gs_analyse(A, cfg=None):
     """Chain/tile schedule of a CSR matrix for the exact-order GS sweep (host).
 
@@ -216,12 +269,12 @@ def gs_analyse(A, cfg=None):
     # e.g. a grid line): keep chains whole and pick the widest tile whose
     # position-major window still fits; split chains only if one warp cannot hold them
     _lib.check(L.mvamg_gs_analyse(n, c_ip, c_ix, min(cfg.max_chain, 1 << 30), 1, 1 << 30, ctypes.byref(nch),
-                                  ctypes.byref(nt), None, None, None, None, None), "gs_analyse")
+                                  ctypes.byref(nt), None, None, None, None, None, None), "gs_analyse")
     cp0 = np.empty(nch.value + 1, dtype=np.int32)
     tp0 = np.empty(nt.value + 1, dtype=np.int32)
     _lib.check(L.mvamg_gs_analyse(n, c_ip, c_ix, min(cfg.max_chain, 1 << 30), 1, 1 << 30, ctypes.byref(nch),
                                   ctypes.byref(nt), cp0.ctypes.data_as(ctypes.c_void_p),
-                                  tp0.ctypes.data_as(ctypes.c_void_p), None, None, None), "gs_analyse")
+                                  tp0.ctypes.data_as(ctypes.c_void_p), None, None, None, None), "gs_analyse")
     lmax = int(np.diff(cp0).max()) if nch.value else 1
     T, slots, max_chain = 32, 0, 1
     for T_ in (256, 128, 64, 32):
@@ -235,15 +288,27 @@ def gs_analyse(A, cfg=None):
         raise ValueError(f"GS ring of {ring_warp} bytes per warp does not fit shared memory")
     T = min(T, max(1, cfg.max_threads))
     max_chain = max(1, min(cfg.max_chain, lmax, slots // max(32, (T + 31) // 32 * 32)))
+    order = None
+    if cfg.block_chains and not cfg.lean_cluster:
+        _lib.check(L.mvamg_gs_analyse(n, c_ip, c_ix, max_chain, T, slots, ctypes.byref(nch),
+                                      ctypes.byref(nt), None, None, None, None, None, None), "gs_analyse")
+        cpn = np.empty(nch.value + 1, dtype=np.int32)
+        tpn = np.empty(nt.value + 1, dtype=np.int32)
+        _lib.check(L.mvamg_gs_analyse(n, c_ip, c_ix, max_chain, T, slots, ctypes.byref(nch), ctypes.byref(nt),
+                                      cpn.ctypes.data_as(ctypes.c_void_p), tpn.ctypes.data_as(ctypes.c_void_p),
+                                      None, None, None, None), "gs_analyse")
+        order = chain_block_order(A, cpn, T)
+    vo = order.ctypes.data_as(ctypes.c_void_p) if order is not None else None
     _lib.check(L.mvamg_gs_analyse(n, c_ip, c_ix, max_chain, T, slots, ctypes.byref(nch),
-                                  ctypes.byref(nt), None, None, None, None, None), "gs_analyse")
+                                  ctypes.byref(nt), None, None, None, None, None, vo), "gs_analyse")
     cp = np.empty(nch.value + 1, dtype=np.int32)
     tp = np.empty(nt.value + 1, dtype=np.int32)
     _lib.check(L.mvamg_gs_analyse(n, c_ip, c_ix, max_chain, T, slots, ctypes.byref(nch),
                                   ctypes.byref(nt), cp.ctypes.data_as(ctypes.c_void_p),
                                   tp.ctypes.data_as(ctypes.c_void_p), ctypes.byref(thr),
-                                  ctypes.byref(win), ctypes.byref(dep)), "gs_analyse")
+                                  ctypes.byref(win), ctypes.byref(dep), vo), "gs_analyse")
     plan = GsPlanHost(nch.value, nt.value, max(32, thr.value), max(win.value, 1), dep.value, cp, tp)
+    plan.chain_order = order
     plan.lean_C, plan.R, plan.D = C, R, D
     plan.smem_budget = cfg.smem_budget
     return plan
@@ -275,13 +340,15 @@ def gs_schedule(A, plan, mode, R=None, uniform_S=0, K=1):
     args = (n, vp(ip), vp(ix), vp(v), plan.ntiles, vp(cp), vp(tp), plan.window, int(mode),
             int(R or plan.R), int(uniform_S), int(K), ctypes.byref(nw), ctypes.byref(nr), ctypes.byref(nwarps),
             ctypes.byref(smax))
-    _lib.check(L.mvamg_gs_schedule(*args, None, None, None, None, None), "gs_schedule")
+    order = getattr(plan, "chain_order", None)
+    vo = vp(np.ascontiguousarray(order, dtype=np.int32)) if order is not None else None
+    _lib.check(L.mvamg_gs_schedule(*args, None, None, None, None, None, vo), "gs_schedule")
     rec = np.zeros(max(2, nw.value), dtype=np.uint64)
     round_off = np.empty(nr.value + 1, dtype=np.int32)
     tbase = np.empty(nwarps.value + 1, dtype=np.int32)
     tile_wbase = np.empty(plan.ntiles + 1, dtype=np.int32)
     perm = np.empty(max(1, n), dtype=np.int32)
-    _lib.check(L.mvamg_gs_schedule(*args, vp(rec), vp(round_off), vp(tbase), vp(tile_wbase), vp(perm)),
+    _lib.check(L.mvamg_gs_schedule(*args, vp(rec), vp(round_off), vp(tbase), vp(tile_wbase), vp(perm), vo),
                "gs_schedule")
     return GsScheduleHost(rec, round_off, tbase, tile_wbase, perm, nr.value, smax.value)
 
@@ -296,6 +363,8 @@ class DeviceGsPlan:
         self.plan = plan or gs_analyse(self.A, self.cfg)
         self.chain_ptr = to_device(self.plan.chain_ptr, np.int32)
         self.tile_ptr = to_device(self.plan.tile_ptr, np.int32)
+        order = getattr(self.plan, "chain_order", None)
+        self.chain_order = to_device(order, np.int32) if order is not None else None
         self.modes = {}
         self._csr = None
 
@@ -357,7 +426,7 @@ class DeviceGsPlan:
             direction, self.A.shape[0], *self._csr.ptrs(), ptr(sch["rec"]), ptr(sch["round_off"]),
             ptr(sch["tbase"]), ptr(sch["tile_wbase"]), ptr(sch["perm"]), ptr(sch["tperm"]), sch["R"],
             sch["D"], sch["lean_C"], sch["slot_words"], sch["rec_words_max"], p.ntiles, ptr(self.chain_ptr), ptr(self.tile_ptr),
-            p.threads, p.window, ptr(b), ptr(x_old), ptr(x_new), ptr(ws), stream or stream_handle()),
+            ptr(self.chain_order), p.threads, p.window, ptr(b), ptr(x_old), ptr(x_new), ptr(ws), stream or stream_handle()),
             "gs_sweep")
 
 
@@ -470,6 +539,107 @@ class DeviceGsLevels:
         _lib.check(_lib.load().mvamg_gs_level_sweep_f64(
             0 if self.mode < 2 else 1, self.n, *self._csr.ptrs(), *self.args(), ptr(b), ptr(x_old),
             ptr(x_new), ptr(ws), stream or stream_handle()), "gs_level_sweep")
+
+
+def stream_ctas(A, mode, cfg=None):
+    """CTAs (1 or a cluster of 2..16) of a streamed sweep of A in `mode`, or 0
+    when none fits.  One SM streams up to ~200k entries per sweep in step with
+    its DAG levels; larger levels spread their rows over a cluster (x sliced
+    across the CTAs' shared memory, remote entries read over DSMEM; zero-guess
+    modes only -- a backward sweep from x_old then runs folded)."""
+    cfg = cfg or GpuConfig()
+    n = A.shape[0]
+    if n > cfg.stream_max_rows:
+        return 0
+    reads = (A.nnz - n) if mode & 1 else (A.nnz - n) / 2
+    want = 1
+    while want < 16 and reads / want > cfg.stream_entries_per_cta:
+        want *= 2
+    if mode & 1 and want > 1:
+        return 0
+    tries = (1,) if mode & 1 else ((want, 16) if want < 16 else (16,))
+    for c in tries:
+        R = -(-n // c)
+        xw = (R + 1) & ~1
+        if xw * 8 * (2 if mode & 1 else 1) + 4 * 8192 <= cfg.smem_limit and (c == 1 or c <= cfg.max_cluster):
+            return c
+    return 0
+
+
+def stream_group(A, mode, exact):
+    """Lanes per row of the streamed sweep: 1 (bit-exact CSR order) in exact
+    mode, else about 8-16 entries per lane."""
+    if exact:
+        return 1
+    n = A.shape[0]
+    avg = (A.nnz - n) / max(1, n) / (1 if mode & 1 else 2)
+    for g, lim in ((1, 6), (2, 16), (4, 40)):
+        if avg < lim:
+            return g
+    return 8
+
+
+class DeviceGsStream:
+    """Streamed level-set GS plan (gs_stream.cuh) of one matrix and sweep mode
+    (0 fwd from x=0, 1 fwd, 2 bwd from x=0 -- also the folded backward sweep
+    from x_old --, 3 bwd), on the device: one SM or a thread-block cluster, x
+    in shared memory, the level packets streamed through a ring of TMA bulk
+    copies."""
+
+    def __init__(self, A, mode, cfg=None, group=None, ncta=None):
+        import torch
+
+        cfg = cfg or GpuConfig()
+        A = as_csr(A)
+        n = A.shape[0]
+        ncta = stream_ctas(A, mode, cfg) if ncta is None else int(ncta)
+        if ncta < 1:
+            raise ValueError("gs stream: the level does not fit one SM or cluster")
+        R = -(-n // ncta) if ncta > 1 else n
+        xw = (R + 1) & ~1
+        budget = cfg.smem_limit - xw * 8 * (2 if mode & 1 else 1)
+        # four slots of up to stream_slot_bytes: big slots carry many DAG levels per stage
+        slot = max(4096, min(int(cfg.stream_slot_bytes), (budget // 4) & ~127))
+        nslots = min(8, budget // slot)
+        if nslots < 2:
+            raise ValueError("gs stream: no room for the ring")
+        L = _lib.load()
+        ip = np.ascontiguousarray(A.indptr, dtype=np.int32)
+        ix = np.ascontiguousarray(A.indices, dtype=np.int32)
+        v = np.ascontiguousarray(A.data, dtype=np.float64)
+        vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        nb, ns, nl = ctypes.c_longlong(), ctypes.c_int(), ctypes.c_int()
+        _lib.check(L.mvamg_gs_stream_plan(n, vp(ip), vp(ix), vp(v), int(mode), slot, ncta, ctypes.byref(nb),
+                                          ctypes.byref(ns), ctypes.byref(nl), None, None), "gs_stream_plan")
+        blob = np.zeros(max(16, nb.value), dtype=np.uint8)
+        off = np.zeros(ns.value * ncta + 1, dtype=np.int64)
+        _lib.check(L.mvamg_gs_stream_plan(n, vp(ip), vp(ix), vp(v), int(mode), slot, ncta, ctypes.byref(nb),
+                                          ctypes.byref(ns), ctypes.byref(nl), vp(blob), vp(off)), "gs_stream_plan")
+        self.n, self.mode, self.nstages, self.nslots, self.slot, self.ncta = n, mode, ns.value, nslots, slot, ncta
+        self.nlev, self.nbytes = nl.value, nb.value
+        self.group = int(group) if group is not None else stream_group(A, mode, cfg.exact_gs)
+        self.blob = to_device(blob)
+        self.stage_off = to_device(off)
+        self.tfold = torch.empty(max(2, n), dtype=torch.float64, device="cuda") if mode == 2 else None
+        self._csr = DeviceCSR(A)
+
+    def args(self):
+        return (self.nstages, self.nslots, self.slot, self.group, self.ncta, ptr(self.blob), ptr(self.stage_off),
+                ptr(self.tfold))
+
+    def sweep(self, b, x_old, x_new, ws=None, stream=None, fold=False):
+        """One sweep; fold (mode-2 plan, x_old given): backward from x_old."""
+        L = _lib.load()
+        s = stream or stream_handle()
+        if fold:
+            _lib.check(L.mvamg_gs_stream_sweep_folded_f64(
+                self.n, *self._csr.ptrs(), self.nstages, self.nslots, self.slot, self.group, self.ncta,
+                ptr(self.blob), ptr(self.stage_off), ptr(self.tfold), ptr(b), ptr(x_old), ptr(x_new), ptr(ws), s),
+                "gs_stream_sweep_folded")
+            return
+        _lib.check(L.mvamg_gs_stream_sweep_f64(self.n, self.mode, self.nstages, self.nslots, self.slot,
+                                               self.group, self.ncta, ptr(self.blob), ptr(self.stage_off), ptr(b),
+                                               ptr(x_old), ptr(x_new), s), "gs_stream_sweep")
 
 
 class DeviceGsRows:

@@ -731,3 +731,112 @@ def test_gs_lean_cluster_tiles_bit_exact(mv, cluster):
             oracle_gs(A, b, want, direction)
             got = _gs_gpu(mv, A, b, x0, direction, zero, cfg)
             assert np.array_equal(got, want), (name, direction, cluster)
+
+
+# ---------------------------------------------------- streamed level-set sweep --
+def _gs_stream_gpu(A, b, x_old, mode, cfg=None, fold=False, slot=None, ncta=None):
+    import torch
+    from paper_1907_04417_b200.device import DeviceGsStream, GpuConfig
+
+    A = sp.csr_matrix(A)
+    cfg = cfg or GpuConfig(exact_gs=True)
+    if slot:
+        import dataclasses
+
+        cfg = dataclasses.replace(cfg, stream_slot_bytes=slot)
+    st = DeviceGsStream(A, mode, cfg, ncta=ncta)
+    xn = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+    ws = torch.zeros(8, dtype=torch.int32, device="cuda")
+    st.sweep(_dev(b), None if x_old is None else _dev(x_old), xn, ws, fold=fold)
+    torch.cuda.synchronize()
+    return xn.cpu().numpy(), st
+
+
+@pytest.mark.parametrize("slot,ncta", [(None, None), (8192, None), (None, 2), (8192, 16)])
+def test_gs_stream_bit_exact(mv, c1, slot, ncta):
+    """gs_stream_kernel with one thread per row: every mode (0 fwd from 0, 1 fwd
+    from x_old, 2 bwd from 0, 3 bwd from x_old, and the folded mode-2 backward
+    sweep from x_old) bit-identical to the serial loop on every structure and
+    on the C1 levels; small slots force levels split over several stages;
+    ncta > 1: the zero-guess plans on a thread-block cluster (x sliced over
+    the CTAs, remote entries over DSMEM)."""
+    rng = np.random.default_rng(21)
+    mats = c1[1]
+    ns = random_spd_csr(300, density=0.03, seed=5).tolil()
+    ns[3, 200] = 0.1  # an entry without its transpose: anti-dependences of the sweeps from x_old
+    ns[250, 7] = -0.2
+    cases = list(_structures()) + [("nonsym", ns.tocsr()), ("c1_l1", mats[1]), ("c1_l2", mats[2]),
+                                   ("c1_l3", mats[3]), ("c1_l0", mats[0])]
+    for name, A in cases:
+        n = A.shape[0]
+        b = rng.standard_normal(n)
+        x0 = rng.standard_normal(n)
+        for mode in ((0, 2) if ncta else (0, 1, 2, 3)):
+            direction = "forward" if mode < 2 else "backward"
+            old = mode & 1
+            want = x0.copy() if old else np.zeros(n)
+            oracle_gs(A, b, want, direction)
+            try:
+                got, st = _gs_stream_gpu(A, b, x0 if old else None, mode, slot=slot, ncta=ncta)
+            except ValueError:
+                continue  # x (and b) do not fit one SM
+            assert np.array_equal(got, want), (name, mode, slot, ncta)
+            if mode == 2:
+                want = x0.copy()
+                oracle_gs(A, b, want, "backward")
+                got, _ = _gs_stream_gpu(A, b, x0, 2, fold=True, slot=slot, ncta=ncta)
+                assert np.array_equal(got, want), (name, "folded", slot, ncta)
+
+
+def test_gs_stream_relaxed(mv, c1):
+    """Tolerance parity (several lanes per row, FMA + shuffle tree): the same
+    dependency order, each sweep within rounding of the serial loop."""
+    cfg = mv.GpuConfig(exact_gs=False)
+    rng = np.random.default_rng(22)
+    mats = c1[1]
+    for name, A in list(_structures()) + [("c1_l1", mats[1]), ("c1_l2", mats[2]), ("c1_l0", mats[0])]:
+        n = A.shape[0]
+        b = rng.standard_normal(n)
+        x0 = rng.standard_normal(n)
+        for mode, ncta in ((0, None), (3, None), (0, 4), (2, 16)):
+            want = x0.copy() if mode & 1 else np.zeros(n)
+            oracle_gs(A, b, want, "forward" if mode < 2 else "backward")
+            try:
+                got, st = _gs_stream_gpu(A, b, x0 if mode & 1 else None, mode, cfg, ncta=ncta)
+            except ValueError:
+                continue
+            assert rel(got, want) <= 1e-12, (name, mode, st.group, ncta)
+
+
+def test_vcycle_stream_sweeps(mv, c1):
+    """A V-cycle whose levels run the streamed sweeps (default config) matches
+    the exact-mode cycle to rounding and the reference golden to 1e-10; with
+    exact_gs the streamed sweeps keep the cycle bit-identical to the other
+    exact schedules."""
+    d, mats, pros = c1[0], c1[1], c1[2]
+    op = mv.GpuMultigridOperator(mats, pros)
+    assert any(lv.get("stream") for lv in op.level_dev), "no level took the streamed sweep"
+    z = op.apply(d["b"])
+    assert rel(z, d["apply_b"]) <= TOL_CYCLE
+    ex = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(exact_gs=True))
+    ref = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(exact_gs=True, stream_gs=False))
+    assert np.array_equal(ex.apply(d["b"]), ref.apply(d["b"]))
+
+
+def test_gs_blocked_chain_tiles_bit_exact(mv):
+    """3-D grid lines grouped into 2-D blocks per tile (chain_block_order): the
+    wavefront sweep stays bit-identical to the serial loop in every mode."""
+    from paper_1907_04417_b200 import problems
+    from paper_1907_04417_b200.device import gs_analyse
+
+    rng = np.random.default_rng(31)
+    for name, A in (("lap3d24", laplacian_3d(24).tocsr()), ("jump32", problems.jump_3d(32, 8, 1))):
+        assert gs_analyse(A).chain_order is not None, name
+        n = A.shape[0]
+        b, x0 = rng.standard_normal(n), rng.standard_normal(n)
+        for direction in ("forward", "backward"):
+            for zero in (True, False):
+                want = np.zeros(n) if zero else x0.copy()
+                oracle_gs(A, b, want, direction)
+                got = _gs_gpu(mv, A, b, x0, direction, zero)
+                assert np.array_equal(got, want), (name, direction, zero)
