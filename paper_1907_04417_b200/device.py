@@ -235,7 +235,7 @@ def chain_block_order(A, chain_ptr, T):
         return None
     Z = nch // G
     bz = 1
-    while bz * bz * 2 <= T:
+    while bz * bz * 2 < T:
         bz *= 2
     by = T // bz
     if by < 8 or Z < 2 * bz:

@@ -830,7 +830,7 @@ def test_gs_blocked_chain_tiles_bit_exact(mv):
     from paper_1907_04417_b200.device import gs_analyse
 
     rng = np.random.default_rng(31)
-    for name, A in (("lap3d24", laplacian_3d(24).tocsr()), ("jump32", problems.jump_3d(32, 8, 1))):
+    for name, A in (("lap3d32", laplacian_3d(32).tocsr()), ("jump32", problems.jump_3d(32, 8, 1))):
         assert gs_analyse(A).chain_order is not None, name
         n = A.shape[0]
         b, x0 = rng.standard_normal(n), rng.standard_normal(n)
