@@ -52,6 +52,13 @@ def parse_args():
 
 # ----------------------------------------------------------------- workloads --
 L2_NOTE = {"c1": "flushed (256 MiB write) before every timed step"}
+# Stated deviation (C5): the MultiVectorAMG() fit of C5 has a numerically singular
+# coarsest level (eigenvalues of both signs at rounding level; the unmodified reference's own
+# fits degrade the same way with the grid: j160 already has a zero eigenvalue, tests/golden/
+# j160_ref.json), so the reference's LU coarse solve returns garbage and PCG stops with
+# NotSpdError.  Both arms then solve the coarsest level with the truncated-eigen pseudo-inverse
+# (eigenvalues <= rtol * lambda_max dropped), applied identically on the GPU and in the oracle.
+COARSE_PINV = {"c5": 1e-12}
 
 
 def workload_config(name):
@@ -65,6 +72,9 @@ def workload_config(name):
     if name == "c1":
         desc = ("C1: 2D Poisson 5-point 128x128 (n=16,384), rhs U[-1,1] seed 0, x0=0, rtol 1e-6; "
                 "hierarchy = the reference's own MultiVectorAMG() fit (golden fixture)")
+    if name in COARSE_PINV:
+        desc += (f"; DEVIATION: coarsest level solved by the truncated-eigen pseudo-inverse (rtol "
+                 f"{COARSE_PINV[name]:g}) -- the fit's coarsest matrix is numerically singular")
     return {"workload": desc, "l2": L2_NOTE.get(name, "inputs larger than L2 (no flush needed)")}
 
 
@@ -200,7 +210,7 @@ def _threads():
     return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
 
 
-def cpu_baseline(mats, pros, b, threads, budget_s=30.0, nit_hint=None):
+def cpu_baseline(mats, pros, b, threads, budget_s=30.0, nit_hint=None, pinv=0.0):
     """The CPU oracle (oracle/: plain-C restatement of the reference solve) on
     `threads` host threads (rows / elements / dots split over OpenMP threads,
     the Gauss-Seidel sweeps serial as in the reference; results independent
@@ -210,7 +220,7 @@ def cpu_baseline(mats, pros, b, threads, budget_s=30.0, nit_hint=None):
     from oracle.oracle import OracleOperator, oracle_pcg, set_threads
 
     used = set_threads(threads)
-    op = OracleOperator(mats, pros)
+    op = OracleOperator(mats, pros, coarse_pinv_rtol=pinv)
     t0 = time.perf_counter()
     _, _, k, _ = oracle_pcg(op, b, rtol=1e-300, itmax=3)
     per_it = (time.perf_counter() - t0) / max(1, k)
@@ -247,9 +257,17 @@ def run_reference(args, world, rank):
 
     threads = set_threads(_threads())
     name = args.config.lower()
+    if name == "c5":
+        from paper_1907_04417_b200 import hcache, problems
+
+        A = problems.CONFIGS[name]["build"]()
+        if hcache.load(hcache.key(name, A, problems.rhs_uniform(A.shape[0], 0), {"estimator": "MultiVectorAMG()"})) is None:
+            print(json.dumps({"impl": "reference", "unavailable": "C5's host-only setup takes hours; run the B200 "
+                              "arm first on this box (it caches the hierarchy both arms then solve)"}), flush=True)
+            return
     mats, pros, b, info = load_workload(name, setup="host")
     steps = args.steps if args.steps is not None else 10
-    op = OracleOperator(mats, pros)
+    op = OracleOperator(mats, pros, coarse_pinv_rtol=COARSE_PINV.get(name, 0.0))
     for _ in range(max(1, args.warmup)):
         _, hist, nit, conv = oracle_pcg(op, b, rtol=1e-6)
     times = []
@@ -455,7 +473,8 @@ def run_b200(args, world, rank, local):
     name = args.config.lower()
     mats, pros, b, info = load_workload(name, setup="gpu")
     n = mats[0].shape[0]
-    op = mv.GpuMultigridOperator(mats, pros)
+    pinv = COARSE_PINV.get(name, 0.0)
+    op = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(coarse_pinv_rtol=pinv))
     h = op.handle
     s = stream_handle()
     steps = args.steps if args.steps is not None else (50 if n < 100000 else 20)
@@ -659,13 +678,13 @@ def run_b200(args, world, rank, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle.oracle import OracleOperator, oracle_pcg
 
-        cb, cnit = cpu_baseline(mats, pros, b, _threads(), nit_hint=n_iters)
+        cb, cnit = cpu_baseline(mats, pros, b, _threads(), nit_hint=n_iters, pinv=pinv)
         cb["nit"] = cnit
         out["cpu_baseline"] = cb
-        cb1, _ = cpu_baseline(mats, pros, b, 1, budget_s=20.0, nit_hint=n_iters)
+        cb1, _ = cpu_baseline(mats, pros, b, 1, budget_s=20.0, nit_hint=n_iters, pinv=pinv)
         out["cpu_baseline_1core"] = cb1
         # parity of the timed GPU solve against the oracle on the same hierarchy
-        _, hist_o, nit_o, _ = oracle_pcg(OracleOperator(mats, pros), b, rtol=1e-6)
+        _, hist_o, nit_o, _ = oracle_pcg(OracleOperator(mats, pros, coarse_pinv_rtol=pinv), b, rtol=1e-6)
         m = min(len(hist_o), len(hist_gpu))
         out["details"]["oracle_nit"] = nit_o
         out["details"]["history_rel_max_vs_oracle"] = float(np.max(np.abs(hist_gpu[:m] - hist_o[:m]) / hist_o[:m]))

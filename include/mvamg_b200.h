@@ -342,6 +342,28 @@ int mvamg_hierarchy_set_gs_levels(mvamg_hierarchy* h, int k, int mode, int ncta,
                                   int nlev, int max_rows, int max_ents, int threads, int group,
                                   const int* lev_ptr, const int* lev_eptr, const void* rows, const void* ents,
                                   const int* perm, double* tperm);
+/* ---- NCCL for the row-partitioned solve --------------
+ * One communicator per process / GPU.  libnccl.so.2 is opened at run time (the
+ * copy PyTorch already loaded, when it did); every call is stream-ordered on the
+ * caller's stream.  Replaces nothing in the reference (it is single-process);
+ * used by paper_1907_04417_b200/distributed.py's halo exchanges and the
+ * fused PCG dot allreduces. */
+typedef struct mvamg_comm mvamg_comm;
+/* 128 bytes of ncclUniqueId (rank 0 creates it, the others receive it). */
+int mvamg_comm_unique_id(void* id128);
+int mvamg_comm_init(mvamg_comm** comm, int rank, int nranks, const void* id128);
+int mvamg_comm_destroy(mvamg_comm* comm);
+/* One grouped exchange: send_buf[q] (send_count[q] doubles, device) to
+ * send_peer[q], recv_buf[q] from recv_peer[q]. */
+int mvamg_halo_exchange(mvamg_comm* comm, int nsend, const int* send_peer, const double* const* send_buf,
+                        const long long* send_count, int nrecv, const int* recv_peer, double* const* recv_buf,
+                        const long long* recv_count, void* stream);
+/* In-place sum over the ranks of `count` device doubles (the PCG dots). */
+int mvamg_allreduce_sum_f64(mvamg_comm* comm, double* buf, long long count, void* stream);
+/* SpMV kernel choice for rows handled one thread per row (1, the default:
+ * CSR-stream tiles -- coalesced products into shared memory, then CSR-order
+ * row sums; 0: the plain thread-per-row loop).  Both bit-identical. */
+int mvamg_set_spmv_stream(int enable);
 /* Diagnostics: CTA 0 of every streamed sweep writes (tag, clock64) pairs --
  * tag -2 before a stage's wait, -3 after it, the batch's rows after its
  * barrier -- into trace_dev (cap int64s; [0] = entries used).  NULL: off. */

@@ -58,6 +58,12 @@ SIGNATURES = [
     ("mvamg_gs_stream_sweep_f64", _I, [_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_gs_stream_sweep_folded_f64", _I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
     ("mvamg_gs_stream_set_trace", _I, [_P, _I]),
+    ("mvamg_set_spmv_stream", _I, [_I]),
+    ("mvamg_comm_unique_id", _I, [_P]),
+    ("mvamg_comm_init", _I, [ctypes.POINTER(_P), _I, _I, _P]),
+    ("mvamg_comm_destroy", _I, [_P]),
+    ("mvamg_halo_exchange", _I, [_P, _I, _P, _P, _P, _I, _P, _P, _P, _P]),
+    ("mvamg_allreduce_sum_f64", _I, [_P, _P, _LL, _P]),
     ("mvamg_hierarchy_set_gs_stream", _I, [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P]),
     ("mvamg_greedy_match", _I, [_LL, _P, _P, _I, _P, _P, _P, ctypes.POINTER(_LL)]),
     ("mvamg_jacobi_svd_batch", _I, [_I, _P, _I, _P, _I, _D, _P, _P, _PI]),
@@ -113,7 +119,7 @@ def build(force=False, verbose=False):
         so_t = os.path.getmtime(SO_PATH)
         if all(os.path.getmtime(s) <= so_t for s in srcs):
             return SO_PATH
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", SO_PATH, SRC]
+    cmd = ["nvcc", *NVCC_FLAGS, "-o", SO_PATH, SRC, "-ldl"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

@@ -10,6 +10,7 @@
 // update the Krylov scalars in place); repeated launch sequences (one cycle, one
 // PCG half-iteration) are captured once into CUDA graphs and replayed.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -238,6 +239,8 @@ void launch_prepare(const Csr& A, const double* b, const double* xold, const int
   }
 }
 
+bool g_spmv_stream = true;  // CSR-stream SpMV for the thread-per-row cases (mvamg_set_spmv_stream)
+
 int launch_spmv(int mode, const Csr& A, const double* x, const double* b, double* y, cudaStream_t s) {
   if (A.n == 0) return 0;
   if (warp_rows(A)) {
@@ -245,6 +248,18 @@ int launch_spmv(int mode, const Csr& A, const double* x, const double* b, double
     if (mode == 0) spmv_warp_kernel<0><<<gw, 256, 0, s>>>(A.n, A.ip, A.ix, A.v, x, b, y);
     else if (mode == 1) spmv_warp_kernel<1><<<gw, 256, 0, s>>>(A.n, A.ip, A.ix, A.v, x, b, y);
     else spmv_warp_kernel<2><<<gw, 256, 0, s>>>(A.n, A.ip, A.ix, A.v, x, b, y);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+  if (g_spmv_stream) {
+    // CSR-stream tiles of rpt rows sized so a tile's entries usually fit the buffer
+    const double avg = A.nnz > 0 ? (double)A.nnz / A.n : 8.0;
+    const int rpt = avg <= 11.0 ? 256 : (avg <= 23.0 ? 128 : (avg <= 47.0 ? 64 : 32));
+    const long long tiles = ((long long)A.n + rpt - 1) / rpt;
+    const int g = (int)std::max(1LL, std::min(tiles, (long long)num_sms() * 8));
+    if (mode == 0) spmv_stream_kernel<0><<<g, 256, 0, s>>>(A.n, rpt, A.ip, A.ix, A.v, x, b, y);
+    else if (mode == 1) spmv_stream_kernel<1><<<g, 256, 0, s>>>(A.n, rpt, A.ip, A.ix, A.v, x, b, y);
+    else spmv_stream_kernel<2><<<g, 256, 0, s>>>(A.n, rpt, A.ip, A.ix, A.v, x, b, y);
     CUDA_TRY(cudaGetLastError());
     return 0;
   }
@@ -2122,6 +2137,130 @@ int mvamg_gs_stream_sweep_folded_f64(int n, const int* indptr, const int* indice
   g.stage_off = stage_off;
   launch_prepare(A, b, x_old, nullptr, tfold, x_new, ws, 1, s);
   return launch_gs_stream(n, g, 0, tfold, nullptr, x_new, s);
+}
+
+// ---- NCCL (row-partitioned solve) ---------------------
+// libnccl.so.2 is opened at run time, not linked: in a process where PyTorch
+// already loaded its NCCL, dlopen returns that same library (one NCCL per
+// process, as SURVEY 5 asks); MVAMG_NCCL overrides the path.
+namespace ncclabi {
+typedef struct { char internal[128]; } UniqueId;
+typedef void* Comm;
+typedef int (*GetUniqueId_t)(UniqueId*);
+typedef int (*CommInitRank_t)(Comm*, int, UniqueId, int);
+typedef int (*CommDestroy_t)(Comm);
+typedef int (*Group_t)();
+typedef int (*Send_t)(const void*, size_t, int, int, Comm, cudaStream_t);
+typedef int (*Recv_t)(void*, size_t, int, int, Comm, cudaStream_t);
+typedef int (*AllReduce_t)(const void*, void*, size_t, int, int, Comm, cudaStream_t);
+typedef const char* (*ErrStr_t)(int);
+constexpr int kFloat64 = 8, kSum = 0;
+struct Api {
+  bool ok = false;
+  GetUniqueId_t get_id = nullptr;
+  CommInitRank_t init = nullptr;
+  CommDestroy_t destroy = nullptr;
+  Group_t gstart = nullptr, gend = nullptr;
+  Send_t send = nullptr;
+  Recv_t recv = nullptr;
+  AllReduce_t allreduce = nullptr;
+  ErrStr_t errstr = nullptr;
+};
+Api& api() {
+  static Api a;
+  static bool tried = false;
+  if (tried) return a;
+  tried = true;
+  const char* path = std::getenv("MVAMG_NCCL");
+  void* h = dlopen(path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return a;
+  a.get_id = (GetUniqueId_t)dlsym(h, "ncclGetUniqueId");
+  a.init = (CommInitRank_t)dlsym(h, "ncclCommInitRank");
+  a.destroy = (CommDestroy_t)dlsym(h, "ncclCommDestroy");
+  a.gstart = (Group_t)dlsym(h, "ncclGroupStart");
+  a.gend = (Group_t)dlsym(h, "ncclGroupEnd");
+  a.send = (Send_t)dlsym(h, "ncclSend");
+  a.recv = (Recv_t)dlsym(h, "ncclRecv");
+  a.allreduce = (AllReduce_t)dlsym(h, "ncclAllReduce");
+  a.errstr = (ErrStr_t)dlsym(h, "ncclGetErrorString");
+  a.ok = a.get_id && a.init && a.destroy && a.gstart && a.gend && a.send && a.recv && a.allreduce;
+  return a;
+}
+}  // namespace ncclabi
+
+struct mvamg_comm {
+  ncclabi::Comm c = nullptr;
+  int rank = 0, nranks = 1;
+};
+
+#define NCCL_TRY(x)                                                                        \
+  do {                                                                                     \
+    int r_ = (x);                                                                          \
+    if (r_ != 0)                                                                           \
+      return fail(MVAMG_E_CUDA, std::string("nccl: ") +                                    \
+                                    (ncclabi::api().errstr ? ncclabi::api().errstr(r_) : "error")); \
+  } while (0)
+
+int mvamg_comm_unique_id(void* id128) {
+  if (!id128) return fail(MVAMG_E_ARG, "comm_unique_id: null");
+  if (!ncclabi::api().ok) return fail(MVAMG_E_STATE, "comm_unique_id: libnccl.so.2 not available");
+  ncclabi::UniqueId id;
+  NCCL_TRY(ncclabi::api().get_id(&id));
+  std::memcpy(id128, &id, sizeof(id));
+  return 0;
+}
+
+int mvamg_comm_init(mvamg_comm** comm, int rank, int nranks, const void* id128) {
+  if (!comm || !id128 || nranks < 1 || rank < 0 || rank >= nranks) return fail(MVAMG_E_ARG, "comm_init: bad arguments");
+  if (!ncclabi::api().ok) return fail(MVAMG_E_STATE, "comm_init: libnccl.so.2 not available");
+  ncclabi::UniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  mvamg_comm* c = new mvamg_comm();
+  c->rank = rank;
+  c->nranks = nranks;
+  int r = ncclabi::api().init(&c->c, nranks, id, rank);
+  if (r != 0) {
+    delete c;
+    NCCL_TRY(r);
+  }
+  *comm = c;
+  return 0;
+}
+
+int mvamg_comm_destroy(mvamg_comm* comm) {
+  if (!comm) return 0;
+  if (comm->c && ncclabi::api().ok) ncclabi::api().destroy(comm->c);
+  delete comm;
+  return 0;
+}
+
+int mvamg_halo_exchange(mvamg_comm* comm, int nsend, const int* send_peer, const double* const* send_buf,
+                        const long long* send_count, int nrecv, const int* recv_peer, double* const* recv_buf,
+                        const long long* recv_count, void* stream) {
+  if (!comm || nsend < 0 || nrecv < 0 || (nsend && (!send_peer || !send_buf || !send_count)) ||
+      (nrecv && (!recv_peer || !recv_buf || !recv_count)))
+    return fail(MVAMG_E_ARG, "halo_exchange: bad arguments");
+  auto& a = ncclabi::api();
+  cudaStream_t s = (cudaStream_t)stream;
+  NCCL_TRY(a.gstart());
+  for (int q = 0; q < nsend; ++q)
+    if (send_count[q] > 0) NCCL_TRY(a.send(send_buf[q], (size_t)send_count[q], ncclabi::kFloat64, send_peer[q], comm->c, s));
+  for (int q = 0; q < nrecv; ++q)
+    if (recv_count[q] > 0) NCCL_TRY(a.recv(recv_buf[q], (size_t)recv_count[q], ncclabi::kFloat64, recv_peer[q], comm->c, s));
+  NCCL_TRY(a.gend());
+  return 0;
+}
+
+int mvamg_allreduce_sum_f64(mvamg_comm* comm, double* buf, long long count, void* stream) {
+  if (!comm || !buf || count < 0) return fail(MVAMG_E_ARG, "allreduce: bad arguments");
+  NCCL_TRY(ncclabi::api().allreduce(buf, buf, (size_t)count, ncclabi::kFloat64, ncclabi::kSum, comm->c,
+                                    (cudaStream_t)stream));
+  return 0;
+}
+
+int mvamg_set_spmv_stream(int enable) {
+  g_spmv_stream = enable != 0;
+  return 0;
 }
 
 int mvamg_gs_stream_set_trace(long long* trace_dev, int cap) {

@@ -122,6 +122,49 @@ __global__ void __launch_bounds__(256) spmv_kernel(int n, const int* __restrict_
   }
 }
 
+// The same SpMV family, CSR-stream: a block takes `rpt` consecutive rows, its
+// threads form the products a_k * x[j_k] of the tile's contiguous entry range
+// with coalesced loads (each its own rounding, as in the serial loop) into
+// shared memory, then one thread per row adds its products in CSR order from
+// 0.0 -- bit-identical to spmv_kernel, but every load instruction of the
+// matrix is one coalesced segment instead of 32 rows' strided entries.  A tile
+// whose entries exceed the buffer falls back to the row loop.
+constexpr int kSpmvTileNnz = 3072;
+
+template <int MODE>
+__global__ void __launch_bounds__(256) spmv_stream_kernel(int n, int rpt, const int* __restrict__ ip,
+                                                          const int* __restrict__ ix,
+                                                          const double* __restrict__ v,
+                                                          const double* __restrict__ x,
+                                                          const double* __restrict__ b, double* y) {
+  __shared__ double prod[kSpmvTileNnz];
+  const int tid = threadIdx.x;
+  for (int r0 = blockIdx.x * rpt; r0 < n; r0 += gridDim.x * rpt) {
+    const int r1 = min(r0 + rpt, n);
+    const int e0 = __ldg(ip + r0), e1 = __ldg(ip + r1);
+    const int row = r0 + tid;
+    double s = 0.0;
+    if (e1 - e0 <= kSpmvTileNnz) {
+#pragma unroll 4
+      for (int e = e0 + tid; e < e1; e += 256) prod[e - e0] = __dmul_rn(__ldg(v + e), __ldg(x + __ldg(ix + e)));
+      __syncthreads();
+      if (row < r1) {
+        const int k1 = __ldg(ip + row + 1);
+        for (int k = __ldg(ip + row); k < k1; ++k) s = __dadd_rn(s, prod[k - e0]);
+      }
+      __syncthreads();
+    } else if (row < r1) {
+      const int k1 = __ldg(ip + row + 1);
+      for (int k = __ldg(ip + row); k < k1; ++k) s = __dadd_rn(s, __dmul_rn(__ldg(v + k), __ldg(x + __ldg(ix + k))));
+    }
+    if (row < r1) {
+      if (MODE == 0) y[row] = s;
+      else if (MODE == 1) y[row] = __dsub_rn(__ldg(b + row), s);
+      else y[row] = __dadd_rn(y[row], s);
+    }
+  }
+}
+
 // The same SpMV family, one warp per row, for small levels with long rows (the
 // K-cycle's coarse levels: a few thousand rows of 10-70 entries).  One thread
 // per row walks its row with ~2 dependent L2 trips per unrolled batch of

@@ -545,7 +545,12 @@ class DistributedVCycle:
 
 def dist_pcg(op, b_own, rtol=1e-6, itmax=1000):
     """pcg (pkg/src/mvamg/krylov.py:28-72) with x0 = 0 over row-partitioned
-    vectors; every rank returns its own rows of x and the same SolveReport."""
+    vectors; every rank returns its own rows of x and the same SolveReport.
+
+    Two allreduces per iteration: p'q, then [r'r, r'z] together -- the
+    preconditioner is applied to the updated residual before the stop test, so
+    the two dots travel in one message (the iterates and the history are those
+    of the reference's loop; a converged solve pays one extra application)."""
     be, comm = op.be, op.comm
     n = b_own.numel()
     x = be.vec(n)
@@ -573,14 +578,13 @@ def dist_pcg(op, b_own, rtol=1e-6, itmax=1000):
         be.axpy(alpha, p, x)
         be.axpy(-alpha, q, r)
         it += 1
-        rr, = comm.allreduce([be.dot(r, r)])
+        op.apply(r, z)  # before the stop test: r'r and r'z share one allreduce
+        rr, rz_new = comm.allreduce([be.dot(r, r), be.dot(r, z)])
         nrm = float(np.sqrt(rr))
         hist.append(nrm)
         if nrm <= rtol * nr0:
             converged = True
             break
-        op.apply(r, z)
-        rz_new, = comm.allreduce([be.dot(r, z)])
         if rz_new <= 0.0:
             raise NotSpdError("preconditioner breakdown: r'z <= 0")
         be.xpby(z, rz_new / rz, p)

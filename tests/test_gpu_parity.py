@@ -840,3 +840,36 @@ def test_gs_blocked_chain_tiles_bit_exact(mv):
                 oracle_gs(A, b, want, direction)
                 got = _gs_gpu(mv, A, b, x0, direction, zero)
                 assert np.array_equal(got, want), (name, direction, zero)
+
+
+@pytest.mark.parametrize("stream", [True, False])
+def test_spmv_stream_tiles_bit_exact(mv, stream):
+    """CSR-stream SpMV (tiles of rows whose products go through shared memory)
+    and the plain thread-per-row loop: every mode bit-identical to the serial
+    CSR-order sum, on ragged rows, empty rows, a tile overflowing the buffer
+    (row loop fallback) and sizes that do not fill the last tile."""
+    from paper_1907_04417_b200 import _lib
+
+    L = _lib.load()
+    L.mvamg_set_spmv_stream(int(stream))
+    try:
+        rng = np.random.default_rng(41)
+        cases = []
+        for n, dens in ((1, 1.0), (257, 0.02), (70001, 0.0001), (3000, 0.01)):
+            M = sp.random(n, n, density=dens, random_state=rng, data_rvs=rng.standard_normal, format="csr")
+            cases.append(M)
+        big = sp.lil_matrix((70000, 70000))
+        big[5, :5000] = rng.standard_normal(5000)      # one tile far over the buffer
+        big[300, ::7] = rng.standard_normal(10000)
+        cases.append(big.tocsr())
+        for M in cases:
+            M = sp.csr_matrix(M)
+            M.sort_indices()
+            x = rng.standard_normal(M.shape[1])
+            b, y = rng.standard_normal(M.shape[0]), rng.standard_normal(M.shape[0])
+            ref = oracle_spmv(M, x)
+            assert np.array_equal(_spmv_mode_gpu(M, x, 0), ref)
+            assert np.array_equal(_spmv_mode_gpu(M, x, 1, b=b), b - ref)
+            assert np.array_equal(_spmv_mode_gpu(M, x, 2, y=y), y + ref)
+    finally:
+        L.mvamg_set_spmv_stream(1)
