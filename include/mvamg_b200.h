@@ -241,10 +241,13 @@ int mvamg_gs_scan_sweep_f64(int mode, int n, const int* indptr, const int* indic
  * (wofs[w] + u) * 32 + l, padded to the warp's longest row; src is the row of
  * the value, with bit 31 set for an x_old value (modes 1 and 3).  Query with
  * rowid == NULL first (*nslots = total slice rows, so coef / src hold
- * 32 * nslots elements; wofs holds ceil(n/32) + 1 ints). */
+ * 32 * nslots elements; wofs holds ceil(n/32) + 1 ints).  row_lo, row_hi:
+ * only rows [row_lo, row_hi) become positions (-1, -1: all); the others are
+ * external inputs -- the ghosts of a row-partitioned level -- read, never
+ * written (perm still holds n entries; the position arrays row_hi - row_lo). */
 int mvamg_gs_rows(int n, const int* indptr, const int* indices, const double* data, int mode, int entry_order,
                   long long* nslots, int* nlev, int* rowid, int* cnt, int* crit, double* dg, double* rdg,
-                  int* perm, int* wofs, double* coef, int* src);
+                  int* perm, int* wofs, double* coef, int* src, int row_lo, int row_hi);
 /* One GS sweep with a row schedule of `mode` (gs_row_kernel: one thread per
  * row over the whole GPU, x_new itself as the ready flag, each row's CSR-order
  * chain advanced as its inputs are published).  A mode-2 schedule with x_old
@@ -258,6 +261,29 @@ int mvamg_gs_row_sweep_f64(int mode, int n, const int* indptr, const int* indice
                            const int* perm, const int* wofs, const double* coef, const int* src,
                            int threads, int ctas, int max_tile_slots, double* tperm, const double* b,
                            const double* x_old, double* x_new, int* ws, void* stream);
+/* Pipelined sweep of one rank of a row-partitioned level (distributed.py;
+ * SURVEY.md 8(e)): a row schedule of mode 0 / 2 built with row range
+ * [row_lo, row_hi) = the own rows of the extended layout [lower ghosts | own |
+ * upper ghosts] (n_ext rows; indptr covers all, ghost rows empty).  Ghost
+ * inputs are polled in x_ext at system scope: their owners' kernels store them
+ * there over NVLink the moment they are final (mirror_dst[mirror_ptr[p]..] =
+ * peer << 24 | slot into peers[peer], device pointers from mvamg_ipc_open), so
+ * the exact-order sweep runs as one wavefront across the ranks instead of a
+ * rank-by-rank relay.  Own and ghost slots of x_ext must hold the sentinel
+ * (all-ones bytes) when any rank starts; x_old_ext (mode 2 only) folds the old
+ * lower neighbours into the right-hand side first.  ws: >= 2 device ints. */
+int mvamg_gs_row_sweep_ext_f64(int mode, int n_ext, int row_lo, int row_hi, const int* indptr, const int* indices,
+                               const double* data, const int* rowid, const int* cnt, const int* crit,
+                               const double* dg, const double* rdg, const int* wofs, const double* coef,
+                               const int* src, int threads, int ctas, int max_tile_slots, double* tperm,
+                               const double* b_own, const double* x_old_ext, double* x_ext,
+                               const int* mirror_ptr, const unsigned* mirror_dst, double* const* peers,
+                               int* ws, void* stream);
+/* CUDA IPC of a device buffer: its 64-byte handle, and open / close of a
+ * peer's (the extended x a rank's mirror stores go to). */
+int mvamg_ipc_handle(const void* dptr, void* handle64);
+int mvamg_ipc_open(const void* handle64, void** dptr);
+int mvamg_ipc_close(void* dptr);
 /* z = Inv r, Inv dense row-major n x n (coarsest solve; cycles.py:88-97). */
 int mvamg_dense_gemv_f64(int n, const double* inv, const double* r, double* z, void* stream);
 /* *result = x . y (deterministic two-level reduction; device scalar).

@@ -51,7 +51,12 @@ SIGNATURES = [
     ("mvamg_gs_level_sweep_f64", _I, [_I, _I, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P,
                                       _P, _P, _P, _P, _P]),
     ("mvamg_gs_rows", _I, [_I, _P, _P, _P, _I, _I, ctypes.POINTER(_LL), _PI, _P, _P, _P, _P, _P, _P, _P, _P,
-                           _P]),
+                           _P, _I, _I]),
+    ("mvamg_gs_row_sweep_ext_f64", _I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I,
+                                        _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    ("mvamg_ipc_handle", _I, [_P, _P]),
+    ("mvamg_ipc_open", _I, [_P, ctypes.POINTER(_P)]),
+    ("mvamg_ipc_close", _I, [_P]),
     ("mvamg_gs_row_sweep_f64", _I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P,
                                     _P, _P, _P, _P, _P]),
     ("mvamg_gs_stream_plan", _I, [_I, _P, _P, _P, _I, _I, _I, ctypes.POINTER(_LL), _PI, _PI, _P, _P]),

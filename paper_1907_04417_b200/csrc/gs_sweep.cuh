@@ -1249,7 +1249,23 @@ struct GsRowArgs {
   int* status;
   long long* trace;     // diagnostics: per position, %globaltimer when the row was published, then iterations
   int debug;            // > 0: nanosleep after a failed poll (ns)
+  // row-partitioned (pipelined) sweeps: each final value is also stored into
+  // the peers that read the row as a ghost -- mirror_dst[mirror_ptr[p]..] =
+  // peer << 24 | slot, peers[peer] that rank's extended x -- and inputs are
+  // polled at system scope (a peer GPU writes them over NVLink)
+  const int* mirror_ptr;
+  const unsigned* mirror_dst;
+  double* const* peers;
+  int sys;
 };
+
+__device__ __forceinline__ void ld_global_sys_if(unsigned long long& v, bool p, const void* gaddr) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n @q ld.relaxed.sys.global.u64 %0, [%2];\n}"
+               : "+l"(v) : "r"((unsigned)p), "l"(gaddr));
+}
+__device__ __forceinline__ void st_relaxed_sys_f64(double* p, double v) {
+  asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
 
 __device__ __forceinline__ long long globaltimer_ns() {
   long long t;
@@ -1346,7 +1362,8 @@ __global__ void __launch_bounds__(128) gs_row_kernel(GsRowArgs a) {
           const double* src = a.xnew + j;
           if (OLD && j < 0) src = a.xold + (j & 0x7fffffff);
           xb[u] = kSentinel;
-          ld_global_if(xb[u], v, src);
+          if (a.sys) ld_global_sys_if(xb[u], v, src);
+          else ld_global_if(xb[u], v, src);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -1372,7 +1389,16 @@ __global__ void __launch_bounds__(128) gs_row_kernel(GsRowArgs a) {
         sc = m > 0 ? 4 : sc + 4;
         if (sc >= min(cnt - kc, 64)) sc = 4;
         if (kc == cnt) {
-          st_relaxed_f64(a.xnew + i, div_rn_markstein(s, dg, rdg));
+          const double xi = div_rn_markstein(s, dg, rdg);
+          if (a.mirror_ptr) {  // peers that read this row as a ghost (pipelined row partition)
+            const int m1 = __ldg(a.mirror_ptr + p + 1);
+            for (int m = __ldg(a.mirror_ptr + p); m < m1; ++m) {
+              const unsigned d = __ldg(a.mirror_dst + m);
+              st_relaxed_sys_f64(a.peers[d >> 24] + (d & 0xffffffu), xi);
+            }
+          }
+          if (a.sys) st_relaxed_sys_f64(a.xnew + i, xi);
+          else st_relaxed_f64(a.xnew + i, xi);
           if (a.trace) {
             a.trace[p] = globaltimer_ns();
             a.trace[a.n + p] = progress;

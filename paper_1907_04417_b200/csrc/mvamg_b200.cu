@@ -763,6 +763,10 @@ int launch_gs_rows(const Csr& A, const GsRows& g, const double* b, const double*
   a.status = status;
   a.trace = g_gs_trace;
   a.debug = g_row_sleep;
+  a.mirror_ptr = nullptr;
+  a.mirror_dst = nullptr;
+  a.peers = nullptr;
+  a.sys = 0;
   const int grid = std::max(1, std::min(a.ntiles, g.ctas > 0 ? g.ctas : num_sms()));
   if (g.mode == 1 || g.mode == 3) gs_row_kernel<true><<<grid, g.threads, smem, s>>>(a);
   else gs_row_kernel<false><<<grid, g.threads, smem, s>>>(a);
@@ -2280,16 +2284,22 @@ int mvamg_hierarchy_set_gs_stream(mvamg_hierarchy* h, int k, int mode, int nstag
   return 0;
 }
 
-int mvamg_gs_rows(int n, const int* indptr, const int* indices, const double* data, int mode, int entry_order,
+int mvamg_gs_rows(int n_all, const int* indptr, const int* indices, const double* data, int mode, int entry_order,
                   long long* nslots, int* nlev, int* rowid, int* cnt, int* crit, double* dg, double* rdg,
-                  int* perm, int* wofs, double* coef, int* src) {
-  if (n < 0 || !indptr || !nslots || !nlev || mode < 0 || mode > 3) return fail(MVAMG_E_ARG, "gs_rows: bad arguments");
+                  int* perm, int* wofs, double* coef, int* src, int row_lo, int row_hi) {
+  if (n_all < 0 || !indptr || !nslots || !nlev || mode < 0 || mode > 3) return fail(MVAMG_E_ARG, "gs_rows: bad arguments");
+  // rows [row_lo, row_hi) are swept (positions); the others are external inputs
+  // (ghosts of a row-partitioned level, final before or published during the sweep)
+  if (row_lo < 0 && row_hi < 0) { row_lo = 0; row_hi = n_all; }
+  if (row_lo < 0 || row_hi < row_lo || row_hi > n_all) return fail(MVAMG_E_ARG, "gs_rows: bad row range");
+  const int n = row_hi - row_lo;
   const bool fwd = mode < 2, zero = (mode % 2) == 0;
-  // level sets of the sweep's dependency DAG
-  std::vector<int> lvl(n > 0 ? n : 1, 0), c(n > 0 ? n : 1, 0);
+  auto swept = [&](int j) { return j >= row_lo && j < row_hi; };
+  // level sets of the sweep's dependency DAG (external inputs: level -1)
+  std::vector<int> lvl(n_all > 0 ? n_all : 1, -1), c(n_all > 0 ? n_all : 1, 0);
   int nl = 0;
   for (int q = 0; q < n; ++q) {
-    const int i = fwd ? q : n - 1 - q;
+    const int i = fwd ? row_lo + q : row_hi - 1 - q;
     int m = 0;
     for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
       const int j = indices[k];
@@ -2298,7 +2308,7 @@ int mvamg_gs_rows(int n, const int* indptr, const int* indices, const double* da
     lvl[i] = m;
     nl = std::max(nl, m + 1);
   }
-  for (int i = 0; i < n; ++i) {
+  for (int i = row_lo; i < row_hi; ++i) {
     int m = 0;
     for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
       const int j = indices[k];
@@ -2310,7 +2320,7 @@ int mvamg_gs_rows(int n, const int* indptr, const int* indices, const double* da
   }
   // topological positions: by level, then longest row first (uniform warps)
   std::vector<int> order(n > 0 ? n : 1);
-  for (int i = 0; i < n; ++i) order[i] = i;
+  for (int q = 0; q < n; ++q) order[q] = row_lo + q;
   std::stable_sort(order.begin(), order.begin() + n, [&](int x, int y) {
     if (lvl[x] != lvl[y]) return lvl[x] < lvl[y];
     return c[x] > c[y];
@@ -2369,7 +2379,7 @@ int mvamg_gs_rows(int n, const int* indptr, const int* indices, const double* da
           const size_t e = (size_t)(off + u) * 32 + l;
           coef[e] = data[k];
           src[e] = isnew ? j : (int)(0x80000000u | (unsigned)j);
-          if (isnew && lvl[j] >= lmax) { lmax = lvl[j]; e1 = u; }
+          if (isnew && lvl[j] >= lmax && swept(j)) { lmax = lvl[j]; e1 = u; }
           ++u;
         }
         // wait hints: e1 = the entry of the latest input; e2 = the latest one
@@ -2412,6 +2422,110 @@ int mvamg_gs_row_sweep_f64(int mode, int n, const int* indptr, const int* indice
   g.rowid = rowid; g.cnt = cnt; g.crit = crit; g.wofs = wofs;
   g.coef = coef; g.src = src; g.dg = dg; g.rdg = rdg; g.perm = perm; g.tperm = tperm;
   return launch_gs_rows(A, g, b, x_old, x_new, ws, ws + 1, (cudaStream_t)stream);
+}
+
+// Pipelined sweep of one rank's rows of a row-partitioned level over its
+// extended layout [lower ghosts | own rows | upper ghosts] (distributed.py):
+// positions are the own rows (mvamg_gs_rows with row range [row_lo, row_hi)),
+// ghost inputs are polled in x_ext -- their owners' kernels store them there
+// over NVLink as they finish them (mirror tables) -- and every own row's value
+// goes to x_ext and to the peers that read it.  x_ext's own and ghost slots
+// must hold the sentinel (all-ones) when the ranks start (the caller resets
+// them, then synchronises the ranks); for a backward sweep from x_old the old
+// lower neighbours (own and ghost, x_old_ext) are folded into the right-hand
+// side first, in CSR order.
+__global__ void __launch_bounds__(256) gs_prepare_ext_kernel(int npos, const int* __restrict__ rowid, int row_lo,
+                                                             const int* __restrict__ ip, const int* __restrict__ ix,
+                                                             const double* __restrict__ v,
+                                                             const double* __restrict__ b_own,
+                                                             const double* __restrict__ xold_ext, double* tperm,
+                                                             int* ticket, int fold) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npos; p += gridDim.x * blockDim.x) {
+    const int i = __ldg(rowid + p);
+    double s = __ldg(b_own + (i - row_lo));
+    if (fold) {
+      const int k1 = __ldg(ip + i + 1);
+      for (int k = __ldg(ip + i); k < k1; ++k) {
+        const int j = __ldg(ix + k);
+        if (j >= i) break;
+        s = __dsub_rn(s, __dmul_rn(__ldg(v + k), __ldg(xold_ext + j)));
+      }
+    }
+    tperm[p] = s;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0;
+}
+
+int mvamg_gs_row_sweep_ext_f64(int mode, int n_ext, int row_lo, int row_hi, const int* indptr, const int* indices,
+                               const double* data, const int* rowid, const int* cnt, const int* crit,
+                               const double* dg, const double* rdg, const int* wofs, const double* coef,
+                               const int* src, int threads, int ctas, int max_tile_slots, double* tperm,
+                               const double* b_own, const double* x_old_ext, double* x_ext,
+                               const int* mirror_ptr, const unsigned* mirror_dst, double* const* peers,
+                               int* ws, void* stream) {
+  if (mode != 0 && mode != 2) return fail(MVAMG_E_ARG, "gs rows ext: zero-guess schedules (0, 2) only");
+  if (row_lo < 0 || row_hi < row_lo || row_hi > n_ext) return fail(MVAMG_E_ARG, "gs rows ext: bad row range");
+  if (threads < 32 || threads > 128 || threads % 32) return fail(MVAMG_E_ARG, "gs rows ext: threads must be 32..128");
+  if (x_old_ext && mode != 2) return fail(MVAMG_E_ARG, "gs rows ext: x_old only with the backward schedule");
+  const int npos = row_hi - row_lo;
+  if (npos == 0) return 0;
+  set_kernel_attrs();
+  if (!g_row_attr) {
+    g_row_attr = true;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(gs_row_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+    cudaFuncSetAttribute(gs_row_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+    cudaGetLastError();
+  }
+  const size_t smem = (size_t)max_tile_slots * 384;
+  if (smem > (size_t)g_max_dyn_smem) return fail(MVAMG_E_ARG, "gs rows ext: tile slices exceed shared memory");
+  cudaStream_t s = (cudaStream_t)stream;
+  gs_prepare_ext_kernel<<<grid_for(npos), 256, 0, s>>>(npos, rowid, row_lo, indptr, indices, data, b_own,
+                                                         x_old_ext, tperm, ws, x_old_ext ? 1 : 0);
+  GsRowArgs a;
+  a.n = npos;
+  a.ntiles = (npos + threads - 1) / threads;
+  a.rowid = rowid; a.cnt = cnt; a.crit = crit; a.wofs = wofs; a.coef = coef; a.src = src;
+  a.dg = dg; a.rdg = rdg; a.tperm = tperm;
+  a.xold = nullptr;
+  a.xnew = x_ext;
+  a.ticket = ws;
+  a.status = ws + 1;
+  a.trace = nullptr;
+  a.debug = 0;
+  a.mirror_ptr = mirror_ptr;
+  a.mirror_dst = mirror_dst;
+  a.peers = peers;
+  a.sys = 1;
+  const int grid = std::max(1, std::min(a.ntiles, ctas > 0 ? ctas : num_sms()));
+  gs_row_kernel<false><<<grid, threads, smem, s>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// CUDA IPC of a device buffer (the extended x of a rank, for its peers' mirror
+// stores): 64-byte handle out / open / close.
+int mvamg_ipc_handle(const void* dptr, void* handle64) {
+  if (!dptr || !handle64) return fail(MVAMG_E_ARG, "ipc_handle: null");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)));
+  std::memcpy(handle64, &h, sizeof(h));
+  return 0;
+}
+
+int mvamg_ipc_open(const void* handle64, void** dptr) {
+  if (!handle64 || !dptr) return fail(MVAMG_E_ARG, "ipc_open: null");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  CUDA_TRY(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return 0;
+}
+
+int mvamg_ipc_close(void* dptr) {
+  if (dptr) CUDA_TRY(cudaIpcCloseMemHandle(dptr));
+  return 0;
 }
 
 int mvamg_hierarchy_set_gs_rows(mvamg_hierarchy* h, int k, int mode, const int* rowid, const int* cnt,

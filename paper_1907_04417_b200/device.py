@@ -647,13 +647,19 @@ class DeviceGsRows:
     (0 fwd from x=0, 1 fwd, 2 bwd from x=0 -- also the folded backward sweep
     from x_old --, 3 bwd), on the device."""
 
-    def __init__(self, A, mode, cfg=None):
+    def __init__(self, A, mode, cfg=None, row_range=None):
+        """row_range (lo, hi): only those rows are swept (the own rows of a
+        row-partitioned level over its extended layout; the others are ghost
+        inputs, mvamg_gs_row_sweep_ext_f64)."""
         import torch
 
         cfg = cfg or GpuConfig()
         A = as_csr(A)
         L = _lib.load()
-        n = A.shape[0]
+        n_all = A.shape[0]
+        lo, hi = row_range if row_range is not None else (-1, -1)
+        n = n_all if row_range is None else hi - lo
+        self.row_range = row_range
         ip = np.ascontiguousarray(A.indptr, dtype=np.int32)
         ix = np.ascontiguousarray(A.indices, dtype=np.int32)
         v = np.ascontiguousarray(A.data, dtype=np.float64)
@@ -661,24 +667,25 @@ class DeviceGsRows:
         ns, nlev = ctypes.c_longlong(), ctypes.c_int()
         order = 0 if cfg.exact_gs else 1  # 1: entries by input level (tolerance parity)
         self.order = order
-        _lib.check(L.mvamg_gs_rows(n, vp(ip), vp(ix), vp(v), int(mode), order, ctypes.byref(ns),
-                                   ctypes.byref(nlev), None, None, None, None, None, None, None, None, None),
-                   "gs_rows")
+        _lib.check(L.mvamg_gs_rows(n_all, vp(ip), vp(ix), vp(v), int(mode), order, ctypes.byref(ns),
+                                   ctypes.byref(nlev), None, None, None, None, None, None, None, None, None,
+                                   lo, hi), "gs_rows")
         nw = -(-n // 32)
         rowid = np.empty(max(1, n), dtype=np.int32)
         cnt = np.empty(max(1, n), dtype=np.int32)
         crit = np.empty(max(1, n), dtype=np.int32)
         dg = np.empty(max(1, n), dtype=np.float64)
         rdg = np.empty(max(1, n), dtype=np.float64)
-        perm = np.empty(max(1, n), dtype=np.int32)
+        perm = np.empty(max(1, n_all), dtype=np.int32)
         wofs = np.empty(nw + 1, dtype=np.int32)
         coef = np.empty(max(32, 32 * ns.value), dtype=np.float64)
         src = np.empty(max(32, 32 * ns.value), dtype=np.int32)
-        _lib.check(L.mvamg_gs_rows(n, vp(ip), vp(ix), vp(v), int(mode), order, ctypes.byref(ns),
+        _lib.check(L.mvamg_gs_rows(n_all, vp(ip), vp(ix), vp(v), int(mode), order, ctypes.byref(ns),
                                    ctypes.byref(nlev), vp(rowid), vp(cnt), vp(crit), vp(dg), vp(rdg), vp(perm),
-                                   vp(wofs), vp(coef), vp(src)),
+                                   vp(wofs), vp(coef), vp(src), lo, hi),
                    "gs_rows")
         self.n, self.mode, self.nlev, self.nslots = n, mode, nlev.value, ns.value
+        self.n_all = n_all
         # threads per tile: the configured width, halved while the widest
         # tile's staged slices (384 B per slice row) exceed the budget
         T = int(cfg.row_gs_threads)
@@ -702,6 +709,17 @@ class DeviceGsRows:
         self.perm, self.wofs, self.coef, self.src = to_device(perm), to_device(wofs), to_device(coef), to_device(src)
         self.tperm = torch.empty(max(2, n + 2), dtype=torch.float64, device="cuda")
         self._csr = DeviceCSR(A)
+
+    def sweep_ext(self, b_own, x_old_ext, x_ext, mirror_ptr, mirror_dst, peers, ws, stream=None):
+        """Pipelined sweep of the own rows (row_range) over the extended layout
+        (mvamg_gs_row_sweep_ext_f64); x_ext's own and ghost slots must hold the
+        sentinel when the ranks start."""
+        lo, hi = self.row_range
+        _lib.check(_lib.load().mvamg_gs_row_sweep_ext_f64(
+            self.mode, self.n_all, lo, hi, *self._csr.ptrs(), ptr(self.rowid), ptr(self.cnt), ptr(self.crit),
+            ptr(self.dg), ptr(self.rdg), ptr(self.wofs), ptr(self.coef), ptr(self.src), self.threads, self.ctas,
+            self.max_tile_slots, ptr(self.tperm), ptr(b_own), ptr(x_old_ext), ptr(x_ext), ptr(mirror_ptr),
+            ptr(mirror_dst), ptr(peers), ptr(ws), stream or stream_handle()), "gs_row_sweep_ext")
 
     def args(self):
         return (ptr(self.rowid), ptr(self.cnt), ptr(self.crit), ptr(self.dg), ptr(self.rdg), ptr(self.perm),

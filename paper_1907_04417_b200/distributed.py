@@ -5,12 +5,21 @@ Coarse levels are gathered to rank 0, as SURVEY 8(e) specifies.  One V-cycle
 application on rank r (pkg/src/mvamg/cycles.py:150-179 with the default
 smoothers) runs as follows.
 
-1. Forward GS from x = 0 over the own rows, in rank order (a relay).  Rank r
-   receives the final values of its lower ghosts from the ranks below.  It
-   folds them into the right-hand side and sweeps its block with the
-   single-GPU exact-order kernels (lean wavefront or dataflow row sweep).  It
-   then sends the rows the ranks above need.  Upper ghosts are still zero in
-   this sweep, so they contribute nothing.
+1. Forward GS from x = 0 over the own rows.  Pipelined (one GPU per rank):
+   every rank launches its sweep at once over its extended layout
+   [lower ghosts | own rows | upper ghosts]; its kernel polls a ghost input
+   until the owner's kernel -- running concurrently on the neighbour GPU --
+   stores the final value straight into this rank's extended x over NVLink
+   (CUDA IPC pointers, mirror tables built here; the value's NaN sentinel is
+   its own ready flag, as between the tiles of one GPU).  The sweep is one
+   wavefront across the GPUs: a slab starts as soon as the first rows it
+   needs from the slab below are final, not when that slab is done, so the
+   critical path is the global DAG depth plus one hop per slab boundary
+   (C5 at N GPUs: 958 levels + (N - 1) hops) instead of the relay's sum of
+   the slabs' depths (N (40 + 319 + 319) levels at N = 8).  Fallback (ranks
+   sharing a GPU, or a backend without it): a relay in rank order -- rank r
+   receives the final lower ghosts, folds them into the right-hand side and
+   sweeps its block with the single-GPU kernels.
 2. t = r - A x through the x halo (ghosts before and after the own rows, in
    global column order, so each row's sum keeps the scipy CSR order).
 3. Restriction.  Each aggregate belongs to the rank owning its smallest
@@ -19,25 +28,26 @@ smoothers) runs as follows.
 4. The owned coarse values are gathered to rank 0.  Rank 0 runs the V-cycle
    of levels 1..L (a GpuMultigridOperator) and broadcasts x_c.
 5. x += P x_c on the own rows.
-6. Backward GS from x, in reverse rank order.  Lower ghosts keep their old
-   values (one x halo exchange); upper ghosts get the new values from the
-   ranks above.  Both are folded into the right-hand side.
+6. Backward GS from x: pipelined as 1 in the other direction (the old lower
+   neighbours, own and ghost, folded into the right-hand side first, in CSR
+   order); or relayed in reverse rank order (old lower ghosts and new upper
+   ghosts folded into the right-hand side).
 
 `dist_pcg` is krylov.py:28-72 over distributed vectors.  q = A p uses the halo
-SpMV; each dot is a local partial followed by one allreduce (r'z and r'r share
-it).
+SpMV; two allreduces per iteration (p'q, then r'r and r'z together).
 
 Parity (north star): at one rank the result is bit-identical to the
-single-GPU path.  With more ranks the exact GS order is kept, and so is every
-row sum that has no ghost term.  What changes is the rounding of the folded
-ghost terms, of the fold at the upper boundary of the backward sweep, and of
-the cross-rank dot sums.  Cycle applications stay within 1e-10 relative; the
-PCG iteration count stays equal or within +-1 (tests/test_distributed*.py).
+single-GPU path.  The pipelined sweeps keep both the dependency order and
+every row's CSR summation order, so a V-cycle at any rank count is
+bit-identical to one GPU (tests/test_distributed.py emulates it across
+processes on the CPU; tests/test_gpu_distributed.py runs the kernel rank by
+rank on one GPU).  The relay rounds the folded upper ghosts of the backward
+sweep differently (cycle within 1e-10).  Dots are summed across ranks:
+PCG histories within 1e-10, iteration count equal or +-1.
 
 Scaling.  SpMV, restriction, prolongation and the vector updates shard.  The
-exact-order sweeps are a relay: rank r starts once the ranks below are done.
-Their critical path therefore does not shrink with the GPU count (DESIGN.md
-(e)), and a pipelined relay over NVLink peer memory is listed under next steps.
+exact-order sweeps cannot: their critical path is the DAG depth (DESIGN.md
+(e)); the pipelined wavefront keeps it at one GPU's depth plus the hops.
 
 Communication goes through `Comm`, a thin wrapper over torch.distributed.
 NCCL moves device buffers directly.  Other backends (gloo: the CPU tests and
@@ -176,6 +186,9 @@ class RankPlan:
     P_own: object               # own rows of P_0 (n_own x n_1)
     n: int
     nc: int
+    M_ext: object = None        # pipelined sweeps: n_ext x n_ext, own rows over the extended layout, ghost rows empty
+    mirror_fwd: dict = None     # own local row -> [(peer, ext slot)]: peers reading it as a lower ghost
+    mirror_bwd: dict = None     # ... as an upper ghost
 
 
 def plan_rank(A, P, part, rank):
@@ -206,8 +219,30 @@ def plan_rank(A, P, part, rank):
     for M in (A_own, A_lg, A_ug):
         M.sort_indices()
     R_ext = _remap(R[lists[rank]], th)
-    return RankPlan(part, rank, xh, th, A_ext, A_own, A_lg, A_ug, R_ext, lists[rank],
-                    np.array([len(x) for x in lists]), lists, P[lo:hi].tocsr(), n, nc)
+    pl = RankPlan(part, rank, xh, th, A_ext, A_own, A_lg, A_ug, R_ext, lists[rank],
+                  np.array([len(x) for x in lists]), lists, P[lo:hi].tocsr(), n, nc)
+    # pipelined sweeps: the own rows as rows [n_lower, n_lower + n_own) of a square
+    # matrix over the extended layout (ghost rows empty; global order kept, so a
+    # row's CSR order and its lower / upper split are the single-GPU ones), and for
+    # every own row the peers that read it as a ghost, with its slot in their layout
+    n_ext = xh.n_own + xh.n_ghost
+    ip = np.zeros(n_ext + 1, dtype=np.int64)
+    ip[xh.n_lower + 1:xh.n_lower + xh.n_own + 1] = np.diff(A_ext.indptr)
+    np.cumsum(ip, out=ip)
+    pl.M_ext = sp.csr_matrix((A_ext.data, A_ext.indices, ip), shape=(n_ext, n_ext))
+    pl.mirror_fwd, pl.mirror_bwd = {}, {}
+    for q in range(nr):
+        if q == rank:
+            continue
+        hq = make_halo(part, q, need_x)
+        sel = np.nonzero((hq.ghosts >= lo) & (hq.ghosts < hi))[0]
+        for g in sel:
+            own = int(hq.ghosts[g] - lo)
+            if g < hq.n_lower:   # q reads it as a lower ghost: the forward sweep feeds q
+                pl.mirror_fwd.setdefault(own, []).append((q, int(g)))
+            else:                # an upper ghost of q: the backward sweep feeds q
+                pl.mirror_bwd.setdefault(own, []).append((q, int(g) + hq.n_own))
+    return pl
 
 
 # -------------------------------------------------------------------- comm ---
@@ -397,6 +432,69 @@ class DeviceBackend:
         else:
             obj[0 if direction == 0 else 2].sweep(b, x_old, x_new, self._ws)
 
+    # pipelined fine-level sweeps across the ranks (DistributedVCycle.pipelined)
+    def pipe_ok(self, comm):
+        """Only with one GPU per rank (NCCL): ranks whose kernels poll each other
+        must not share a GPU (one could hold every SM while the other waits)."""
+        return comm.nccl
+
+    def pipe_plan(self, M_ext, row_range, mode, mirror_rows):
+        """Row schedule of the own rows over the extended layout plus the
+        position-indexed mirror table (peer << 24 | slot) of mvamg_gs_row_sweep_ext_f64."""
+        from .device import DeviceGsRows, to_device
+
+        rows = DeviceGsRows(M_ext, mode, self.cfg, row_range=row_range)
+        lo = row_range[0]
+        rowid = rows.rowid.cpu().numpy()[:rows.n]
+        ptr_, dst = [0], []
+        for i in rowid:
+            for q, slot in mirror_rows.get(int(i) - lo, ()):
+                if slot >= (1 << 24) or q >= 256:
+                    raise ValueError("pipelined sweep: mirror slot / peer out of range")
+                dst.append((q << 24) | slot)
+            ptr_.append(len(dst))
+        return {"rows": rows, "mptr": to_device(np.asarray(ptr_, dtype=np.int32)),
+                "mdst": to_device(np.asarray(dst or [0], dtype=np.uint32).view(np.int32))}
+
+    def pipe_share(self, comm, n):
+        """This rank's extended x for the pipelined sweeps and a device array of
+        every rank's (CUDA IPC: the peers' kernels store into it over NVLink)."""
+        import ctypes
+
+        torch = self.torch
+        xp = torch.empty(max(1, n), dtype=torch.float64, device="cuda")
+        handle = ctypes.create_string_buffer(64)
+        self._lib.check(self.L.mvamg_ipc_handle(ctypes.c_void_p(xp.data_ptr()), handle), "ipc_handle")
+        handles = [handle.raw]
+        if comm.size > 1:
+            handles = [None] * comm.size
+            comm.dist.all_gather_object(handles, handle.raw, group=comm.group)
+        ptrs = []
+        self._ipc_open = []
+        for q, h in enumerate(handles):
+            if q == comm.rank:
+                ptrs.append(xp.data_ptr())
+                continue
+            p = ctypes.c_void_p()
+            self._lib.check(self.L.mvamg_ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(p)), "ipc_open")
+            self._ipc_open.append(p)
+            ptrs.append(p.value)
+        peers = torch.tensor(ptrs, dtype=torch.int64, device="cuda")
+        return xp[:n], peers
+
+    def fill_sentinel(self, t):
+        t.view(self.torch.int64).fill_(-1)  # all-ones: the NaN no arithmetic produces (not-yet-final)
+        self.torch.cuda.synchronize()       # executed, not just queued, before the ranks synchronise
+
+    def pipe_sweep(self, plan, b_own, x_old_ext, x_ext, peers):
+        from .device import ptr  # noqa: F401
+
+        plan["rows"].sweep_ext(b_own, x_old_ext, x_ext, plan["mptr"], plan["mdst"], peers, self._ws, self._s())
+        self.torch.cuda.synchronize()
+        st = int(self._ws[1].item())
+        if st:
+            raise RuntimeError(f"pipelined GS sweep: status {st} (timeout waiting on a ghost)")
+
     def coarse(self, mats, pros):
         from .cycles import CycleSpec, GpuMultigridOperator
 
@@ -410,7 +508,14 @@ class DeviceBackend:
 class DistributedVCycle:
     """One rank's share of the row-partitioned V-cycle (module docstring)."""
 
-    def __init__(self, matrices, prolongators, comm=None, backend=None, part=None):
+    def __init__(self, matrices, prolongators, comm=None, backend=None, part=None, pipelined=None):
+        """pipelined (default: whenever there are several ranks and the backend
+        supports it): the fine-level sweeps run as one wavefront across the
+        ranks -- every rank sweeps its rows at once, polling its ghost inputs,
+        which their owners store into its extended x the moment they are final
+        (mvamg_gs_row_sweep_ext_f64) -- instead of the rank-by-rank relay.  Both
+        keep the serial loop's dependency order; the pipelined sweep also keeps
+        every row's CSR summation order, so the cycle is bit-identical to one GPU."""
         self.comm = comm or Comm()
         self.be = backend or DeviceBackend()
         mats = [as_csr(M) for M in matrices]
@@ -448,6 +553,15 @@ class DistributedVCycle:
         self.xc = be.vec(nc)
         self.pe = be.vec(xh.n_own + xh.n_ghost)        # PCG direction, extended
         self._bufs = {}
+        if pipelined is None:
+            pipelined = self.comm.size > 1 and hasattr(be, "pipe_plan") and be.pipe_ok(self.comm)
+        self.pipelined = bool(pipelined)
+        if self.pipelined:
+            lo_e, hi_e = xh.n_lower, xh.n_lower + xh.n_own
+            self.pipe_fwd = be.pipe_plan(pl.M_ext, (lo_e, hi_e), 0, pl.mirror_fwd)
+            self.pipe_bwd = be.pipe_plan(pl.M_ext, (lo_e, hi_e), 2, pl.mirror_bwd)
+            # the pipelined sweeps' extended x, which the peers store into, and theirs
+            self.xp, self.peers = be.pipe_share(self.comm, xh.n_own + xh.n_ghost)
 
     # ---- halo exchanges --------------------------------------------------
     def _buf(self, key, n):
@@ -494,11 +608,15 @@ class DistributedVCycle:
         x_own = self._xsl(xh, xe)
         lower = xe[:xh.n_lower]
         upper = xe[xh.n_lower + xh.n_own:]
-        # 1. forward GS from x = 0, relayed in rank order
-        self.exchange(xh, xe, self.x_send, peers_to=(), peers_from=range(rank))
-        be.residual(self.A_lg, r_own, lower, self.b_fold)
-        be.gs(self.sm, 0, self.b_fold, None, x_own)
-        self.exchange(xh, xe, self.x_send, peers_to=range(rank + 1, nr), peers_from=())
+        # 1. forward GS from x = 0: one wavefront across the ranks, or relayed in rank order
+        if self.pipelined:
+            self._pipe_sweep(self.pipe_fwd, r_own, None)
+            self._xsl(xh, xe).copy_(self._xsl(xh, self.xp))
+        else:
+            self.exchange(xh, xe, self.x_send, peers_to=(), peers_from=range(rank))
+            be.residual(self.A_lg, r_own, lower, self.b_fold)
+            be.gs(self.sm, 0, self.b_fold, None, x_own)
+            self.exchange(xh, xe, self.x_send, peers_to=range(rank + 1, nr), peers_from=())
         # 2. t = r - A x over the full x halo
         self.exchange(xh, xe, self.x_send)
         t_own = self._xsl(th, self.te)
@@ -522,8 +640,13 @@ class DistributedVCycle:
         comm.broadcast(self.xc, 0)
         # 5. x += P x_c on the own rows
         be.spmv_add(self.P_own, self.xc, x_own)
-        # 6. backward GS from x, relayed in reverse rank order
+        # 6. backward GS from x: one wavefront across the ranks, or relayed in reverse rank order
         self.exchange(xh, xe, self.x_send)                   # old values of every ghost
+        if self.pipelined:
+            self._pipe_sweep(self.pipe_bwd, r_own, xe)
+            x_own.copy_(self._xsl(xh, self.xp))
+            z_own.copy_(x_own)
+            return z_own
         self.exchange(xh, xe, self.x_send, peers_to=(), peers_from=range(rank + 1, nr))
         be.residual(self.A_lg, r_own, lower, self.b_fold)
         be.residual(self.A_ug, self.b_fold, upper, self.b_fold)
@@ -532,6 +655,15 @@ class DistributedVCycle:
         self.exchange(xh, xe, self.x_send, peers_to=range(rank), peers_from=())
         z_own.copy_(x_own)
         return z_own
+
+    def _pipe_sweep(self, plan, b_own, x_old_ext):
+        """Reset the shared extended x to the sentinel, synchronise the ranks (no
+        peer may store a value before the reset), then sweep: every rank's kernel
+        polls its ghosts while its peers' kernels are still running."""
+        self.be.fill_sentinel(self.xp)
+        self.comm.barrier()
+        self.be.pipe_sweep(plan, b_own, x_old_ext, self.xp, self.peers)
+        self.comm.barrier()  # every peer's stores into this rank's x are done
 
     # ---- distributed operator pieces for PCG ---------------------------------
     def matvec(self, p_own, q_own):

@@ -113,6 +113,57 @@ def test_distributed_pcg_gloo(world, direct):
     assert np.linalg.norm(d["b"] - mats[0] @ x) <= 1e-6 * np.linalg.norm(d["b"]) * 1.0001
 
 
+def _worker_pipelined(rank, world, port, out, tag):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    be = None
+    try:
+        from _dist_backend import PipelinedOracleBackend
+        from paper_1907_04417_b200.distributed import Comm
+
+        d = golden("c1")
+        mats, pros = hierarchy(d, "mv")
+        be = PipelinedOracleBackend(tag)
+        s = DistributedSolver(mats, pros, comm=Comm(), backend=be)
+        op = s.op
+        assert op.pipelined
+        z = op.be.vec(op.n_own)
+        op.apply(op.be.from_host(s.own_rows(d["b"])), z)
+        x, rep = s.solve(d["b"])
+        out[rank] = (z.numpy().copy(), x, rep.iterations, rep.residual_history)
+        dist.barrier()
+    finally:
+        if be is not None:
+            be.close()
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_pipelined_sweeps_gloo(world):
+    """The pipelined fine-level sweeps (every rank sweeps at once, polling its
+    ghosts, which their owners -- other processes -- store into its shared
+    extended x as they finish them): the same dependency order and the same
+    CSR summation order as the serial loop, so one V-cycle is bit-identical to
+    the single-process oracle's (the relay folds the upper ghosts out of
+    order: 1e-10).  PCG as the single-process solve (dots: tolerance)."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    mp.spawn(_worker_pipelined, args=(world, port, out, f"t{port}"), nprocs=world, join=True)
+    d = golden("c1")
+    mats, pros = hierarchy(d, "mv")
+    ref = OracleOperator(mats, pros)
+    z = np.concatenate([out[r][0] for r in range(world)])
+    assert np.array_equal(z, ref.apply(d["b"]))
+    _, hist, nit, _ = oracle_pcg(ref, d["b"])
+    for r in range(world):
+        assert out[r][2] == nit
+    h = out[0][3]
+    assert np.max(np.abs(h - hist[:len(h)]) / hist[:len(h)]) <= 1e-10
+    x = np.concatenate([out[r][1] for r in range(world)])
+    assert np.linalg.norm(d["b"] - mats[0] @ x) <= 1e-6 * np.linalg.norm(d["b"]) * 1.0001
+
+
 def test_cycle_needs_two_levels():
     from _dist_backend import OracleBackend
 

@@ -12,7 +12,9 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from _fixtures import golden, hierarchy
-from oracle.oracle import OracleOperator, oracle_pcg
+from oracle.oracle import OracleOperator, oracle_gs, oracle_pcg
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 pytestmark = pytest.mark.gpu
 
@@ -55,8 +57,9 @@ def _worker(rank, world, port, out):
 
         d = golden("c1")
         mats, pros = hierarchy(d, "mv")
-        s = DistributedSolver(mats, pros)
+        s = DistributedSolver(mats, pros)  # gloo on one GPU: the relay (no kernel waits on a peer)
         op = s.op
+        assert not op.pipelined
         z = op.be.vec(op.n_own)
         op.apply(op.be.from_host(s.own_rows(d["b"])), z)
         x, rep = s.solve(d["b"])
@@ -81,3 +84,78 @@ def test_distributed_two_ranks_one_gpu():
     h = out[0][3]
     m = min(len(h), len(hist))
     assert np.max(np.abs(h[:m] - hist[:m]) / hist[:m]) <= 1e-10
+
+
+def test_pipelined_ext_sweeps_bit_exact_sequential():
+    """The pipelined fine-level sweep kernel (mvamg_gs_row_sweep_ext_f64) of a
+    2- and 3-rank row partition, run rank after rank on one GPU (forward in
+    rank order, backward in reverse -- no kernel waits on another concurrently
+    running one): each rank's rows over its extended layout, ghost inputs read
+    from the slots its peers' kernels stored into, CSR summation order kept --
+    bit-identical to the serial sweep of the whole matrix."""
+    import torch
+
+    from paper_1907_04417_b200.device import GpuConfig
+    from paper_1907_04417_b200.distributed import DeviceBackend, RowPartition, plan_rank
+
+    d = golden("c1")
+    mats, pros = hierarchy(d, "mv")
+    A, P = mats[0], pros[0]
+    n = A.shape[0]
+    rng = np.random.default_rng(7)
+    b, x0 = rng.standard_normal(n), rng.standard_normal(n)
+    be = DeviceBackend(GpuConfig(exact_gs=True))
+    for nr in (2, 3):
+        part = RowPartition.balanced(A, nr)
+        plans = [plan_rank(A, P, part, r) for r in range(nr)]
+        xps = [torch.empty(p.xhalo.n_own + p.xhalo.n_ghost, dtype=torch.float64, device="cuda") for p in plans]
+        peers = torch.tensor([t.data_ptr() for t in xps], dtype=torch.int64, device="cuda")
+        for mode, direction in ((0, "forward"), (2, "backward")):
+            want = np.zeros(n) if mode == 0 else x0.copy()
+            oracle_gs(A, b, want, direction)
+            for t in xps:
+                be.fill_sentinel(t)
+            order = range(nr) if mode == 0 else range(nr - 1, -1, -1)
+            got = np.empty(n)
+            for r in order:
+                pl, h = plans[r], plans[r].xhalo
+                mirror = pl.mirror_fwd if mode == 0 else pl.mirror_bwd
+                pp = be.pipe_plan(pl.M_ext, (h.n_lower, h.n_lower + h.n_own), mode, mirror)
+                xo = None
+                if mode == 2:
+                    ext = np.concatenate([x0[h.ghosts[:h.n_lower]], x0[h.lo:h.hi], x0[h.ghosts[h.n_lower:]]])
+                    xo = torch.from_numpy(ext).cuda()
+                be.pipe_sweep(pp, torch.from_numpy(b[h.lo:h.hi].copy()).cuda(), xo, xps[r], peers)
+                got[h.lo:h.hi] = xps[r][h.n_lower:h.n_lower + h.n_own].cpu().numpy()
+            assert np.array_equal(got, want), (nr, direction)
+
+
+def test_ipc_handle_opened_by_another_process():
+    """mvamg_ipc_handle / mvamg_ipc_open: a child process opens this process's
+    buffer and stores into it (what a peer rank's pipelined sweep does)."""
+    import ctypes
+    import subprocess
+    import sys
+
+    import torch
+
+    from paper_1907_04417_b200 import _lib
+
+    L = _lib.load()
+    buf = torch.zeros(16, dtype=torch.float64, device="cuda")
+    h = ctypes.create_string_buffer(64)
+    _lib.check(L.mvamg_ipc_handle(ctypes.c_void_p(buf.data_ptr()), h), "ipc_handle")
+    torch.cuda.synchronize()
+    code = (
+        "import ctypes, sys, torch\n"
+        "sys.path.insert(0, %r)\n"
+        "from paper_1907_04417_b200 import _lib\n"
+        "L = _lib.load()\n"
+        "p = ctypes.c_void_p()\n"
+        "_lib.check(L.mvamg_ipc_open(ctypes.create_string_buffer(bytes.fromhex(%r), 64), ctypes.byref(p)), 'open')\n"
+        "src = torch.arange(16, dtype=torch.float64, device='cuda')\n"
+        "torch.cuda.cudart().cudaMemcpy(p.value, src.data_ptr(), 128, 4)\n"
+        "torch.cuda.synchronize()\n"
+        "_lib.check(L.mvamg_ipc_close(p), 'close')\n" % (ROOT, h.raw.hex()))
+    subprocess.run([sys.executable, "-c", code], check=True, timeout=300)
+    assert np.array_equal(buf.cpu().numpy(), np.arange(16.0))
