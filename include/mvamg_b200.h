@@ -208,25 +208,6 @@ int mvamg_gs_level_sweep_folded_f64(int n, const int* indptr, const int* indices
                                     const void* rows, const void* ents, const int* perm,
                                     double* tperm, const double* b, const double* x_old,
                                     double* x_new, int* ws, void* stream);
-/* Chain-scan GS sweep (tolerance parity; csrc/gs_scan.cuh) for levels with
- * chain structure (grid lines): one CTA, chains round-robin over its warps, a
- * warp composes 32 rows' affine updates x_i = o_i + s_i x_{i-1} with a shuffle
- * scan.  Same dependency order as _kernels.py:15-38; sums reassociated.  The
- * schedule comes from paper_1907_04417_b200/gs_scan.py: chains in sweep order;
- * per record (slope, coefficients) double pairs and four ring addresses; per
- * segment a 32-byte header (two waits, the deferred source of its last row,
- * its coefficient); the row -> record map and RN(1/diag); the distinct
- * source-chain distances as a host array of ndelta <= 4 ints.  window > 0
- * (power of two, single distance 1): ring slots keep positions mod window.  mode: 0 fwd from 0, 1 fwd from
- * x_old, 2 bwd from 0, 3 bwd from x_old.  o0: device scratch in the record
- * layout (padding entries zero).  ws: >= 2 device ints (ws[1]: timeout). */
-int mvamg_gs_scan_sweep_f64(int mode, int n, const int* indptr, const int* indices, const double* data,
-                            int nchains, int S, int ring_len, int ndelta, const int* deltas, int K, int threads,
-                            int window, const int* seg_ptr, const int* chain_start, const int* chain_len,
-                            const void* recv, const void* addr, const void* seginfo, double* o0, const int* rec,
-                            const double* rdiag, const double* b, const double* x_old, double* x_new, int* ws,
-                            void* stream);
-
 /* GS dataflow row schedule for mid-size coarse levels (host).  mode as in
  * mvamg_gs_levels.  Rows are put in topological order of the sweep's DAG
  * (level, then longest row first); position p holds row rowid[p] with cnt[p]
@@ -400,28 +381,12 @@ int mvamg_gs_stream_set_trace(long long* trace_dev, int cap);
  * neighbours are folded into the right-hand side first (same roundings). */
 int mvamg_hierarchy_set_gs_stream(mvamg_hierarchy* h, int k, int mode, int nstages, int nslots, int slot_bytes,
                                   int group, int ncta, const void* blob, const long long* stage_off, double* tfold);
-/* Diagnostics: 4 x int64 %globaltimer stamps per segment written by the
- * chain-scan sweeps into trace_dev (NULL turns it off). */
-int mvamg_gs_scan_set_trace(long long* trace_dev);
-/* Chain-scan schedule of level k for sweep `mode` (see mvamg_gs_scan_sweep_f64);
- * used before any other schedule of that mode when set. */
-int mvamg_hierarchy_set_gs_scan(mvamg_hierarchy* h, int k, int mode, int nchains, int S, int ring_len,
-                                int ndelta, const int* deltas, int K, int threads, int window,
-                                const int* seg_ptr, const int* chain_start, const int* chain_len, const void* recv,
-                                const void* addr, const void* seginfo, double* o0, const int* rec,
-                                const double* rdiag);
 /* Dataflow row schedule of level k for sweep `mode` (see mvamg_gs_rows);
  * used when set and no level-set schedule is set for that mode. */
 int mvamg_hierarchy_set_gs_rows(mvamg_hierarchy* h, int k, int mode, const int* rowid, const int* cnt,
                                 const int* crit, const double* dg, const double* rdg, const int* perm, const int* wofs,
                                 const double* coef, const int* src, int threads, int ctas,
                                 int max_tile_slots, double* tperm);
-/* Run every level >= k0 of the cycle in one thread block (coarse_mega_kernel:
- * the K-cycle's nested FCG / V recursion, GS sweeps, transfers and coarsest
- * solve with no kernel launches inside).  Needs the bound workspace, the
- * default smoothers and single-CTA level-set schedules (modes 0 and 2) on
- * levels k0..L-2; k0 < 0 turns it off.  A V-cycle is bit-identical either way. */
-int mvamg_hierarchy_set_mega(mvamg_hierarchy* h, int k0);
 /* Transfer k: P (n_k x n_{k+1}) and R = P^T (n_{k+1} x n_k), device CSR.
  * Levels k and k+1 must be set first (their sizes give P's and R's shapes):
  * otherwise MVAMG_E_STATE.  Synchronises the device once to read nnz(P), nnz(R). */

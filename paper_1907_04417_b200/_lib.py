@@ -83,7 +83,6 @@ SIGNATURES = [
     ("mvamg_hierarchy_set_gs_schedule", _I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I]),
     ("mvamg_hierarchy_set_gs_levels", _I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_hierarchy_set_gs_rows", _I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P]),
-    ("mvamg_hierarchy_set_mega", _I, [_P, _I]),
     ("mvamg_hierarchy_set_transfer", _I, [_P, _I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_hierarchy_set_coarse", _I, [_P, _P]),
     ("mvamg_hierarchy_workspace_bytes", _I, [_P, ctypes.POINTER(_LL)]),
@@ -101,9 +100,6 @@ SIGNATURES = [
     ("mvamg_galerkin_f64", _I, [_I, _I, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_P), ctypes.POINTER(_LL), _P, _P]),
     ("mvamg_spmat_copy", _I, [_P, _P, _P, _P, _P]),
     ("mvamg_spmat_destroy", _I, [_P]),
-    ("mvamg_gs_scan_sweep_f64", _I, [_I, _I, _P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _I] + [_P] * 14),
-    ("mvamg_hierarchy_set_gs_scan", _I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _I] + [_P] * 9),
-    ("mvamg_gs_scan_set_trace", _I, [_P]),
     ("mvamg_greedy_match_device", _I, [_I, _P, _P, _P, _P, _P, _D, _P, _PI, _P]),
     ("mvamg_jacobi_svd_batch_device", _I, [_I, _P, _I, _P, _I, _D, _P, _P, _PI, _P]),
     ("mvamg_gather_f64", _I, [_I, _P, _P, _P, _P]),

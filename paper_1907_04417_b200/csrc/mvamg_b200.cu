@@ -24,9 +24,7 @@
 
 #include "../../include/mvamg_b200.h"
 #include "mvamg_kernels.cuh"
-#include "coarse_mega.cuh"
 #include "galerkin.cuh"
-#include "gs_scan.cuh"
 #include "gs_stream.cuh"
 #include "matching.cuh"
 #include "svd.cuh"
@@ -56,15 +54,6 @@ int g_gs_debug = [] {
   const char* e = getenv("MVAMG_GS_DEBUG");
   return e ? atoi(e) : 0;
 }();  // kernels launched by this library (graph nodes counted per replay)
-int g_scan_spin = [] {  // chain-scan sweep: busy polls before __nanosleep back-off
-  const char* e = getenv("MVAMG_SCAN_SPIN");
-  return e ? atoi(e) : 64;
-}();
-int g_scan_sleep = [] {
-  const char* e = getenv("MVAMG_SCAN_SLEEP");
-  return e ? atoi(e) : 32;
-}();
-long long* g_scan_trace = nullptr;  // diagnostics: chain-scan per-segment timestamps (mvamg_gs_scan_set_trace)
 int g_row_sleep = [] {
   const char* e = getenv("MVAMG_ROW_SLEEP");
   return e ? atoi(e) : 0;
@@ -182,22 +171,6 @@ struct GsStream {
   const unsigned char* blob = nullptr;
   const long long* stage_off = nullptr;
   double* tfold = nullptr;  // n doubles: folded right-hand side (mode-2 plan used from x_old)
-};
-
-// Chain-scan schedule (gs_scan.cuh) of one sweep mode (tolerance parity).
-struct GsScan {
-  int nchains = 0, S = 0, ring_len = 0, K = 0, threads = 0, window = 0;
-  int cluster = 0;  // > 1: chains spread over a cluster of that many CTAs (window mode)
-  int ndelta = 0, delta[gsscan::kMaxDeps] = {0, 0, 0, 0};  // distinct source-chain distances
-  const int* seg_ptr = nullptr;
-  const int* chain_start = nullptr;
-  const int* chain_len = nullptr;
-  const void* recv = nullptr;
-  const void* addr = nullptr;
-  const void* seginfo = nullptr;
-  double* o0 = nullptr;
-  const int* rec = nullptr;
-  const double* rdiag = nullptr;
 };
 
 // Dataflow row schedule (gs_row_kernel) of one sweep mode.
@@ -608,114 +581,6 @@ int launch_gs_levels(const Csr& A, const GsLevels& g, bool zero, const double* b
   return 0;
 }
 
-int set_deltas(GsScan& g, int ndelta, const int* deltas) {
-  if (ndelta < 0 || ndelta > gsscan::kMaxDeps || (ndelta && !deltas))
-    return fail(MVAMG_E_ARG, "gs scan: 0..4 distinct source-chain distances");
-  g.ndelta = ndelta;
-  for (int d = 0; d < ndelta; ++d) {
-    if (deltas[d] < 1 || deltas[d] >= g.S) return fail(MVAMG_E_ARG, "gs scan: distance outside the ring");
-    g.delta[d] = deltas[d];
-  }
-  return 0;
-}
-
-int gs_scan_stage_bytes(int K) { return 256 + ((K + 2) / 2) * 512 + 512 + 32; }
-size_t gs_scan_smem(const GsScan& g) {
-  const size_t nw = (size_t)g.threads / 32;
-  return ((8 * (size_t)((g.S + 1) & ~1) + 8 * (size_t)g.S * g.ring_len + 127) & ~(size_t)127) +
-         nw * gsscan::kStages * (size_t)gs_scan_stage_bytes(g.K) + nw * gsscan::kStages * 8 +
-         (g.cluster > 1 ? 16 + nw * 512 : 0);  // cluster kernel: two 32-value x staging buffers per warp
-}
-
-// mode: 0 fwd from 0, 1 fwd from x_old, 2 bwd from 0, 3 bwd from x_old.
-int launch_gs_scan(const Csr& A, const GsScan& g, int mode, const double* b, const double* xold, double* xnew,
-                   int* status, cudaStream_t s) {
-  using namespace gsscan;
-  static bool attr = false;
-  if (!attr) {
-    attr = true;
-    int dev = 0, optin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncSetAttribute(gs_scan_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-    cudaFuncSetAttribute(gs_scan_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-    cudaFuncSetAttribute(gs_scan_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-    cudaFuncSetAttribute(gs_scan_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-    cudaGetLastError();
-  }
-  const int n = A.n;
-  if (n == 0) return 0;
-  if (g.K < 1 || g.K > 4) return fail(MVAMG_E_ARG, "gs scan: 1..4 cross-chain sources per row");
-  if (g.threads < 32 || g.threads > 1024 || g.threads % 32) return fail(MVAMG_E_ARG, "gs scan: bad thread count");
-  const size_t smem = gs_scan_smem(g);
-  if (smem > (size_t)g_max_dyn_smem + 1024) return fail(MVAMG_E_ARG, "gs scan: ring exceeds shared memory");
-  const int old = (mode & 1) ? ((mode < 2) ? 1 : 2) : 0;
-  if (old && !xold) return fail(MVAMG_E_ARG, "gs scan: mode needs x_old");
-  gs_scan_prepass_kernel<<<grid_for(n), 256, 0, s>>>(n, A.ip, A.ix, A.v, g.rdiag, g.rec, b, xold, old, g.o0);
-  ScanArgs a;
-  a.nchains = g.nchains;
-  a.S = g.S;
-  a.ring_len = g.ring_len;
-  a.window = g.window;
-  a.stage_bytes = gs_scan_stage_bytes(g.K);
-  a.spin_polls = g_scan_spin;
-  a.sleep_ns = g_scan_sleep;
-  a.ndelta = g.ndelta;
-  for (int d = 0; d < kMaxDeps; ++d) a.delta[d] = g.delta[d];
-  a.n = n;
-  a.fwd = mode < 2 ? 1 : 0;
-  a.seg_ptr = g.seg_ptr;
-  a.chain_start = g.chain_start;
-  a.chain_len = g.chain_len;
-  a.recv = static_cast<const double2*>(g.recv);
-  a.addr = static_cast<const uint4*>(g.addr);
-  a.seginfo = static_cast<const SegInfo*>(g.seginfo);
-  a.o0 = g.o0;
-  a.xnew = xnew;
-  a.status = status;
-  a.trace = g_scan_trace;
-  if (g.cluster > 1) {
-    static bool cattr = false;
-    if (!cattr) {
-      cattr = true;
-      cudaFuncSetAttribute(gs_scan_cluster_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(gs_scan_cluster_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(gs_scan_cluster_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(gs_scan_cluster_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaGetLastError();
-    }
-    if (!g.window || g.ndelta != 1 || g.delta[0] != 1)
-      return fail(MVAMG_E_ARG, "gs scan: the cluster sweep needs window mode (sources one chain back)");
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(g.cluster);
-    cfg.blockDim = dim3(g.threads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = g.cluster;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    switch (g.K) {
-      case 1: CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_scan_cluster_kernel<1>, a)); break;
-      case 2: CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_scan_cluster_kernel<2>, a)); break;
-      case 3: CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_scan_cluster_kernel<3>, a)); break;
-      default: CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_scan_cluster_kernel<4>, a)); break;
-    }
-    return 0;
-  }
-  switch (g.K) {
-    case 1: gs_scan_kernel<1><<<1, g.threads, smem, s>>>(a); break;
-    case 2: gs_scan_kernel<2><<<1, g.threads, smem, s>>>(a); break;
-    case 3: gs_scan_kernel<3><<<1, g.threads, smem, s>>>(a); break;
-    default: gs_scan_kernel<4><<<1, g.threads, smem, s>>>(a); break;
-  }
-  CUDA_TRY(cudaGetLastError());
-  return 0;
-}
-
 bool g_row_attr = false;
 // Dataflow row sweep: prepare (rhs in position order, fold, sentinel fill,
 // ticket reset), then gs_row_kernel on `ctas` resident CTAs (0 = one per SM).
@@ -788,7 +653,6 @@ struct Level {
   GsStream gss[4];  // streamed single-SM schedules (used first when set)
   GsLevels glv[4];  // small-level single-CTA schedules (used when set)
   GsRows grw[4];    // dataflow row schedules (used when set and glv is not)
-  GsScan gsc[4];    // chain-scan schedules (tolerance parity; used first when set)
   Csr P, R;  // valid for k < L-1
   double *xa = nullptr, *xb = nullptr, *t = nullptr, *r = nullptr, *z = nullptr;
   double *fr = nullptr, *fx = nullptr, *fp[2] = {nullptr, nullptr}, *fap[2] = {nullptr, nullptr};
@@ -811,8 +675,6 @@ struct mvamg_hierarchy {
   DevScalars* host_sc = nullptr;  // pinned mirror
   std::map<std::string, cudaGraphExec_t> graphs;
   std::map<std::string, int> graph_kernels;
-  int mega_k0 = -1;                 // levels >= mega_k0 run in coarse_mega_kernel (-1: off)
-  MegaLevel* mega_dev = nullptr;
 
   ReduceCtx ctx(FcgScalars* fs = nullptr, double* out = nullptr) const {
     ReduceCtx c;
@@ -829,27 +691,6 @@ struct mvamg_hierarchy {
   ~mvamg_hierarchy() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     if (host_sc) cudaFreeHost(host_sc);
-    if (mega_dev) cudaFree(mega_dev);
-  }
-
-  // ---- the small coarse levels in one block (coarse_mega.cuh) --------------
-  // entry: descend(k0, r) or, on an FCG level, fcg(k0, r); result in `out`.
-  int launch_mega(int k0, const double* r, const double*& out, cudaStream_t s) {
-    MegaArgs a;
-    a.k0 = k0;
-    a.L = L;
-    a.entry_fcg = fcg_level(k0) ? 1 : 0;
-    a.kcycle = kind == MVAMG_CYCLE_K ? 1 : 0;
-    a.inner = inner;
-    a.nL = lv[L - 1].A.n;
-    a.lv = mega_dev;
-    a.inv = inv;
-    a.in = r;
-    a.status = status_ptr();
-    coarse_mega_kernel<<<1, kMegaThreads, 0, s>>>(a);
-    CUDA_TRY(cudaGetLastError());
-    out = a.entry_fcg ? lv[k0].fx : (k0 == L - 1 ? lv[k0].z : lv[k0].xa);
-    return 0;
   }
 
   // ---- smoothing (cycles.py:139-148) ----------------------------------------
@@ -883,8 +724,6 @@ struct mvamg_hierarchy {
           // neighbours into the right-hand side first (same roundings, CSR order)
           launch_prepare(l.A, b, x_cur, nullptr, l.gss[2].tfold, out, ticket, 1, s);
           st = launch_gs_stream(l.A.n, l.gss[2], 0, l.gss[2].tfold, nullptr, out, s);
-        } else if (l.gsc[lmode].nchains) {
-          st = launch_gs_scan(l.A, l.gsc[lmode], lmode, b, x_cur, out, status_ptr(), s);
         } else if (!fwd && x_cur != nullptr && l.glv[2].rows) {
           st = launch_gs_levels(l.A, l.glv[2], false, b, x_cur, out, ticket, s, /*fold=*/true);
         } else if (l.glv[lmode].rows) {
@@ -925,8 +764,7 @@ struct mvamg_hierarchy {
     if ((st = launch_spmv(1, l.A, x, r, l.t, s))) return st;     // t = r - A x
     if ((st = launch_spmv(0, l.R, l.t, nullptr, c.r, s))) return st;  // rc = R t
     const double* xc = nullptr;
-    if (mega_k0 == k + 1) st = launch_mega(k + 1, c.r, xc, s);
-    else if (fcg_level(k + 1)) st = fcg(k + 1, c.r, xc, s);
+    if (fcg_level(k + 1)) st = fcg(k + 1, c.r, xc, s);
     else st = descend(k + 1, c.r, xc, s);
     if (st) return st;
     if ((st = launch_spmv(2, l.P, xc, nullptr, x, s))) return st;  // x += P xc
@@ -968,7 +806,6 @@ struct mvamg_hierarchy {
   // z = B r for the level-0 cycle.  `r` must stay valid while the sequence runs.
   int cycle(const double* r, const double*& out, cudaStream_t s) {
     if (L == 1) return coarse(r, out, s);
-    if (mega_k0 == 0) return launch_mega(0, r, out, s);
     return descend(0, r, out, s);
   }
 
@@ -2540,48 +2377,6 @@ int mvamg_hierarchy_set_gs_rows(mvamg_hierarchy* h, int k, int mode, const int* 
   return 0;
 }
 
-int mvamg_hierarchy_set_mega(mvamg_hierarchy* h, int k0) {
-  if (!h) return fail(MVAMG_E_ARG, "set_mega: null handle");
-  if (k0 < 0) {
-    h->mega_k0 = -1;
-    for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
-    h->graphs.clear();
-    return 0;
-  }
-  if (k0 > h->L - 2) return fail(MVAMG_E_ARG, "set_mega: k0 must leave at least one level above the coarsest");
-  if (h->L > kMegaMaxLevels) return fail(MVAMG_E_ARG, "set_mega: too many levels");
-  if (!h->bound) return fail(MVAMG_E_STATE, "set_mega: bind the workspace first");
-  if (h->pre.kind != MVAMG_GS_FORWARD || h->pre.sweeps != 1 || h->post.kind != MVAMG_GS_BACKWARD ||
-      h->post.sweeps != 1)
-    return fail(MVAMG_E_ARG, "set_mega: needs the default smoothers (1 forward / 1 backward GS sweep)");
-  std::vector<MegaLevel> ml(h->L);
-  for (int k = k0; k < h->L; ++k) {
-    Level& l = h->lv[k];
-    MegaLevel& m = ml[k];
-    std::memset(&m, 0, sizeof(m));
-    m.n = l.A.n;
-    m.ip = l.A.ip; m.ix = l.A.ix; m.v = l.A.v;
-    m.xa = l.xa; m.t = l.t; m.r = l.r; m.z = l.z; m.fr = l.fr; m.fx = l.fx;
-    m.fp0 = l.fp[0]; m.fp1 = l.fp[1]; m.fap0 = l.fap[0]; m.fap1 = l.fap[1];
-    if (k == h->L - 1) continue;
-    const GsLevels& g0 = l.glv[0];
-    const GsLevels& g2 = l.glv[2];
-    if (!g0.rows || !g2.rows || g0.ncta != 1 || g2.ncta != 1)
-      return fail(MVAMG_E_STATE, "set_mega: level " + std::to_string(k) +
-                                     " needs single-CTA level-set schedules for modes 0 and 2");
-    m.nlev0 = g0.nlev; m.lp0 = g0.lev_ptr; m.rows0 = g0.rows; m.ents0 = g0.ents;
-    m.nlev2 = g2.nlev; m.lp2 = g2.lev_ptr; m.rows2 = g2.rows; m.ents2 = g2.ents;
-    m.rip = l.R.ip; m.rix = l.R.ix; m.rv = l.R.v;
-    m.pip = l.P.ip; m.pix = l.P.ix; m.pv = l.P.v;
-  }
-  if (!h->mega_dev) CUDA_TRY(cudaMalloc(&h->mega_dev, sizeof(MegaLevel) * h->L));
-  CUDA_TRY(cudaMemcpy(h->mega_dev, ml.data(), sizeof(MegaLevel) * h->L, cudaMemcpyHostToDevice));
-  h->mega_k0 = k0;
-  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
-  h->graphs.clear();  // recapture with the new cycle
-  return 0;
-}
-
 // ---- setup helpers (host) ---------------------------------------------------
 int mvamg_greedy_match(long long ne, const long long* ei, const long long* ej, int n, long long* partner,
                        long long* pair_i, long long* pair_j, long long* npairs) {
@@ -3093,52 +2888,6 @@ int mvamg_xpby_f64(int n, const double* x, double beta, double* y, void* stream)
   xpby_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(n, x, beta, y);
   ++g_kernel_launches;
   CUDA_TRY(cudaGetLastError());
-  return 0;
-}
-
-
-int mvamg_gs_scan_sweep_f64(int mode, int n, const int* indptr, const int* indices, const double* data,
-                            int nchains, int S, int ring_len, int ndelta, const int* deltas, int K, int threads,
-                            int window, const int* seg_ptr, const int* chain_start, const int* chain_len,
-                            const void* recv, const void* addr, const void* seginfo, double* o0, const int* rec,
-                            const double* rdiag, const double* b, const double* x_old, double* x_new, int* ws,
-                            void* stream) {
-  if (mode < 0 || mode > 3 || n < 0 || !ws) return fail(MVAMG_E_ARG, "gs scan: bad arguments");
-  set_kernel_attrs();
-  Csr A;
-  A.n = n; A.ip = indptr; A.ix = indices; A.v = data;
-  GsScan g;
-  g.nchains = nchains; g.S = S; g.ring_len = ring_len; g.K = K; g.threads = threads;
-  if (int e = set_deltas(g, ndelta, deltas)) return e;
-  g.seg_ptr = seg_ptr; g.chain_start = chain_start; g.chain_len = chain_len; g.recv = recv; g.addr = addr;
-  g.seginfo = seginfo; g.o0 = o0; g.rec = rec; g.rdiag = rdiag; g.window = window & 0xffff;
-  g.cluster = window >> 16;
-  if (g.window && (g.window & (g.window - 1))) return fail(MVAMG_E_ARG, "gs scan: window must be a power of two");
-  return launch_gs_scan(A, g, mode, b, x_old, x_new, ws + 1, (cudaStream_t)stream);
-}
-
-int mvamg_hierarchy_set_gs_scan(mvamg_hierarchy* h, int k, int mode, int nchains, int S, int ring_len,
-                                int ndelta, const int* deltas, int K, int threads, int window,
-                                const int* seg_ptr, const int* chain_start, const int* chain_len, const void* recv,
-                                const void* addr, const void* seginfo, double* o0, const int* rec,
-                                const double* rdiag) {
-  if (!h || k < 0 || k >= h->L || mode < 0 || mode > 3) return fail(MVAMG_E_ARG, "set_gs_scan: bad index");
-  if (K < 1 || K > 4) return fail(MVAMG_E_ARG, "set_gs_scan: 1..4 cross-chain sources per row");
-  GsScan& g = h->lv[k].gsc[mode];
-  g.nchains = nchains; g.S = S; g.ring_len = ring_len; g.K = K; g.threads = threads;
-  if (int e = set_deltas(g, ndelta, deltas)) return e;
-  g.seg_ptr = seg_ptr; g.chain_start = chain_start; g.chain_len = chain_len; g.recv = recv; g.addr = addr;
-  g.seginfo = seginfo; g.o0 = o0; g.rec = rec; g.rdiag = rdiag; g.window = window & 0xffff;
-  g.cluster = window >> 16;
-  if (g.window && (g.window & (g.window - 1))) return fail(MVAMG_E_ARG, "gs scan: window must be a power of two");
-  return 0;
-}
-
-
-/* Diagnostics: device buffer of 4 int64 per segment that the chain-scan
- * sweeps fill with %globaltimer stamps (null: off). */
-int mvamg_gs_scan_set_trace(long long* trace_dev) {
-  g_scan_trace = trace_dev;
   return 0;
 }
 

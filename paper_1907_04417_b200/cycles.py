@@ -19,7 +19,7 @@ import scipy.sparse.linalg as spla
 from . import _lib
 from .device import (DeviceCSR, DeviceGsLevels, DeviceGsPlan, DeviceGsRows, DeviceGsStream, GpuConfig, as_csr,
                      stream_ctas,
-                     autotune_coarse_gs, autotune_scan_gs,
+                     autotune_coarse_gs,
                      level_gs_fits, ptr, row_gs_fits,
                      stream_handle, to_device, torch_cuda)
 from .exceptions import NotSpdError
@@ -158,18 +158,6 @@ class GpuMultigridOperator:
                     return None
         return need
 
-    def _gs_scan_modes(self):
-        """Sweep modes of the chain-scan schedule (0 fwd x=0, 1 fwd, 2 bwd x=0, 3 bwd)."""
-        modes = set()
-        for spec, first_zero in ((self.pre_smoother, True), (self.post_smoother, False)):
-            if spec.kind == WEIGHTED_JACOBI or spec.sweeps == 0:
-                continue
-            base = 0 if spec.kind == GS_FORWARD else 2
-            modes.add(base + (0 if first_zero else 1))
-            if first_zero and spec.sweeps > 1:
-                modes.add(base + 1)
-        return sorted(modes)
-
     def _init_plain(self, A):
         """Single-level handle used only for its matrix (pcg with precond=None)."""
         self.matrices = [as_csr(A)]
@@ -197,32 +185,13 @@ class GpuMultigridOperator:
         self.gs_plans = []
         self.level_dev = []
         self._dA = []
-        # small coarse levels: one thread block runs them (coarse_mega_kernel)
-        self.mega_k0 = -1
         cfg = self.config
-        if (cfg.coarse_mega and not plain and nl >= 2 and not cfg.generic_gs
-                and pre.kind == GS_FORWARD and pre.sweeps == 1 and post.kind == GS_BACKWARD
-                and post.sweeps == 1):
-            k = nl - 2
-            while k >= 0 and self.matrices[k].shape[0] <= cfg.mega_max_rows:
-                k -= 1
-            if k + 1 <= nl - 2:
-                self.mega_k0 = k + 1
         for k, A in enumerate(self.matrices):
             dA = DeviceCSR(A)
             self._dA.append(dA)
             if k < nl - 1:
                 dd = to_device(self.diagonals[k], np.float64)
                 self._keep.append(dd)
-                if 0 <= self.mega_k0 <= k:
-                    small = {m: DeviceGsLevels(A, m, dataclasses.replace(cfg, max_cluster=1, exact_gs=True)) for m in (0, 2)}
-                    self.gs_plans.append(None)
-                    self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=small, mega=True))
-                    _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
-                                                           None, 0, None, None, None, 32, 0), "set_level")
-                    for m, s in small.items():
-                        _lib.check(L.mvamg_hierarchy_set_gs_levels(h, k, m, *s.args()), "set_gs_levels")
-                    continue
                 smodes = (self._gs_stream_modes(A) if cfg.stream_gs and not cfg.generic_gs
                           and not cfg.force_level_gs and not cfg.force_row_gs else None)
                 if smodes:
@@ -294,12 +263,6 @@ class GpuMultigridOperator:
                     continue
                 self.gs_plans.append(gp.plan)
                 self.level_dev.append(dict(A=dA, gs=gp, plan=gp.plan, levels=None))
-                if not cfg.exact_gs and cfg.scan_gs:
-                    # tolerance parity: the chain-scan sweep where it is faster (timed once)
-                    scans = autotune_scan_gs(A, gp, self._gs_scan_modes(), cfg)
-                    self.level_dev[-1]["scan"] = scans
-                    for m, sc in scans.items():
-                        _lib.check(L.mvamg_hierarchy_set_gs_scan(h, k, m, *sc.args()), "set_gs_scan")
                 _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
                                                        None, gp.plan.ntiles, ptr(gp.chain_ptr),
                                                        ptr(gp.tile_ptr), ptr(gp.chain_order), gp.plan.threads,
@@ -330,8 +293,6 @@ class GpuMultigridOperator:
         self._ws = torch.empty(max(8, nbytes.value), dtype=torch.uint8, device="cuda")
         _lib.check(L.mvamg_hierarchy_bind_workspace(h, ptr(self._ws), stream_handle()), "bind_workspace")
         _lib.check(L.mvamg_hierarchy_set_graphs(h, int(bool(self.config.graphs))), "set_graphs")
-        if self.mega_k0 >= 0:
-            _lib.check(L.mvamg_hierarchy_set_mega(h, self.mega_k0), "set_mega")
 
     def _coarse_inverse(self):
         """Dense coarsest operator applied by one GEMV per visit: the inverse

@@ -81,11 +81,6 @@ class GpuConfig:
     device_galerkin: bool = True    # setup forms P'AP with the device kernel (bit-identical to scipy's)
     device_matching: bool = True    # setup matches with the device kernel (identical pairs and order)
     device_svd: bool = True         # setup's local SVDs on the device kernel (bit-identical U, sigma)
-    scan_gs: bool = False           # (with exact_gs False) time the chain-scan sweep on chain-structured levels
-                                    # at upload and keep it when faster (off: single-SM issue-bound, slower
-                                    # than the wavefront on C2/C3, and the timing costs setup time)
-    scan_cluster: int = 0           # CTAs of the cluster chain-scan sweep (window-mode levels; 0/1 = one CTA;
-                                    # 8 measured 2.85 ms vs 2.1 ms one-CTA on C2, tools/scan_trace.py)
     level_gs_small_rows: int = 2000  # tolerance parity: coarse levels up to this size use the level-set sweep
     lean_ring: tuple = None         # (R, D) of the lean kernel's record ring, overriding ring_bytes
     lean_cluster: int = 0           # wavefront tiles as thread-block clusters of this many CTAs (0: off);
@@ -100,9 +95,6 @@ class GpuConfig:
     autotune_gs: bool = True        # coarse levels: time row and level-set sweeps once, keep the faster per mode
     min_chain_rows: float = 8.0     # a level whose wavefront chains average fewer rows uses the row sweep
                                     # (e.g. interleaved multi-dof systems, where row i rarely couples to i-1)
-    coarse_mega: bool = False       # run the small coarse levels of a cycle in one thread block (opt-in:
-                                    # launch-free but L2-latency bound; slower than the multi-kernel path today)
-    mega_max_rows: int = 8192       # levels from the first one with at most this many rows down
     block_chains: bool = True       # 3-D grid lines: tiles of 2-D blocks of lines (chain_block_order), so a
                                     # line's z-neighbour is mostly in the same tile's shared window
     stream_gs: bool = True          # levels whose x (and b) fit one SM's shared memory: the streamed level-set
@@ -850,34 +842,3 @@ def galerkin_product_device(P, A, timing=None):
         timing["total_ms"] = float(sum(ph))
     k = nnz.value
     return sp.csr_matrix((v.cpu().numpy()[:k], ix.cpu().numpy()[:k], ip.cpu().numpy()), shape=(nc, nc))
-
-
-def autotune_scan_gs(A, gp, modes, cfg):
-    """For a chain-structured level: per sweep mode, keep the chain-scan sweep
-    (gs_scan.py, tolerance parity) if one timed run beats the wavefront sweep
-    `gp`.  Returns {mode: DeviceGsScan} for the modes it wins."""
-    from .gs_scan import DeviceGsScan, plan_scan
-
-    torch = torch_cuda()
-    n = A.shape[0]
-    g = torch.Generator(device="cuda").manual_seed(0)
-    b = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
-    xo = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
-    xn = torch.empty(n, dtype=torch.float64, device="cuda")
-    ws = torch.zeros(8, dtype=torch.int32, device="cuda")
-    out = {}
-    for m in modes:
-        p = plan_scan(A, m, cfg)
-        if p is None:
-            continue
-        sc = DeviceGsScan(A, m, cfg, plan=p)
-        xold = xo if m % 2 else None
-        t_scan = time_sweep(lambda: sc.sweep(b, xold, xn, ws))
-        if int(ws[1].item()) != 0:
-            raise DeviceError("gs scan sweep timed out (schedule error)")
-        direction = 0 if m < 2 else 1
-        t_wave = time_sweep(lambda: gp.sweep(direction, b, xold, xn, ws))
-        if t_scan < t_wave:
-            out[m] = sc
-    return out
-

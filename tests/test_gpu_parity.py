@@ -541,50 +541,6 @@ def test_fit_c1_end_to_end(mv):
     assert abs(est.estimate_convergence_factor() - float(d["rho_est"])) <= 1e-6
 
 
-# ------------------------------------------------------- coarse megakernel ----
-def test_mega_vcycle_bit_identical(mv, c1):
-    """V-cycle through the one-block coarse kernel == the multi-kernel path, bit for bit."""
-    d, mats, pros, _, _ = c1
-    op = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(coarse_mega=True, exact_gs=True))
-    off = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(coarse_mega=False, exact_gs=True))
-    assert op.mega_k0 == 1 and off.mega_k0 == -1
-    for key in ("b", "r1"):
-        assert np.array_equal(op.apply(d[key]), off.apply(d[key]))
-    assert np.array_equal(op.error_propagation(d["x2"]), off.error_propagation(d["x2"]))
-
-
-@pytest.mark.parametrize("k0_rows", [2000, 600, 200])
-def test_mega_kcycle_matches(mv, c1, k0_rows):
-    """K-cycles with the megakernel entered at different levels agree with the
-    multi-kernel path (FCG dots differ only in summation order) and with the
-    reference golden."""
-    d, mats = c1[0], c1[1]
-    m, p = hierarchy(d, "c0", fine=mats[0])
-    on = mv.GpuMultigridOperator(m, p, cycle=mv.CycleSpec("K", 2),
-                                 config=mv.GpuConfig(coarse_mega=True, mega_max_rows=k0_rows))
-    off = mv.GpuMultigridOperator(m, p, cycle=mv.CycleSpec("K", 2), config=mv.GpuConfig(coarse_mega=False))
-    assert on.mega_k0 >= 1
-    z_on, z_off = on.apply(d["r3"]), off.apply(d["r3"])
-    assert rel(z_on, z_off) <= 1e-12
-    assert rel(z_on, d["kapply_c0_r3"]) <= TOL_CYCLE
-
-
-def test_mega_composite_pcg(mv, c1):
-    """H2 PCG (symmetrized composite of K-cycles) with and without the
-    megakernel: same iteration count, histories within 1e-10."""
-    d, mats = c1[0], c1[1]
-    res = []
-    for cfg in (mv.GpuConfig(coarse_mega=True), mv.GpuConfig(coarse_mega=False)):
-        ops = []
-        for c in range(int(d["n_comp"])):
-            m, p = hierarchy(d, f"c{c}", fine=mats[0])
-            ops.append(mv.GpuMultigridOperator(m, p, cycle=mv.CycleSpec("K", 2), config=cfg))
-        pc = mv.GpuCompositePreconditioner(mv.GpuComposite(ops))
-        res.append(mv.pcg(mats[0], d["b"], precond=pc, rtol=1e-6)[1])
-    assert res[0].iterations == res[1].iterations == int(d["h2pcg_nit"])
-    assert np.max(np.abs(res[0].residual_history - res[1].residual_history) / res[1].residual_history) <= 1e-10
-
-
 def test_short_chain_level_uses_row_sweep(mv, c1):
     """A fine level without chain structure (rows interleaved so row i rarely
     couples to i-1, as with interleaved multi-dof systems) runs the dataflow
@@ -608,65 +564,6 @@ def test_short_chain_level_uses_row_sweep(mv, c1):
     z = op.apply(b)
     assert np.array_equal(z, wf.apply(b))
     assert rel(z, OracleOperator(pm, pp).apply(b)) <= TOL_CYCLE
-
-
-# ------------------------------------------------------- chain-scan sweep ----
-@pytest.mark.parametrize("cluster", [8, 0])
-@pytest.mark.parametrize("mode", [0, 1, 2, 3])
-def test_gs_scan_kernel(mv, c1, mode, cluster):
-    """Chain-scan sweep (tolerance parity): each sweep within rounding of the
-    reference's serial loop, on grid structures (K = 1, 2, 3) and C1's fine
-    level; lines longer than the 128-position window run the cluster sweep
-    (cluster = 8) or the one-CTA window sweep (cluster = 0)."""
-    import torch
-    from paper_1907_04417_b200 import problems
-    from paper_1907_04417_b200.gs_scan import DeviceGsScan
-
-    cfg = mv.GpuConfig(scan_cluster=cluster)
-    rng = np.random.default_rng(20 + mode)
-    cases = [("lap2d", laplacian_2d(40)), ("lap3d", laplacian_3d(12)), ("q1", problems.anisotropic_q1(70)),
-             ("jump3d", problems.jump_3d(16, 4, 1)), ("c1_l0", c1[1][0]), ("lap1d", laplacian_1d(100)),
-             ("lap2d_long", laplacian_2d(260)), ("q1_long", problems.anisotropic_q1(300)),
-             ("lap1d_long", laplacian_1d(1000))]
-    seen_cluster = False
-    for name, A in cases:
-        n = A.shape[0]
-        b = rng.standard_normal(n)
-        x0 = rng.standard_normal(n)
-        want = np.zeros(n) if mode % 2 == 0 else x0.copy()
-        oracle_gs(A, b, want, "forward" if mode < 2 else "backward")
-        sc = DeviceGsScan(A, mode, cfg)
-        seen_cluster |= sc.plan.cluster > 1
-        xn = torch.empty(n, dtype=torch.float64, device="cuda")
-        ws = torch.zeros(8, dtype=torch.int32, device="cuda")
-        sc.sweep(_dev(b), None if mode % 2 == 0 else _dev(x0), xn, ws)
-        torch.cuda.synchronize()
-        assert int(ws[1].item()) == 0, name
-        assert rel(xn.cpu().numpy(), want) <= 1e-12, (name, mode, cluster)
-    assert seen_cluster == (cluster > 1)
-
-
-def test_vcycle_with_scan_sweeps(mv, c1):
-    """A hierarchy whose fine level runs the chain-scan sweeps (forced) matches
-    the reference cycle within the north-star tolerance and PCG keeps nit."""
-    d, mats, pros = c1[0], c1[1], c1[2]
-    op = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(exact_gs=False))
-    from paper_1907_04417_b200.gs_scan import DeviceGsScan
-
-    # force the scan schedules on level 0 for both smoother modes
-    L = __import__("paper_1907_04417_b200._lib", fromlist=["load"]).load()
-    keep = []
-    for m in (0, 3):
-        sc = DeviceGsScan(mats[0], m)
-        keep.append(sc)
-        L.mvamg_hierarchy_set_gs_scan(op.handle, 0, m, *sc.args())
-    op._scan_keep = keep
-    L.mvamg_hierarchy_set_graphs(op.handle, 0)
-    z = op.apply(d["b"])
-    assert rel(z, d["apply_b"]) <= TOL_CYCLE
-    x, rep = mv.pcg(mats[0], d["b"], op, rtol=1e-6)
-    assert rep.iterations == int(d["pcg_nit"])
-    assert np.max(np.abs(rep.residual_history - d["pcg_hist"]) / d["pcg_hist"]) <= 1e-10
 
 
 def test_composite_graphs_not_reused_across_composites(mv, c1, c1_comps):
