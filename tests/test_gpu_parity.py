@@ -770,3 +770,49 @@ def test_spmv_stream_tiles_bit_exact(mv, stream):
             assert np.array_equal(_spmv_mode_gpu(M, x, 2, y=y), y + ref)
     finally:
         L.mvamg_set_spmv_stream(1)
+
+
+def test_integration_option_a_from_reference(mv, c1):
+    """INTEGRATION.md Option A: a reference MultigridOperator (duck-typed
+    stand-in with the reference's attributes and spec values, cycles.py:100-128)
+    wrapped by GpuMultigridOperator.from_reference, then driven the way the
+    reference's own pcg drives `operator_.apply` (host arrays, krylov.py:28-72)."""
+    from types import SimpleNamespace
+
+    d, mats, pros = c1[0], c1[1], c1[2]
+    ref_like = SimpleNamespace(
+        matrices=mats, prolongators=pros, cycle=SimpleNamespace(kind="V", inner_fcg_iters=2),
+        pre_smoother=SimpleNamespace(kind="gauss_seidel_forward", sweeps=1, omega=1.0),
+        post_smoother=SimpleNamespace(kind="gauss_seidel_backward", sweeps=1, omega=1.0))
+    op = mv.GpuMultigridOperator.from_reference(ref_like)
+    assert rel(op.apply(d["b"]), d["apply_b"]) <= TOL_CYCLE
+    # the reference's pcg loop (krylov.py:28-72) calling the wrapped operator
+    A, b = mats[0], d["b"]
+    x = np.zeros_like(b)
+    r = b.copy()
+    r0 = np.linalg.norm(r)
+    hist = [r0]
+    z = op.apply(r)
+    rz = float(np.dot(r, z))
+    p = z.copy()
+    k = 0
+    while k < 1000:
+        q = A @ p
+        alpha = rz / float(np.dot(p, q))
+        x += alpha * p
+        r -= alpha * q
+        k += 1
+        hist.append(np.linalg.norm(r))
+        if hist[-1] <= 1e-6 * r0:
+            break
+        z = op.apply(r)
+        rzn = float(np.dot(r, z))
+        p = z + (rzn / rz) * p
+        rz = rzn
+    assert k == int(d["pcg_nit"])
+    assert np.max(np.abs(np.asarray(hist) - d["pcg_hist"]) / d["pcg_hist"]) <= 1e-10
+    kop = mv.GpuMultigridOperator.from_reference(SimpleNamespace(
+        matrices=hierarchy(d, "c0", fine=mats[0])[0], prolongators=hierarchy(d, "c0", fine=mats[0])[1],
+        cycle=SimpleNamespace(kind="K", inner_fcg_iters=2), pre_smoother=ref_like.pre_smoother,
+        post_smoother=ref_like.post_smoother))
+    assert rel(kop.apply(d["r3"]), d["kapply_c0_r3"]) <= TOL_CYCLE
