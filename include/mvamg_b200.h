@@ -116,12 +116,15 @@ int mvamg_csr_spmv_mode_f64(int mode, int n, int nnz, const int* indptr, const i
  * rec == NULL for *nwords / *nrounds / *nwarps / *max_S; then round_off holds
  * nrounds+1, tbase nwarps+1, tile_wbase ntiles+1, perm n ints.  chain_order:
  * as in mvamg_gs_analyse (every inter-warp input must lie in an earlier warp
- * of that order; MVAMG_E_ARG otherwise). */
+ * of that order; MVAMG_E_ARG otherwise).  wpos > 0 (a power of two; one-warp
+ * tiles): the shared window keeps chain positions modulo wpos -- 32 x wpos
+ * slots instead of 32 x the chain length, so several tiles fit an SM -- and
+ * every window read is verified to come before its slot's next write. */
 int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double* data, int ntiles,
                       const int* chain_ptr, const int* tile_ptr, int window, int mode, int R,
                       int uniform_S, int rows_per_round, long long* nwords, int* nrounds, int* nwarps,
                       int* max_S, unsigned long long* rec, int* round_off, int* tbase, int* tile_wbase,
-                      int* perm, const int* chain_order);
+                      int* perm, const int* chain_order, int wpos);
 /* One lexicographic GS sweep (_kernels.py:15-38) on device data.  direction
  * 0 = forward, 1 = backward; x_old is the iterate before the sweep (NULL for a
  * zero guess); x_new receives the result and must not alias x_old.  The CSR
@@ -141,7 +144,8 @@ int mvamg_gs_sweep_f64(int direction, int n, const int* indptr, const int* indic
                        const int* tile_wbase, const int* perm, double* tperm, int R, int D,
                        int lean_C, int slot_words, int rec_words_max, int ntiles,
                        const int* chain_ptr, const int* tile_ptr, const int* chain_order, int threads,
-                       int window, const double* b, const double* x_old, double* x_new, int* ws, void* stream);
+                       int window, int wpos, const double* b, const double* x_old, double* x_new, int* ws,
+                       void* stream);
 /* GS level-set schedule for small / mid-size levels (host).  mode 0 forward
  * from x = 0, 1 forward, 2 backward from x = 0, 3 backward.  Rows are
  * block-partitioned over a cluster of ncta (1..16) CTAs and, per CTA, ordered
@@ -337,7 +341,8 @@ int mvamg_hierarchy_destroy(mvamg_hierarchy* h);
 int mvamg_hierarchy_set_level(mvamg_hierarchy* h, int k, int n, int nnz, const int* indptr,
                               const int* indices, const double* data, const double* diag,
                               const double* rdiag, int ntiles, const int* chain_ptr,
-                              const int* tile_ptr, const int* chain_order, int gs_threads, int gs_window);
+                              const int* tile_ptr, const int* chain_order, int gs_threads, int gs_window,
+                              int gs_wpos);
 /* GS schedule of level k for sweep `mode` (see mvamg_gs_schedule), device. */
 int mvamg_hierarchy_set_gs_schedule(mvamg_hierarchy* h, int k, int mode, const unsigned long long* rec,
                                     const int* round_off, const int* tbase, const int* tile_wbase,

@@ -43,9 +43,9 @@ SIGNATURES = [
     ("mvamg_csr_spmv_mode_f64", _I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
     ("mvamg_csr_spmv_add_f64", _I, [_I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_gs_schedule", _I, [_I, _P, _P, _P, _I, _P, _P, _I, _I, _I, _I, _I, ctypes.POINTER(_LL), _PI, _PI,
-                               _PI, _P, _P, _P, _P, _P, _P]),
+                               _PI, _P, _P, _P, _P, _P, _P, _I]),
     ("mvamg_gs_sweep_f64", _I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P,
-                                _P, _I, _I, _P, _P, _P, _P, _P]),
+                                _P, _I, _I, _I, _P, _P, _P, _P, _P]),
     ("mvamg_gs_levels", _I, [_I, _P, _P, _P, _I, _I, _I, _I, _PI, ctypes.POINTER(_LL), _PI, _PI, _PI, _P, _P,
                              _P, _P, _P]),
     ("mvamg_gs_level_sweep_f64", _I, [_I, _I, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P,
@@ -79,7 +79,7 @@ SIGNATURES = [
     ("mvamg_dot_ws_bytes", _I, []),
     ("mvamg_hierarchy_create", _I, [ctypes.POINTER(_P), _I, _I, _I, _I, _I, _D, _I, _I, _D]),
     ("mvamg_hierarchy_destroy", _I, [_P]),
-    ("mvamg_hierarchy_set_level", _I, [_P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _I, _I]),
+    ("mvamg_hierarchy_set_level", _I, [_P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _I, _I, _I]),
     ("mvamg_hierarchy_set_gs_schedule", _I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I]),
     ("mvamg_hierarchy_set_gs_levels", _I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_hierarchy_set_gs_rows", _I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P]),

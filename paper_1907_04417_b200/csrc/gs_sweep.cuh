@@ -67,6 +67,7 @@ struct GsArgs {
   const int* chain_ptr;
   const int* tile_ptr;           // tiles: ranges of the chain order
   const int* chain_order;        // processing order of the chains (nullptr: natural order)
+  int wmask;                     // window positions mod (wmask + 1) (one-warp tiles; -1: the whole chain)
   const double* tperm;           // right-hand side in (round, lane) order
   const double* xold;
   double* xnew;
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(256, 1) gs_sweep_kernel(GsArgs a) {
                                             : div_rn_markstein(s, __longlong_as_double((long long)rec[32]),
                                                                __longlong_as_double((long long)rec[64]));
             const int i = FWD ? cs + q : ce - 1 - q;
-            if (!(a.debug & 4)) wslot[q * TS] = (unsigned long long)__double_as_longlong(xi);
+            if (!(a.debug & 4)) wslot[(q & a.wmask) * TS] = (unsigned long long)__double_as_longlong(xi);
             if (!(a.debug & 2)) a.xnew[i] = xi;
             xprev = xi;
             ++q;
@@ -581,7 +582,7 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
       if (active) {
         const double xi = div_rn_markstein(sacc, __longlong_as_double((long long)rec[32]),
                                            __longlong_as_double((long long)rec[64]));
-        wslot[q * TS] = (unsigned long long)__double_as_longlong(xi);
+        wslot[(q & a.wmask) * TS] = (unsigned long long)__double_as_longlong(xi);
         a.xnew[FWD ? cs + q : ce - 1 - q] = xi;
         xprev = xi;
         ++q;
@@ -720,7 +721,7 @@ __global__ void __launch_bounds__(256, 1) gs_lean_kernel(GsArgs a) {
             }
             if (kact[kk]) {
               const double xi = div_rn_markstein(sacc, kdg[kk], krd[kk]);
-              wslot[q * TS] = (unsigned long long)__double_as_longlong(xi);
+              wslot[(q & a.wmask) * TS] = (unsigned long long)__double_as_longlong(xi);
               a.xnew[FWD ? cs + q : ce - 1 - q] = xi;
               xprev = xi;
               ++q;

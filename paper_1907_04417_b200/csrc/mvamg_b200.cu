@@ -133,6 +133,7 @@ struct GsPlan {
   const int* chain_ptr = nullptr;
   const int* tile_ptr = nullptr;     // tiles: ranges of the chain order
   const int* chain_order = nullptr;  // processing order of the chains (nullptr: natural)
+  int wmask = -1;                    // window positions mod (wmask + 1); -1: whole chains
 };
 
 // Static round schedule of one sweep mode (0 forward from x = 0, 1 forward,
@@ -316,6 +317,7 @@ int launch_gs(bool fwd, const Csr& A, const GsList& ls, const GsPlan& p, const d
   a.chain_ptr = p.chain_ptr;
   a.tile_ptr = p.tile_ptr;
   a.chain_order = p.chain_order;
+  a.wmask = p.wmask;
   a.tperm = ls.tperm;
   a.xold = xold;
   a.xnew = xnew;
@@ -1333,7 +1335,7 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
                       const int* chain_ptr, const int* tile_ptr, int window, int mode, int R,
                       int uniform_S, int rows_per_round, long long* nwords, int* nrounds, int* nwarps,
                       int* max_S, unsigned long long* rec, int* round_off, int* tbase, int* tile_wbase,
-                      int* perm, const int* chain_order) {
+                      int* perm, const int* chain_order, int wpos) {
   if (n < 0 || !indptr || !chain_ptr || !tile_ptr || !nwords || !nrounds || !nwarps || mode < 0 ||
       mode > 2 || R < 1 || R > 31)
     return fail(MVAMG_E_ARG, "gs_schedule: bad arguments");
@@ -1358,6 +1360,13 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
   };
   auto lower = [&](int i, int j) { return fwd ? (j < i) : (j > i); };
   const int nch = tile_ptr[ntiles];
+  // wpos > 0: a tile's shared window keeps chain positions modulo wpos (one-warp
+  // tiles only: every window read is then a same-warp value of an earlier
+  // round, and each read is checked below to precede the slot's next write)
+  if (wpos < 0 || (wpos & (wpos - 1))) return fail(MVAMG_E_ARG, "gs_schedule: wpos must be 0 or a power of two");
+  if (wpos > 0)
+    for (int t = 0; t < ntiles; ++t)
+      if (tile_ptr[t + 1] - tile_ptr[t] > 32) return fail(MVAMG_E_ARG, "gs_schedule: wpos needs one-warp tiles");
   if (chain_order && cluster > 1) return fail(MVAMG_E_ARG, "gs_schedule: chain order and cluster tiles exclude each other");
   // chains are ranges of rows; warps / tiles are ranges of the chain order
   // (position cl holds chain ord(cl)); `pos_of` inverts it
@@ -1494,7 +1503,18 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
               } else if (tile_of_chain[chain_of[j]] == t) {
                 const int cj = chain_of[j];
                 const int pos = fwd ? j - chain_ptr[cj] : chain_ptr[cj + 1] - 1 - j;
-                const long long slot = (long long)pos * TS + (pos_of[cj] - c0);
+                long long slot = (long long)pos * TS + (pos_of[cj] - c0);
+                if (wpos > 0) {
+                  slot = (long long)(pos & (wpos - 1)) * TS + (pos_of[cj] - c0);
+                  // the slot's next write: chain cj's row wpos positions later
+                  const int pn = pos + wpos, len = chain_ptr[cj + 1] - chain_ptr[cj];
+                  if (pn < len) {
+                    const int jn = fwd ? chain_ptr[cj] + pn : chain_ptr[cj + 1] - 1 - pn;
+                    if (rnd[lidx[jn]] <= r)
+                      return fail(MVAMG_E_ARG, "gs_schedule: window of " + std::to_string(wpos) +
+                                                   " positions too short for this schedule");
+                  }
+                }
                 if (slot >= window) return fail(MVAMG_E_ARG, "gs_schedule: window slot out of range");
                 code = (int)(slot << 2) | 1;
               } else {
@@ -1553,7 +1573,8 @@ int mvamg_gs_sweep_f64(int direction, int n, const int* indptr, const int* indic
                        const int* tile_wbase, const int* perm, double* tperm, int R, int D,
                        int lean_C, int slot_words, int rec_words_max, int ntiles,
                        const int* chain_ptr, const int* tile_ptr, const int* chain_order, int threads,
-                       int window, const double* b, const double* x_old, double* x_new, int* ws, void* stream) {
+                       int window, int wpos, const double* b, const double* x_old, double* x_new, int* ws,
+                       void* stream) {
   if (threads < 32 || threads > 256 || threads % 32) return fail(MVAMG_E_ARG, "gs: threads must be 32..256, multiple of 32");
   if (R != 1 && R != 2 && R != 4 && R != 8) return fail(MVAMG_E_ARG, "gs: R must be 1, 2, 4 or 8");
   if (D != 2 && D != 3 && D != 4 && D != 8) return fail(MVAMG_E_ARG, "gs: D must be 2, 3, 4 or 8");
@@ -1574,6 +1595,8 @@ int mvamg_gs_sweep_f64(int direction, int n, const int* indptr, const int* indic
   GsPlan p;
   p.ntiles = ntiles; p.threads = threads; p.window = window; p.chain_ptr = chain_ptr; p.tile_ptr = tile_ptr;
   p.chain_order = chain_order;
+  if (wpos < 0 || (wpos & (wpos - 1))) return fail(MVAMG_E_ARG, "gs: wpos must be 0 or a power of two");
+  p.wmask = wpos > 0 ? wpos - 1 : -1;
   return launch_gs(direction == 0, A, ls, p, b, x_old, x_new, ws, ws + 1, (cudaStream_t)stream);
 }
 
@@ -2528,7 +2551,8 @@ int mvamg_hierarchy_destroy(mvamg_hierarchy* h) {
 int mvamg_hierarchy_set_level(mvamg_hierarchy* h, int k, int n, int nnz, const int* indptr,
                               const int* indices, const double* data, const double* diag,
                               const double* rdiag, int ntiles, const int* chain_ptr,
-                              const int* tile_ptr, const int* chain_order, int gs_threads, int gs_window) {
+                              const int* tile_ptr, const int* chain_order, int gs_threads, int gs_window,
+                              int gs_wpos) {
   if (!h || k < 0 || k >= h->L) return fail(MVAMG_E_ARG, "set_level: bad level index");
   Level& l = h->lv[k];
   l.A.n = n; l.A.m = n; l.A.nnz = nnz; l.A.ip = indptr; l.A.ix = indices; l.A.v = data;
@@ -2538,6 +2562,8 @@ int mvamg_hierarchy_set_level(mvamg_hierarchy* h, int k, int n, int nnz, const i
   l.plan.chain_ptr = chain_ptr;
   l.plan.tile_ptr = tile_ptr;
   l.plan.chain_order = chain_order;
+  if (gs_wpos < 0 || (gs_wpos & (gs_wpos - 1))) return fail(MVAMG_E_ARG, "set_level: wpos must be 0 or a power of two");
+  l.plan.wmask = gs_wpos > 0 ? gs_wpos - 1 : -1;
   l.plan.threads = gs_threads;
   l.plan.window = gs_window;
   return 0;

@@ -200,7 +200,7 @@ class GpuMultigridOperator:
                     self.gs_plans.append(None)
                     self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=None, rows=None, stream=plans))
                     _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
-                                                           None, 0, None, None, None, 32, 0), "set_level")
+                                                           None, 0, None, None, None, 32, 0, 0), "set_level")
                     for pm, sp in plans.items():
                         _lib.check(L.mvamg_hierarchy_set_gs_stream(h, k, pm, *sp.args()), "set_gs_stream")
                     continue
@@ -212,7 +212,7 @@ class GpuMultigridOperator:
                     self.gs_plans.append(None)
                     lv = dict(A=dA, gs=None, plan=None, levels=None, rows=None)
                     _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
-                                                           None, 0, None, None, None, 32, 0), "set_level")
+                                                           None, 0, None, None, None, 32, 0, 0), "set_level")
                     for m, s in pick.items():
                         if isinstance(s, DeviceGsRows):
                             lv["rows"] = lv["rows"] or {}
@@ -230,7 +230,7 @@ class GpuMultigridOperator:
                     self.gs_plans.append(None)
                     self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=None, rows=rows))
                     _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
-                                                           None, 0, None, None, None, 32, 0), "set_level")
+                                                           None, 0, None, None, None, 32, 0, 0), "set_level")
                     for m, s in rows.items():
                         _lib.check(L.mvamg_hierarchy_set_gs_rows(h, k, m, *s.hierarchy_args()), "set_gs_rows")
                     continue
@@ -245,7 +245,7 @@ class GpuMultigridOperator:
                     self.gs_plans.append(None)
                     self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=small))
                     _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
-                                                           None, 0, None, None, None, 32, 0), "set_level")
+                                                           None, 0, None, None, None, 32, 0, 0), "set_level")
                     for m, s in small.items():
                         _lib.check(L.mvamg_hierarchy_set_gs_levels(h, k, m, *s.args()), "set_gs_levels")
                     continue
@@ -257,7 +257,7 @@ class GpuMultigridOperator:
                     self.gs_plans.append(None)
                     self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=None, rows=rows))
                     _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
-                                                           None, 0, None, None, None, 32, 0), "set_level")
+                                                           None, 0, None, None, None, 32, 0, 0), "set_level")
                     for m, s in rows.items():
                         _lib.check(L.mvamg_hierarchy_set_gs_rows(h, k, m, *s.hierarchy_args()), "set_gs_rows")
                     continue
@@ -266,7 +266,7 @@ class GpuMultigridOperator:
                 _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
                                                        None, gp.plan.ntiles, ptr(gp.chain_ptr),
                                                        ptr(gp.tile_ptr), ptr(gp.chain_order), gp.plan.threads,
-                                                       gp.plan.window), "set_level")
+                                                       gp.plan.window, gp.plan.wpos), "set_level")
                 for m in self._gs_modes():
                     sch = gp.mode(m)
                     _lib.check(L.mvamg_hierarchy_set_gs_schedule(
@@ -275,7 +275,7 @@ class GpuMultigridOperator:
                         sch["lean_C"], sch["slot_words"], sch["rec_words_max"]), "set_gs_schedule")
             else:
                 _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), None, None, 0,
-                                                       None, None, None, 32, 0), "set_level")
+                                                       None, None, None, 32, 0, 0), "set_level")
         for k, (P, R) in enumerate(zip(self.prolongators, self.restrictions)):
             dP, dR = DeviceCSR(P), DeviceCSR(R)
             self._keep += [dP, dR]

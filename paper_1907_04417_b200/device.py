@@ -95,6 +95,8 @@ class GpuConfig:
     autotune_gs: bool = True        # coarse levels: time row and level-set sweeps once, keep the faster per mode
     min_chain_rows: float = 8.0     # a level whose wavefront chains average fewer rows uses the row sweep
                                     # (e.g. interleaved multi-dof systems, where row i rarely couples to i-1)
+    lean_wpos: int = 64             # lean sweeps: one-warp tiles with a window of this many positions per chain
+                                    # (power of two; 0: the whole chain, which caps tiles per SM and chain length)
     block_chains: bool = True       # 3-D grid lines: tiles of 2-D blocks of lines (chain_block_order), so a
                                     # line's z-neighbour is mostly in the same tile's shared window
     stream_gs: bool = True          # levels whose x (and b) fit one SM's shared memory: the streamed level-set
@@ -280,6 +282,16 @@ def gs_analyse(A, cfg=None):
         raise ValueError(f"GS ring of {ring_warp} bytes per warp does not fit shared memory")
     T = min(T, max(1, cfg.max_threads))
     max_chain = max(1, min(cfg.max_chain, lmax, slots // max(32, (T + 31) // 32 * 32)))
+    # lean sweeps with a modular window: one-warp tiles of whole chains whose shared
+    # window keeps lean_wpos positions per chain (32 x wpos slots), so several tiles
+    # share an SM -- the window no longer caps the chain length or the tile count
+    # (only where the whole-chain window already forces tiles of at most one warp: C2 1.21 ->
+    # 1.08 ms, C5 5.5 -> 2.6 ms per sweep; C3's two-warp tiles of 8 x 8 lines stay faster)
+    wpos = 0
+    if (C > 0 and cfg.lean_wpos > 0 and not cfg.generic_gs and not cfg.lean_cluster and lmax > cfg.lean_wpos
+            and T <= 32):
+        wpos = int(cfg.lean_wpos)
+        T, slots, max_chain = 32, 1 << 30, max(1, min(cfg.max_chain, lmax))
     order = None
     if cfg.block_chains and not cfg.lean_cluster:
         _lib.check(L.mvamg_gs_analyse(n, c_ip, c_ix, max_chain, T, slots, ctypes.byref(nch),
@@ -301,6 +313,9 @@ def gs_analyse(A, cfg=None):
                                   ctypes.byref(win), ctypes.byref(dep), vo), "gs_analyse")
     plan = GsPlanHost(nch.value, nt.value, max(32, thr.value), max(win.value, 1), dep.value, cp, tp)
     plan.chain_order = order
+    plan.wpos = wpos
+    if wpos:
+        plan.window = 32 * wpos
     plan.lean_C, plan.R, plan.D = C, R, D
     plan.smem_budget = cfg.smem_budget
     return plan
@@ -334,13 +349,14 @@ def gs_schedule(A, plan, mode, R=None, uniform_S=0, K=1):
             ctypes.byref(smax))
     order = getattr(plan, "chain_order", None)
     vo = vp(np.ascontiguousarray(order, dtype=np.int32)) if order is not None else None
-    _lib.check(L.mvamg_gs_schedule(*args, None, None, None, None, None, vo), "gs_schedule")
+    wpos = int(getattr(plan, "wpos", 0))
+    _lib.check(L.mvamg_gs_schedule(*args, None, None, None, None, None, vo, wpos), "gs_schedule")
     rec = np.zeros(max(2, nw.value), dtype=np.uint64)
     round_off = np.empty(nr.value + 1, dtype=np.int32)
     tbase = np.empty(nwarps.value + 1, dtype=np.int32)
     tile_wbase = np.empty(plan.ntiles + 1, dtype=np.int32)
     perm = np.empty(max(1, n), dtype=np.int32)
-    _lib.check(L.mvamg_gs_schedule(*args, vp(rec), vp(round_off), vp(tbase), vp(tile_wbase), vp(perm), vo),
+    _lib.check(L.mvamg_gs_schedule(*args, vp(rec), vp(round_off), vp(tbase), vp(tile_wbase), vp(perm), vo, wpos),
                "gs_schedule")
     return GsScheduleHost(rec, round_off, tbase, tile_wbase, perm, nr.value, smax.value)
 
@@ -418,7 +434,8 @@ class DeviceGsPlan:
             direction, self.A.shape[0], *self._csr.ptrs(), ptr(sch["rec"]), ptr(sch["round_off"]),
             ptr(sch["tbase"]), ptr(sch["tile_wbase"]), ptr(sch["perm"]), ptr(sch["tperm"]), sch["R"],
             sch["D"], sch["lean_C"], sch["slot_words"], sch["rec_words_max"], p.ntiles, ptr(self.chain_ptr), ptr(self.tile_ptr),
-            ptr(self.chain_order), p.threads, p.window, ptr(b), ptr(x_old), ptr(x_new), ptr(ws), stream or stream_handle()),
+            ptr(self.chain_order), p.threads, p.window, int(getattr(p, "wpos", 0)), ptr(b), ptr(x_old), ptr(x_new),
+            ptr(ws), stream or stream_handle()),
             "gs_sweep")
 
 

@@ -816,3 +816,34 @@ def test_integration_option_a_from_reference(mv, c1):
         cycle=SimpleNamespace(kind="K", inner_fcg_iters=2), pre_smoother=ref_like.pre_smoother,
         post_smoother=ref_like.post_smoother))
     assert rel(kop.apply(d["r3"]), d["kapply_c0_r3"]) <= TOL_CYCLE
+
+
+@pytest.mark.parametrize("wpos", [2, 8, 64])
+def test_gs_modular_window_bit_exact(mv, wpos):
+    """Lean sweeps whose one-warp tiles keep only `wpos` chain positions in the
+    shared window (GpuConfig.lean_wpos): bit-identical to the serial loop in
+    every mode, on 1-D / 2-D / 3-D grids (blocked lines) and the Q1 9-point
+    stencil; a window too short for the schedule is refused, not wrong."""
+    from paper_1907_04417_b200 import problems
+    from paper_1907_04417_b200.device import gs_analyse
+
+    rng = np.random.default_rng(51)
+    cfg = mv.GpuConfig(lean_wpos=wpos, exact_gs=True)
+    cases = [("lap1d", laplacian_1d(300).tocsr()), ("lap2d", laplacian_2d(100).tocsr()),
+             ("lap3d", laplacian_3d(32).tocsr()), ("jump", problems.jump_3d(40, 8, 1)),
+             ("q1", problems.anisotropic_q1(96))]
+    for name, A in cases:
+        n = A.shape[0]
+        b, x0 = rng.standard_normal(n), rng.standard_normal(n)
+        for direction in ("forward", "backward"):
+            for zero in (True, False):
+                want = np.zeros(n) if zero else x0.copy()
+                oracle_gs(A, b, want, direction)
+                try:
+                    got = _gs_gpu(mv, A, b, x0, direction, zero, cfg)
+                except ValueError as exc:
+                    assert "too short" in str(exc) and wpos == 2, (name, exc)
+                    continue
+                assert np.array_equal(got, want), (name, direction, zero, wpos)
+        if wpos == 8:
+            assert gs_analyse(A, cfg).wpos == 8 or name in ("lap3d",), name

@@ -31,12 +31,23 @@ for v in variants:
         key, val = part.split("=", 1)
         kw[key.strip()] = ast.literal_eval(val.strip())
     try:
-        op = GpuMultigridOperator(mats, pros, config=GpuConfig(**kw))
+        if k == 0:  # the fine level's wavefront plan alone (no coarse levels to build)
+            from types import SimpleNamespace
+
+            from paper_1907_04417_b200.device import DeviceGsPlan
+
+            gp = DeviceGsPlan(mats[0], GpuConfig(**kw))
+            op = SimpleNamespace(level_dev=[dict(gs=gp)])
+        else:
+            op = GpuMultigridOperator(mats, pros, config=GpuConfig(**kw))
         f, bw, fname, bname = bench._level_sweeps(op, k, bk, xo, xn, ws, s)
         tf = bench._event_time(f, 20, stream) * 1e6
         tb = bench._event_time(bw, 20, stream) * 1e6
         p = op.level_dev[k].get("gs")
-        extra = f"tiles {p.plan.ntiles} threads {p.plan.threads}" if p is not None else ""
+        extra = ""
+        if p is not None:
+            extra = (f"tiles {p.plan.ntiles} threads {p.plan.threads} window {p.plan.window} "
+                     f"ring R{p.plan.R}xD{p.plan.D} blocked {getattr(p.plan, 'chain_order', None) is not None}")
         print(f"level {k} [{v or 'default'}]: fwd {tf:.1f} us ({fname})  bwd {tb:.1f} us ({bname})  {extra}", flush=True)
         del op
     except Exception as exc:
