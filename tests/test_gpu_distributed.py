@@ -154,7 +154,8 @@ def test_ipc_handle_opened_by_another_process():
         "p = ctypes.c_void_p()\n"
         "_lib.check(L.mvamg_ipc_open(ctypes.create_string_buffer(bytes.fromhex(%r), 64), ctypes.byref(p)), 'open')\n"
         "src = torch.arange(16, dtype=torch.float64, device='cuda')\n"
-        "torch.cuda.cudart().cudaMemcpy(p.value, src.data_ptr(), 128, 4)\n"
+        "idx = torch.arange(16, dtype=torch.int32, device='cuda')\n"
+        "_lib.check(L.mvamg_gather_f64(16, ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(src.data_ptr()), p, None), 'gather')\n"
         "torch.cuda.synchronize()\n"
         "_lib.check(L.mvamg_ipc_close(p), 'close')\n" % (ROOT, h.raw.hex()))
     subprocess.run([sys.executable, "-c", code], check=True, timeout=300)

@@ -387,13 +387,23 @@ def test_kcycle_matches_reference(c1, c1_comps):
     assert rel(gpu[1].error_propagation(d["r3"]), d["kerr_c1_r3"]) <= TOL_CYCLE
 
 
+# Chained applications: the north star bounds ONE cycle application at 1e-10
+# relative; a symmetrized composite chains 2r K-cycle error propagators, the
+# bootstrap test phase nu such composites.  The bounds below are that per-
+# application bound times the number of chained applications (r = 4 components
+# on C1, nu = 15), not a loosened tolerance.
+def _chain_bound(applications):
+    return applications * TOL_CYCLE
+
+
 def test_composite_matches_reference(mv, c1, c1_comps):
     d = c1[0]
     gpu, cpu = c1_comps
     comp = mv.GpuComposite(gpu)
     y = comp.apply_symmetrized(d["x4"])
-    assert rel(y, d["comp_x4"]) <= 1e-9
-    assert rel(y, oracle_composite(cpu, d["x4"])) <= 1e-9
+    bound = _chain_bound(2 * len(gpu))                      # 2r = 8 K-cycles: 8e-10
+    assert rel(y, d["comp_x4"]) <= bound
+    assert rel(y, oracle_composite(cpu, d["x4"])) <= bound
 
 
 def test_small_goldens(mv):
@@ -486,7 +496,8 @@ def test_pcg_composite_h2(mv, c1, c1_comps):
     prec = mv.GpuComposite(gpu).as_preconditioner()
     x, rep = mv.pcg(mats[0], d["b"], prec, rtol=1e-6)
     assert rep.iterations == int(d["h2pcg_nit"])
-    assert np.max(np.abs(rep.residual_history - d["h2pcg_hist"]) / d["h2pcg_hist"]) <= 1e-9
+    # one preconditioner application = 2r chained K-cycles
+    assert np.max(np.abs(rep.residual_history - d["h2pcg_hist"]) / d["h2pcg_hist"]) <= _chain_bound(2 * len(gpu))
 
 
 def test_pcg_api_edge_cases(mv):
@@ -517,8 +528,9 @@ def test_test_phase_matches_reference(mv, c1, c1_comps):
     d, mats = c1[0], c1[1]
     comp = mv.GpuComposite(c1_comps[0])
     rep, w = mv.test_phase(comp, mats[0], 15, np.random.default_rng(5))
-    assert np.max(np.abs(rep.per_iteration_anorms - d["testphase_anorms"]) / d["testphase_anorms"]) <= 1e-8
-    assert rel(w, d["testphase_w"]) <= 1e-8
+    bound = _chain_bound(15 * 2 * len(c1_comps[0]))         # nu = 15 composites of 2r K-cycles: 1.2e-8
+    assert np.max(np.abs(rep.per_iteration_anorms - d["testphase_anorms"]) / d["testphase_anorms"]) <= bound
+    assert rel(w, d["testphase_w"]) <= bound
 
 
 # ------------------------------------------------------------ full setup ----
@@ -534,6 +546,8 @@ def test_fit_c1_end_to_end(mv):
     assert est.composite_.n_components == int(d["n_comp"])
     assert est.hierarchy_.sizes() == [16384, 1665, 522, 160]
     ref = np.asarray(d["smooth_vectors"])
+    # smooth vector k comes out of k test phases (15 k (k + 1) chained K-cycles; the
+    # chain bound would allow 3e-8 for k = 4 -- the measured agreement is far tighter)
     for k, v in enumerate(est.smooth_vectors_):
         assert rel(v, ref[k]) <= 1e-9, k
     x, rep = est.solve(d["b"], rtol=1e-6)
@@ -578,7 +592,7 @@ def test_composite_graphs_not_reused_across_composites(mv, c1, c1_comps):
     for ncomp in (1, 2, 3, 4, 2):
         comp = mv.GpuComposite(gpu[:ncomp])
         y = comp.apply_symmetrized(x)
-        assert rel(y, oracle_composite(cpu[:ncomp], x)) <= 1e-9, ncomp
+        assert rel(y, oracle_composite(cpu[:ncomp], x)) <= _chain_bound(2 * ncomp), ncomp
         del comp
         gc.collect()
 
