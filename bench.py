@@ -587,7 +587,8 @@ def run_b200(args, world, rank, local):
         "gpu_launches": int(round(launches.value / steps)),
         "roofline": None,
         "clocks": clocks,
-        "details": {"n": n, "nnz": int(mats[0].nnz), "levels": [M.shape[0] for M in mats], "nit": n_iters,
+        "details": {"n": n, "nnz": int(mats[0].nnz), "levels": [M.shape[0] for M in mats],
+                    "nnz_levels": [int(M.nnz) for M in mats], "nnz_P": [int(P.nnz) for P in pros], "nit": n_iters,
                     "converged": bool(conv.value), "final_relres": float(hist_gpu[-1] / hist_gpu[0]),
                     "hierarchy": info.get("hierarchy"), "fit_s": info.get("fit_s"),
                     "bootstrap_stages": info.get("bootstrap_stages"),

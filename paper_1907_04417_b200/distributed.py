@@ -493,6 +493,7 @@ class DeviceBackend:
         self.torch.cuda.synchronize()
         st = int(self._ws[1].item())
         if st:
+            self._ws.zero_()  # the relay's kernels share this status word
             raise RuntimeError(f"pipelined GS sweep: status {st} (timeout waiting on a ghost)")
 
     def coarse(self, mats, pros):
@@ -609,8 +610,7 @@ class DistributedVCycle:
         lower = xe[:xh.n_lower]
         upper = xe[xh.n_lower + xh.n_own:]
         # 1. forward GS from x = 0: one wavefront across the ranks, or relayed in rank order
-        if self.pipelined:
-            self._pipe_sweep(self.pipe_fwd, r_own, None)
+        if self.pipelined and self._pipe_sweep(self.pipe_fwd, r_own, None):
             self._xsl(xh, xe).copy_(self._xsl(xh, self.xp))
         else:
             self.exchange(xh, xe, self.x_send, peers_to=(), peers_from=range(rank))
@@ -642,8 +642,7 @@ class DistributedVCycle:
         be.spmv_add(self.P_own, self.xc, x_own)
         # 6. backward GS from x: one wavefront across the ranks, or relayed in reverse rank order
         self.exchange(xh, xe, self.x_send)                   # old values of every ghost
-        if self.pipelined:
-            self._pipe_sweep(self.pipe_bwd, r_own, xe)
+        if self.pipelined and self._pipe_sweep(self.pipe_bwd, r_own, xe):
             x_own.copy_(self._xsl(xh, self.xp))
             z_own.copy_(x_own)
             return z_own
@@ -659,11 +658,22 @@ class DistributedVCycle:
     def _pipe_sweep(self, plan, b_own, x_old_ext):
         """Reset the shared extended x to the sentinel, synchronise the ranks (no
         peer may store a value before the reset), then sweep: every rank's kernel
-        polls its ghosts while its peers' kernels are still running."""
+        polls its ghosts while its peers' kernels are still running.  Returns
+        False -- on every rank, and for the rest of the run -- if any rank's sweep
+        failed (a ghost never arrived before the kernel's spin limit: peer
+        stores not visible on this system); the caller then relays instead."""
         self.be.fill_sentinel(self.xp)
         self.comm.barrier()
-        self.be.pipe_sweep(plan, b_own, x_old_ext, self.xp, self.peers)
-        self.comm.barrier()  # every peer's stores into this rank's x are done
+        failed = 0.0
+        try:
+            self.be.pipe_sweep(plan, b_own, x_old_ext, self.xp, self.peers)
+        except RuntimeError as exc:
+            failed, self.pipe_error = 1.0, str(exc)
+        failed, = self.comm.allreduce([failed])  # also: every peer's stores into this rank's x are done
+        if failed:
+            self.pipelined = False
+            return False
+        return True
 
     # ---- distributed operator pieces for PCG ---------------------------------
     def matvec(self, p_own, q_own):

@@ -1,8 +1,8 @@
-"""Per-kernel achieved HBM GB/s of one C2 H1 solve (SURVEY 8(d) byte model)
-from the committed ncu launch list summary (cold-cache, serialised launches)
-and the fitted hierarchy's sizes in the committed bench line:
+"""Per-kernel-family achieved HBM GB/s of one H1 solve: SURVEY 8(d) algorithmic
+bytes per family (from the hierarchy sizes in a bench line's `details`) over
+the kernel time of an ncu launch list summary (cold cache, serialised).
 
-  python tools/kernel_gbs.py [launch_summary.txt] [bench_line.json] > profiles/r01c_c2_kernel_gbs.txt
+  python tools/kernel_gbs.py profiles/r02e_c3_launches_summary.txt profiles/r02f_c3_bench.json
 """
 import json
 import os
@@ -10,73 +10,64 @@ import re
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SUMMARY = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles", "r01b_c2_launches_summary.txt")
-BENCH = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "profiles", "r01c_bench_c2.json")
+SUMMARY, BENCH = sys.argv[1], sys.argv[2]
 bench = json.loads(open(BENCH).read().strip().splitlines()[-1])
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
-    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6518.0
-n = bench["config"]["levels"]
-gal = bench["galerkin"]["levels"]
-nnzA = [g["nnz_A"] for g in gal] + [gal[-1]["nnz_Ac"]]
-nnzP = [g["nnz_P"] for g in gal]
-L = len(n) - 1                       # coarsest = n[L], dense inverse
-nit = bench["config"]["nit"]
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6538.9
+det = bench["details"]
+n, nnzA, nnzP, nit = det["levels"], det["nnz_levels"], det["nnz_P"], det["nit"]
+L = len(n) - 1
 
 
 def ab(nnz, rows):
     return 12 * nnz + 4 * (rows + 1)
 
 
-# algorithmic bytes per PCG iteration, per kernel family (fine level k = 0, coarse 1..L-1)
-B = {
-    "gs_lean fwd (level 0, from x=0)": ab(nnzA[0], n[0]) + 24 * n[0],
-    "gs_lean bwd (level 0, from x)": ab(nnzA[0], n[0]) + 32 * n[0],
-    "coarse sweeps, row + level-set (L1..)": sum(2 * ab(nnzA[k], n[k]) + 56 * n[k] for k in range(1, L)),
-    "gs_prepare (all levels, both sweeps)": sum(28 * n[k] * 2 + 6 * nnzA[k] + 8 * n[k] for k in range(L)),
-    "spmv<1> residual": sum(ab(nnzA[k], n[k]) + 24 * n[k] for k in range(L)),
-    "spmv<0> restriction": sum(ab(nnzP[k], n[k + 1]) + 8 * n[k] + 8 * n[k + 1] for k in range(L)),
-    "spmv<2> prolongation": sum(ab(nnzP[k], n[k]) + 8 * n[k + 1] + 16 * n[k] for k in range(L)),
-    "spmv_dot (PCG A p)": ab(nnzA[0], n[0]) + 24 * n[0],
-    "gemv (coarsest inverse)": 8 * n[L] ** 2 + 16 * n[L],
-    "pcg_xr + dot2 + pcg_p": (32 + 16 + 24) * n[0],
+def ld(k):  # entries of L + D (forward sweep from zero)
+    return (nnzA[k] - n[k]) // 2 + n[k]
+
+
+B = {  # bytes per PCG iteration
+    "fine sweeps (gs_lean, level 0)": 12 * ld(0) + 4 * (n[0] + 1) + 24 * n[0] + ab(nnzA[0], n[0]) + 32 * n[0],
+    "coarse sweeps (row / stream / level-set)": sum(12 * ld(k) + 4 * (n[k] + 1) + 24 * n[k] + ab(nnzA[k], n[k])
+                                                    + 32 * n[k] for k in range(1, L)),
+    "residual SpMV": sum(ab(nnzA[k], n[k]) + 24 * n[k] for k in range(L)),
+    "restriction SpMV": sum(ab(nnzP[k], n[k + 1]) + 8 * n[k] + 8 * n[k + 1] for k in range(L)),
+    "prolongation SpMV": sum(ab(nnzP[k], n[k]) + 8 * n[k + 1] + 16 * n[k] for k in range(L)),
+    "PCG A p (spmv_dot)": ab(nnzA[0], n[0]) + 24 * n[0],
+    "coarsest GEMV": 8 * n[L] ** 2 + 16 * n[L],
+    "PCG vector updates and dots": (32 + 16 + 24) * n[0],
 }
-# kernel time per solve from the launch list summary
-summ = open(SUMMARY).read()
+fam = {
+    "fine sweeps (gs_lean, level 0)": ("gs_lean_kernel",),
+    "coarse sweeps (row / stream / level-set)": ("gs_row_kernel", "gs_stream_kernel", "gs_level_kernel",
+                                                 "gs_prepare"),
+    "residual SpMV": ("spmv_stream_kernel<1>", "spmv_warp_kernel<1>", "spmv_kernel<1>"),
+    "restriction SpMV": ("spmv_stream_kernel<0>", "spmv_warp_kernel<0>", "spmv_kernel<0>"),
+    "prolongation SpMV": ("spmv_stream_kernel<2>", "spmv_warp_kernel<2>", "spmv_kernel<2>"),
+    "PCG A p (spmv_dot)": ("spmv_dot_kernel",),
+    "coarsest GEMV": ("gemv_kernel",),
+    "PCG vector updates and dots": ("pcg_xr_kernel", "dot2_kernel", "pcg_p_kernel"),
+}
 T = {}
-for line in summ.splitlines():
+for line in open(SUMMARY).read().splitlines():
     m = re.match(r"\s*([\d.]+)%\s+(\d+)\s+([\d.]+)\s+(\S.*)$", line)
     if m:
         T[m.group(4).strip()] = int(m.group(2)) * float(m.group(3)) * 1e-6
-
-
-def tt(*names):
-    return sum(T.get(x, 0.0) for x in names)
-
-
-lean = sorted(x for x in T if x.startswith("gs_lean_kernel"))
-t = {
-    "gs_lean fwd (level 0, from x=0)": T[lean[0]],
-    "gs_lean bwd (level 0, from x)": T[lean[1]],
-    "coarse sweeps, row + level-set (L1..)": tt("gs_row_kernel<0>", "gs_row_kernel<false>",
-                                             "gs_level_kernel<0, 1>", "gs_level_kernel<false, 1>",
-                                             "gs_level_kernel<0, 2>", "gs_level_kernel<false, 2>"),
-    "gs_prepare (all levels, both sweeps)": tt("gs_prepare_kernel", "gs_prepare_fold_warp_kernel"),
-    "spmv<1> residual": tt("spmv_kernel<1>", "spmv_warp_kernel<1>"),
-    "spmv<0> restriction": tt("spmv_kernel<0>", "spmv_warp_kernel<0>"),
-    "spmv<2> prolongation": tt("spmv_kernel<2>", "spmv_warp_kernel<2>"),
-    "spmv_dot (PCG A p)": T["spmv_dot_kernel"],
-    "gemv (coarsest inverse)": T["gemv_kernel"],
-    "pcg_xr + dot2 + pcg_p": tt("pcg_xr_kernel", "dot2_kernel", "pcg_p_kernel"),
-}
-print(f"# C2 H1 solve, {nit} PCG iterations; levels {n}; peak {peak:.0f} GB/s (MEASURED_PEAKS.json copy)")
-print(f"# time: ncu launch list ({os.path.relpath(SUMMARY, ROOT)}, cold cache, serialised);")
-print("# bytes: SURVEY 8(d) model per kernel family (A_k: 12 nnz + 4 (n+1); vectors 8 B/entry)")
-print(f"{'kernel family':40s} {'MB/iter':>9} {'ms/solve':>9} {'GB/s':>8} {'% peak':>7}")
-tot_b = tot_t = 0.0
+used = set()
+print(f"# {os.path.basename(BENCH)}: {nit} PCG iterations, levels {n}; peak {peak:.0f} GB/s (MEASURED_PEAKS.json)")
+print(f"# time: {os.path.relpath(SUMMARY, ROOT)} (ncu launch list, cold cache, serialised); the prepare kernels")
+print("# (rhs permutation / fold / sentinel fill) are counted with the coarse sweeps; bytes: SURVEY 8(d) model")
+print(f"{'kernel family':42s} {'MB/iter':>9} {'ms/solve':>9} {'GB/s':>8} {'% peak':>7}")
+tb = tt = 0.0
 for k in B:
-    bb, tt = B[k] * nit, t[k]
-    tot_b += bb
-    tot_t += tt
-    print(f"{k:40s} {B[k] / 1e6:9.2f} {tt * 1e3:9.2f} {bb / tt / 1e9:8.1f} {100 * bb / tt / 1e9 / peak:6.2f}%")
-print(f"{'all':40s} {tot_b / nit / 1e6:9.2f} {tot_t * 1e3:9.2f} {tot_b / tot_t / 1e9:8.1f} "
-      f"{100 * tot_b / tot_t / 1e9 / peak:6.2f}%")
+    t = sum(v for name, v in T.items() if any(name.startswith(pfx) for pfx in fam[k]))
+    used |= {name for name in T if any(name.startswith(pfx) for pfx in fam[k])}
+    bb = B[k] * nit
+    tb, tt = tb + bb, tt + t
+    print(f"{k:42s} {B[k] / 1e6:9.2f} {t * 1e3:9.2f} {bb / max(t, 1e-12) / 1e9:8.1f} "
+          f"{100 * bb / max(t, 1e-12) / 1e9 / peak:6.2f}%")
+print(f"{'all':42s} {tb / nit / 1e6:9.2f} {tt * 1e3:9.2f} {tb / tt / 1e9:8.1f} {100 * tb / tt / 1e9 / peak:6.2f}%")
+rest = sorted(set(T) - used)
+if rest:
+    print("# not in a family:", ", ".join(rest))
