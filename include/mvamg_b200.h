@@ -246,6 +246,43 @@ int mvamg_gs_row_sweep_f64(int mode, int n, const int* indptr, const int* indice
                            const int* perm, const int* wofs, const double* coef, const int* src,
                            int threads, int ctas, int max_tile_slots, double* tperm, const double* b,
                            const double* x_old, double* x_new, int* ws, void* stream);
+/* Cluster dataflow sweep (gs_cluster_kernel): the sweep's rows in topological
+ * order, one warp per row, run by ONE thread-block cluster of ncta CTAs (1, 2,
+ * 4, 8 or 16) x wpc worker warps (1..32) with the iterate in the cluster's
+ * distributed shared memory: a row is published by a local st.shared and
+ * polled with ld.shared::cluster, so no dependency crosses L2 (a few hundred
+ * ns per DAG level instead of ~1.4 us).  Replaces pkg/src/mvamg/_kernels.py:
+ * 15-38 on coarse levels whose x fits the cluster (8 bytes per row, spread
+ * over the CTAs' shared memory).  Same row
+ * order as the serial loop; row sums in a fixed tree (reproducible, tolerance
+ * parity -- not the CSR-order roundings).
+ * mvamg_gs_cluster_plan (host): the rows in topological (DAG level) order
+ * are dealt to the ncta * wpc worker warps (worker g = warp * ncta + cta) --
+ * a row to the CTA owning its latest input while that CTA holds no more than
+ * its share of the row's level (*local_late = rows so placed), round-robin
+ * over that CTA's warps -- and stored worker by worker (q = a row's index in
+ * that storage; rows wptr[g] .. wptr[g+1]; rowid: q -> row, perm: row -> q) as
+ * row records packed into pages of page_bytes (a multiple of 128; pages
+ * wpage[g] .. wpage[g+1], which the warp streams through shared memory with
+ * TMA bulk copies).  Page: int nrows, 12 bytes of padding, then records {int
+ * cnt, early, row, slot; double diag, RN(1/diag); cnt coefficients; cnt
+ * sources; padding to 16 bytes}; a record's entries are ordered by the DAG level of their
+ * inputs (old values first), entries early .. cnt-1 (same, last level, at
+ * most 4) being its late tail; source = cta << 24 | slot of the value, or
+ * bit 31 | row for an x_old value (modes 1, 3).  Query with blob == NULL
+ * first (*npages, *nlev DAG levels, *slots_per_cta 8-byte x slots per CTA);
+ * MVAMG_E_ARG when a row's record does not fit a page. */
+int mvamg_gs_cluster_plan(int n, const int* indptr, const int* indices, const double* data, int mode, int ncta,
+                          int wpc, int page_bytes, long long* npages, int* nlev, int* slots_per_cta,
+                          int* local_late, int* wptr, int* wpage, int* rowid, int* perm, void* blob);
+/* One sweep (device pointers; a mode-2 plan with x_old runs the folded
+ * backward sweep).  Shared memory per CTA: 8 * slots + 2 * wpc * (page_bytes +
+ * 8).  sleep_ns: back-off of a warp whose poll found nothing new.  tperm: n
+ * doubles of scratch; ws: >= 2 device ints (ticket, status). */
+int mvamg_gs_cluster_sweep_f64(int mode, int n, const int* indptr, const int* indices, const double* data,
+                               const int* wptr, const int* wpage, const void* blob, const int* perm, int ncta,
+                               int wpc, int slots, int page_bytes, int sleep_ns, double* tperm, const double* b,
+                               const double* x_old, double* x_new, int* ws, void* stream);
 /* Pipelined sweep of one rank of a row-partitioned level (distributed.py;
  * SURVEY.md 8(e)): a row schedule of mode 0 / 2 built with row range
  * [row_lo, row_hi) = the own rows of the extended layout [lower ghosts | own |
@@ -392,6 +429,12 @@ int mvamg_hierarchy_set_gs_rows(mvamg_hierarchy* h, int k, int mode, const int* 
                                 const int* crit, const double* dg, const double* rdg, const int* perm, const int* wofs,
                                 const double* coef, const int* src, int threads, int ctas,
                                 int max_tile_slots, double* tperm);
+/* Cluster dataflow plan of level k for sweep `mode` (mvamg_gs_cluster_plan);
+ * used before every other schedule of that mode; a mode-2 plan also serves
+ * backward sweeps from x_old (folded). */
+int mvamg_hierarchy_set_gs_cluster(mvamg_hierarchy* h, int k, int mode, const int* wptr, const int* wpage,
+                                   const void* blob, const int* perm, int ncta, int wpc, int slots,
+                                   int page_bytes, int sleep_ns, double* tperm);
 /* Transfer k: P (n_k x n_{k+1}) and R = P^T (n_{k+1} x n_k), device CSR.
  * Levels k and k+1 must be set first (their sizes give P's and R's shapes):
  * otherwise MVAMG_E_STATE.  Synchronises the device once to read nnz(P), nnz(R). */

@@ -26,6 +26,7 @@
 #include "mvamg_kernels.cuh"
 #include "galerkin.cuh"
 #include "gs_stream.cuh"
+#include "gs_cluster.cuh"
 #include "matching.cuh"
 #include "svd.cuh"
 
@@ -57,6 +58,14 @@ int g_gs_debug = [] {
 int g_row_sleep = [] {
   const char* e = getenv("MVAMG_ROW_SLEEP");
   return e ? atoi(e) : 0;
+}();
+int g_cluster_local = [] {  // diagnostics: 0 = the cluster plan ignores where a row's latest input lives
+  const char* e = getenv("MVAMG_CLUSTER_LOCAL");
+  return e ? atoi(e) : 1;
+}();
+int g_cluster_sleep = [] {  // diagnostics: overrides a cluster schedule's poll back-off (ns)
+  const char* e = getenv("MVAMG_CLUSTER_SLEEP");
+  return e ? atoi(e) : -1;
 }();
 
 int num_sms() {
@@ -185,6 +194,17 @@ struct GsRows {
   const int* src = nullptr;
   const double* dg = nullptr;
   const double* rdg = nullptr;
+  const int* perm = nullptr;
+  double* tperm = nullptr;
+};
+
+// Cluster dataflow schedule (gs_cluster_kernel) of one sweep mode
+// (mvamg_gs_cluster_plan).
+struct GsCluster {
+  int mode = 0, ncta = 0, wpc = 0, slots = 0, page_bytes = 0, sleep_ns = 0;
+  const int* wptr = nullptr;
+  const int* wpage = nullptr;
+  const unsigned char* blob = nullptr;
   const int* perm = nullptr;
   double* tperm = nullptr;
 };
@@ -641,6 +661,74 @@ int launch_gs_rows(const Csr& A, const GsRows& g, const double* b, const double*
   return 0;
 }
 
+
+bool g_cluster_attr = false;
+// Cluster dataflow sweep: prepare (rhs in position order, fold), then ONE
+// thread-block cluster of g.ncta CTAs x g.wpc worker warps with x in its
+// distributed shared memory.
+int launch_gs_cluster(const Csr& A, const GsCluster& g, const double* b, const double* xold, double* xnew,
+                      int* ticket, int* status, cudaStream_t s) {
+  const int n = A.n;
+  if (n == 0) return 0;
+  if (!g.blob) return fail(MVAMG_E_STATE, "gs cluster: plan for this sweep mode was not set");
+  set_kernel_attrs();
+  if (g.ncta < 1 || g.ncta > 16 || (g.ncta & (g.ncta - 1))) return fail(MVAMG_E_ARG, "gs cluster: 1, 2, 4, 8 or 16 CTAs");
+  if (g.wpc < 1 || g.wpc > 32) return fail(MVAMG_E_ARG, "gs cluster: 1..32 worker warps per CTA");
+  bool fold = false;
+  if (xold) {
+    if (g.mode == 2) fold = true;
+    else if (g.mode == 0) return fail(MVAMG_E_ARG, "gs cluster: zero-guess forward schedule with x_old");
+  } else if (g.mode == 1 || g.mode == 3) {
+    return fail(MVAMG_E_ARG, "gs cluster: schedule needs x_old");
+  }
+  if (!g_cluster_attr) {
+    g_cluster_attr = true;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(gs_cluster_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+    cudaFuncSetAttribute(gs_cluster_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+    cudaFuncSetAttribute(gs_cluster_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(gs_cluster_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaGetLastError();
+  }
+  if (g.page_bytes < 128 || g.page_bytes % 128) return fail(MVAMG_E_ARG, "gs cluster: pages of a multiple of 128 bytes");
+  // x slice | wpc rings of kClusterRing pages | their mbarriers
+  const size_t smem = (((size_t)g.slots * 8 + 127) & ~(size_t)127) +
+                      (size_t)g.wpc * kClusterRing * ((size_t)g.page_bytes + 8);
+  if (smem > (size_t)g_max_dyn_smem) return fail(MVAMG_E_ARG, "gs cluster: x slice and page rings exceed shared memory");
+  launch_prepare(A, b, xold, g.perm, g.tperm, xnew, ticket, fold ? 1 : 0, s);
+  GsClusterArgs a;
+  a.n = n;
+  a.wpc = g.wpc;
+  a.slots = g.slots;
+  a.page_bytes = g.page_bytes;
+  a.wptr = g.wptr;
+  a.wpage = g.wpage;
+  a.blob = g.blob;
+  a.tperm = g.tperm;
+  a.xold = xold;
+  a.xnew = xnew;
+  a.status = status;
+  a.trace = g_gs_trace;
+  a.sleep_ns = g_cluster_sleep >= 0 ? g_cluster_sleep : g.sleep_ns;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g.ncta);
+  cfg.blockDim = dim3(g.wpc * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = g.ncta;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (g.mode == 1 || g.mode == 3) CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_cluster_kernel<true>, a));
+  else CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_cluster_kernel<false>, a));
+  return 0;
+}
+
 }  // namespace
 
 // ============================================================================
@@ -655,6 +743,7 @@ struct Level {
   GsStream gss[4];  // streamed single-SM schedules (used first when set)
   GsLevels glv[4];  // small-level single-CTA schedules (used when set)
   GsRows grw[4];    // dataflow row schedules (used when set and glv is not)
+  GsCluster gcl[4]; // cluster dataflow schedules (used first when set)
   Csr P, R;  // valid for k < L-1
   double *xa = nullptr, *xb = nullptr, *t = nullptr, *r = nullptr, *z = nullptr;
   double *fr = nullptr, *fx = nullptr, *fp[2] = {nullptr, nullptr}, *fap[2] = {nullptr, nullptr};
@@ -719,7 +808,11 @@ struct mvamg_hierarchy {
       } else {
         bool fwd = sp.kind == MVAMG_GS_FORWARD;
         int lmode = (fwd ? 0 : 2) + (x_cur == nullptr ? 0 : 1);
-        if (l.gss[lmode].nstages) {
+        if (!fwd && x_cur != nullptr && l.gcl[2].blob) {
+          st = launch_gs_cluster(l.A, l.gcl[2], b, x_cur, out, ticket, status_ptr(), s);
+        } else if (l.gcl[lmode].blob) {
+          st = launch_gs_cluster(l.A, l.gcl[lmode], b, x_cur, out, ticket, status_ptr(), s);
+        } else if (l.gss[lmode].nstages) {
           st = launch_gs_stream(l.A.n, l.gss[lmode], x_cur != nullptr, b, x_cur, out, s);
         } else if (!fwd && x_cur != nullptr && l.gss[2].nstages && l.gss[2].tfold) {
           // backward from x_old with the zero-guess plan: fold the old lower
@@ -2397,6 +2490,190 @@ int mvamg_hierarchy_set_gs_rows(mvamg_hierarchy* h, int k, int mode, const int* 
   g.mode = mode; g.threads = threads; g.ctas = ctas; g.max_tile_slots = max_tile_slots;
   g.rowid = rowid; g.cnt = cnt; g.crit = crit; g.wofs = wofs;
   g.coef = coef; g.src = src; g.dg = dg; g.rdg = rdg; g.perm = perm; g.tperm = tperm;
+  return 0;
+}
+
+int mvamg_gs_cluster_plan(int n, const int* indptr, const int* indices, const double* data, int mode, int ncta,
+                          int wpc, int page_bytes, long long* npages, int* nlev, int* slots_per_cta,
+                          int* local_late, int* wptr, int* wpage, int* rowid, int* perm, void* blob) {
+  if (n < 0 || !indptr || !npages || !nlev || !slots_per_cta || mode < 0 || mode > 3)
+    return fail(MVAMG_E_ARG, "gs_cluster_plan: bad arguments");
+  if (ncta < 1 || ncta > 16 || (ncta & (ncta - 1)) || wpc < 1 || wpc > 32)
+    return fail(MVAMG_E_ARG, "gs_cluster_plan: ncta in {1,2,4,8,16}, wpc in 1..32");
+  if (page_bytes < 128 || page_bytes % 128) return fail(MVAMG_E_ARG, "gs_cluster_plan: pages of a multiple of 128 bytes");
+  const bool fwd = mode < 2, zero = (mode % 2) == 0;
+  const int G = ncta * wpc;
+  // level sets of the sweep's dependency DAG; crit[i] = an input of the last level
+  std::vector<int> lvl(n > 0 ? n : 1, 0), crit(n > 0 ? n : 1, -1), cn(n > 0 ? n : 1, 0);
+  int nl = 0;
+  for (int q = 0; q < n; ++q) {
+    const int i = fwd ? q : n - 1 - q;
+    int m = 0, cj = -1, cc = 0;
+    for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+      const int j = indices[k];
+      if (j == i) continue;
+      const bool isnew = fwd ? j < i : j > i;
+      if (isnew && lvl[j] + 1 >= m) { m = lvl[j] + 1; cj = j; }
+      if (isnew || !zero) ++cc;
+    }
+    lvl[i] = m;
+    crit[i] = cj;
+    cn[i] = cc;
+    if (kClusterPageHdr + cluster_row_bytes(cc) > page_bytes)
+      return fail(MVAMG_E_ARG, "gs_cluster_plan: a row record exceeds the page");
+    nl = std::max(nl, m + 1);
+  }
+  *nlev = n > 0 ? nl : 0;
+  // topological positions: by level, original order within a level (stable)
+  std::vector<int> order(n > 0 ? n : 1);
+  for (int q = 0; q < n; ++q) order[q] = q;
+  std::stable_sort(order.begin(), order.begin() + n, [&](int x, int y) { return lvl[x] < lvl[y]; });
+  // CTA of every row: its critical input's, while that CTA holds no more than 1.5x
+  // its share of the row's DAG level and 1.1x its share of all rows so far; else the
+  // CTA with the fewest rows of the level (then the fewest overall)
+  std::vector<int> cta(n > 0 ? n : 1, 0), nin(ncta, 0), load(ncta, 0);
+  int hits = 0;
+  for (int p0 = 0; p0 < n;) {
+    int p1 = p0;
+    while (p1 < n && lvl[order[p1]] == lvl[order[p0]]) ++p1;
+    const int w = p1 - p0;
+    const int cap = (3 * w + 2 * ncta - 1) / (2 * ncta);
+    std::fill(load.begin(), load.end(), 0);
+    for (int p = p0; p < p1; ++p) {
+      const int i = order[p];
+      int c = (g_cluster_local && crit[i] >= 0) ? cta[crit[i]] : -1;
+      if (c >= 0 && load[c] < cap && 10LL * nin[c] <= 11LL * (p / ncta) + 10LL * wpc) {
+        ++hits;
+      } else {
+        c = 0;
+        for (int t = 1; t < ncta; ++t)
+          if (load[t] < load[c] || (load[t] == load[c] && nin[t] < nin[c])) c = t;
+      }
+      cta[i] = c;
+      ++load[c];
+      ++nin[c];
+    }
+    p0 = p1;
+  }
+  int slots = 2;
+  for (int c = 0; c < ncta; ++c) slots = std::max(slots, nin[c]);
+  if (slots >= (1 << 24)) return fail(MVAMG_E_ARG, "gs_cluster_plan: too many slots per CTA");
+  *slots_per_cta = slots;
+  if (local_late) *local_late = hits;
+  // a CTA's rows go round-robin to its warps in position order; worker g = warp * ncta + cta
+  std::vector<int> seen(ncta, 0), wcount(G + 1, 0), wk(n > 0 ? n : 1, 0), sl(n > 0 ? n : 1, 0);
+  for (int p = 0; p < n; ++p) {
+    const int i = order[p], c = cta[i];
+    sl[i] = seen[c];
+    wk[i] = (seen[c] % wpc) * ncta + c;
+    ++seen[c];
+    ++wcount[wk[i] + 1];
+  }
+  for (int g = 0; g < G; ++g) wcount[g + 1] += wcount[g];
+  std::vector<int> fill(wcount.begin(), wcount.end() - 1), qrow(n > 0 ? n : 1, 0);
+  for (int p = 0; p < n; ++p) {
+    const int i = order[p];
+    qrow[fill[wk[i]]++] = i;
+  }
+  // pages: each worker's records back to back, no record across a page boundary
+  std::vector<int> pg_first(G + 1, 0);
+  long long pages = 0;
+  for (int g = 0; g < G; ++g) {
+    pg_first[g] = (int)pages;
+    int used = page_bytes;  // forces a first page when the worker has rows
+    for (int q = wcount[g]; q < wcount[g + 1]; ++q) {
+      const int rb = cluster_row_bytes(cn[qrow[q]]);
+      if (used + rb > page_bytes) { ++pages; used = kClusterPageHdr; }
+      used += rb;
+    }
+  }
+  pg_first[G] = (int)pages;
+  if (pages * (long long)page_bytes >= (1LL << 40)) return fail(MVAMG_E_ARG, "gs_cluster_plan: too many pages");
+  *npages = pages;
+  if (!blob) return 0;
+  if (!wptr || !wpage || !rowid || !perm) return fail(MVAMG_E_ARG, "gs_cluster_plan: missing outputs");
+  for (int g = 0; g <= G; ++g) { wptr[g] = wcount[g]; wpage[g] = pg_first[g]; }
+  unsigned char* out = static_cast<unsigned char*>(blob);
+  std::memset(out, 0, (size_t)pages * page_bytes);
+  std::vector<int> ents;
+  for (int g = 0; g < G; ++g) {
+    long long pg = pg_first[g] - 1;
+    int used = page_bytes, rows_in_page = 0;
+    for (int q = wcount[g]; q < wcount[g + 1]; ++q) {
+      const int i = qrow[q];
+      rowid[q] = i;
+      perm[i] = q;
+      const int cnt = cn[i], rb = cluster_row_bytes(cnt);
+      if (used + rb > page_bytes) {
+        if (pg >= pg_first[g]) std::memcpy(out + (size_t)pg * page_bytes, &rows_in_page, 4);
+        ++pg;
+        used = kClusterPageHdr;
+        rows_in_page = 0;
+      }
+      unsigned char* rec = out + (size_t)pg * page_bytes + used;
+      double dgv = 0.0;
+      ents.clear();
+      for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+        const int j = indices[k];
+        if (j == i) { dgv = data[k]; continue; }
+        const bool isnew = fwd ? j < i : j > i;
+        if (zero && !isnew) continue;
+        ents.push_back(k);
+      }
+      // by the level at which each input becomes final (old values first), CSR order within
+      // one -- but the critical input (whose CTA this row mostly shares) last of all
+      auto avail = [&](int k) {
+        const int j = indices[k];
+        if (!(fwd ? j < i : j > i)) return -1;
+        return 2 * lvl[j] + (j == crit[i] ? 1 : 0);
+      };
+      std::stable_sort(ents.begin(), ents.end(), [&](int x, int y) { return avail(x) < avail(y); });
+      // the late tail: the inputs of the last level (at most kClusterLate of them)
+      int late = 0;
+      while (late < kClusterLate && late < cnt && avail(ents[cnt - 1 - late]) >= 0 &&
+             avail(ents[cnt - 1 - late]) / 2 == avail(ents[cnt - 1]) / 2)
+        ++late;
+      const int hdr[4] = {cnt, cnt - late, i, sl[i]};
+      const double dd[2] = {dgv, 1.0 / dgv};
+      std::memcpy(rec, hdr, 16);
+      std::memcpy(rec + 16, dd, 16);
+      double* cf = reinterpret_cast<double*>(rec + kClusterRowHdr);
+      unsigned* sc = reinterpret_cast<unsigned*>(rec + kClusterRowHdr + 8 * (size_t)cnt);
+      for (int u = 0; u < cnt; ++u) {
+        const int k = ents[u], j = indices[k];
+        const bool isnew = fwd ? j < i : j > i;
+        cf[u] = data[k];
+        sc[u] = isnew ? (((unsigned)cta[j] << 24) | (unsigned)sl[j]) : (0x80000000u | (unsigned)j);
+      }
+      used += rb;
+      ++rows_in_page;
+    }
+    if (pg >= pg_first[g]) std::memcpy(out + (size_t)pg * page_bytes, &rows_in_page, 4);
+  }
+  return 0;
+}
+
+int mvamg_gs_cluster_sweep_f64(int mode, int n, const int* indptr, const int* indices, const double* data,
+                               const int* wptr, const int* wpage, const void* blob, const int* perm, int ncta,
+                               int wpc, int slots, int page_bytes, int sleep_ns, double* tperm, const double* b,
+                               const double* x_old, double* x_new, int* ws, void* stream) {
+  if (mode < 0 || mode > 3) return fail(MVAMG_E_ARG, "gs cluster: bad mode");
+  if (x_old != nullptr && x_old == x_new) return fail(MVAMG_E_ARG, "gs cluster: x_new must not alias x_old");
+  Csr A;
+  A.n = n; A.ip = indptr; A.ix = indices; A.v = data;
+  GsCluster g;
+  g.mode = mode; g.ncta = ncta; g.wpc = wpc; g.slots = slots; g.page_bytes = page_bytes; g.sleep_ns = sleep_ns;
+  g.wptr = wptr; g.wpage = wpage; g.blob = static_cast<const unsigned char*>(blob); g.perm = perm; g.tperm = tperm;
+  return launch_gs_cluster(A, g, b, x_old, x_new, ws, ws + 1, (cudaStream_t)stream);
+}
+
+int mvamg_hierarchy_set_gs_cluster(mvamg_hierarchy* h, int k, int mode, const int* wptr, const int* wpage,
+                                   const void* blob, const int* perm, int ncta, int wpc, int slots,
+                                   int page_bytes, int sleep_ns, double* tperm) {
+  if (!h || k < 0 || k >= h->L || mode < 0 || mode > 3) return fail(MVAMG_E_ARG, "set_gs_cluster: bad index");
+  GsCluster& g = h->lv[k].gcl[mode];
+  g.mode = mode; g.ncta = ncta; g.wpc = wpc; g.slots = slots; g.page_bytes = page_bytes; g.sleep_ns = sleep_ns;
+  g.wptr = wptr; g.wpage = wpage; g.blob = static_cast<const unsigned char*>(blob); g.perm = perm; g.tperm = tperm;
   return 0;
 }
 

@@ -17,7 +17,8 @@ import scipy.linalg
 import scipy.sparse.linalg as spla
 
 from . import _lib
-from .device import (DeviceCSR, DeviceGsLevels, DeviceGsPlan, DeviceGsRows, DeviceGsStream, GpuConfig, as_csr,
+from .device import (DeviceCSR, DeviceGsCluster, DeviceGsLevels, DeviceGsPlan, DeviceGsRows, DeviceGsStream, GpuConfig,
+                     as_csr,
                      stream_ctas,
                      autotune_coarse_gs,
                      level_gs_fits, ptr, row_gs_fits,
@@ -194,6 +195,21 @@ class GpuMultigridOperator:
                 self._keep.append(dd)
                 # streamed sweeps on the V-cycle's levels (C3 H1: 1.15-1.3x the level-set kernel); the K-cycle
                 # components of H2 stay on the level-set kernel (C3 H2 solve 2.22 s vs 2.43 s streamed)
+                if (k >= 1 and cfg.cluster_gs and not cfg.exact_gs and not cfg.generic_gs and not cfg.force_level_gs
+                        and not cfg.force_row_gs and A.shape[0] <= cfg.cluster_max_rows):
+                    # cluster dataflow sweeps: x in one thread-block cluster's distributed shared memory
+                    try:
+                        plans = {m: DeviceGsCluster(A, m, cfg) for m in self._gs_level_modes()}
+                    except ValueError:
+                        plans = None
+                    if plans is not None:
+                        self.gs_plans.append(None)
+                        self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=None, rows=None, cluster=plans))
+                        _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
+                                                               None, 0, None, None, None, 32, 0, 0), "set_level")
+                        for m, cp in plans.items():
+                            _lib.check(L.mvamg_hierarchy_set_gs_cluster(h, k, m, *cp.args()), "set_gs_cluster")
+                        continue
                 smodes = (self._gs_stream_modes(A) if cfg.stream_gs and self.cycle.kind == "V" and not cfg.generic_gs
                           and not cfg.force_level_gs and not cfg.force_row_gs else None)
                 if smodes:

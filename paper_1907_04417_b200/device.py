@@ -106,6 +106,15 @@ class GpuConfig:
                                     # (clusters measured slower than the row sweep on C3: off by default)
     stream_max_rows: int = 4096     # levels up to this size stream (C3: 1.3-1.9x the level-set / row sweeps
                                     # at <= 1.8k rows, equal at 5k)
+    cluster_gs: bool = True         # (tolerance parity) coarse levels whose x fits one thread-block cluster's
+                                    # shared memory: the cluster dataflow sweep (gs_cluster.cuh), before any other
+    cluster_max_rows: int = 60000   # ... up to this size (C3: 1.2x the row sweep at 53k rows, 2.3-4x at <= 16k;
+                                    # slower at 160k, where one cluster's 16 SMs cannot keep up)
+    cluster_min_warps: int = 8      # worker warps per CTA, at least
+    cluster_max_warps: int = 32     # ... and at most
+    cluster_page_bytes: int = 2048  # page of row records a worker warp streams per TMA bulk copy (doubled while
+                                    # a row's record does not fit)
+    cluster_sleep_ns: int = 0       # back-off (ns) of a worker warp whose poll found nothing new
     coarse_pinv_rtol: float = 0.0   # 0: the coarsest inverse from the reference's LU factors (cycles.py:88-97);
                                     # > 0: the stated C5 deviation -- truncated-eigen pseudo-inverse dropping
                                     # eigenvalues <= rtol * lambda_max (a numerically singular A_L)
@@ -649,6 +658,90 @@ class DeviceGsStream:
         _lib.check(L.mvamg_gs_stream_sweep_f64(self.n, self.mode, self.nstages, self.nslots, self.slot,
                                                self.group, self.ncta, ptr(self.blob), ptr(self.stage_off), ptr(b),
                                                ptr(x_old), ptr(x_new), s), "gs_stream_sweep")
+
+
+def cluster_shape(n, nlev, cfg=None):
+    """(ncta, wpc) of the cluster dataflow sweep of a level with n rows.  One
+    warp sweeps one row at a time (~1,200 cycles each), so the sweep wants many
+    worker warps -- measured on C3's levels (tools/cluster_bench.py): 16 CTAs
+    from ~1k rows up, 8 to 32 warps each, about 15 rows per warp."""
+    cfg = cfg or GpuConfig()
+    if n < 1:
+        return None
+    ncta = 16 if n >= 1000 else (8 if n >= 300 else 4)
+    ncta = max(1, min(ncta, cfg.max_cluster))
+    wpc = int(min(cfg.cluster_max_warps, max(cfg.cluster_min_warps, -(-n // (15 * ncta)))))
+    return ncta, wpc
+
+
+def cluster_smem(slots, wpc, page_bytes):
+    """Shared memory per CTA of the cluster sweep: x slice, page rings, mbarriers."""
+    return ((slots * 8 + 127) & ~127) + wpc * 2 * (page_bytes + 8)
+
+
+class DeviceGsCluster:
+    """Cluster dataflow GS plan (gs_cluster_kernel, mvamg_gs_cluster_plan) of one
+    matrix and sweep mode (0 fwd from x=0, 1 fwd, 2 bwd from x=0 -- also the
+    folded backward sweep from x_old --, 3 bwd), on the device."""
+
+    def __init__(self, A, mode, cfg=None, ncta=None, wpc=None, sleep_ns=None):
+        import torch
+
+        cfg = cfg or GpuConfig()
+        A = as_csr(A)
+        L = _lib.load()
+        n = A.shape[0]
+        ip = np.ascontiguousarray(A.indptr, dtype=np.int32)
+        ix = np.ascontiguousarray(A.indices, dtype=np.int32)
+        v = np.ascontiguousarray(A.data, dtype=np.float64)
+        vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        npg, nlev, slots, hits = ctypes.c_longlong(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        page = int(cfg.cluster_page_bytes)
+
+        def plan(c, w, *out):
+            return L.mvamg_gs_cluster_plan(n, vp(ip), vp(ix), vp(v), int(mode), int(c), int(w), page,
+                                           ctypes.byref(npg), ctypes.byref(nlev), ctypes.byref(slots),
+                                           ctypes.byref(hits), *out)
+
+        while plan(ncta or 1, wpc or 1, *([None] * 5)) != 0:  # a row too long for the page: larger pages
+            page *= 2
+            if page > 16384:
+                raise ValueError("gs cluster: a row's record exceeds the largest page")
+        if ncta is None or wpc is None:
+            shape = cluster_shape(n, nlev.value, cfg)
+            if shape is None:
+                raise ValueError("gs cluster: the level's x does not fit one thread-block cluster")
+            ncta, wpc = (ncta or shape[0]), (wpc or shape[1])
+        _lib.check(plan(ncta, wpc, *([None] * 5)), "gs_cluster_plan")
+        # worker warps per CTA: as many as leave room for their page rings beside the x slice
+        while wpc > 1 and cluster_smem(slots.value, wpc, page) > cfg.smem_limit:
+            wpc -= 1
+            _lib.check(plan(ncta, wpc, *([None] * 5)), "gs_cluster_plan")
+        if cluster_smem(slots.value, wpc, page) > cfg.smem_limit:
+            raise ValueError("gs cluster: x slice and page rings exceed shared memory")
+        wptr = np.empty(ncta * wpc + 1, dtype=np.int32)
+        wpage = np.empty(ncta * wpc + 1, dtype=np.int32)
+        rowid = np.empty(max(1, n), dtype=np.int32)
+        perm = np.empty(max(1, n), dtype=np.int32)
+        blob = np.zeros(max(1, npg.value) * page, dtype=np.uint8)
+        _lib.check(plan(ncta, wpc, vp(wptr), vp(wpage), vp(rowid), vp(perm), vp(blob)), "gs_cluster_plan")
+        self.n, self.mode, self.nlev, self.npages, self.page_bytes = n, mode, nlev.value, npg.value, page
+        self.ncta, self.wpc, self.slots, self.local_late = int(ncta), int(wpc), slots.value, hits.value
+        self.sleep_ns = int(cfg.cluster_sleep_ns if sleep_ns is None else sleep_ns)
+        self.wptr, self.wpage, self.blob = to_device(wptr), to_device(wpage), to_device(blob)
+        self.rowid, self.perm = to_device(rowid), to_device(perm)
+        self.tperm = torch.empty(max(2, n + 2), dtype=torch.float64, device="cuda")
+        self._csr = DeviceCSR(A)
+
+    def args(self):
+        return (ptr(self.wptr), ptr(self.wpage), ptr(self.blob), ptr(self.perm), self.ncta, self.wpc, self.slots,
+                self.page_bytes, self.sleep_ns, ptr(self.tperm))
+
+    def sweep(self, b, x_old, x_new, ws, stream=None):
+        """One sweep; with x_old a mode-2 plan runs the folded backward sweep."""
+        _lib.check(_lib.load().mvamg_gs_cluster_sweep_f64(
+            self.mode, self.n, *self._csr.ptrs(), *self.args(), ptr(b), ptr(x_old), ptr(x_new), ptr(ws),
+            stream or stream_handle()), "gs_cluster_sweep")
 
 
 class DeviceGsRows:

@@ -345,6 +345,88 @@ def test_gs_row_kernel_relaxed(mv, c1, cfg):
                     assert rel(folded, want) <= 1e-13, (name, "folded", cfg)
 
 
+def _gs_cluster_gpu(A, b, x_old, direction, zero, config, fold=False, **shape):
+    import torch
+    from paper_1907_04417_b200.device import DeviceGsCluster
+
+    A = sp.csr_matrix(A)
+    base = 0 if direction == "forward" else 2
+    mode = base if (zero or fold) else base + 1
+    cl = DeviceGsCluster(A, mode, config, **shape)
+    bd = _dev(b)
+    xo = None if zero else _dev(x_old)
+    xn = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+    ws = torch.zeros(8, dtype=torch.int32, device="cuda")
+    cl.sweep(bd, xo, xn, ws)
+    torch.cuda.synchronize()
+    assert int(ws[1].item()) == 0, "gs cluster sweep timed out"
+    first = xn.cpu().numpy().copy()
+    xn.fill_(0.0)
+    cl.sweep(bd, xo, xn, ws)
+    torch.cuda.synchronize()
+    assert np.array_equal(first, xn.cpu().numpy()), "cluster sweep not reproducible"
+    return first
+
+
+@pytest.mark.parametrize("shape", [dict(), dict(ncta=1, wpc=1), dict(ncta=2, wpc=3), dict(ncta=8, wpc=32),
+                                   dict(ncta=16, wpc=8)])
+def test_gs_cluster_kernel(mv, c1, shape):
+    """The cluster dataflow sweep (gs_cluster.cuh: x in a thread-block cluster's
+    distributed shared memory, one warp per row, TMA-streamed row records) in
+    all four modes and folded, on every structure and the C1 levels: the serial
+    sweep's row order (_kernels.py:15-38), each row sum in a fixed tree, so
+    within rounding of the serial loop and identical run to run."""
+    config = mv.GpuConfig()
+    rng = np.random.default_rng(15)
+    mats = c1[1]
+    cases = list(_structures()) + [("c1_l1", mats[1]), ("c1_l2", mats[2]), ("c1_l0", mats[0])]
+    for name, A in cases:
+        n = A.shape[0]
+        b = rng.standard_normal(n)
+        x0 = rng.standard_normal(n)
+        for direction in ("forward", "backward"):
+            for zero in (True, False):
+                want = np.zeros(n) if zero else x0.copy()
+                oracle_gs(A, b, want, direction)
+                got = _gs_cluster_gpu(A, b, x0, direction, zero, config, **shape)
+                assert rel(got, want) <= 1e-13, (name, direction, zero, shape)
+                if direction == "backward" and not zero:
+                    folded = _gs_cluster_gpu(A, b, x0, direction, zero, config, fold=True, **shape)
+                    assert rel(folded, want) <= 1e-13, (name, "folded", shape)
+
+
+def test_gs_cluster_long_rows_and_pages(mv):
+    """Rows longer than 32 and 64 entries (several early chunks), a row record
+    larger than the default page (the plan doubles the page), several late
+    inputs of one level."""
+    rng = np.random.default_rng(16)
+    n = 500
+    D = sp.csr_matrix(np.full((n, n), 0.01) + np.eye(n) * n)       # every row reads all earlier rows
+    B = random_spd_csr(700, density=0.15, seed=4)                    # ~100 entries per row
+    for name, A in (("dense500", D), ("rand700", B)):
+        b, x0 = rng.standard_normal(A.shape[0]), rng.standard_normal(A.shape[0])
+        for direction in ("forward", "backward"):
+            for zero in (True, False):
+                want = np.zeros(A.shape[0]) if zero else x0.copy()
+                oracle_gs(A, b, want, direction)
+                got = _gs_cluster_gpu(A, b, x0, direction, zero, mv.GpuConfig(), ncta=4, wpc=4)
+                assert rel(got, want) <= 1e-13, (name, direction, zero)
+
+
+def test_vcycle_cluster_sweeps(mv, c1):
+    """A V-cycle whose coarse levels run the cluster sweep (the default in
+    tolerance mode) against the reference golden, and with the cluster sweep
+    switched off: both within the north-star tolerance."""
+    d, mats, pros = c1[0], c1[1], c1[2]
+    r = d["b"]
+    op = mv.GpuMultigridOperator(mats, pros)
+    assert any(lv.get("cluster") for lv in op.level_dev), "no level took the cluster sweep"
+    assert rel(op.apply(r), d["apply_b"]) <= TOL_CYCLE
+    off = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(cluster_gs=False))
+    assert not any(lv.get("cluster") for lv in off.level_dev)
+    assert rel(off.apply(r), op.apply(r)) <= 1e-12
+
+
 def test_gs_hand_recurrence(mv):
     # pkg/tests/test_cycles.py:30-38
     A = laplacian_1d(3)
@@ -720,16 +802,17 @@ def test_gs_stream_relaxed(mv, c1):
 
 
 def test_vcycle_stream_sweeps(mv, c1):
-    """A V-cycle whose levels run the streamed sweeps (default config) matches
-    the exact-mode cycle to rounding and the reference golden to 1e-10; with
-    exact_gs the streamed sweeps keep the cycle bit-identical to the other
+    """A V-cycle whose levels run the streamed sweeps (the default without the
+    cluster sweep, and in exact mode) matches the reference golden to 1e-10;
+    with exact_gs the streamed sweeps keep the cycle bit-identical to the other
     exact schedules."""
     d, mats, pros = c1[0], c1[1], c1[2]
-    op = mv.GpuMultigridOperator(mats, pros)
+    op = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(cluster_gs=False))
     assert any(lv.get("stream") for lv in op.level_dev), "no level took the streamed sweep"
     z = op.apply(d["b"])
     assert rel(z, d["apply_b"]) <= TOL_CYCLE
     ex = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(exact_gs=True))
+    assert any(lv.get("stream") for lv in ex.level_dev) and not any(lv.get("cluster") for lv in ex.level_dev)
     ref = mv.GpuMultigridOperator(mats, pros, config=mv.GpuConfig(exact_gs=True, stream_gs=False))
     assert np.array_equal(ex.apply(d["b"]), ref.apply(d["b"]))
 

@@ -137,3 +137,143 @@ def test_row_schedule_over_a_row_range():
     assert np.all(perm[:lo] == -1) and np.all(perm[hi:] == -1)     # ghosts are never written
     assert list(rowid) == list(range(lo, hi))                      # a chain: topological = natural order
     assert src[0] == lo - 1                                        # the first row reads its lower ghost
+
+
+# ---- cluster dataflow plan (mvamg_gs_cluster_plan, gs_cluster.cuh) -------------------------------
+def _cluster_plan(A, mode, ncta, wpc, page=2048):
+    A = sp.csr_matrix(A)
+    n = A.shape[0]
+    L = _lib.load()
+    ip = np.ascontiguousarray(A.indptr, dtype=np.int32)
+    ix = np.ascontiguousarray(A.indices, dtype=np.int32)
+    v = np.ascontiguousarray(A.data, dtype=np.float64)
+    npg, nl, sl, hits = ctypes.c_longlong(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    head = (n, vp(ip), vp(ix), vp(v), mode, ncta, wpc, page, ctypes.byref(npg), ctypes.byref(nl), ctypes.byref(sl),
+            ctypes.byref(hits))
+    _lib.check(L.mvamg_gs_cluster_plan(*head, None, None, None, None, None), "plan")
+    G = ncta * wpc
+    wptr, wpage = np.empty(G + 1, dtype=np.int32), np.empty(G + 1, dtype=np.int32)
+    rowid, perm = np.empty(max(1, n), dtype=np.int32), np.empty(max(1, n), dtype=np.int32)
+    blob = np.zeros(max(1, npg.value) * page, dtype=np.uint8)
+    _lib.check(L.mvamg_gs_cluster_plan(*head, vp(wptr), vp(wpage), vp(rowid), vp(perm), vp(blob)), "plan")
+    return dict(wptr=wptr, wpage=wpage, rowid=rowid, perm=perm, blob=blob, nlev=nl.value, slots=sl.value,
+                local=hits.value, page=page, npages=npg.value)
+
+
+def _cluster_streams(pl, G):
+    """Per worker, its rows in order: (cnt, early, row, slot, diag, coef[], src[]) decoded as the kernel reads them."""
+    page, blob = pl["page"], pl["blob"]
+    out = []
+    for g in range(G):
+        rows = []
+        for pg in range(pl["wpage"][g], pl["wpage"][g + 1]):
+            base = pg * page
+            nrows = int(blob[base:base + 4].view(np.int32)[0])
+            off = base + 16
+            for _ in range(nrows):
+                assert off % 16 == 0
+                cnt, ne, row, slot = (int(t) for t in blob[off:off + 16].view(np.int32))
+                dg, rdg = blob[off + 16:off + 32].view(np.float64)
+                assert rdg == 1.0 / dg
+                cf = blob[off + 32:off + 32 + 8 * cnt].view(np.float64)
+                sc = blob[off + 32 + 8 * cnt:off + 32 + 12 * cnt].view(np.uint32)
+                assert 0 <= ne <= cnt and cnt - ne <= 2
+                rows.append((cnt, ne, row, slot, float(dg), cf, sc))
+                off += (32 + 12 * cnt + 15) & ~15
+            assert off <= base + page                              # no record straddles a page
+        assert len(rows) == pl["wptr"][g + 1] - pl["wptr"][g]
+        for t, rw in enumerate(rows):
+            assert pl["rowid"][pl["wptr"][g] + t] == rw[2] and pl["perm"][rw[2]] == pl["wptr"][g] + t
+        out.append(rows)
+    return out
+
+
+def _cluster_emulate(A, pl, ncta, wpc, mode, b, x_old):
+    """Run the plan as the kernel does -- every worker takes its rows in order, a
+    row only when all its polled inputs are published -- and return x."""
+    n = A.shape[0]
+    G = ncta * wpc
+    streams = _cluster_streams(pl, G)
+    xs = np.full((ncta, pl["slots"]), np.nan)
+    cur = [0] * G
+    x = np.zeros(n)
+    left = n
+    while left:
+        progressed = False
+        for g in range(G):
+            if cur[g] >= len(streams[g]):
+                continue
+            cnt, ne, row, slot, dg, cf, sc = streams[g][cur[g]]
+            vals = np.empty(cnt)
+            for u in range(cnt):
+                s = int(sc[u])
+                vals[u] = x_old[s & 0x7fffffff] if s >> 31 else xs[(s >> 24) & 15, s & 0xffffff]
+            if np.isnan(vals).any():
+                continue
+            xi = (b[row] - np.dot(cf, vals)) / dg
+            assert np.isnan(xs[g % ncta, slot])                     # every slot is written once
+            xs[g % ncta, slot] = xi
+            x[row] = xi
+            cur[g] += 1
+            left -= 1
+            progressed = True
+        assert progressed, "the plan deadlocks"
+    return x
+
+
+@pytest.mark.parametrize("ncta,wpc", [(1, 1), (2, 3), (4, 8), (16, 32)])
+def test_cluster_plan_is_the_serial_sweep(ncta, wpc):
+    rng = np.random.default_rng(5)
+    cases = [laplacian_1d(70), laplacian_2d(13), random_spd_csr(300, density=0.05, seed=1),
+             random_spd_csr(90, density=0.9, seed=2), sp.diags(np.linspace(1, 2, 9)).tocsr(),
+             sp.csr_matrix(np.array([[2.0]]))]
+    for A in cases:
+        A = sp.csr_matrix(A)
+        n = A.shape[0]
+        d = A.diagonal()
+        b, x0 = rng.standard_normal(n), rng.standard_normal(n)
+        for mode in range(4):
+            pl = _cluster_plan(A, mode, ncta, wpc)
+            x_old = np.zeros(n) if mode % 2 == 0 else x0
+            got = _cluster_emulate(A, pl, ncta, wpc, mode, b, x_old)
+            want = x_old.copy()                                     # the serial loop, _kernels.py:15-38
+            for i in (range(n) if mode < 2 else range(n - 1, -1, -1)):
+                s = b[i]
+                for k in range(A.indptr[i], A.indptr[i + 1]):
+                    j = A.indices[k]
+                    if j != i:
+                        s -= A.data[k] * want[j]
+                want[i] = s / d[i]
+            assert np.max(np.abs(got - want)) <= 1e-13 * max(1.0, np.max(np.abs(want))), (n, mode)
+            assert sorted(pl["rowid"][:n].tolist()) == list(range(n))
+            counts = np.diff(pl["wptr"])
+            assert counts.sum() == n
+
+
+def test_cluster_plan_balance_and_locality():
+    """Rows follow their latest input's CTA where the level's share allows, and no CTA ends up with much more
+    than its share of the rows (its x slice must fit shared memory)."""
+    A = random_spd_csr(4000, density=0.01, seed=3)
+    pl = _cluster_plan(A, 0, 16, 8)
+    assert pl["local"] >= 0.5 * 4000
+    assert pl["slots"] <= 1.25 * 4000 / 16 + 8
+    per_worker = np.diff(pl["wptr"])
+    assert per_worker.max() <= 1.25 * 4000 / 128 + 2
+
+
+def test_cluster_plan_long_rows_need_larger_pages():
+    n = 400
+    D = sp.csr_matrix(np.ones((n, n)) * 0.01 + np.eye(n) * n)
+    L = _lib.load()
+    ip, ix = np.ascontiguousarray(D.indptr, dtype=np.int32), np.ascontiguousarray(D.indices, dtype=np.int32)
+    v = np.ascontiguousarray(D.data)
+    npg, nl, sl, hits = ctypes.c_longlong(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    rc = L.mvamg_gs_cluster_plan(n, vp(ip), vp(ix), vp(v), 0, 2, 2, 2048, ctypes.byref(npg), ctypes.byref(nl),
+                                 ctypes.byref(sl), ctypes.byref(hits), None, None, None, None, None)
+    assert rc == _lib.E_ARG                                        # 399 entries: 4,832 bytes > one 2 KiB page
+    pl = _cluster_plan(D, 0, 2, 2, page=8192)
+    rng = np.random.default_rng(0)
+    b = rng.standard_normal(n)
+    got = _cluster_emulate(D, pl, 2, 2, 0, b, np.zeros(n))
+    want = np.linalg.solve(np.tril(D.toarray()), b)
+    assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want))
