@@ -271,18 +271,23 @@ int mvamg_gs_row_sweep_f64(int mode, int n, const int* indptr, const int* indice
  * most 4) being its late tail; source = cta << 24 | slot of the value, or
  * bit 31 | row for an x_old value (modes 1, 3).  Query with blob == NULL
  * first (*npages, *nlev DAG levels, *slots_per_cta 8-byte x slots per CTA);
- * MVAMG_E_ARG when a row's record does not fit a page. */
-int mvamg_gs_cluster_plan(int n, const int* indptr, const int* indices, const double* data, int mode, int ncta,
-                          int wpc, int page_bytes, long long* npages, int* nlev, int* slots_per_cta,
+ * MVAMG_E_ARG when a row's record does not fit a page.
+ * grid != 0: the grid form -- the same workers on ncta ordinary CTAs (1 ..
+ * the SM count, all resident), early inputs and other CTAs' late inputs
+ * polled in x_new through L2, only a late input of the row's own CTA in
+ * shared memory; sources are then the input's row, or bit 30 | slot for such
+ * a local late input. */
+int mvamg_gs_cluster_plan(int n, const int* indptr, const int* indices, const double* data, int mode, int grid,
+                          int ncta, int wpc, int page_bytes, long long* npages, int* nlev, int* slots_per_cta,
                           int* local_late, int* wptr, int* wpage, int* rowid, int* perm, void* blob);
 /* One sweep (device pointers; a mode-2 plan with x_old runs the folded
  * backward sweep).  Shared memory per CTA: 8 * slots + 2 * wpc * (page_bytes +
  * 8).  sleep_ns: back-off of a warp whose poll found nothing new.  tperm: n
  * doubles of scratch; ws: >= 2 device ints (ticket, status). */
 int mvamg_gs_cluster_sweep_f64(int mode, int n, const int* indptr, const int* indices, const double* data,
-                               const int* wptr, const int* wpage, const void* blob, const int* perm, int ncta,
-                               int wpc, int slots, int page_bytes, int sleep_ns, double* tperm, const double* b,
-                               const double* x_old, double* x_new, int* ws, void* stream);
+                               const int* wptr, const int* wpage, const void* blob, const int* perm, int grid,
+                               int ncta, int wpc, int slots, int page_bytes, int sleep_ns, double* tperm,
+                               const double* b, const double* x_old, double* x_new, int* ws, void* stream);
 /* Pipelined sweep of one rank of a row-partitioned level (distributed.py;
  * SURVEY.md 8(e)): a row schedule of mode 0 / 2 built with row range
  * [row_lo, row_hi) = the own rows of the extended layout [lower ghosts | own |
@@ -433,7 +438,7 @@ int mvamg_hierarchy_set_gs_rows(mvamg_hierarchy* h, int k, int mode, const int* 
  * used before every other schedule of that mode; a mode-2 plan also serves
  * backward sweeps from x_old (folded). */
 int mvamg_hierarchy_set_gs_cluster(mvamg_hierarchy* h, int k, int mode, const int* wptr, const int* wpage,
-                                   const void* blob, const int* perm, int ncta, int wpc, int slots,
+                                   const void* blob, const int* perm, int grid, int ncta, int wpc, int slots,
                                    int page_bytes, int sleep_ns, double* tperm);
 /* Transfer k: P (n_k x n_{k+1}) and R = P^T (n_{k+1} x n_k), device CSR.
  * Levels k and k+1 must be set first (their sizes give P's and R's shapes):

@@ -59,11 +59,11 @@ SIGNATURES = [
     ("mvamg_ipc_close", _I, [_P]),
     ("mvamg_gs_row_sweep_f64", _I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P,
                                     _P, _P, _P, _P, _P]),
-    ("mvamg_gs_cluster_plan", _I, [_I, _P, _P, _P, _I, _I, _I, _I, ctypes.POINTER(_LL), _PI, _PI, _PI, _P, _P, _P,
-                                   _P, _P]),
-    ("mvamg_gs_cluster_sweep_f64", _I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P,
-                                        _P]),
-    ("mvamg_hierarchy_set_gs_cluster", _I, [_P, _I, _I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P]),
+    ("mvamg_gs_cluster_plan", _I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, ctypes.POINTER(_LL), _PI, _PI, _PI, _P, _P,
+                                   _P, _P, _P]),
+    ("mvamg_gs_cluster_sweep_f64", _I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P,
+                                        _P, _P]),
+    ("mvamg_hierarchy_set_gs_cluster", _I, [_P, _I, _I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     ("mvamg_gs_stream_plan", _I, [_I, _P, _P, _P, _I, _I, _I, ctypes.POINTER(_LL), _PI, _PI, _P, _P]),
     ("mvamg_gs_stream_sweep_f64", _I, [_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     ("mvamg_gs_stream_sweep_folded_f64", _I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),

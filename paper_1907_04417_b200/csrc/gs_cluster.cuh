@@ -23,8 +23,8 @@
 // One row at a time per warp, lanes = entries.  The plan orders a row's
 // entries by the DAG level at which their inputs become final and splits off
 // the last (up to) kClusterLate of them:
-//   early entries   one per lane (chunks of 32): polled once, usually landed;
-//                   lane-local FMAs, then a fixed xor-shuffle tree;
+//   early entries   one per lane (two chunks of 32 in flight): polled once,
+//                   usually landed; lane-local FMAs, then a fixed xor-shuffle tree;
 //   late entries    (the last level's inputs, at most kClusterLate, the critical
 //                   one last) polled by lane 0 alone in a tight loop -- ld.shared
 //                   when the input lives in this CTA, as the plan mostly arranges
@@ -42,6 +42,17 @@
 // LDS away when its turn comes, never a global-memory round trip.  The right-
 // hand sides (written per sweep by gs_prepare_kernel in the same q order) are
 // read 32 rows at a time, one per lane, and handed out by shuffle.
+//
+// Grid form (GRID = true; levels too large or too wide for one cluster): the
+// same workers on ordinary CTAs, one per SM over the whole GPU.  Only the
+// critical chain stays in shared memory -- a late input owned by the row's own
+// CTA is still an ld.shared poll -- while early inputs (a level or more old,
+// so latency-tolerant) and the few late inputs of other CTAs are polled in
+// x_new through L2 like gs_row_kernel's (gs_prepare_kernel fills it with the
+// sentinel).  That removes the cluster's limits -- 16 SMs, and their DSMEM
+// request rate (~0.3 remote loads per cycle and SM, which bounds the cluster
+// form from ~15k rows up) -- at the price of an L2 round trip per early chunk.
+// All CTAs must be resident (grid <= SMs), as for gs_row_kernel.
 //
 // Rounding: fixed per plan (tree + ordered tail), so results are reproducible
 // run to run, but not the serial loop's CSR-order roundings: this kernel
@@ -67,7 +78,8 @@ struct GsClusterArgs {
   int page_bytes;        // bytes per page (multiple of 128)
   const int* wptr;       // worker -> first q (NC * wpc + 1)
   const int* wpage;      // worker -> first page (NC * wpc + 1)
-  const unsigned char* blob;  // pages
+  const unsigned char* blob;  // pages; sources: cluster form cta << 24 | slot; grid form the row (late entries: bit
+                         // 30 | slot when the row's own CTA owns the input); bit 31 | row: an x_old value
   const double* tperm;   // q -> right-hand side (folded for backward sweeps from x_old)
   const double* xold;
   double* xnew;
@@ -102,13 +114,13 @@ __device__ __forceinline__ unsigned long long ld_cluster_u64(unsigned caddr) {
   return v;
 }
 
-template <bool OLD>
+template <bool OLD, bool GRID>
 __global__ void __launch_bounds__(1024, 1) gs_cluster_kernel(GsClusterArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int NB = kClusterRing;
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned NC = cluster_nctas(), cr = cluster_rank();
+  const unsigned NC = GRID ? gridDim.x : cluster_nctas(), cr = GRID ? blockIdx.x : cluster_rank();
   unsigned long long* xs = reinterpret_cast<unsigned long long*>(smem_raw);
   const unsigned xbase = (unsigned)__cvta_generic_to_shared(xs);
   const unsigned xbytes = ((unsigned)a.slots * 8u + 127u) & ~127u;
@@ -120,7 +132,8 @@ __global__ void __launch_bounds__(1024, 1) gs_cluster_kernel(GsClusterArgs a) {
     for (int b = 0; b < NB; ++b) mbar_init(bars + 8u * b, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  cluster_sync();  // every slice holds the sentinel before any remote poll
+  if (GRID) __syncthreads();  // the slice is only ever read by this CTA
+  else cluster_sync();        // every slice holds the sentinel before any remote poll
   const int g = warp * (int)NC + (int)cr;
   bool abort = false;
   // a poll that has failed kGsIdleLimit times (or another warp's) ends the sweep with ST_GS_TIMEOUT
@@ -165,31 +178,40 @@ __global__ void __launch_bounds__(1024, 1) gs_cluster_kernel(GsClusterArgs a) {
         rn = qb + 32 + lane < q1 ? __ldg(a.tperm + qb + 32 + lane) : 0.0;
       }
       const double rhs = __shfl_sync(FULL, rr, q - qb);
-      // ---- early entries: one per lane, 32 at a time ----------------------------
+      // ---- early entries: one per lane, two chunks of 32 in flight together -----------
       double sum = 0.0;
       long long spins = 0;
-      for (int base = 0; base < ne; base += 32) {
-        const int idx = base + lane;
-        double cf = 0.0;
-        unsigned long long v = 0ull;
-        unsigned ad = xbase;
-        if (idx < ne) {
-          cf = lds_f64(cbase + 8u * (unsigned)idx);
-          const unsigned sc = lds_u32(sbase + 4u * (unsigned)idx);
-          if (OLD && (sc >> 31)) {
-            v = (unsigned long long)__double_as_longlong(__ldg(a.xold + (sc & 0x7fffffffu)));
-          } else {
-            v = kSentinel;
-            ad = map_rank(xbase + 8u * (sc & 0xffffffu), (sc >> 24) & 15u);
+      for (int base = 0; base < ne; base += 64) {
+        double cf[2];
+        unsigned long long v[2];
+        unsigned ad[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int idx = base + 32 * c + lane;
+          cf[c] = 0.0;
+          v[c] = 0ull;
+          ad[c] = xbase;
+          if (idx < ne) {
+            cf[c] = lds_f64(cbase + 8u * (unsigned)idx);
+            const unsigned sc = lds_u32(sbase + 4u * (unsigned)idx);
+            if (OLD && (sc >> 31)) {
+              v[c] = (unsigned long long)__double_as_longlong(__ldg(a.xold + (sc & 0x7fffffffu)));
+            } else {
+              v[c] = kSentinel;
+              ad[c] = GRID ? (sc & 0x3fffffffu) : map_rank(xbase + 8u * (sc & 0xffffffu), (sc >> 24) & 15u);
+            }
           }
         }
         for (;;) {
-          if (!gs_published(v)) v = ld_cluster_u64(ad);
-          if (!__any_sync(FULL, !gs_published(v))) break;
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            if (!gs_published(v[c])) v[c] = GRID ? ld_relaxed_u64(a.xnew + ad[c]) : ld_cluster_u64(ad[c]);
+          if (!__any_sync(FULL, !gs_published(v[0]) || !gs_published(v[1]))) break;
           if (a.sleep_ns > 0) __nanosleep((unsigned)a.sleep_ns);
           if (__any_sync(FULL, timed_out(spins))) { abort = true; break; }
         }
-        sum = fma(cf, __longlong_as_double((long long)v), sum);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) sum = fma(cf[c], __longlong_as_double((long long)v[c]), sum);
       }
       if (a.trace && lane == 0) a.trace[2 * (size_t)a.n + q] = clock64();
 #pragma unroll
@@ -203,9 +225,13 @@ __global__ void __launch_bounds__(1024, 1) gs_cluster_kernel(GsClusterArgs a) {
           unsigned long long v;
           if (OLD && (sc >> 31)) {
             v = (unsigned long long)__double_as_longlong(__ldg(a.xold + (sc & 0x7fffffffu)));
-          } else if (((sc >> 24) & 15u) == cr) {  // the usual case: the input lives in this CTA
+          } else if (GRID ? (sc >> 30) != 0u : ((sc >> 24) & 15u) == cr) {  // the usual case: this CTA's input
             const unsigned ad = xbase + 8u * (sc & 0xffffffu);
             while (!gs_published(v = ld_shared_volatile_u64(ad)))
+              if (timed_out(spins)) { abort = true; break; }
+          } else if (GRID) {
+            const double* ad = a.xnew + (sc & 0x3fffffffu);
+            while (!gs_published(v = ld_relaxed_u64(ad)))
               if (timed_out(spins)) { abort = true; break; }
           } else {
             const unsigned ad = map_rank(xbase + 8u * (sc & 0xffffffu), (sc >> 24) & 15u);
@@ -217,7 +243,8 @@ __global__ void __launch_bounds__(1024, 1) gs_cluster_kernel(GsClusterArgs a) {
         if (!abort) {
           const double xi = div_rn_markstein(s, dg, rdg);
           st_shared_f64(xbase + 8u * (unsigned)slot, xi);
-          a.xnew[row] = xi;
+          if (GRID) st_relaxed_f64(a.xnew + row, xi);  // polled by other CTAs
+          else a.xnew[row] = xi;
           if (a.trace) a.trace[(size_t)a.n + q] = clock64();
         }
       }
@@ -228,7 +255,7 @@ __global__ void __launch_bounds__(1024, 1) gs_cluster_kernel(GsClusterArgs a) {
     __syncwarp();
     if (lane == 0 && pg + NB < pg1) fetch(pg + NB, b);
   }
-  cluster_sync();  // no CTA leaves while a peer may still poll its slice
+  if (!GRID) cluster_sync();  // no CTA leaves while a peer may still poll its slice
 }
 
 }  // namespace mvamg

@@ -201,7 +201,7 @@ struct GsRows {
 // Cluster dataflow schedule (gs_cluster_kernel) of one sweep mode
 // (mvamg_gs_cluster_plan).
 struct GsCluster {
-  int mode = 0, ncta = 0, wpc = 0, slots = 0, page_bytes = 0, sleep_ns = 0;
+  int mode = 0, ncta = 0, wpc = 0, slots = 0, page_bytes = 0, sleep_ns = 0, grid = 0;
   const int* wptr = nullptr;
   const int* wpage = nullptr;
   const unsigned char* blob = nullptr;
@@ -672,7 +672,8 @@ int launch_gs_cluster(const Csr& A, const GsCluster& g, const double* b, const d
   if (n == 0) return 0;
   if (!g.blob) return fail(MVAMG_E_STATE, "gs cluster: plan for this sweep mode was not set");
   set_kernel_attrs();
-  if (g.ncta < 1 || g.ncta > 16 || (g.ncta & (g.ncta - 1))) return fail(MVAMG_E_ARG, "gs cluster: 1, 2, 4, 8 or 16 CTAs");
+  if (g.grid ? (g.ncta < 1 || g.ncta > num_sms()) : (g.ncta < 1 || g.ncta > 16 || (g.ncta & (g.ncta - 1))))
+    return fail(MVAMG_E_ARG, "gs cluster: 1, 2, 4, 8 or 16 CTAs (grid form: 1 .. the number of SMs)");
   if (g.wpc < 1 || g.wpc > 32) return fail(MVAMG_E_ARG, "gs cluster: 1..32 worker warps per CTA");
   bool fold = false;
   if (xold) {
@@ -686,10 +687,12 @@ int launch_gs_cluster(const Csr& A, const GsCluster& g, const double* b, const d
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncSetAttribute(gs_cluster_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
-    cudaFuncSetAttribute(gs_cluster_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
-    cudaFuncSetAttribute(gs_cluster_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(gs_cluster_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(gs_cluster_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+    cudaFuncSetAttribute(gs_cluster_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+    cudaFuncSetAttribute(gs_cluster_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+    cudaFuncSetAttribute(gs_cluster_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+    cudaFuncSetAttribute(gs_cluster_kernel<false, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(gs_cluster_kernel<true, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaGetLastError();
   }
   if (g.page_bytes < 128 || g.page_bytes % 128) return fail(MVAMG_E_ARG, "gs cluster: pages of a multiple of 128 bytes");
@@ -724,8 +727,14 @@ int launch_gs_cluster(const Csr& A, const GsCluster& g, const double* b, const d
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (g.mode == 1 || g.mode == 3) CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_cluster_kernel<true>, a));
-  else CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_cluster_kernel<false>, a));
+  if (g.grid) {  // ordinary CTAs, all resident; x_new (sentinel-filled by the prepare kernel) carries the early inputs
+    if (g.mode == 1 || g.mode == 3) gs_cluster_kernel<true, true><<<g.ncta, g.wpc * 32, smem, s>>>(a);
+    else gs_cluster_kernel<false, true><<<g.ncta, g.wpc * 32, smem, s>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+  if (g.mode == 1 || g.mode == 3) CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_cluster_kernel<true, false>, a));
+  else CUDA_TRY(cudaLaunchKernelEx(&cfg, gs_cluster_kernel<false, false>, a));
   return 0;
 }
 
@@ -2493,13 +2502,14 @@ int mvamg_hierarchy_set_gs_rows(mvamg_hierarchy* h, int k, int mode, const int* 
   return 0;
 }
 
-int mvamg_gs_cluster_plan(int n, const int* indptr, const int* indices, const double* data, int mode, int ncta,
-                          int wpc, int page_bytes, long long* npages, int* nlev, int* slots_per_cta,
+int mvamg_gs_cluster_plan(int n, const int* indptr, const int* indices, const double* data, int mode, int grid,
+                          int ncta, int wpc, int page_bytes, long long* npages, int* nlev, int* slots_per_cta,
                           int* local_late, int* wptr, int* wpage, int* rowid, int* perm, void* blob) {
   if (n < 0 || !indptr || !npages || !nlev || !slots_per_cta || mode < 0 || mode > 3)
     return fail(MVAMG_E_ARG, "gs_cluster_plan: bad arguments");
-  if (ncta < 1 || ncta > 16 || (ncta & (ncta - 1)) || wpc < 1 || wpc > 32)
-    return fail(MVAMG_E_ARG, "gs_cluster_plan: ncta in {1,2,4,8,16}, wpc in 1..32");
+  if (wpc < 1 || wpc > 32 || ncta < 1 || (grid ? ncta > 1024 : (ncta > 16 || (ncta & (ncta - 1)))))
+    return fail(MVAMG_E_ARG, "gs_cluster_plan: ncta in {1,2,4,8,16} (grid form: 1..1024), wpc in 1..32");
+  if (grid && n >= (1 << 30)) return fail(MVAMG_E_ARG, "gs_cluster_plan: too many rows");
   if (page_bytes < 128 || page_bytes % 128) return fail(MVAMG_E_ARG, "gs_cluster_plan: pages of a multiple of 128 bytes");
   const bool fwd = mode < 2, zero = (mode % 2) == 0;
   const int G = ncta * wpc;
@@ -2643,7 +2653,9 @@ int mvamg_gs_cluster_plan(int n, const int* indptr, const int* indices, const do
         const int k = ents[u], j = indices[k];
         const bool isnew = fwd ? j < i : j > i;
         cf[u] = data[k];
-        sc[u] = isnew ? (((unsigned)cta[j] << 24) | (unsigned)sl[j]) : (0x80000000u | (unsigned)j);
+        if (!isnew) sc[u] = 0x80000000u | (unsigned)j;
+        else if (!grid) sc[u] = ((unsigned)cta[j] << 24) | (unsigned)sl[j];
+        else sc[u] = (u >= cnt - late && cta[j] == cta[i]) ? (0x40000000u | (unsigned)sl[j]) : (unsigned)j;
       }
       used += rb;
       ++rows_in_page;
@@ -2654,25 +2666,27 @@ int mvamg_gs_cluster_plan(int n, const int* indptr, const int* indices, const do
 }
 
 int mvamg_gs_cluster_sweep_f64(int mode, int n, const int* indptr, const int* indices, const double* data,
-                               const int* wptr, const int* wpage, const void* blob, const int* perm, int ncta,
-                               int wpc, int slots, int page_bytes, int sleep_ns, double* tperm, const double* b,
-                               const double* x_old, double* x_new, int* ws, void* stream) {
+                               const int* wptr, const int* wpage, const void* blob, const int* perm, int grid,
+                               int ncta, int wpc, int slots, int page_bytes, int sleep_ns, double* tperm,
+                               const double* b, const double* x_old, double* x_new, int* ws, void* stream) {
   if (mode < 0 || mode > 3) return fail(MVAMG_E_ARG, "gs cluster: bad mode");
   if (x_old != nullptr && x_old == x_new) return fail(MVAMG_E_ARG, "gs cluster: x_new must not alias x_old");
   Csr A;
   A.n = n; A.ip = indptr; A.ix = indices; A.v = data;
   GsCluster g;
   g.mode = mode; g.ncta = ncta; g.wpc = wpc; g.slots = slots; g.page_bytes = page_bytes; g.sleep_ns = sleep_ns;
+  g.grid = grid;
   g.wptr = wptr; g.wpage = wpage; g.blob = static_cast<const unsigned char*>(blob); g.perm = perm; g.tperm = tperm;
   return launch_gs_cluster(A, g, b, x_old, x_new, ws, ws + 1, (cudaStream_t)stream);
 }
 
 int mvamg_hierarchy_set_gs_cluster(mvamg_hierarchy* h, int k, int mode, const int* wptr, const int* wpage,
-                                   const void* blob, const int* perm, int ncta, int wpc, int slots,
+                                   const void* blob, const int* perm, int grid, int ncta, int wpc, int slots,
                                    int page_bytes, int sleep_ns, double* tperm) {
   if (!h || k < 0 || k >= h->L || mode < 0 || mode > 3) return fail(MVAMG_E_ARG, "set_gs_cluster: bad index");
   GsCluster& g = h->lv[k].gcl[mode];
   g.mode = mode; g.ncta = ncta; g.wpc = wpc; g.slots = slots; g.page_bytes = page_bytes; g.sleep_ns = sleep_ns;
+  g.grid = grid;
   g.wptr = wptr; g.wpage = wpage; g.blob = static_cast<const unsigned char*>(blob); g.perm = perm; g.tperm = tperm;
   return 0;
 }

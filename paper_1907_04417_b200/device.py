@@ -108,8 +108,11 @@ class GpuConfig:
                                     # at <= 1.8k rows, equal at 5k)
     cluster_gs: bool = True         # (tolerance parity) coarse levels whose x fits one thread-block cluster's
                                     # shared memory: the cluster dataflow sweep (gs_cluster.cuh), before any other
-    cluster_max_rows: int = 60000   # ... up to this size (C3: 1.2x the row sweep at 53k rows, 2.3-4x at <= 16k;
-                                    # slower at 160k, where one cluster's 16 SMs cannot keep up)
+    cluster_max_rows: int = 4000000  # ... up to this size (what decides is whether a CTA's x slice and page rings
+                                    # fit its shared memory)
+    cluster_grid_rows: int = 10000  # above: the grid form (ordinary CTAs over the whole GPU, early inputs through L2;
+                                    # C3: 2-3x the row sweep at 53k and 160k rows, level with the cluster form at 16k)
+    cluster_grid_ctas: int = 0      # CTAs of the grid form (0: one per SM)
     cluster_min_warps: int = 8      # worker warps per CTA, at least
     cluster_max_warps: int = 32     # ... and at most
     cluster_page_bytes: int = 2048  # page of row records a worker warp streams per TMA bulk copy (doubled while
@@ -660,18 +663,35 @@ class DeviceGsStream:
                                                ptr(x_old), ptr(x_new), s), "gs_stream_sweep")
 
 
-def cluster_shape(n, nlev, cfg=None):
-    """(ncta, wpc) of the cluster dataflow sweep of a level with n rows.  One
-    warp sweeps one row at a time (~1,200 cycles each), so the sweep wants many
-    worker warps -- measured on C3's levels (tools/cluster_bench.py): 16 CTAs
-    from ~1k rows up, 8 to 32 warps each, about 15 rows per warp."""
+def cluster_shape(n, nlev, cfg=None, grid=None):
+    """(grid, ncta, wpc) of the cluster dataflow sweep of a level with n rows.
+    One warp sweeps one row at a time (~1,200 cycles each), so the sweep wants
+    many worker warps -- measured on C3's levels (tools/cluster_bench.py).
+    Cluster form (x in distributed shared memory) up to cfg.cluster_grid_rows
+    rows: 16 CTAs from ~1k rows up, 8 to 32 warps each, about 15 rows per warp.
+    Above, the grid form: one CTA per SM, early inputs through L2."""
     cfg = cfg or GpuConfig()
     if n < 1:
         return None
-    ncta = 16 if n >= 1000 else (8 if n >= 300 else 4)
-    ncta = max(1, min(ncta, cfg.max_cluster))
+    if grid is None:
+        grid = n > cfg.cluster_grid_rows
+    if grid:
+        ncta = max(1, min(cfg.cluster_grid_ctas or _num_sms(), -(-n // 256)))
+    else:
+        ncta = 16 if n >= 1000 else (8 if n >= 300 else 4)
+        ncta = max(1, min(ncta, cfg.max_cluster))
     wpc = int(min(cfg.cluster_max_warps, max(cfg.cluster_min_warps, -(-n // (15 * ncta)))))
-    return ncta, wpc
+    return bool(grid), ncta, wpc
+
+
+_NUM_SMS = None
+
+
+def _num_sms():
+    global _NUM_SMS
+    if _NUM_SMS is None:
+        _NUM_SMS = torch_cuda().cuda.get_device_properties(0).multi_processor_count
+    return _NUM_SMS
 
 
 def cluster_smem(slots, wpc, page_bytes):
@@ -684,7 +704,7 @@ class DeviceGsCluster:
     matrix and sweep mode (0 fwd from x=0, 1 fwd, 2 bwd from x=0 -- also the
     folded backward sweep from x_old --, 3 bwd), on the device."""
 
-    def __init__(self, A, mode, cfg=None, ncta=None, wpc=None, sleep_ns=None):
+    def __init__(self, A, mode, cfg=None, ncta=None, wpc=None, sleep_ns=None, grid=None):
         import torch
 
         cfg = cfg or GpuConfig()
@@ -699,7 +719,7 @@ class DeviceGsCluster:
         page = int(cfg.cluster_page_bytes)
 
         def plan(c, w, *out):
-            return L.mvamg_gs_cluster_plan(n, vp(ip), vp(ix), vp(v), int(mode), int(c), int(w), page,
+            return L.mvamg_gs_cluster_plan(n, vp(ip), vp(ix), vp(v), int(mode), int(bool(grid)), int(c), int(w), page,
                                            ctypes.byref(npg), ctypes.byref(nlev), ctypes.byref(slots),
                                            ctypes.byref(hits), *out)
 
@@ -708,14 +728,17 @@ class DeviceGsCluster:
             if page > 16384:
                 raise ValueError("gs cluster: a row's record exceeds the largest page")
         if ncta is None or wpc is None:
-            shape = cluster_shape(n, nlev.value, cfg)
+            shape = cluster_shape(n, nlev.value, cfg, grid)
             if shape is None:
                 raise ValueError("gs cluster: the level's x does not fit one thread-block cluster")
-            ncta, wpc = (ncta or shape[0]), (wpc or shape[1])
+            grid, ncta, wpc = shape[0], (ncta or shape[1]), (wpc or shape[2])
+        grid = bool(grid)
         _lib.check(plan(ncta, wpc, *([None] * 5)), "gs_cluster_plan")
         # worker warps per CTA: as many as leave room for their page rings beside the x slice
+        # (the slice depends on wpc only through the plan's balance slack: re-plan and re-check)
         while wpc > 1 and cluster_smem(slots.value, wpc, page) > cfg.smem_limit:
-            wpc -= 1
+            room = cfg.smem_limit - ((slots.value * 8 + 127) & ~127)
+            wpc = max(1, min(wpc - 1, room // (2 * (page + 8))))
             _lib.check(plan(ncta, wpc, *([None] * 5)), "gs_cluster_plan")
         if cluster_smem(slots.value, wpc, page) > cfg.smem_limit:
             raise ValueError("gs cluster: x slice and page rings exceed shared memory")
@@ -727,6 +750,7 @@ class DeviceGsCluster:
         _lib.check(plan(ncta, wpc, vp(wptr), vp(wpage), vp(rowid), vp(perm), vp(blob)), "gs_cluster_plan")
         self.n, self.mode, self.nlev, self.npages, self.page_bytes = n, mode, nlev.value, npg.value, page
         self.ncta, self.wpc, self.slots, self.local_late = int(ncta), int(wpc), slots.value, hits.value
+        self.grid = grid
         self.sleep_ns = int(cfg.cluster_sleep_ns if sleep_ns is None else sleep_ns)
         self.wptr, self.wpage, self.blob = to_device(wptr), to_device(wpage), to_device(blob)
         self.rowid, self.perm = to_device(rowid), to_device(perm)
@@ -734,8 +758,8 @@ class DeviceGsCluster:
         self._csr = DeviceCSR(A)
 
     def args(self):
-        return (ptr(self.wptr), ptr(self.wpage), ptr(self.blob), ptr(self.perm), self.ncta, self.wpc, self.slots,
-                self.page_bytes, self.sleep_ns, ptr(self.tperm))
+        return (ptr(self.wptr), ptr(self.wpage), ptr(self.blob), ptr(self.perm), int(self.grid), self.ncta, self.wpc,
+                self.slots, self.page_bytes, self.sleep_ns, ptr(self.tperm))
 
     def sweep(self, b, x_old, x_new, ws, stream=None):
         """One sweep; with x_old a mode-2 plan runs the folded backward sweep."""

@@ -369,13 +369,15 @@ def _gs_cluster_gpu(A, b, x_old, direction, zero, config, fold=False, **shape):
 
 
 @pytest.mark.parametrize("shape", [dict(), dict(ncta=1, wpc=1), dict(ncta=2, wpc=3), dict(ncta=8, wpc=32),
-                                   dict(ncta=16, wpc=8)])
+                                   dict(ncta=16, wpc=8), dict(grid=True), dict(grid=True, ncta=1, wpc=2),
+                                   dict(grid=True, ncta=148, wpc=32), dict(grid=True, ncta=37, wpc=5)])
 def test_gs_cluster_kernel(mv, c1, shape):
     """The cluster dataflow sweep (gs_cluster.cuh: x in a thread-block cluster's
     distributed shared memory, one warp per row, TMA-streamed row records) in
     all four modes and folded, on every structure and the C1 levels: the serial
     sweep's row order (_kernels.py:15-38), each row sum in a fixed tree, so
-    within rounding of the serial loop and identical run to run."""
+    within rounding of the serial loop and identical run to run.  grid: the
+    grid form (ordinary CTAs over the GPU, early inputs through L2)."""
     config = mv.GpuConfig()
     rng = np.random.default_rng(15)
     mats = c1[1]
@@ -409,8 +411,9 @@ def test_gs_cluster_long_rows_and_pages(mv):
             for zero in (True, False):
                 want = np.zeros(A.shape[0]) if zero else x0.copy()
                 oracle_gs(A, b, want, direction)
-                got = _gs_cluster_gpu(A, b, x0, direction, zero, mv.GpuConfig(), ncta=4, wpc=4)
-                assert rel(got, want) <= 1e-13, (name, direction, zero)
+                for shape in (dict(ncta=4, wpc=4), dict(grid=True, ncta=20, wpc=4)):
+                    got = _gs_cluster_gpu(A, b, x0, direction, zero, mv.GpuConfig(), **shape)
+                    assert rel(got, want) <= 1e-13, (name, direction, zero, shape)
 
 
 def test_vcycle_cluster_sweeps(mv, c1):

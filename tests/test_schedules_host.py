@@ -140,7 +140,7 @@ def test_row_schedule_over_a_row_range():
 
 
 # ---- cluster dataflow plan (mvamg_gs_cluster_plan, gs_cluster.cuh) -------------------------------
-def _cluster_plan(A, mode, ncta, wpc, page=2048):
+def _cluster_plan(A, mode, ncta, wpc, page=2048, grid=0):
     A = sp.csr_matrix(A)
     n = A.shape[0]
     L = _lib.load()
@@ -148,8 +148,8 @@ def _cluster_plan(A, mode, ncta, wpc, page=2048):
     ix = np.ascontiguousarray(A.indices, dtype=np.int32)
     v = np.ascontiguousarray(A.data, dtype=np.float64)
     npg, nl, sl, hits = ctypes.c_longlong(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
-    head = (n, vp(ip), vp(ix), vp(v), mode, ncta, wpc, page, ctypes.byref(npg), ctypes.byref(nl), ctypes.byref(sl),
-            ctypes.byref(hits))
+    head = (n, vp(ip), vp(ix), vp(v), mode, grid, ncta, wpc, page, ctypes.byref(npg), ctypes.byref(nl),
+            ctypes.byref(sl), ctypes.byref(hits))
     _lib.check(L.mvamg_gs_cluster_plan(*head, None, None, None, None, None), "plan")
     G = ncta * wpc
     wptr, wpage = np.empty(G + 1, dtype=np.int32), np.empty(G + 1, dtype=np.int32)
@@ -157,7 +157,7 @@ def _cluster_plan(A, mode, ncta, wpc, page=2048):
     blob = np.zeros(max(1, npg.value) * page, dtype=np.uint8)
     _lib.check(L.mvamg_gs_cluster_plan(*head, vp(wptr), vp(wpage), vp(rowid), vp(perm), vp(blob)), "plan")
     return dict(wptr=wptr, wpage=wpage, rowid=rowid, perm=perm, blob=blob, nlev=nl.value, slots=sl.value,
-                local=hits.value, page=page, npages=npg.value)
+                local=hits.value, page=page, npages=npg.value, grid=grid)
 
 
 def _cluster_streams(pl, G):
@@ -195,6 +195,8 @@ def _cluster_emulate(A, pl, ncta, wpc, mode, b, x_old):
     G = ncta * wpc
     streams = _cluster_streams(pl, G)
     xs = np.full((ncta, pl["slots"]), np.nan)
+    xg = np.full(n, np.nan)                                          # x_new in global memory (grid form)
+    grid = pl["grid"]
     cur = [0] * G
     x = np.zeros(n)
     left = n
@@ -207,12 +209,21 @@ def _cluster_emulate(A, pl, ncta, wpc, mode, b, x_old):
             vals = np.empty(cnt)
             for u in range(cnt):
                 s = int(sc[u])
-                vals[u] = x_old[s & 0x7fffffff] if s >> 31 else xs[(s >> 24) & 15, s & 0xffffff]
+                if s >> 31:
+                    vals[u] = x_old[s & 0x7fffffff]
+                elif not grid:
+                    vals[u] = xs[(s >> 24) & 15, s & 0xffffff]
+                elif s >> 30:                                        # a late input this CTA owns: its shared slot
+                    assert u >= ne
+                    vals[u] = xs[g % ncta, s & 0xffffff]
+                else:
+                    vals[u] = xg[s]
             if np.isnan(vals).any():
                 continue
             xi = (b[row] - np.dot(cf, vals)) / dg
             assert np.isnan(xs[g % ncta, slot])                     # every slot is written once
             xs[g % ncta, slot] = xi
+            xg[row] = xi
             x[row] = xi
             cur[g] += 1
             left -= 1
@@ -221,8 +232,9 @@ def _cluster_emulate(A, pl, ncta, wpc, mode, b, x_old):
     return x
 
 
-@pytest.mark.parametrize("ncta,wpc", [(1, 1), (2, 3), (4, 8), (16, 32)])
-def test_cluster_plan_is_the_serial_sweep(ncta, wpc):
+@pytest.mark.parametrize("ncta,wpc,grid", [(1, 1, 0), (2, 3, 0), (4, 8, 0), (16, 32, 0), (1, 2, 1), (37, 5, 1),
+                                           (148, 8, 1)])
+def test_cluster_plan_is_the_serial_sweep(ncta, wpc, grid):
     rng = np.random.default_rng(5)
     cases = [laplacian_1d(70), laplacian_2d(13), random_spd_csr(300, density=0.05, seed=1),
              random_spd_csr(90, density=0.9, seed=2), sp.diags(np.linspace(1, 2, 9)).tocsr(),
@@ -233,7 +245,7 @@ def test_cluster_plan_is_the_serial_sweep(ncta, wpc):
         d = A.diagonal()
         b, x0 = rng.standard_normal(n), rng.standard_normal(n)
         for mode in range(4):
-            pl = _cluster_plan(A, mode, ncta, wpc)
+            pl = _cluster_plan(A, mode, ncta, wpc, grid=grid)
             x_old = np.zeros(n) if mode % 2 == 0 else x0
             got = _cluster_emulate(A, pl, ncta, wpc, mode, b, x_old)
             want = x_old.copy()                                     # the serial loop, _kernels.py:15-38
@@ -268,7 +280,7 @@ def test_cluster_plan_long_rows_need_larger_pages():
     ip, ix = np.ascontiguousarray(D.indptr, dtype=np.int32), np.ascontiguousarray(D.indices, dtype=np.int32)
     v = np.ascontiguousarray(D.data)
     npg, nl, sl, hits = ctypes.c_longlong(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
-    rc = L.mvamg_gs_cluster_plan(n, vp(ip), vp(ix), vp(v), 0, 2, 2, 2048, ctypes.byref(npg), ctypes.byref(nl),
+    rc = L.mvamg_gs_cluster_plan(n, vp(ip), vp(ix), vp(v), 0, 0, 2, 2, 2048, ctypes.byref(npg), ctypes.byref(nl),
                                  ctypes.byref(sl), ctypes.byref(hits), None, None, None, None, None)
     assert rc == _lib.E_ARG                                        # 399 entries: 4,832 bytes > one 2 KiB page
     pl = _cluster_plan(D, 0, 2, 2, page=8192)

@@ -1,12 +1,11 @@
-# cluster sweep: unit tests, whole GPU suite, C3 bench (the reference arm first so both arms share the hierarchy)
+# cluster / grid sweeps: whole GPU suite, C3 bench
 set -x
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "cluster" 2>&1 | tail -5 | tee gpurun_out/r2g_cluster_tests.log
-timeout 2400 python -m pytest tests -q -m gpu 2>&1 | tail -8 | tee gpurun_out/r2g_gpu_tests.log
-timeout 1800 python bench.py --steps 20 --warmup 5 > gpurun_out/r2g_b200_c3.json 2> gpurun_out/r2g_b200_c3.err
+timeout 2400 python -m pytest tests -q -m gpu 2>&1 | tail -8 | tee gpurun_out/r2j_gpu_tests.log
+timeout 1800 python bench.py --steps 20 --warmup 5 > gpurun_out/r2j_b200_c3.json 2> gpurun_out/r2j_b200_c3.err
 python -c "
-import json; d=json.loads(open('gpurun_out/r2g_b200_c3.json').read().strip().splitlines()[-1])
+import json; d=json.loads(open('gpurun_out/r2j_b200_c3.json').read().strip().splitlines()[-1])
 print('value', d['value'], 'e2e', d['e2e']['value'], 'cycle', d['cycle'], 'nit', d['details']['nit'], d['details'].get('history_rel_max_vs_oracle'))
 print('roofline', d['roofline']); print('h2', d.get('h2'))
 for s in d['sweeps']: print(s['level'], s['kernel'], s['sweep'][:8], round(s['ms']*1e3,1), 'us')
 "
-tail -3 gpurun_out/r2g_b200_c3.err
+tail -3 gpurun_out/r2j_b200_c3.err

@@ -66,16 +66,17 @@ def main():
             shapes = [None]
             sleeps = [cfg.cluster_sleep_ns]
             if grid:
-                shapes = [(c, w) for c in (4, 8, 16) for w in (8, 16, 24, 32)]
+                shapes = ([(False, c, w) for c in (16,) for w in (16, 32)] +
+                          [(True, c, w) for c in (74, 148) for w in (8, 16, 32)])
                 sleeps = [0]
             best = None
             for shape in shapes:
                 try:
                     cl = (DeviceGsCluster(M, mode, cfg) if shape is None else
-                          DeviceGsCluster(M, mode, cfg, ncta=shape[0], wpc=shape[1]))
+                          DeviceGsCluster(M, mode, cfg, grid=shape[0], ncta=shape[1], wpc=shape[2]))
                 except ValueError:
                     continue
-                shape = (cl.ncta, cl.wpc, 0)
+                shape = (cl.ncta, cl.wpc, int(cl.grid))
                 for sl in sleeps:
                     cl.sleep_ns = sl
                     xn.fill_(0.0)
@@ -91,7 +92,7 @@ def main():
                     t = timed(lambda: cl.sweep(b, xold, xn, ws))
                     if best is None or t < best[0]:
                         best = (t, shape, sl)
-                    print(f"   cluster {shape[0]:2d} x {shape[1]:2d} warps nbuf {shape[2]} sleep {sl:3d}: {t:7.1f} us "
+                    print(f"   cluster {shape[0]:2d} x {shape[1]:2d} warps grid {shape[2]} sleep {sl:3d}: {t:7.1f} us "
                           f"({t * 1e3 / cl.nlev:.0f} ns/level) rel err vs serial {err:.1e} vs row sweep {dr:.1e}",
                           flush=True)
                 del cl
