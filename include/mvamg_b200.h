@@ -276,7 +276,8 @@ int mvamg_gs_row_sweep_f64(int mode, int n, const int* indptr, const int* indice
  * the SM count, all resident), early inputs and other CTAs' late inputs
  * polled in x_new through L2, only a late input of the row's own CTA in
  * shared memory; sources are then the input's row, or bit 30 | slot for such
- * a local late input. */
+ * a local late input, and only rows polled that way get an x slot (slot -1
+ * otherwise). */
 int mvamg_gs_cluster_plan(int n, const int* indptr, const int* indices, const double* data, int mode, int grid,
                           int ncta, int wpc, int page_bytes, long long* npages, int* nlev, int* slots_per_cta,
                           int* local_late, int* wptr, int* wpage, int* rowid, int* perm, void* blob);

@@ -63,7 +63,7 @@
 
 namespace mvamg {
 
-constexpr int kClusterLate = 2;    // late entries per row (lane 0)
+constexpr int kClusterLate = 4;    // late entries per row (lane 0)
 constexpr int kClusterRing = 2;    // pages in flight per worker warp
 constexpr int kClusterRowHdr = 32; // bytes: int cnt, ne, row, slot; double dg, rdg
 constexpr int kClusterPageHdr = 16; // bytes: int nrows, pad
@@ -198,14 +198,23 @@ __global__ void __launch_bounds__(1024, 1) gs_cluster_kernel(GsClusterArgs a) {
               v[c] = (unsigned long long)__double_as_longlong(__ldg(a.xold + (sc & 0x7fffffffu)));
             } else {
               v[c] = kSentinel;
-              ad[c] = GRID ? (sc & 0x3fffffffu) : map_rank(xbase + 8u * (sc & 0xffffffu), (sc >> 24) & 15u);
+              if (GRID) {
+                ad[c] = sc & 0x3fffffffu;
+              } else {  // bit 0 of the address: a slot of this CTA (ld.shared instead of the cluster load)
+                const unsigned ct = (sc >> 24) & 15u, la = xbase + 8u * (sc & 0xffffffu);
+                ad[c] = ct == cr ? (la | 1u) : map_rank(la, ct);
+              }
             }
           }
         }
         for (;;) {
 #pragma unroll
-          for (int c = 0; c < 2; ++c)
-            if (!gs_published(v[c])) v[c] = GRID ? ld_relaxed_u64(a.xnew + ad[c]) : ld_cluster_u64(ad[c]);
+          for (int c = 0; c < 2; ++c) {
+            if (gs_published(v[c])) continue;
+            if (GRID) v[c] = ld_relaxed_u64(a.xnew + ad[c]);
+            else if (ad[c] & 1u) v[c] = ld_shared_volatile_u64(ad[c] & ~1u);
+            else v[c] = ld_cluster_u64(ad[c]);
+          }
           if (!__any_sync(FULL, !gs_published(v[0]) || !gs_published(v[1]))) break;
           if (a.sleep_ns > 0) __nanosleep((unsigned)a.sleep_ns);
           if (__any_sync(FULL, timed_out(spins))) { abort = true; break; }
@@ -242,7 +251,7 @@ __global__ void __launch_bounds__(1024, 1) gs_cluster_kernel(GsClusterArgs a) {
         }
         if (!abort) {
           const double xi = div_rn_markstein(s, dg, rdg);
-          st_shared_f64(xbase + 8u * (unsigned)slot, xi);
+          if (!GRID || slot >= 0) st_shared_f64(xbase + 8u * (unsigned)slot, xi);  // grid form: only if polled here
           if (GRID) st_relaxed_f64(a.xnew + row, xi);  // polled by other CTAs
           else a.xnew[row] = xi;
           if (a.trace) a.trace[(size_t)a.n + q] = clock64();

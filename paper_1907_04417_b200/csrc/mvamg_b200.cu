@@ -220,12 +220,14 @@ inline bool warp_rows(const Csr& A) {
   return A.n > 0 && A.n <= kWarpRowMaxRows && (long long)A.nnz >= (long long)kWarpRowMinAvg * A.n;
 }
 
-// GS preparation (gs_prepare_kernel); the backward fold of a small long-row
-// level runs one warp per row (bit-identical)
+// GS preparation (gs_prepare_kernel); the backward fold of a long-row level
+// runs one warp per row (bit-identical)
 void launch_prepare(const Csr& A, const double* b, const double* xold, const int* perm, double* tperm,
                     double* xnew, int* ticket, int fold, cudaStream_t s) {
   const int n = A.n;
-  if (fold && warp_rows(A)) {
+  // long rows (>= 16 entries on average) at any size: the lanes read a row's entries coalesced
+  // (C5 levels 1-4, ~70 entries per row: the thread-per-row fold was 14% of the solve)
+  if (fold && (warp_rows(A) || (A.n > 0 && (long long)A.nnz >= 16LL * A.n))) {
     const int gw = std::max(1, std::min((n + 7) / 8, num_sms() * 8));
     gs_prepare_fold_warp_kernel<<<gw, 256, 0, s>>>(n, A.ip, A.ix, A.v, b, xold, perm, tperm, xnew, ticket);
   } else {
@@ -2565,20 +2567,58 @@ int mvamg_gs_cluster_plan(int n, const int* indptr, const int* indices, const do
     }
     p0 = p1;
   }
-  int slots = 2;
-  for (int c = 0; c < ncta; ++c) slots = std::max(slots, nin[c]);
-  if (slots >= (1 << 24)) return fail(MVAMG_E_ARG, "gs_cluster_plan: too many slots per CTA");
-  *slots_per_cta = slots;
-  if (local_late) *local_late = hits;
+  // a row's entries in consumption order and its late tail: by the level at which each input
+  // becomes final (old values first), CSR order within one -- but the critical input (whose CTA
+  // the row mostly shares) last of all; late = the inputs of the last level, at most kClusterLate
+  auto row_entries = [&](int i, std::vector<int>& ents) -> int {
+    ents.clear();
+    for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+      const int j = indices[k];
+      if (j == i) continue;
+      const bool isnew = fwd ? j < i : j > i;
+      if (zero && !isnew) continue;
+      ents.push_back(k);
+    }
+    auto avail = [&](int k) {
+      const int j = indices[k];
+      if (!(fwd ? j < i : j > i)) return -1;
+      return 2 * lvl[j] + (j == crit[i] ? 1 : 0);
+    };
+    std::stable_sort(ents.begin(), ents.end(), [&](int x, int y) { return avail(x) < avail(y); });
+    const int cnt = (int)ents.size();
+    int late = 0;
+    while (late < kClusterLate && late < cnt && avail(ents[cnt - 1 - late]) >= 0 &&
+           avail(ents[cnt - 1 - late]) / 2 == avail(ents[cnt - 1]) / 2)
+      ++late;
+    return late;
+  };
+  // x slots: every row in the cluster form (peers read them over DSMEM); in the grid form only
+  // the rows some row of the same CTA polls as a late input -- shared memory holds nothing else
+  std::vector<int> ents;
+  std::vector<char> need(n > 0 ? n : 1, grid ? 0 : 1);
+  if (grid) {
+    for (int i = 0; i < n; ++i) {
+      const int late = row_entries(i, ents), cnt = (int)ents.size();
+      for (int u = cnt - late; u < cnt; ++u) {
+        const int j = indices[ents[u]];
+        if (cta[j] == cta[i]) need[j] = 1;
+      }
+    }
+  }
   // a CTA's rows go round-robin to its warps in position order; worker g = warp * ncta + cta
-  std::vector<int> seen(ncta, 0), wcount(G + 1, 0), wk(n > 0 ? n : 1, 0), sl(n > 0 ? n : 1, 0);
+  std::vector<int> seen(ncta, 0), nslot(ncta, 0), wcount(G + 1, 0), wk(n > 0 ? n : 1, 0), sl(n > 0 ? n : 1, -1);
   for (int p = 0; p < n; ++p) {
     const int i = order[p], c = cta[i];
-    sl[i] = seen[c];
+    if (need[i]) sl[i] = nslot[c]++;
     wk[i] = (seen[c] % wpc) * ncta + c;
     ++seen[c];
     ++wcount[wk[i] + 1];
   }
+  int slots = 2;
+  for (int c = 0; c < ncta; ++c) slots = std::max(slots, nslot[c]);
+  if (slots >= (1 << 24)) return fail(MVAMG_E_ARG, "gs_cluster_plan: too many slots per CTA");
+  *slots_per_cta = slots;
+  if (local_late) *local_late = hits;
   for (int g = 0; g < G; ++g) wcount[g + 1] += wcount[g];
   std::vector<int> fill(wcount.begin(), wcount.end() - 1), qrow(n > 0 ? n : 1, 0);
   for (int p = 0; p < n; ++p) {
@@ -2605,7 +2645,6 @@ int mvamg_gs_cluster_plan(int n, const int* indptr, const int* indices, const do
   for (int g = 0; g <= G; ++g) { wptr[g] = wcount[g]; wpage[g] = pg_first[g]; }
   unsigned char* out = static_cast<unsigned char*>(blob);
   std::memset(out, 0, (size_t)pages * page_bytes);
-  std::vector<int> ents;
   for (int g = 0; g < G; ++g) {
     long long pg = pg_first[g] - 1;
     int used = page_bytes, rows_in_page = 0;
@@ -2622,27 +2661,9 @@ int mvamg_gs_cluster_plan(int n, const int* indptr, const int* indices, const do
       }
       unsigned char* rec = out + (size_t)pg * page_bytes + used;
       double dgv = 0.0;
-      ents.clear();
-      for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
-        const int j = indices[k];
-        if (j == i) { dgv = data[k]; continue; }
-        const bool isnew = fwd ? j < i : j > i;
-        if (zero && !isnew) continue;
-        ents.push_back(k);
-      }
-      // by the level at which each input becomes final (old values first), CSR order within
-      // one -- but the critical input (whose CTA this row mostly shares) last of all
-      auto avail = [&](int k) {
-        const int j = indices[k];
-        if (!(fwd ? j < i : j > i)) return -1;
-        return 2 * lvl[j] + (j == crit[i] ? 1 : 0);
-      };
-      std::stable_sort(ents.begin(), ents.end(), [&](int x, int y) { return avail(x) < avail(y); });
-      // the late tail: the inputs of the last level (at most kClusterLate of them)
-      int late = 0;
-      while (late < kClusterLate && late < cnt && avail(ents[cnt - 1 - late]) >= 0 &&
-             avail(ents[cnt - 1 - late]) / 2 == avail(ents[cnt - 1]) / 2)
-        ++late;
+      for (int k = indptr[i]; k < indptr[i + 1]; ++k)
+        if (indices[k] == i) dgv = data[k];
+      const int late = row_entries(i, ents);
       const int hdr[4] = {cnt, cnt - late, i, sl[i]};
       const double dd[2] = {dgv, 1.0 / dgv};
       std::memcpy(rec, hdr, 16);

@@ -110,6 +110,8 @@ class GpuConfig:
                                     # shared memory: the cluster dataflow sweep (gs_cluster.cuh), before any other
     cluster_max_rows: int = 4000000  # ... up to this size (what decides is whether a CTA's x slice and page rings
                                     # fit its shared memory)
+    cluster_full_rows: int = 1000   # cluster form: 16 CTAs from this size up, cluster_small_ctas below
+    cluster_small_ctas: int = 8
     cluster_grid_rows: int = 10000  # above: the grid form (ordinary CTAs over the whole GPU, early inputs through L2;
                                     # C3: 2-3x the row sweep at 53k and 160k rows, level with the cluster form at 16k)
     cluster_grid_ctas: int = 0      # CTAs of the grid form (0: one per SM)
@@ -678,7 +680,7 @@ def cluster_shape(n, nlev, cfg=None, grid=None):
     if grid:
         ncta = max(1, min(cfg.cluster_grid_ctas or _num_sms(), -(-n // 256)))
     else:
-        ncta = 16 if n >= 1000 else (8 if n >= 300 else 4)
+        ncta = 16 if n >= cfg.cluster_full_rows else max(1, cfg.cluster_small_ctas)
         ncta = max(1, min(ncta, cfg.max_cluster))
     wpc = int(min(cfg.cluster_max_warps, max(cfg.cluster_min_warps, -(-n // (15 * ncta)))))
     return bool(grid), ncta, wpc

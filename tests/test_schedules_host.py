@@ -177,7 +177,7 @@ def _cluster_streams(pl, G):
                 assert rdg == 1.0 / dg
                 cf = blob[off + 32:off + 32 + 8 * cnt].view(np.float64)
                 sc = blob[off + 32 + 8 * cnt:off + 32 + 12 * cnt].view(np.uint32)
-                assert 0 <= ne <= cnt and cnt - ne <= 2
+                assert 0 <= ne <= cnt and cnt - ne <= 4
                 rows.append((cnt, ne, row, slot, float(dg), cf, sc))
                 off += (32 + 12 * cnt + 15) & ~15
             assert off <= base + page                              # no record straddles a page
@@ -221,8 +221,11 @@ def _cluster_emulate(A, pl, ncta, wpc, mode, b, x_old):
             if np.isnan(vals).any():
                 continue
             xi = (b[row] - np.dot(cf, vals)) / dg
-            assert np.isnan(xs[g % ncta, slot])                     # every slot is written once
-            xs[g % ncta, slot] = xi
+            if slot >= 0:                                           # grid form: only rows polled in this CTA
+                assert np.isnan(xs[g % ncta, slot])                 # every slot is written once
+                xs[g % ncta, slot] = xi
+            else:
+                assert grid
             xg[row] = xi
             x[row] = xi
             cur[g] += 1

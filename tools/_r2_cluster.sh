@@ -1,11 +1,12 @@
 # cluster / grid sweeps: whole GPU suite, C3 bench
 set -x
-timeout 2400 python -m pytest tests -q -m gpu 2>&1 | tail -8 | tee gpurun_out/r2j_gpu_tests.log
-timeout 1800 python bench.py --steps 20 --warmup 5 > gpurun_out/r2j_b200_c3.json 2> gpurun_out/r2j_b200_c3.err
+timeout 800 python tools/cluster_bench.py scratch/c3_coarse.npz levels=1,2,3 > gpurun_out/cl16.log 2>&1; grep -v "best" gpurun_out/cl16.log | cut -c1-110
+timeout 2400 python -m pytest tests -q -m gpu 2>&1 | tail -4 | tee gpurun_out/r2l_gpu_tests.log
+timeout 1800 python bench.py --steps 20 --warmup 5 > gpurun_out/r2l_b200_c3.json 2> gpurun_out/r2l_b200_c3.err
 python -c "
-import json; d=json.loads(open('gpurun_out/r2j_b200_c3.json').read().strip().splitlines()[-1])
+import json; d=json.loads(open('gpurun_out/r2l_b200_c3.json').read().strip().splitlines()[-1])
 print('value', d['value'], 'e2e', d['e2e']['value'], 'cycle', d['cycle'], 'nit', d['details']['nit'], d['details'].get('history_rel_max_vs_oracle'))
-print('roofline', d['roofline']); print('h2', d.get('h2'))
+print('h2', d.get('h2',{}).get('value'))
 for s in d['sweeps']: print(s['level'], s['kernel'], s['sweep'][:8], round(s['ms']*1e3,1), 'us')
 "
-tail -3 gpurun_out/r2j_b200_c3.err
+tail -3 gpurun_out/r2l_b200_c3.err

@@ -66,8 +66,11 @@ def main():
             shapes = [None]
             sleeps = [cfg.cluster_sleep_ns]
             if grid:
-                shapes = ([(False, c, w) for c in (16,) for w in (16, 32)] +
-                          [(True, c, w) for c in (74, 148) for w in (8, 16, 32)])
+                if kw.get("small", "0") == "1":
+                    shapes = [(False, c, w) for c in (1, 2, 4, 8, 16) for w in (4, 8, 16, 32)]
+                else:
+                    shapes = ([(False, c, w) for c in (16,) for w in (16, 32)] +
+                              [(True, c, w) for c in (74, 148) for w in (8, 16, 32)])
                 sleeps = [0]
             best = None
             for shape in shapes:

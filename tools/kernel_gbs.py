@@ -29,7 +29,7 @@ def ld(k):  # entries of L + D (forward sweep from zero)
 
 B = {  # bytes per PCG iteration
     "fine sweeps (gs_lean, level 0)": 12 * ld(0) + 4 * (n[0] + 1) + 24 * n[0] + ab(nnzA[0], n[0]) + 32 * n[0],
-    "coarse sweeps (row / stream / level-set)": sum(12 * ld(k) + 4 * (n[k] + 1) + 24 * n[k] + ab(nnzA[k], n[k])
+    "coarse sweeps (cluster / grid / row / stream)": sum(12 * ld(k) + 4 * (n[k] + 1) + 24 * n[k] + ab(nnzA[k], n[k])
                                                     + 32 * n[k] for k in range(1, L)),
     "residual SpMV": sum(ab(nnzA[k], n[k]) + 24 * n[k] for k in range(L)),
     "restriction SpMV": sum(ab(nnzP[k], n[k + 1]) + 8 * n[k] + 8 * n[k + 1] for k in range(L)),
@@ -40,8 +40,8 @@ B = {  # bytes per PCG iteration
 }
 fam = {
     "fine sweeps (gs_lean, level 0)": ("gs_lean_kernel",),
-    "coarse sweeps (row / stream / level-set)": ("gs_row_kernel", "gs_stream_kernel", "gs_level_kernel",
-                                                 "gs_prepare"),
+    "coarse sweeps (cluster / grid / row / stream)": ("gs_cluster_kernel", "gs_row_kernel", "gs_stream_kernel",
+                                                 "gs_level_kernel", "gs_prepare"),
     "residual SpMV": ("spmv_stream_kernel<1>", "spmv_warp_kernel<1>", "spmv_kernel<1>"),
     "restriction SpMV": ("spmv_stream_kernel<0>", "spmv_warp_kernel<0>", "spmv_kernel<0>"),
     "prolongation SpMV": ("spmv_stream_kernel<2>", "spmv_warp_kernel<2>", "spmv_kernel<2>"),
