@@ -416,9 +416,10 @@ def _level_sweeps(op, k, b_dev, x_old, x_new, ws, s):
     names = ["", ""]
     cl = lv.get("cluster") or {}
     if cl:
+        bm = 3 if 3 in cl else 2
         return ((lambda: cl[0].sweep(b_dev, None, x_new, ws, s)) if 0 in cl else None,
-                (lambda: cl[2].sweep(b_dev, x_old, x_new, ws, s)) if 2 in cl else None,
-                "gs_cluster_kernel", "gs_cluster_kernel+fold")
+                (lambda: cl[bm].sweep(b_dev, x_old, x_new, ws, s)) if bm in cl else None,
+                "gs_cluster_kernel", "gs_cluster_kernel" if bm == 3 else "gs_cluster_kernel+fold")
     st = lv.get("stream") or {}
     if 0 in st:
         fwd, names[0] = (lambda: st[0].sweep(b_dev, None, x_new, ws, s)), "gs_stream_kernel"

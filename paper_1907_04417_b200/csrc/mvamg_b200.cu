@@ -220,14 +220,14 @@ inline bool warp_rows(const Csr& A) {
   return A.n > 0 && A.n <= kWarpRowMaxRows && (long long)A.nnz >= (long long)kWarpRowMinAvg * A.n;
 }
 
-// GS preparation (gs_prepare_kernel); the backward fold of a long-row level
-// runs one warp per row (bit-identical)
+// GS preparation (gs_prepare_kernel); the backward fold of a small long-row
+// level runs one warp per row (bit-identical)
 void launch_prepare(const Csr& A, const double* b, const double* xold, const int* perm, double* tperm,
                     double* xnew, int* ticket, int fold, cudaStream_t s) {
   const int n = A.n;
-  // long rows (>= 16 entries on average) at any size: the lanes read a row's entries coalesced
-  // (C5 levels 1-4, ~70 entries per row: the thread-per-row fold was 14% of the solve)
-  if (fold && (warp_rows(A) || (A.n > 0 && (long long)A.nnz >= 16LL * A.n))) {
+  // (one warp per row at any size was measured level with the thread-per-row fold on C5's
+  // 2.86M- and 900k-row levels -- its CSR-order shuffle chain costs what the coalescing saves)
+  if (fold && warp_rows(A)) {
     const int gw = std::max(1, std::min((n + 7) / 8, num_sms() * 8));
     gs_prepare_fold_warp_kernel<<<gw, 256, 0, s>>>(n, A.ip, A.ix, A.v, b, xold, perm, tperm, xnew, ticket);
   } else {
@@ -819,10 +819,10 @@ struct mvamg_hierarchy {
       } else {
         bool fwd = sp.kind == MVAMG_GS_FORWARD;
         int lmode = (fwd ? 0 : 2) + (x_cur == nullptr ? 0 : 1);
-        if (!fwd && x_cur != nullptr && l.gcl[2].blob) {
-          st = launch_gs_cluster(l.A, l.gcl[2], b, x_cur, out, ticket, status_ptr(), s);
-        } else if (l.gcl[lmode].blob) {
+        if (l.gcl[lmode].blob) {
           st = launch_gs_cluster(l.A, l.gcl[lmode], b, x_cur, out, ticket, status_ptr(), s);
+        } else if (!fwd && x_cur != nullptr && l.gcl[2].blob) {  // folded backward sweep from x_old
+          st = launch_gs_cluster(l.A, l.gcl[2], b, x_cur, out, ticket, status_ptr(), s);
         } else if (l.gss[lmode].nstages) {
           st = launch_gs_stream(l.A.n, l.gss[lmode], x_cur != nullptr, b, x_cur, out, s);
         } else if (!fwd && x_cur != nullptr && l.gss[2].nstages && l.gss[2].tfold) {

@@ -141,6 +141,25 @@ class GpuMultigridOperator:
                 modes.add(1)
         return sorted(modes)
 
+    def _gs_cluster_modes(self, A):
+        """Cluster / grid plans the cycle needs for level matrix A (0 fwd x=0, 1 fwd, 2 bwd x=0 -- with
+        x_old the folded backward sweep --, 3 bwd).  A backward sweep from x_old runs as its own mode-3
+        plan (x_old entries read in the kernel) up to config.cluster_fused_fold_rows rows, else folded."""
+        modes = set()
+        for spec, first_zero in ((self.pre_smoother, True), (self.post_smoother, False)):
+            if spec.kind == WEIGHTED_JACOBI or spec.sweeps == 0:
+                continue
+            if spec.kind == GS_BACKWARD:
+                if first_zero:
+                    modes.add(2)
+                if not first_zero or spec.sweeps > 1:
+                    modes.add(3 if A.shape[0] <= self.config.cluster_fused_fold_rows else 2)
+            else:
+                modes.add(0 if first_zero else 1)
+                if first_zero and spec.sweeps > 1:
+                    modes.add(1)
+        return sorted(modes)
+
     def _gs_stream_modes(self, A):
         """Stream plans the cycle needs for level matrix A: {mode: plan mode}
         (a backward sweep from x_old that does not fit with b in shared memory
@@ -199,7 +218,7 @@ class GpuMultigridOperator:
                         and not cfg.force_row_gs and A.shape[0] <= cfg.cluster_max_rows):
                     # cluster dataflow sweeps: x in one thread-block cluster's distributed shared memory
                     try:
-                        plans = {m: DeviceGsCluster(A, m, cfg) for m in self._gs_level_modes()}
+                        plans = {m: DeviceGsCluster(A, m, cfg) for m in self._gs_cluster_modes(A)}
                     except ValueError:
                         plans = None
                     if plans is not None:

@@ -117,6 +117,9 @@ class GpuConfig:
     cluster_grid_ctas: int = 0      # CTAs of the grid form (0: one per SM)
     cluster_min_warps: int = 8      # worker warps per CTA, at least
     cluster_max_warps: int = 32     # ... and at most
+    cluster_fused_fold_rows: int = 300000  # levels up to this size sweep backward from x_old with a mode-3 plan
+                                    # (x_old entries read inside the kernel) instead of the fold kernel + the
+                                    # zero-guess plan (C3: H1 70.6 -> 67.8 ms with every level fused)
     cluster_page_bytes: int = 2048  # page of row records a worker warp streams per TMA bulk copy (doubled while
                                     # a row's record does not fit)
     cluster_sleep_ns: int = 0       # back-off (ns) of a worker warp whose poll found nothing new
