@@ -50,13 +50,19 @@ fam = {
     "PCG vector updates and dots": ("pcg_xr_kernel", "dot2_kernel", "pcg_p_kernel"),
 }
 T = {}
+its = 0
 for line in open(SUMMARY).read().splitlines():
     m = re.match(r"\s*([\d.]+)%\s+(\d+)\s+([\d.]+)\s+(\S.*)$", line)
     if m:
         T[m.group(4).strip()] = int(m.group(2)) * float(m.group(3)) * 1e-6
+        if m.group(4).strip().startswith("spmv_dot_kernel"):
+            its = int(m.group(2))  # one A p per PCG iteration: the iterations the launch list covers
+scale = nit / its if its else 1.0  # kernel time per solve of nit iterations
+T = {k: v * scale for k, v in T.items()}
 used = set()
 print(f"# {os.path.basename(BENCH)}: {nit} PCG iterations, levels {n}; peak {peak:.0f} GB/s (MEASURED_PEAKS.json)")
-print(f"# time: {os.path.relpath(SUMMARY, ROOT)} (ncu launch list, cold cache, serialised); the prepare kernels")
+print(f"# time: {os.path.relpath(SUMMARY, ROOT)} (ncu launch list, cold cache, serialised; {its} iterations listed,")
+print(f"# scaled to one solve of {nit}); the prepare kernels")
 print("# (rhs permutation / fold / sentinel fill) are counted with the coarse sweeps; bytes: SURVEY 8(d) model")
 print(f"{'kernel family':42s} {'MB/iter':>9} {'ms/solve':>9} {'GB/s':>8} {'% peak':>7}")
 tb = tt = 0.0
