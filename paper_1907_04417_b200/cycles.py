@@ -289,7 +289,22 @@ class GpuMultigridOperator:
                 gp = DeviceGsPlan(A, self.config)
                 if (not self.config.generic_gs and gp.plan.nchains > 0
                         and A.shape[0] / gp.plan.nchains < self.config.min_chain_rows):
-                    # no chain structure for the wavefront: dataflow row sweeps instead
+                    # no chain structure for the wavefront: the grid-form dataflow sweep (tolerance mode;
+                    # C4's fine level, 525k rows of 2 interleaved dofs: 4x the row sweep), else row sweeps
+                    plans = None
+                    if cfg.cluster_gs and not cfg.exact_gs and not cfg.force_row_gs and A.shape[0] <= cfg.cluster_max_rows:
+                        try:
+                            plans = {m: DeviceGsCluster(A, m, cfg, grid=True) for m in self._gs_cluster_modes(A)}
+                        except ValueError:
+                            plans = None
+                    if plans is not None:
+                        self.gs_plans.append(None)
+                        self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=None, rows=None, cluster=plans))
+                        _lib.check(L.mvamg_hierarchy_set_level(h, k, dA.n, dA.nnz, *dA.ptrs(), ptr(dd),
+                                                               None, 0, None, None, None, 32, 0, 0), "set_level")
+                        for m, cp in plans.items():
+                            _lib.check(L.mvamg_hierarchy_set_gs_cluster(h, k, m, *cp.args()), "set_gs_cluster")
+                        continue
                     rows = {m: DeviceGsRows(A, m, self.config) for m in self._gs_level_modes()}
                     self.gs_plans.append(None)
                     self.level_dev.append(dict(A=dA, gs=None, plan=None, levels=None, rows=rows))

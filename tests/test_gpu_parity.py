@@ -663,6 +663,11 @@ def test_short_chain_level_uses_row_sweep(mv, c1):
     z = op.apply(b)
     assert np.array_equal(z, wf.apply(b))
     assert rel(z, OracleOperator(pm, pp).apply(b)) <= TOL_CYCLE
+    # tolerance mode: such a level takes the grid-form dataflow sweep
+    tol = mv.GpuMultigridOperator(pm, pp)
+    cl = tol.level_dev[0].get("cluster")
+    assert cl is not None and all(p.grid for p in cl.values())
+    assert rel(tol.apply(b), z) <= 1e-12
 
 
 def test_composite_graphs_not_reused_across_composites(mv, c1, c1_comps):

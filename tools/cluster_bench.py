@@ -72,6 +72,8 @@ def main():
                     shapes = ([(False, c, w) for c in (16,) for w in (16, 32)] +
                               [(True, c, w) for c in (74, 148) for w in (8, 16, 32)])
                 sleeps = [0]
+            if "sleeps" in kw:
+                sleeps = [int(x) for x in kw["sleeps"].split(",")]
             best = None
             for shape in shapes:
                 try:
