@@ -134,7 +134,7 @@ int mvamg_gs_schedule(int n, const int* indptr, const int* indices, const double
  * 2, 4, 8), slot_words (>= R*(32*max_S+32), even) and rec_words_max
  * (R*32*max_S) size the per-warp TMA ring.  lean_C > 0 selects the lean
  * kernel: records built with uniform_S = 3 + 2*C, no x_old sources,
- * (R, D) in {(8,3), (8,2), (4,4), (2,8), (1,8)}; lean_C = C | K << 8 with
+ * (R, D) in {(8,3), (8,2), (4,4), (4,2), (2,8), (2,2), (1,8)}; lean_C = C | K << 8 with
  * K > 1 rows per lane per round (C <= 4, (R, D, K) in {(2,2,4), (2,3,4),
  * (4,2,2)}).  ws: device
  * int workspace (>= 4 ints: tile ticket, status word).  Bit-identical to the

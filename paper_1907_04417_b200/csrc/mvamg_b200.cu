@@ -114,8 +114,8 @@ void set_kernel_attrs() {
   ok &= cudaFuncSetAttribute(gs_lean_kernel<F, CC, RR, DD, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                              maxsm) == cudaSuccess;
 #define MVAMG_LEAN_ATTR_C(F, RR, DD) MVAMG_LEAN_ATTR(F, 2, RR, DD) MVAMG_LEAN_ATTR(F, 4, RR, DD) MVAMG_LEAN_ATTR(F, 8, RR, DD)
-  MVAMG_LEAN_ATTR_C(true, 8, 3) MVAMG_LEAN_ATTR_C(true, 8, 2) MVAMG_LEAN_ATTR_C(true, 4, 4) MVAMG_LEAN_ATTR_C(true, 2, 8) MVAMG_LEAN_ATTR_C(true, 1, 8)
-  MVAMG_LEAN_ATTR_C(false, 8, 3) MVAMG_LEAN_ATTR_C(false, 8, 2) MVAMG_LEAN_ATTR_C(false, 4, 4) MVAMG_LEAN_ATTR_C(false, 2, 8) MVAMG_LEAN_ATTR_C(false, 1, 8)
+  MVAMG_LEAN_ATTR_C(true, 8, 3) MVAMG_LEAN_ATTR_C(true, 8, 2) MVAMG_LEAN_ATTR_C(true, 4, 4) MVAMG_LEAN_ATTR_C(true, 4, 2) MVAMG_LEAN_ATTR_C(true, 2, 2) MVAMG_LEAN_ATTR_C(true, 2, 8) MVAMG_LEAN_ATTR_C(true, 1, 8)
+  MVAMG_LEAN_ATTR_C(false, 8, 3) MVAMG_LEAN_ATTR_C(false, 8, 2) MVAMG_LEAN_ATTR_C(false, 4, 4) MVAMG_LEAN_ATTR_C(false, 4, 2) MVAMG_LEAN_ATTR_C(false, 2, 2) MVAMG_LEAN_ATTR_C(false, 2, 8) MVAMG_LEAN_ATTR_C(false, 1, 8)
 #define MVAMG_LEANK_ATTR(F, CC, RR, DD, KK) \
   ok &= cudaFuncSetAttribute(gs_lean_kernel<F, CC, RR, DD, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) == cudaSuccess;
 #define MVAMG_LEANK_ATTR_F(F)                                                               \
@@ -383,8 +383,10 @@ int launch_gs(bool fwd, const Csr& A, const GsList& ls, const GsPlan& p, const d
   do {                                                                            \
     if (ls.R >= 8 && ls.D >= 3) MVAMG_LEAN_C(F, 8, 3);                            \
     else if (ls.R >= 8) MVAMG_LEAN_C(F, 8, 2);                                    \
-    else if (ls.R >= 4) MVAMG_LEAN_C(F, 4, 4);                                    \
-    else if (ls.R >= 2) MVAMG_LEAN_C(F, 2, 8);                                    \
+    else if (ls.R >= 4 && ls.D >= 4) MVAMG_LEAN_C(F, 4, 4);                       \
+    else if (ls.R >= 4) MVAMG_LEAN_C(F, 4, 2);                                    \
+    else if (ls.R >= 2 && ls.D >= 8) MVAMG_LEAN_C(F, 2, 8);                       \
+    else if (ls.R >= 2) MVAMG_LEAN_C(F, 2, 2);                                    \
     else MVAMG_LEAN_C(F, 1, 8);                                                   \
   } while (0)
     if (fwd) MVAMG_LEAN_R(true); else MVAMG_LEAN_R(false);
@@ -1690,8 +1692,9 @@ int mvamg_gs_sweep_f64(int direction, int n, const int* indptr, const int* indic
   ls.tperm = tperm; ls.R = R; ls.D = D; ls.slot_words = slot_words; ls.rec_words_max = rec_words_max;
   ls.lean_C = lean_C;
   const int lean_K = (lean_C >> 8) & 0xff;
-  if (lean_C > 0 && lean_K <= 1 && ((R == 8 && D != 2 && D != 3) || (R == 4 && D != 4) || (R <= 2 && D != 8)))
-    return fail(MVAMG_E_ARG, "gs: lean kernel ring must be (R, D) in {(8,3), (8,2), (4,4), (2,8), (1,8)}");
+  if (lean_C > 0 && lean_K <= 1 && ((R == 8 && D != 2 && D != 3) || (R == 4 && D != 4 && D != 2) || (R == 2 && D != 8 && D != 2) ||
+                                    (R == 1 && D != 8)))
+    return fail(MVAMG_E_ARG, "gs: lean kernel ring must be (R, D) in {(8,3), (8,2), (4,4), (4,2), (2,8), (2,2), (1,8)}");
   if (lean_K > 1 && ((lean_C & 0xff) > 4 ||
                      !((lean_K == 4 && R == 2 && (D == 2 || D == 3)) || (lean_K == 2 && R == 4 && D == 2))))
     return fail(MVAMG_E_ARG, "gs: lean kernel with K rows per round needs C <= 4 and (R, D, K) in "

@@ -95,6 +95,8 @@ class GpuConfig:
     autotune_gs: bool = True        # coarse levels: time row and level-set sweeps once, keep the faster per mode
     min_chain_rows: float = 8.0     # a level whose wavefront chains average fewer rows uses the row sweep
                                     # (e.g. interleaved multi-dof systems, where row i rarely couples to i-1)
+    lean_small_ring_tiles: int = 148  # lean sweeps with at least this many tiles use the (4, 2) TMA ring (0: never)
+    lean_many_tiles: int = 1184     # ... and with this many one-warp tiles a modular window of 16 positions
     lean_wpos: int = 64             # lean sweeps: one-warp tiles with a window of this many positions per chain
                                     # (power of two; 0: the whole chain, which caps tiles per SM and chain length)
     block_chains: bool = True       # 3-D grid lines: tiles of 2-D blocks of lines (chain_block_order), so a
@@ -385,13 +387,46 @@ class DeviceGsPlan:
     def __init__(self, A, cfg=None, plan=None):
         self.A = as_csr(A)
         self.cfg = cfg or GpuConfig()
-        self.plan = plan or gs_analyse(self.A, self.cfg)
-        self.chain_ptr = to_device(self.plan.chain_ptr, np.int32)
-        self.tile_ptr = to_device(self.plan.tile_ptr, np.int32)
-        order = getattr(self.plan, "chain_order", None)
+        self._csr = None
+        self._set_plan(plan or gs_analyse(self.A, self.cfg))
+        if plan is None:
+            self._tune_for_many_tiles()
+
+    def _set_plan(self, plan):
+        self.plan = plan
+        self.chain_ptr = to_device(plan.chain_ptr, np.int32)
+        self.tile_ptr = to_device(plan.tile_ptr, np.int32)
+        order = getattr(plan, "chain_order", None)
         self.chain_order = to_device(order, np.int32) if order is not None else None
         self.modes = {}
-        self._csr = None
+
+    def _tune_for_many_tiles(self):
+        """Lean sweeps with (many) more tiles than the GPU holds at once are bound by the tiles resident
+        per SM, i.e. by each tile's shared memory, not by a tile's latency: halve the TMA ring to (R, D) =
+        (4, 2) from one tile per SM up (C3: 325 / 353 -> 305 / 327 us), and with >= cfg.lean_many_tiles
+        one-warp tiles also cut the modular window to 16 positions (C5: 2.56 / 2.67 -> 1.97 / 2.08 ms per
+        sweep; same bits).  A window too short for the matrix's reads fails the schedule's check
+        (ValueError): then the standard plan stays."""
+        import dataclasses
+
+        p, cfg = self.plan, self.cfg
+        if not (p.lean_C > 0 and (p.lean_C >> 8) <= 1 and cfg.lean_ring is None and not cfg.lean_cluster
+                and not cfg.generic_gs and (p.R, p.D) == (8, 2) and p.ntiles >= cfg.lean_small_ring_tiles > 0):
+            return
+        wpos = int(getattr(p, "wpos", 0))
+        many = wpos > 16 and p.ntiles >= cfg.lean_many_tiles > 0
+        cfg2 = dataclasses.replace(cfg, lean_ring=(4, 2), lean_wpos=16 if many else cfg.lean_wpos,
+                                   max_threads=p.threads)  # the smaller ring must not widen the tiles
+        base = p
+        try:
+            self._set_plan(gs_analyse(self.A, cfg2))
+            if (self.plan.threads, self.plan.ntiles) != (base.threads, base.ntiles):
+                raise ValueError("tile shape changed")
+            if many:  # the shorter window must pass the schedule's read-before-overwrite check
+                for m in (0, 2):
+                    self.mode(m)
+        except ValueError:
+            self._set_plan(base)
 
     def mode(self, m):
         """Device schedule dict for mode m."""
