@@ -1,6 +1,8 @@
-// Gauss-Seidel in the reference's row order for coarse levels whose iterate
-// fits the shared memory of ONE thread-block cluster (up to 16 SMs x ~220 KB:
-// ~400k rows): dataflow over distributed shared memory, one warp per row.
+// Gauss-Seidel in the reference's row order for levels without grid structure
+// (the coarse levels; a fine level of interleaved dofs): dataflow with one warp
+// per row and the critical dependency chain in shared memory.  Cluster form:
+// the iterate in the distributed shared memory of ONE thread-block cluster
+// (small levels).  Grid form: one CTA per SM, see below.
 //
 // The serial loop (pkg/src/mvamg/_kernels.py:15-38) makes row i wait for every
 // x_new[j] it reads.  gs_row_kernel (gs_sweep.cuh) publishes and polls those
@@ -8,8 +10,8 @@
 // 162-188, so 0.25-0.33 ms per sweep whatever the level's size).  Here the
 // iterate lives in the cluster's shared memory -- position p of the
 // topological order in a fixed slot of a fixed CTA -- so a row is published by
-// one local st.shared and polled with ld.shared::cluster (~200 cycles across
-// SMs, ~40 inside one): no L2 round trip on the critical path.
+// one local st.shared and polled with ld.shared (own CTA, ~30 cycles) or
+// ld.shared::cluster (a peer's slot): no L2 round trip on the critical path.
 //
 // Work split (mvamg_gs_cluster_plan): every row of the topological order is
 // given to one of the cluster's G = NC x wpc worker warps (worker g = warp *
@@ -28,8 +30,10 @@
 //   late entries    (the last level's inputs, at most kClusterLate, the critical
 //                   one last) polled by lane 0 alone in a tight loop -- ld.shared
 //                   when the input lives in this CTA, as the plan mostly arranges
-//                   -- which then finishes the row: s = (b - early) - a1 x1 - a2 x2,
+//                   -- which then finishes the row: s = (b - early) - a1 x1 - a2 x2 ...,
 //                   the division (Markstein) and the publishing stores.
+// A sweep from a nonzero guess reads its x_old entries (sorted first) straight
+// from global memory in the early phase: no separate fold pass.
 // So after a row's last input lands its own value is one (mostly local) load
 // plus a few dependent FP64 operations away, and a waiting warp costs one
 // lane's polls (DSMEM moves only ~17 B/cycle per SM).

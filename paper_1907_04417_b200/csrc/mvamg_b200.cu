@@ -59,6 +59,14 @@ int g_row_sleep = [] {
   const char* e = getenv("MVAMG_ROW_SLEEP");
   return e ? atoi(e) : 0;
 }();
+int g_cluster_cap10 = [] {  // diagnostics: a CTA's share of a DAG level (x10) the plan lets it exceed ...
+  const char* e = getenv("MVAMG_CLUSTER_CAP10");
+  return e ? atoi(e) : 15;
+}();
+int g_cluster_tot10 = [] {  // ... and of all rows so far (x10), when a row follows its latest input's CTA
+  const char* e = getenv("MVAMG_CLUSTER_TOT10");
+  return e ? atoi(e) : 11;
+}();
 int g_cluster_local = [] {  // diagnostics: 0 = the cluster plan ignores where a row's latest input lives
   const char* e = getenv("MVAMG_CLUSTER_LOCAL");
   return e ? atoi(e) : 1;
@@ -2552,12 +2560,12 @@ int mvamg_gs_cluster_plan(int n, const int* indptr, const int* indices, const do
     int p1 = p0;
     while (p1 < n && lvl[order[p1]] == lvl[order[p0]]) ++p1;
     const int w = p1 - p0;
-    const int cap = (3 * w + 2 * ncta - 1) / (2 * ncta);
+    const int cap = (g_cluster_cap10 * w + 10 * ncta - 1) / (10 * ncta);
     std::fill(load.begin(), load.end(), 0);
     for (int p = p0; p < p1; ++p) {
       const int i = order[p];
       int c = (g_cluster_local && crit[i] >= 0) ? cta[crit[i]] : -1;
-      if (c >= 0 && load[c] < cap && 10LL * nin[c] <= 11LL * (p / ncta) + 10LL * wpc) {
+      if (c >= 0 && load[c] < cap && 10LL * nin[c] <= (long long)g_cluster_tot10 * (p / ncta) + 10LL * wpc) {
         ++hits;
       } else {
         c = 0;

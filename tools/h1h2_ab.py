@@ -1,7 +1,7 @@
 """A/B of GpuConfig variants on a bench workload: H1 PCG solve (V-cycle) and
 H2 PCG solve (symmetrized composite of the bootstrap K-cycles), device time.
 
-  python tools/h1h2_ab.py c3 "" "stream_gs=False" "stream_max_rows=1024"
+  python tools/h1h2_ab.py c3 "" "stream_gs=False" "stream_max_rows=1024"   [--h1: skip H2]
 Each variant: semicolon-separated GpuConfig fields (python literals)."""
 import ast
 import sys
@@ -14,8 +14,10 @@ import bench  # noqa: E402
 import paper_1907_04417_b200 as mv  # noqa: E402
 from paper_1907_04417_b200.krylov import pcg  # noqa: E402
 
-cfg_name = sys.argv[1]
-variants = sys.argv[2:] or [""]
+h1_only = "--h1" in sys.argv
+argv = [a for a in sys.argv if a != "--h1"]
+cfg_name = argv[1]
+variants = argv[2:] or [""]
 mats, pros, b, info = bench.load_workload(cfg_name)
 comps = info["components"]
 
@@ -38,6 +40,10 @@ for v in variants:
     cfg = mv.GpuConfig(**kw)
     op = mv.GpuMultigridOperator(mats, pros, config=cfg)
     t1, (_, r1) = timed(lambda: pcg(mats[0], b, precond=op, rtol=1e-6), 5)
+    if h1_only:
+        print(f"[{v or 'default'}] H1 {t1 * 1e3:.1f} ms (nit {r1.iterations})", flush=True)
+        del op
+        continue
     ops = [mv.GpuMultigridOperator(m, p, cycle=mv.CycleSpec("K", 2), config=cfg) for m, p in comps]
     pc = mv.GpuCompositePreconditioner(mv.GpuComposite(ops))
     t2, (_, r2) = timed(lambda: pcg(mats[0], b, precond=pc, rtol=1e-6), 2)
