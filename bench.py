@@ -6,8 +6,15 @@ multi-vector V-cycle (the reference's solve path, pkg/src/mvamg/estimator.py:
 138-145 -> krylov.py:28-72 -> cycles.py:150-179) on a hierarchy resident in
 HBM.  Prints ONE JSON line (rank 0).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c3|c4]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c3|c4|c5]
   python bench.py --impl reference ...   # the reference algorithm on host cores
+
+Default workload: C3, the largest BASELINE.json configuration BOTH arms can run
+inside a driver run -- the reference arm must build its hierarchy on host cores
+only (no GPU library in its process: ~100 s for C3; hours for C5's 32.8M rows)
+and time full solves (3.2 s each on C3; 139 s each on C5).  `--config c5` runs
+the metric's 1-GPU configuration on the B200 arm (fit ~400 s on the GPU,
+untimed; solve ~1.1 s; stated coarse-solve deviation, COARSE_PINV below).
 
 Keys beyond the base contract:
   roofline      dominant kernel (fine-level exact-order GS sweep) GB/s vs the

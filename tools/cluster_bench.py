@@ -1,7 +1,8 @@
 """Cluster dataflow GS sweep (gs_cluster.cuh) against the row / streamed sweeps
 on the coarse levels of a hierarchy dump (GPU).
 
-  python tools/cluster_bench.py scratch/c3_coarse.npz [levels=1,2,3] [grid=1] [exact=1]
+  python tools/dump_levels.py c3 scratch/c3_coarse.npz
+  python tools/cluster_bench.py scratch/c3_coarse.npz [levels=1,2,3] [grid=1] [small=1] [sleeps=0,50]
 
 Per level and sweep (forward from x=0, folded backward from x_old): CUDA-event
 times of the row / streamed schedule and of the cluster sweep (default shape,
