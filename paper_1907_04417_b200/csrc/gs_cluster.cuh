@@ -141,9 +141,9 @@ __global__ void __launch_bounds__(1024, 1) gs_cluster_kernel(GsClusterArgs a) {
   const int g = warp * (int)NC + (int)cr;
   bool abort = false;
   // a poll that has failed kGsIdleLimit times (or another warp's) ends the sweep with ST_GS_TIMEOUT
-  auto timed_out = [&](long long& spins) -> bool {
-    if ((++spins & 1023) != 0) return false;
-    if (spins > kGsIdleLimit) atomicOr(a.status, ST_GS_TIMEOUT);
+  auto timed_out = [&](unsigned& spins) -> bool {
+    if ((++spins & 1023u) != 0u) return false;
+    if (spins > (unsigned)kGsIdleLimit) atomicOr(a.status, ST_GS_TIMEOUT);
     return (*reinterpret_cast<volatile int*>(a.status) & ST_GS_TIMEOUT) != 0;
   };
   const int q0 = __ldg(a.wptr + g), q1 = __ldg(a.wptr + g + 1);
@@ -176,6 +176,12 @@ __global__ void __launch_bounds__(1024, 1) gs_cluster_kernel(GsClusterArgs a) {
       double dg, rdg;
       asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(dg), "=d"(rdg) : "r"(off + 16u));
       const unsigned cbase = off + kClusterRowHdr, sbase = cbase + 8u * (unsigned)cnt;
+      // the publishing addresses, formed now and pinned in registers: nothing but the last input's
+      // FMA, the division and the two stores is left between that input's arrival and the publish
+      unsigned my_saddr = xbase + 8u * (unsigned)slot;
+      double* my_gaddr = a.xnew + row;
+      asm volatile("" : "+r"(my_saddr));
+      asm volatile("" : "+l"(my_gaddr));
       if (q - qb == 32) {
         qb += 32;
         rr = rn;
@@ -184,7 +190,7 @@ __global__ void __launch_bounds__(1024, 1) gs_cluster_kernel(GsClusterArgs a) {
       const double rhs = __shfl_sync(FULL, rr, q - qb);
       // ---- early entries: one per lane, two chunks of 32 in flight together -----------
       double sum = 0.0;
-      long long spins = 0;
+      unsigned spins = 0;
       for (int base = 0; base < ne; base += 64) {
         double cf[2];
         unsigned long long v[2];
@@ -255,9 +261,9 @@ __global__ void __launch_bounds__(1024, 1) gs_cluster_kernel(GsClusterArgs a) {
         }
         if (!abort) {
           const double xi = div_rn_markstein(s, dg, rdg);
-          if (!GRID || slot >= 0) st_shared_f64(xbase + 8u * (unsigned)slot, xi);  // grid form: only if polled here
-          if (GRID) st_relaxed_f64(a.xnew + row, xi);  // polled by other CTAs
-          else a.xnew[row] = xi;
+          if (!GRID || slot >= 0) st_shared_f64(my_saddr, xi);  // grid form: only if polled here
+          if (GRID) st_relaxed_f64(my_gaddr, xi);  // polled by other CTAs
+          else *my_gaddr = xi;
           if (a.trace) a.trace[(size_t)a.n + q] = clock64();
         }
       }
