@@ -724,14 +724,16 @@ def cluster_shape(n, nlev, cfg=None, grid=None):
     return bool(grid), ncta, wpc
 
 
-_NUM_SMS = None
+_NUM_SMS = {}
 
 
 def _num_sms():
-    global _NUM_SMS
-    if _NUM_SMS is None:
-        _NUM_SMS = torch_cuda().cuda.get_device_properties(0).multi_processor_count
-    return _NUM_SMS
+    """SMs of the current CUDA device (the grid form runs one CTA on each)."""
+    torch = torch_cuda()
+    dev = torch.cuda.current_device()
+    if dev not in _NUM_SMS:
+        _NUM_SMS[dev] = torch.cuda.get_device_properties(dev).multi_processor_count
+    return _NUM_SMS[dev]
 
 
 def cluster_smem(slots, wpc, page_bytes):
