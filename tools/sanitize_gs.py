@@ -4,8 +4,9 @@ composite application -- the workload for compute-sanitizer
 
   compute-sanitizer --tool racecheck python tools/sanitize_gs.py
 
-Each sweep is also checked bit for bit against the CPU oracle, so a run that
-the sanitizer passes is a correct run too."""
+Each sweep is also checked against the CPU oracle -- bit for bit for the
+exact-order schedules, within 1e-12 for the tolerance-mode ones ("-G") -- so a
+run that the sanitizer passes is a correct run too."""
 import os
 import sys
 
@@ -19,8 +20,8 @@ from _fixtures import golden, hierarchy, laplacian_2d, laplacian_3d, random_spd_
 from oracle.oracle import oracle_gs  # noqa: E402
 
 import paper_1907_04417_b200 as mv  # noqa: E402
-from paper_1907_04417_b200.device import (DeviceGsLevels, DeviceGsPlan, DeviceGsRows, DeviceGsStream,  # noqa: E402
-                                          GpuConfig, to_device)
+from paper_1907_04417_b200.device import (DeviceGsCluster, DeviceGsLevels, DeviceGsPlan, DeviceGsRows,  # noqa: E402
+                                          DeviceGsStream, GpuConfig, to_device)
 
 rng = np.random.default_rng(0)
 cases = [("lap2d", laplacian_2d(24).tocsr()), ("lap3d", laplacian_3d(8).tocsr()),
@@ -54,12 +55,20 @@ for name, A in cases:
         runs.append(("stream", lambda xn, st=st: st.sweep(dev(b), dev(x0), xn, ws), want))
         st0 = DeviceGsStream(A, 2 * d, GpuConfig(exact_gs=False))
         runs.append(("stream-G", lambda xn, st=st0: st.sweep(dev(b), None, xn, ws), want0))
+        # cluster / grid dataflow sweeps (tolerance mode: fixed tree + ordered tail, within rounding of the oracle)
+        for what, kw in (("cluster", dict(ncta=4, wpc=4)), ("cluster-16", dict(ncta=16, wpc=8)),
+                         ("grid", dict(grid=True, ncta=37, wpc=5))):
+            c1 = DeviceGsCluster(A, 2 * d + 1, GpuConfig(), **kw)
+            runs.append((f"{what}-G", lambda xn, c1=c1: c1.sweep(dev(b), dev(x0), xn, ws), want))
+            c0 = DeviceGsCluster(A, 2 * d, GpuConfig(), **kw)
+            runs.append((f"{what}-zero-G", lambda xn, c0=c0: c0.sweep(dev(b), None, xn, ws), want0))
         for what, fn, ref in runs:
             xn = torch.empty(n, dtype=torch.float64, device="cuda")
             fn(xn)
             torch.cuda.synchronize()
             got = xn.cpu().numpy()
-            good = np.array_equal(got, ref) if what != "stream-G" else np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
+            good = (np.array_equal(got, ref) if not what.endswith("-G") else
+                    np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref)))
             ok &= bool(good)
             print(f"{name:6s} {direction:8s} {what:18s} {'ok' if good else 'MISMATCH'}", flush=True)
 
